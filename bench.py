@@ -1,0 +1,305 @@
+"""Benchmark of the batched NIRVANA cache lookup (BASELINE.json metric) on B200.
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c1] [--batch B]
+python bench.py --impl reference ...     (the fp64 CPU oracle, timed on the host cores)
+
+One step = one full lookup batch through the C ABI: query ingest (normalise + bf16), exact
+cosine scan of every cached entry with fused top-k, cross-split merge + Fig. 11 K map + hole
+rule, latent gather of the hit states and LCBFU access counters.  Inputs are seeded,
+synthetic, resident in HBM; L2 is flushed (a 512 MiB write) between timed steps and the
+step time is taken with CUDA events on the launching stream.  For N > 1 every rank holds
+its own replica of the cache and serves its own batches (weak scaling, no data-path
+collective); the max over ranks is reported.  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "cache lookups/sec (top-1+K+latent gather) at 1/2/4/8 B200; % of roofline"
+UNIT = "lookups/s"
+D = 768
+L = 4 * 64 * 64 * 2
+CONFIGS = {
+    # BASELINE.json configs[1]: the headline single-GPU workload
+    "c2": dict(n=100_000, b=4096, workload="C2: 100K cached entries x 768-d bf16, 4,096-query batches, "
+                                          "K in {5,10,15,20,25}, 4x64x64 fp16 latents, 1 GPU (tensor-core path)"),
+    # configs[2]: 1M entries, full per-K latent store, small batches (streaming/gather path)
+    "c3": dict(n=1_000_000, b=32, workload="C3: 1M cached entries x 768-d bf16 with the full per-K 4x64x64 "
+                                          "fp16 latent store (164 GB), batch 32"),
+    # configs[0]: the small case the oracle finishes in seconds
+    "c1": dict(n=1000, b=64, workload="C1: 1,000 entries x 768-d, 64 queries"),
+}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], p["bf16_tflops"], "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def build_cache(B, torch, cfg, seed, dev):
+    n = cfg["n"]
+    emb, cl = __import__("synth").entries(n, seed=seed)
+    import synth
+    pres = synth.present_masks(n, seed=seed)
+    g = B.NirvanaCache(entry_capacity=n, dim=D, latent_bytes=L, device=dev)
+    chunk = 8192
+    for s in range(0, n, chunk):
+        m = min(chunk, n - s)
+        lat = synth.latents_torch(s, m, 5, L, seed=seed, device=f"cuda:{dev}")
+        g.insert(torch.from_numpy(emb[s:s + m]).to(f"cuda:{dev}"), lat, present=pres[s:s + m])
+        del lat
+    return g, emb, cl, pres
+
+
+def cpu_baseline(emb, pres, q, budget_s=12.0):
+    """Time the fp64 oracle (as it stands) on a bounded sample of the same workload."""
+    import oracle
+    o = oracle.OracleCache(dim=D, entry_capacity=emb.shape[0], latent_bytes=0)
+    o.insert(emb, present=pres)
+    done, t0 = 0, time.perf_counter()
+    while done < q.shape[0] and time.perf_counter() - t0 < budget_s:
+        o.query(q[done:done + 1], topk=1, want_latents=False)
+        done += 1
+    dt = time.perf_counter() - t0
+    o.close()
+    return dict(value=done / dt, unit=UNIT, cores=1, kind="oracle",
+                sample=f"{done} queries of the same batch against the full {emb.shape[0]}-entry cache "
+                       f"(fp64 scan + full sort + K map + holes; stored without latent payload bytes), "
+                       f"1 thread, {dt:.1f} s")
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import synth
+    n = cfg["n"]
+    emb, cl = synth.entries(n, seed=1000)
+    pres = synth.present_masks(n, seed=1000)
+    q, _, _ = synth.queries(emb, cl, cfg["b"], seed=1001)
+    import oracle
+    o = oracle.OracleCache(dim=D, entry_capacity=n, latent_bytes=0)
+    o.insert(emb, present=pres)
+    per_step = max(1, min(cfg["b"], int(os.environ.get("REF_QUERIES_PER_STEP", "4"))))
+    for w in range(args.warmup):
+        o.query(q[:1], topk=1, want_latents=False)
+    times = []
+    for s in range(args.steps):
+        sel = q[(s * per_step) % cfg["b"]:][:per_step]
+        t0 = time.perf_counter()
+        o.query(sel, topk=1, want_latents=False)
+        times.append(time.perf_counter() - t0)
+    v = per_step * len(times) / sum(times)
+    line = dict(impl="reference", metric=METRIC, value=v, unit=UNIT, n_gpus=args.gpus, steps=args.steps,
+                warmup=args.warmup, ms_per_step=1e3 * statistics.mean(times), higher_is_better=True,
+                scaling="weak", vs_baseline=None, dtype="f64", data="synthetic",
+                config=dict(workload=cfg["workload"], entries=n, batch=cfg["b"]),
+                cpu_baseline=dict(value=v, unit=UNIT, cores=1, kind="oracle",
+                                  sample=f"{per_step} queries per step of the {cfg['b']}-query batch, "
+                                         f"full {n}-entry scan, 1 thread"),
+                e2e=dict(value=v, unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=list(CONFIGS))
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--scorer", default="auto", choices=["auto", "tc", "stream"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    if args.batch:
+        cfg["b"] = args.batch
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2312_04429_b200 import binding as B
+    import synth
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = local
+    g, emb, cl, pres = build_cache(B, torch, cfg, seed=1000, dev=dev)
+    g.set_scorer({"auto": B.SCORER_AUTO, "tc": B.SCORER_TC, "stream": B.SCORER_STREAM}[args.scorer])
+    b = cfg["b"]
+    q_np, _, _ = synth.queries(emb, cl, b, seed=1001 + 7919 * rank)
+    q = torch.from_numpy(q_np).cuda()
+    out = g.alloc_outputs(b, 1, latents=True)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    g.set_profile_events(ev)
+    for _ in range(max(3, args.warmup)):
+        g.query_into(q, out)
+    torch.cuda.synchronize()
+    step_ms, score_ms, prep_ms, fin_ms = [], [], [], []
+    launches0 = g.kernel_launches
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(torch.cuda.current_device()) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            g.query_into(q, out)
+            ev[3].synchronize()
+            step_ms.append(ev[0].elapsed_time(ev[3]))
+            prep_ms.append(ev[0].elapsed_time(ev[1]))
+            score_ms.append(ev[1].elapsed_time(ev[2]))
+            fin_ms.append(ev[2].elapsed_time(ev[3]))
+        torch.cuda.synchronize()
+    launches = g.kernel_launches - launches0
+    g.set_profile_events(None)
+    tot = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([tot], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        tot = float(t.item())
+    value = b * world * args.steps / (tot / 1e3)
+    k_np = out["k"].cpu().numpy()
+    hbm, tflops, peak_src = _peaks()
+    n = cfg["n"]
+    sc_ms = statistics.mean(score_ms)
+    scorer_used = "tc" if (args.scorer == "tc" or (args.scorer == "auto" and b > 4)) else "stream"
+    flops = 2.0 * b * n * D
+    bytes_scan = n * (2 * D + 4)
+    if scorer_used == "tc":
+        achieved = flops / (sc_ms / 1e3) / 1e12
+        roof = dict(bound="tensor", achieved=achieved, peak=tflops, unit="TFLOP/s", frac=achieved / tflops)
+    else:
+        achieved = bytes_scan / (sc_ms / 1e3) / 1e9
+        roof = dict(bound="hbm", achieved=achieved, peak=hbm, unit="GB/s", frac=achieved / hbm)
+    roof["kernel"] = f"score_{scorer_used}"
+    roof["peak_source"] = peak_src
+    roof["traffic"] = _ncu_traffic(scorer_used, args.config)
+    roof["algorithmic_per_launch"] = flops if scorer_used == "tc" else bytes_scan
+    # end-to-end through the public host-buffer API (H2D queries + D2H results incl. latents)
+    e2e = None
+    if not args.no_e2e:
+        qh = torch.from_numpy(q_np).pin_memory()
+        ho = dict(ids=torch.empty((b, 1), dtype=torch.int64).pin_memory(),
+                  scores=torch.empty((b, 1), dtype=torch.float32).pin_memory(),
+                  k=torch.empty(b, dtype=torch.int32).pin_memory(),
+                  status=torch.empty(b, dtype=torch.int32).pin_memory(),
+                  latents=torch.empty((b, L), dtype=torch.uint8).pin_memory())
+        for _ in range(3):
+            g.query_host(qh, out=ho)
+        e_ms = []
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            g.query_host(qh, out=ho)
+            e_ms.append(1e3 * (time.perf_counter() - t0))
+        et = sum(e_ms)
+        if world > 1:
+            t = torch.tensor([et], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            et = float(t.item())
+        e2e = dict(value=b * world * args.steps / (et / 1e3), unit=UNIT, h2d_bytes_per_step=b * D * 4,
+                   d2h_bytes_per_step=b * (8 + 4 + 4 + 4 + L),
+                   note="cache_query_batch_host: pinned host queries in, ids/scores/K/status/latents out; "
+                        "wall clock around the synchronous call")
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(emb, pres, q_np)
+    if rank == 0:
+        line = dict(metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=args.steps, warmup=args.warmup,
+                    ms_per_step=tot / args.steps, higher_is_better=True, scaling="weak", vs_baseline=None,
+                    dtype="bf16", data="synthetic (seeded clustered unit-norm 768-d embeddings, Zipf queries, "
+                                       "hash-stamped latents)",
+                    config=dict(workload=cfg["workload"], entries=n, batch=b, dim=D, latent_bytes=L, topk=1,
+                                scorer=scorer_used, l2="flushed between timed steps (512 MiB write)",
+                                parallelism=f"replicas x{world}" if world > 1 else "single GPU",
+                                hit_rate=float((k_np > 0).mean())),
+                    kernel_ms=dict(ingest=statistics.mean(prep_ms), score=sc_ms, finalize_gather=statistics.mean(fin_ms)),
+                    roofline=roof, cpu_baseline=cpu, e2e=e2e, gpu_launches=launches, clocks=clk.summary())
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _ncu_traffic(scorer, config):
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(f"{config}:{scorer}")
+    except Exception:
+        return None
+
+
+if __name__ == "__main__":
+    main()

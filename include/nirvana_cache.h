@@ -1,0 +1,199 @@
+/*
+ * nirvana_cache.h -- C ABI of the B200-native NIRVANA cache lookup (arXiv 2312.04429).
+ *
+ * The library implements the data-parallel hot path of the paper's approximate cache:
+ * Alg. 1 lines 4-8 for a BATCH of prompt embeddings, plus the LCBFU
+ * cache-maintenance calls.  Citations "P:n" are lines of the paper text
+ * (/root/reference/PAPER.md); "R<n>" are the readings listed in DESIGN.md.
+ *
+ * Conventions (all calls):
+ *   - Device memory: "device pointer" means a pointer returned by cudaMalloc on the cache's
+ *     device (or managed memory).  "host pointer" means ordinary host memory (pinned memory
+ *     is faster for the _host variants).  Every buffer is owned by the caller and must stay
+ *     valid until the call's stream has passed it; the library copies what it keeps
+ *     (embeddings, latents) into storage it owns.
+ *   - Streams: `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - Errors: every call returns a cache_status; argument and state errors are detected
+ *     synchronously and leave the cache unchanged.  Asynchronous CUDA errors surface as
+ *     CACHE_E_CUDA on a later call.  cache_last_error() gives a thread-local message.
+ *   - Concurrency: one writer.  cache_insert / cache_evict must not overlap queries on the
+ *     same handle (SPEC S:222's single-writer contract).
+ *   - Ids: every stored prompt embedding (entry) gets an id = insertion sequence number
+ *     (0, 1, 2, ...), used for deterministic tie-breaking (R3) and reported by queries.
+ *   - Items: an item is one stored intermediate state (entry, K).
+ */
+#ifndef NIRVANA_CACHE_H
+#define NIRVANA_CACHE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct cache_t cache_t; /* opaque handle, one per device (per rank) */
+
+typedef enum {
+    CACHE_OK = 0,
+    CACHE_E_INVALID_ARG = 1, /* bad pointer / size / config value                          */
+    CACHE_E_DIM = 2,         /* dim unsupported (must be a multiple of 64, <= 1024)         */
+    CACHE_E_FULL = 3,        /* insert does not fit entry or latent capacity  */
+    CACHE_E_EVICT_RANGE = 4, /* evict n > live items                          */
+    CACHE_E_BAD_ROWS = 5,    /* some input rows rejected; per-row codes were written       */
+    CACHE_E_CUDA = 6,        /* CUDA runtime/driver error                                  */
+    CACHE_E_NCCL = 7,        /* reserved (multi-rank plumbing lives above the ABI)         */
+    CACHE_E_OOM = 8,         /* device allocation failed                                   */
+    CACHE_E_STATE = 9,       /* call not valid in the handle's state (e.g. id space spent) */
+    CACHE_E_UNSUPPORTED = 10 /* requested variant not built for this configuration         */
+} cache_status;
+
+/* per-row status codes (row_status outputs) */
+enum {
+    CACHE_ROW_OK = 0,
+    CACHE_ROW_NONFINITE = 1, /* a component is NaN/Inf                 */
+    CACHE_ROW_ZERO_NORM = 2, /* zero vector: "degenerate embedding"      */
+    CACHE_ROW_NO_ITEMS = 3   /* insert: present mask selects no K, nothing to store */
+};
+
+/* input element types of embeddings / queries */
+enum { CACHE_DTYPE_F32 = 0, CACHE_DTYPE_BF16 = 1 };
+
+/* scoring kernel selection (cache_set_scorer) */
+enum {
+    CACHE_SCORER_AUTO = 0,   /* library picks by batch size                                */
+    CACHE_SCORER_TC = 1,     /* tcgen05/TMEM tensor-core scan with fused top-k epilogue    */
+    CACHE_SCORER_STREAM = 2  /* CUDA-core HBM-streaming scan (small batches)               */
+};
+
+#define CACHE_MAX_K 8      /* max |K| (the paper uses 5: {5,10,15,20,25})           */
+#define CACHE_MAX_TOPK 16  /* max m nearest neighbours returned per query           */
+#define CACHE_NO_ID UINT64_MAX
+
+typedef struct {
+    int32_t dim;              /* embedding dimension; 768 for CLIP; multiple of 64  */
+    int64_t entry_capacity;   /* max live entries (prompt embeddings)                      */
+    int64_t latent_capacity;  /* max live items (latent-pool slots); decoupled from entries
+                                 as in "1.5 million intermediate-states ... 300k unique
+                                 prompt embedding"                                 */
+    int64_t latent_bytes;     /* bytes per stored intermediate state, opaque; multiple of 16
+                                 (144 KB in the paper P:511; 4x64x64 fp16 = 32768 here)    */
+    int32_t num_k;            /* |K| <= CACHE_MAX_K                                        */
+    int32_t k_values[CACHE_MAX_K];   /* K values, strictly increasing ({5,..,25})   */
+    double thresholds[CACHE_MAX_K];  /* Fig. 11: K = k_values[j] for the largest
+                                        j with s > thresholds[j] (strict), else 0; must be
+                                        non-decreasing ({.65,.75,.85,.90,.95})              */
+    int32_t k_bias;           /* quality-vs-savings knob (R20): on a hit the
+                                 bucket moves up by k_bias (clamped); 0 = Fig. 11 verbatim */
+    int32_t max_topk;         /* largest topk a query may request (<= CACHE_MAX_TOPK)      */
+} cache_config;
+
+typedef struct {
+    int64_t live_entries;     /* prompt embeddings present in the index                   */
+    int64_t live_items;       /* stored (entry, K) intermediate states                    */
+    int64_t holes;            /* missing K among live entries                     */
+    int64_t entry_hwm;        /* high-water mark of entry slots (the scan length)          */
+    uint64_t next_id;         /* id the next inserted entry receives                       */
+    int64_t queries;          /* queries answered so far                                   */
+} cache_stats_t;
+
+/* Fill *cfg with the paper's defaults: dim 768, K = {5,10,15,20,25}, Fig. 11
+ * thresholds, k_bias 0, max_topk 16, latent_bytes 32768. Capacities are set to 0
+ * and must be filled in by the caller. */
+void cache_default_config(cache_config *cfg);
+
+/* Create a cache on CUDA device `device`, allocating all storage up front (HBM footprint
+ * ~ entry_capacity*(2*dim + 4*(2+2*num_k)) + latent_capacity*latent_bytes bytes).
+ * Host-synchronous.  *out receives the handle. */
+cache_status cache_create(const cache_config *cfg, int device, cache_t **out);
+
+/* Free all storage.  Synchronises the device.  NULL is a no-op. */
+cache_status cache_destroy(cache_t *c);
+
+/* LCBFU insertion: store n prompt embeddings and their intermediate states.
+ *   emb        device pointer, n x dim row-major, element type emb_dtype (CACHE_DTYPE_*)
+ *   latents    device pointer, n x num_k x latent_bytes (state of row r at K_j at
+ *              ((r*num_k)+j)*latent_bytes), or NULL to store no payload bytes
+ *   present    device or host pointer, n bitmasks (bit j set = K_j is stored), or NULL = all
+ *   out_ids    host pointer, n ids (CACHE_NO_ID for a rejected row); may be NULL
+ *   row_status host pointer, n CACHE_ROW_* codes; may be NULL
+ * Each accepted row is normalised in fp64 (fixed tree-order sum of squares, correctly
+ * rounded sqrt and division) and rounded to bf16 (RNE) -- reading R2.  Rows with
+ * non-finite components or zero norm are rejected (CACHE_E_BAD_ROWS after the valid rows
+ * are stored).  If the accepted rows exceed the free entry or latent capacity the call
+ * returns CACHE_E_FULL and stores nothing (no automatic eviction, R14).
+ * Synchronises `stream` (slot allocation needs the row statuses). */
+cache_status cache_insert(cache_t *c, int64_t n, const void *emb, int32_t emb_dtype,
+                          const void *latents, const uint8_t *present, uint64_t *out_ids,
+                          int32_t *row_status, void *stream);
+
+/* Batched cache lookup: Alg. 1 lines 4-8 for b queries at once.
+ *   queries        device pointer, b x dim, element type q_dtype
+ *   topk           1..max_topk nearest cached entries to report
+ *   out_ids        device pointer, b x topk u64: entry ids by (score desc, id asc);
+ *                  CACHE_NO_ID where fewer than topk live entries exist
+ *   out_scores     device pointer, b x topk f32 cosine similarities clamped to [-1,1]
+ *                  (-inf where no entry); ranking uses the unclamped value (R4)
+ *   out_k          device pointer, b i32: K used for query i after the Fig. 11 map
+ *                   and the hole rule; 0 = generate from scratch
+ *   latent_out     device pointer, b x latent_bytes: row i receives the stored state
+ *                  (entry top-1, K = out_k[i]) iff out_k[i] > 0; other rows are
+ *                  not written.  May be NULL (no gather).
+ *   out_latent_ptr device pointer, b void*: &latent_out[i*latent_bytes] or NULL; may be NULL
+ *   row_status     device pointer, b i32 CACHE_ROW_*; may be NULL
+ * For every query with out_k[i] > 0 the LCBFU access count f[(entry, K)] is incremented by
+ * one after the batch (R8/R9).  Asynchronous on `stream`; returns after launch.
+ * Cosine similarity is computed exactly over every live entry (R1) on the stored bf16
+ * values with fp32 accumulation: s = fl(fl(<q~,x~> * inv_norm(x~)) * inv_norm(q~)). */
+cache_status cache_query_batch(cache_t *c, int64_t b, const void *queries, int32_t q_dtype,
+                               int32_t topk, uint64_t *out_ids, float *out_scores,
+                               int32_t *out_k, void *latent_out, void **out_latent_ptr,
+                               int32_t *row_status, void *stream);
+
+/* Same lookup with HOST buffers (the end-to-end call a serving process makes): queries,
+ * out_ids, out_scores, out_k, latent_out and row_status are host pointers (pinned memory
+ * recommended); the library stages them through its own device buffers, copies the results
+ * back and synchronises `stream` before returning.  latent_out / row_status may be NULL. */
+cache_status cache_query_batch_host(cache_t *c, int64_t b, const void *queries, int32_t q_dtype,
+                                    int32_t topk, uint64_t *out_ids, float *out_scores,
+                                    int32_t *out_k, void *latent_out, int32_t *row_status,
+                                    void *stream);
+
+/* LCBFU eviction: remove the n stored items with the smallest LCBFU score
+ * f_i x K_i, ties by (entry id, K) ascending (R11); then every entry left with no
+ * stored K is dirty and is removed from the index in the same call (R13).
+ *   out_evicted    host pointer, n u64 (id << 3 | j) in eviction order; may be NULL
+ *   out_dirty_ids  host pointer, capacity n, ids of removed entries ascending; may be NULL
+ *   out_n_dirty    host pointer, number of entries removed; may be NULL
+ * n > live items -> CACHE_E_EVICT_RANGE.  Synchronises `stream`. */
+cache_status cache_evict(cache_t *c, int64_t n, uint64_t *out_evicted, uint64_t *out_dirty_ids,
+                         int64_t *out_n_dirty, void *stream);
+
+/* Counters: read the LCBFU access counts and presence mask of entry `id` (host outputs,
+ * f has num_k slots).  Host-synchronous; intended for tests and maintenance tools. */
+cache_status cache_get_meta(cache_t *c, uint64_t id, uint64_t *f, uint32_t *present_mask);
+
+/* Copy the stored bf16 row of entry `id` to host memory (dim uint16 bit patterns). */
+cache_status cache_get_row(cache_t *c, uint64_t id, uint16_t *out_bf16);
+
+/* Host-synchronous statistics. */
+cache_status cache_stats(cache_t *c, cache_stats_t *out);
+
+/* Force a scoring kernel (CACHE_SCORER_*); AUTO by default. */
+cache_status cache_set_scorer(cache_t *c, int32_t scorer);
+
+/* Profiling hook: `events` points to 4 cudaEvent_t handles (host array, or NULL to disable).
+ * When set, every cache_query_batch records events[0] before query ingest, events[1] before
+ * the scoring kernel, events[2] before the finalize/gather kernel and events[3] after it, on
+ * the call's stream, so a caller can time each kernel with cudaEventElapsedTime. */
+cache_status cache_set_profile_events(cache_t *c, void *const *events);
+
+/* Number of kernels the library launched on this handle so far (for launch accounting). */
+int64_t cache_kernel_launches(const cache_t *c);
+
+/* Thread-local description of the last error (never NULL). */
+const char *cache_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NIRVANA_CACHE_H */

@@ -94,23 +94,39 @@ double oracle_bf16_round(double v)
     return ldexp(r, e - 8);
 }
 
-/* Normalise one row: nu = sqrt(sum_i x_i^2) (fp64, index order); y_i = bf16(x_i / nu).
+/* Sum of squares in one fixed binary-tree order (reading R2, so that the stored rows are
+ * reproducible bit for bit by a parallel implementation): the dim squares are zero-padded to
+ * the next power of two P, then for stride s = P/2, P/4, ..., 1:  t[i] = t[i] + t[i+s], i < s. */
+static double tree_sum_sq(const double *x, int dim)
+{
+    int P = 1, s, i;
+    double *t, r;
+    while (P < dim) P <<= 1;
+    t = (double *)calloc((size_t)P, sizeof(double));
+    if (!t) return NAN;
+    for (i = 0; i < dim; i++) t[i] = x[i] * x[i];
+    for (s = P / 2; s >= 1; s /= 2)
+        for (i = 0; i < s; i++) t[i] = t[i] + t[i + s];
+    r = t[0];
+    free(t);
+    return r;
+}
+
+/* Normalise one row: nu = sqrt(sum_i x_i^2) (fp64, tree order above); y_i = bf16(x_i / nu).
  * Returns the row status (non-finite input or zero norm are rejected). */
 static int normalise_row(const double *x, int dim, double *y)
 {
-    double s = 0.0, nu;
+    double s, nu;
     int i;
     for (i = 0; i < dim; i++)
         if (!isfinite(x[i])) return ORC_ROW_NONFINITE;
-    for (i = 0; i < dim; i++) s = s + x[i] * x[i];
+    s = tree_sum_sq(x, dim);
     if (s == 0.0) return ORC_ROW_ZERO_NORM;
     if (!isfinite(s)) return ORC_ROW_NONFINITE;
     nu = sqrt(s);
     for (i = 0; i < dim; i++) y[i] = oracle_bf16_round(x[i] / nu);
     /* a row can round to all zeros only if every x_i/nu < 2^-134; treat as zero norm */
-    s = 0.0;
-    for (i = 0; i < dim; i++) s = s + y[i] * y[i];
-    if (s == 0.0) return ORC_ROW_ZERO_NORM;
+    if (tree_sum_sq(y, dim) == 0.0) return ORC_ROW_ZERO_NORM;
     return ORC_ROW_OK;
 }
 

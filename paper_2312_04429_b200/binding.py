@@ -1,0 +1,256 @@
+"""Thin ctypes binding of ``libnirvana_cache.so`` (include/nirvana_cache.h).
+
+Argument marshalling only: every step of the lookup runs in the library's CUDA kernels.
+PyTorch provides device memory and streams.  There is no CPU fallback: if the built library
+is missing this module raises on import.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libnirvana_cache.so")
+
+OK, E_INVALID_ARG, E_DIM, E_FULL, E_EVICT_RANGE, E_BAD_ROWS, E_CUDA, E_NCCL, E_OOM, E_STATE, E_UNSUPPORTED = range(11)
+ROW_OK, ROW_NONFINITE, ROW_ZERO_NORM, ROW_NO_ITEMS = range(4)
+DTYPE_F32, DTYPE_BF16 = 0, 1
+SCORER_AUTO, SCORER_TC, SCORER_STREAM = 0, 1, 2
+MAX_K, MAX_TOPK = 8, 16
+NO_ID = 0xFFFFFFFFFFFFFFFF
+
+_STATUS = {OK: "OK", E_INVALID_ARG: "INVALID_ARG", E_DIM: "DIM", E_FULL: "FULL", E_EVICT_RANGE: "EVICT_RANGE",
+           E_BAD_ROWS: "BAD_ROWS", E_CUDA: "CUDA", E_NCCL: "NCCL", E_OOM: "OOM", E_STATE: "STATE",
+           E_UNSUPPORTED: "UNSUPPORTED"}
+
+
+class CacheError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{_STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class CacheConfig(ctypes.Structure):
+    _fields_ = [("dim", ctypes.c_int32), ("entry_capacity", ctypes.c_int64),
+                ("latent_capacity", ctypes.c_int64), ("latent_bytes", ctypes.c_int64),
+                ("num_k", ctypes.c_int32), ("k_values", ctypes.c_int32 * MAX_K),
+                ("thresholds", ctypes.c_double * MAX_K), ("k_bias", ctypes.c_int32),
+                ("max_topk", ctypes.c_int32)]
+
+
+class CacheStats(ctypes.Structure):
+    _fields_ = [("live_entries", ctypes.c_int64), ("live_items", ctypes.c_int64), ("holes", ctypes.c_int64),
+                ("entry_hwm", ctypes.c_int64), ("next_id", ctypes.c_uint64), ("queries", ctypes.c_int64)]
+
+
+EXPORTS = ("cache_default_config", "cache_create", "cache_destroy", "cache_insert", "cache_query_batch",
+           "cache_query_batch_host", "cache_evict", "cache_get_meta", "cache_get_row", "cache_stats",
+           "cache_set_scorer", "cache_set_profile_events", "cache_kernel_launches", "cache_last_error")
+
+
+def load_library(path: str = LIB_PATH):
+    if not os.path.exists(path):
+        raise ImportError(f"CUDA library {path} is missing: run __graft_entry__.build() "
+                          "(there is no CPU fallback)")
+    L = ctypes.CDLL(path)
+    P, I64, I32, U64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64
+    L.cache_default_config.argtypes = [ctypes.POINTER(CacheConfig)]
+    L.cache_create.argtypes = [ctypes.POINTER(CacheConfig), ctypes.c_int, ctypes.POINTER(P)]
+    L.cache_destroy.argtypes = [P]
+    L.cache_insert.argtypes = [P, I64, P, I32, P, P, P, P, P]
+    L.cache_query_batch.argtypes = [P, I64, P, I32, I32, P, P, P, P, P, P, P]
+    L.cache_query_batch_host.argtypes = [P, I64, P, I32, I32, P, P, P, P, P, P]
+    L.cache_evict.argtypes = [P, I64, P, P, P, P]
+    L.cache_get_meta.argtypes = [P, U64, P, P]
+    L.cache_get_row.argtypes = [P, U64, P]
+    L.cache_stats.argtypes = [P, ctypes.POINTER(CacheStats)]
+    L.cache_set_scorer.argtypes = [P, I32]
+    L.cache_set_profile_events.argtypes = [P, P]
+    L.cache_kernel_launches.argtypes = [P]
+    L.cache_kernel_launches.restype = I64
+    L.cache_last_error.restype = ctypes.c_char_p
+    for fn in ("cache_create", "cache_destroy", "cache_insert", "cache_query_batch", "cache_query_batch_host",
+               "cache_evict", "cache_get_meta", "cache_get_row", "cache_stats", "cache_set_scorer",
+               "cache_set_profile_events"):
+        getattr(L, fn).restype = ctypes.c_int
+    return L
+
+
+_lib = load_library()
+
+
+def lib():
+    return _lib
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if isinstance(t, torch.Tensor):
+        return ctypes.c_void_p(t.data_ptr())
+    return t.ctypes.data_as(ctypes.c_void_p)
+
+
+def _stream(stream):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _check(rc, allow=()):
+    if rc != OK and rc not in allow:
+        raise CacheError(rc, _lib.cache_last_error().decode())
+    return rc
+
+
+def default_config(**kw) -> CacheConfig:
+    cfg = CacheConfig()
+    _lib.cache_default_config(ctypes.byref(cfg))
+    for k, v in kw.items():
+        if k in ("k_values", "thresholds"):
+            arr = getattr(cfg, k)
+            for i, x in enumerate(v):
+                arr[i] = x
+            if k == "k_values":
+                cfg.num_k = len(v)
+        else:
+            setattr(cfg, k, v)
+    return cfg
+
+
+class NirvanaCache:
+    """One cache handle on one CUDA device (see include/nirvana_cache.h)."""
+
+    def __init__(self, entry_capacity: int, latent_capacity: int | None = None, dim: int = 768,
+                 latent_bytes: int = 32768, k_values=(5, 10, 15, 20, 25),
+                 thresholds=(0.65, 0.75, 0.85, 0.90, 0.95), k_bias: int = 0, max_topk: int = MAX_TOPK,
+                 device: int | None = None):
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = device
+        if latent_capacity is None:
+            latent_capacity = entry_capacity * len(k_values)
+        self.cfg = default_config(dim=dim, entry_capacity=entry_capacity, latent_capacity=latent_capacity,
+                                  latent_bytes=latent_bytes, k_values=tuple(k_values),
+                                  thresholds=tuple(thresholds), k_bias=k_bias, max_topk=max_topk)
+        self.dim, self.latent_bytes, self.num_k = dim, latent_bytes, len(k_values)
+        self.k_values = tuple(k_values)
+        h = ctypes.c_void_p()
+        _check(_lib.cache_create(ctypes.byref(self.cfg), device, ctypes.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.cache_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------------------------
+    def insert(self, emb: torch.Tensor, latents: torch.Tensor | None = None, present=None, stream=None,
+               raise_on_bad_rows: bool = False):
+        """emb: [n][dim] f32/bf16 cuda; latents: [n][num_k][latent_bytes] u8 cuda or None;
+        present: [n] u8 masks (numpy or tensor) or None.  Returns (ids u64[n], row_status i32[n])."""
+        assert emb.is_cuda and emb.is_contiguous() and emb.dim() == 2 and emb.shape[1] == self.dim
+        n = emb.shape[0]
+        dt = DTYPE_BF16 if emb.dtype == torch.bfloat16 else DTYPE_F32
+        assert emb.dtype in (torch.float32, torch.bfloat16)
+        if latents is not None:
+            assert latents.is_cuda and latents.is_contiguous() and latents.dtype == torch.uint8
+            assert latents.numel() == n * self.num_k * self.latent_bytes
+        pr = None
+        if present is not None:
+            pr = present if isinstance(present, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(present, np.uint8))
+            pr = pr.contiguous()
+        ids = np.empty(n, dtype=np.uint64)
+        st = np.empty(n, dtype=np.int32)
+        rc = _lib.cache_insert(self._h, n, _ptr(emb), dt, _ptr(latents), _ptr(pr), _ptr(ids), _ptr(st),
+                               _stream(stream))
+        _check(rc, allow=() if raise_on_bad_rows else (E_BAD_ROWS,))
+        return ids, st
+
+    def alloc_outputs(self, b: int, topk: int = 1, latents: bool = True):
+        dev = torch.device("cuda", self.device)
+        return dict(ids=torch.empty((b, topk), dtype=torch.int64, device=dev),
+                    scores=torch.empty((b, topk), dtype=torch.float32, device=dev),
+                    k=torch.empty(b, dtype=torch.int32, device=dev),
+                    latents=torch.empty((b, self.latent_bytes), dtype=torch.uint8, device=dev) if latents else None,
+                    ptrs=torch.empty(b, dtype=torch.int64, device=dev),
+                    status=torch.empty(b, dtype=torch.int32, device=dev))
+
+    def query_into(self, q: torch.Tensor, out: dict, topk: int = 1, stream=None):
+        """Asynchronous lookup into preallocated outputs (see alloc_outputs)."""
+        b = q.shape[0]
+        dt = DTYPE_BF16 if q.dtype == torch.bfloat16 else DTYPE_F32
+        rc = _lib.cache_query_batch(self._h, b, _ptr(q), dt, topk, _ptr(out["ids"]), _ptr(out["scores"]),
+                                    _ptr(out["k"]), _ptr(out["latents"]), _ptr(out["ptrs"]),
+                                    _ptr(out["status"]), _stream(stream))
+        _check(rc)
+        return out
+
+    def query(self, q: torch.Tensor, topk: int = 1, latents: bool = True, stream=None):
+        assert q.is_cuda and q.is_contiguous() and q.dim() == 2 and q.shape[1] == self.dim
+        out = self.alloc_outputs(q.shape[0], topk, latents)
+        return self.query_into(q, out, topk, stream)
+
+    def query_host(self, q: np.ndarray, topk: int = 1, latents: bool = True, out: dict | None = None, stream=None):
+        """End-to-end lookup with host buffers (pinned numpy-compatible tensors recommended)."""
+        b = q.shape[0]
+        if out is None:
+            out = dict(ids=np.empty((b, topk), np.uint64), scores=np.empty((b, topk), np.float32),
+                       k=np.empty(b, np.int32), status=np.empty(b, np.int32),
+                       latents=np.empty((b, self.latent_bytes), np.uint8) if latents else None)
+        dt = DTYPE_BF16 if (isinstance(q, torch.Tensor) and q.dtype == torch.bfloat16) else DTYPE_F32
+        rc = _lib.cache_query_batch_host(self._h, b, _ptr(q), dt, topk, _ptr(out["ids"]), _ptr(out["scores"]),
+                                         _ptr(out["k"]), _ptr(out["latents"]), _ptr(out["status"]), _stream(stream))
+        _check(rc)
+        return out
+
+    def evict(self, n: int, stream=None):
+        ev = np.empty(max(n, 1), dtype=np.uint64)
+        dirty = np.empty(max(n, 1), dtype=np.uint64)
+        nd = np.zeros(1, dtype=np.int64)
+        _check(_lib.cache_evict(self._h, n, _ptr(ev), _ptr(dirty), _ptr(nd), _stream(stream)))
+        return ev[:n].copy(), dirty[: int(nd[0])].copy()
+
+    def meta(self, id_: int):
+        f = np.empty(self.num_k, dtype=np.uint64)
+        m = np.zeros(1, dtype=np.uint32)
+        _check(_lib.cache_get_meta(self._h, int(id_), _ptr(f), _ptr(m)))
+        return f, int(m[0])
+
+    def row_bf16(self, id_: int) -> np.ndarray:
+        out = np.empty(self.dim, dtype=np.uint16)
+        _check(_lib.cache_get_row(self._h, int(id_), _ptr(out)))
+        return out
+
+    def stats(self) -> dict:
+        s = CacheStats()
+        _check(_lib.cache_stats(self._h, ctypes.byref(s)))
+        return {k: getattr(s, k) for k, _ in CacheStats._fields_}
+
+    def set_scorer(self, scorer: int):
+        _check(_lib.cache_set_scorer(self._h, scorer))
+
+    def set_profile_events(self, events):
+        """events: 4 torch.cuda.Event(enable_timing=True) (recorded around ingest / score /
+        finalize of every query), or None to disable."""
+        if events is None:
+            _check(_lib.cache_set_profile_events(self._h, None))
+            self._prof = None
+            return
+        for e in events:
+            e.record()          # materialise the underlying cudaEvent_t
+        arr = (ctypes.c_void_p * 4)(*[e.cuda_event for e in events])
+        self._prof = (events, arr)
+        _check(_lib.cache_set_profile_events(self._h, arr))
+
+    @property
+    def kernel_launches(self) -> int:
+        return _lib.cache_kernel_launches(self._h)

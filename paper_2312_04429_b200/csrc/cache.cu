@@ -1,0 +1,565 @@
+// cache.cu -- host engine behind the C ABI (include/nirvana_cache.h): storage layout in HBM,
+// slot allocation, batch dispatch and error plumbing.  Every step of the lookup runs in the
+// kernels of kernels.cu / score_tc.cu; this file only allocates, plans and launches.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "kernels.h"
+
+using namespace nv;
+
+namespace {
+thread_local std::string g_err = "no error";
+
+cache_status fail(cache_status st, const std::string& msg) {
+    g_err = msg;
+    return st;
+}
+
+#define CK(call)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail(e_ == cudaErrorMemoryAllocation ? CACHE_E_OOM : CACHE_E_CUDA,         \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));                  \
+    } while (0)
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    cudaError_t ensure(size_t need) {
+        if (need <= n) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        cudaError_t e = cudaMalloc(&p, std::max<size_t>(need, 1) * sizeof(T));
+        if (e == cudaSuccess) n = need;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 2-D bf16 row-major [rows][dim] tensor map, box = 64 elements (128 B, swizzle-128B) x box_rows.
+bool encode_rows(CUtensorMap* tm, const void* base, int64_t rows, int dim, int box_rows) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t gdim[2] = {(cuuint64_t)dim, (cuuint64_t)rows};
+    cuuint64_t gstride[1] = {(cuuint64_t)dim * 2};
+    cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+    cuuint32_t estride[2] = {1, 1};
+    CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), gdim, gstride, box,
+                     estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+}  // namespace
+
+struct cache_t {
+    cache_config cfg;
+    int device = 0;
+    int dim = 0, num_k = 0, sm_count = 148;
+    int64_t cap = 0, cap_pad = 0, lcap = 0, L = 0;
+    KMap km{};
+    // HBM storage (SoA).  emb rows are 2*dim bytes (1,536 B at d=768), 128-B aligned.
+    __nv_bfloat16* emb = nullptr;   // [cap_pad][dim]  stored x~ = bf16(x/||x||)
+    float* inv_e = nullptr;         // [cap_pad]       f32(1/||x~||); NaN = empty / dirty slot
+    uint32_t* ids = nullptr;        // [cap_pad]       entry id (insertion sequence)
+    uint32_t* present = nullptr;    // [cap_pad]       bit j = K_j stored
+    int32_t* lslot = nullptr;       // [cap_pad][num_k] latent-pool slot (-1 = hole)
+    uint32_t* fcnt = nullptr;       // [cap_pad][num_k] LCBFU access counts f
+    uint8_t* pool = nullptr;        // [lcap][L]       intermediate states
+    CUtensorMap tm_e;               // TMA map of emb (box 64 x 256)
+    bool tm_e_ok = false;
+    // host mirrors / allocators
+    std::vector<uint32_t> h_present, h_ids;
+    std::vector<int32_t> h_lslot;
+    std::vector<int64_t> free_e, free_l;   // sorted descending: back() = lowest free slot
+    std::unordered_map<uint64_t, int64_t> id2slot;
+    int64_t hwm = 0, live_entries = 0, live_items = 0, queries = 0;
+    uint64_t next_id = 0;
+    int scorer = CACHE_SCORER_AUTO;
+    int64_t launches = 0;
+    cudaEvent_t prof[4] = {nullptr, nullptr, nullptr, nullptr};
+    bool prof_on = false;
+    // workspaces
+    DevBuf<__nv_bfloat16> qbuf, ystage;
+    DevBuf<float> invq, invstage;
+    DevBuf<int32_t> qstat, istat;
+    DevBuf<Rec> recs;
+    DevBuf<InsertPlan> iplan;
+    DevBuf<CopyPlan> cplan;
+    DevBuf<uint8_t> hq_in, hq_lat;
+    DevBuf<uint64_t> hq_ids;
+    DevBuf<float> hq_sc;
+    DevBuf<int32_t> hq_k, hq_st;
+    DevBuf<EvictState> est;
+    DevBuf<unsigned int> ehist;
+    DevBuf<unsigned long long> ekey, ecnt;
+    DevBuf<int32_t> elslot;
+    DevBuf<int64_t> edirty;
+};
+
+extern "C" {
+
+const char* cache_last_error(void) { return g_err.c_str(); }
+
+void cache_default_config(cache_config* cfg) {
+    if (!cfg) return;
+    std::memset(cfg, 0, sizeof(*cfg));
+    cfg->dim = 768;                                    // CLIP text embedding
+    cfg->latent_bytes = 4 * 64 * 64 * 2;               // 4x64x64 fp16 latent (BASELINE configs)
+    cfg->num_k = 5;                                    // K in {5,10,15,20,25}
+    const int kv[5] = {5, 10, 15, 20, 25};
+    const double th[5] = {0.65, 0.75, 0.85, 0.90, 0.95};   // Fig. 11
+    for (int j = 0; j < 5; ++j) { cfg->k_values[j] = kv[j]; cfg->thresholds[j] = th[j]; }
+    cfg->k_bias = 0;
+    cfg->max_topk = CACHE_MAX_TOPK;
+}
+
+cache_status cache_create(const cache_config* cfg, int device, cache_t** out) {
+    if (!cfg || !out) return fail(CACHE_E_INVALID_ARG, "cache_create: null argument");
+    *out = nullptr;
+    if (cfg->dim <= 0 || cfg->dim % 64 != 0 || cfg->dim > kMaxDim)
+        return fail(CACHE_E_DIM, "cache_create: dim must be a positive multiple of 64, <= 1024");
+    if (cfg->entry_capacity <= 0 || cfg->entry_capacity > 0xFFFFFFFFll || cfg->latent_capacity < 0 ||
+        cfg->latent_bytes < 0 || cfg->latent_bytes % 16 != 0)
+        return fail(CACHE_E_INVALID_ARG, "cache_create: bad capacity / latent_bytes (multiple of 16)");
+    if (cfg->num_k <= 0 || cfg->num_k > CACHE_MAX_K || cfg->k_bias < 0 || cfg->max_topk <= 0 ||
+        cfg->max_topk > CACHE_MAX_TOPK)
+        return fail(CACHE_E_INVALID_ARG, "cache_create: bad num_k / k_bias / max_topk");
+    if (cfg->k_values[0] <= 0) return fail(CACHE_E_INVALID_ARG, "cache_create: K values must be > 0");
+    for (int j = 1; j < cfg->num_k; ++j)
+        if (cfg->k_values[j] <= cfg->k_values[j - 1] || !(cfg->thresholds[j] >= cfg->thresholds[j - 1]))
+            return fail(CACHE_E_INVALID_ARG,
+                        "cache_create: K values must increase and thresholds must not decrease (R6)");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(CACHE_E_INVALID_ARG, "cache_create: bad device");
+    DeviceGuard g(device);
+    cache_t* c = new cache_t();
+    c->cfg = *cfg;
+    c->device = device;
+    c->dim = cfg->dim;
+    c->num_k = cfg->num_k;
+    c->cap = cfg->entry_capacity;
+    c->cap_pad = (cfg->entry_capacity + kTileN - 1) / kTileN * kTileN;
+    c->lcap = cfg->latent_capacity;
+    c->L = cfg->latent_bytes;
+    for (int j = 0; j < c->num_k; ++j) { c->km.thr[j] = cfg->thresholds[j]; c->km.kv[j] = cfg->k_values[j]; }
+    c->km.num_k = c->num_k;
+    c->km.k_bias = cfg->k_bias;
+    cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+    auto bail = [&](cudaError_t e, const char* what) {
+        cache_destroy(c);
+        return fail(e == cudaErrorMemoryAllocation ? CACHE_E_OOM : CACHE_E_CUDA,
+                    std::string("cache_create: ") + what + ": " + cudaGetErrorString(e));
+    };
+    cudaError_t e;
+    if ((e = cudaMalloc(&c->emb, (size_t)c->cap_pad * c->dim * 2)) != cudaSuccess) return bail(e, "emb");
+    if ((e = cudaMalloc(&c->inv_e, (size_t)c->cap_pad * 4)) != cudaSuccess) return bail(e, "inv_e");
+    if ((e = cudaMalloc(&c->ids, (size_t)c->cap_pad * 4)) != cudaSuccess) return bail(e, "ids");
+    if ((e = cudaMalloc(&c->present, (size_t)c->cap_pad * 4)) != cudaSuccess) return bail(e, "present");
+    if ((e = cudaMalloc(&c->lslot, (size_t)c->cap_pad * c->num_k * 4)) != cudaSuccess) return bail(e, "lslot");
+    if ((e = cudaMalloc(&c->fcnt, (size_t)c->cap_pad * c->num_k * 4)) != cudaSuccess) return bail(e, "f");
+    if (c->lcap > 0 && c->L > 0 && (e = cudaMalloc(&c->pool, (size_t)c->lcap * c->L)) != cudaSuccess)
+        return bail(e, "latent pool");
+    cudaMemset(c->emb, 0, (size_t)c->cap_pad * c->dim * 2);
+    cudaMemset(c->inv_e, 0xFF, (size_t)c->cap_pad * 4);   // 0xFFFFFFFF = NaN: empty slot
+    cudaMemset(c->ids, 0, (size_t)c->cap_pad * 4);
+    cudaMemset(c->present, 0, (size_t)c->cap_pad * 4);
+    cudaMemset(c->lslot, 0xFF, (size_t)c->cap_pad * c->num_k * 4);
+    cudaMemset(c->fcnt, 0, (size_t)c->cap_pad * c->num_k * 4);
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return bail(e, "init");
+    c->tm_e_ok = encode_rows(&c->tm_e, c->emb, c->cap_pad, c->dim, 256);
+    c->h_present.assign(c->cap_pad, 0);
+    c->h_ids.assign(c->cap_pad, 0);
+    c->h_lslot.assign((size_t)c->cap_pad * c->num_k, -1);
+    c->free_e.resize(c->cap);
+    for (int64_t i = 0; i < c->cap; ++i) c->free_e[i] = c->cap - 1 - i;
+    c->free_l.resize(c->lcap);
+    for (int64_t i = 0; i < c->lcap; ++i) c->free_l[i] = c->lcap - 1 - i;
+    *out = c;
+    return CACHE_OK;
+}
+
+cache_status cache_destroy(cache_t* c) {
+    if (!c) return CACHE_OK;
+    DeviceGuard g(c->device);
+    cudaDeviceSynchronize();
+    cudaFree(c->emb); cudaFree(c->inv_e); cudaFree(c->ids); cudaFree(c->present);
+    cudaFree(c->lslot); cudaFree(c->fcnt); cudaFree(c->pool);
+    c->qbuf.release(); c->ystage.release(); c->invq.release(); c->invstage.release();
+    c->qstat.release(); c->istat.release(); c->recs.release(); c->iplan.release(); c->cplan.release();
+    c->hq_in.release(); c->hq_lat.release(); c->hq_ids.release(); c->hq_sc.release(); c->hq_k.release();
+    c->hq_st.release(); c->est.release(); c->ehist.release(); c->ekey.release(); c->ecnt.release();
+    c->elslot.release(); c->edirty.release();
+    delete c;
+    return CACHE_OK;
+}
+
+cache_status cache_insert(cache_t* c, int64_t n, const void* emb, int32_t emb_dtype, const void* latents,
+                          const uint8_t* present, uint64_t* out_ids, int32_t* row_status, void* stream) {
+    if (!c) return fail(CACHE_E_INVALID_ARG, "cache_insert: null cache");
+    if (n < 0 || (n > 0 && !emb) || (emb_dtype != CACHE_DTYPE_F32 && emb_dtype != CACHE_DTYPE_BF16))
+        return fail(CACHE_E_INVALID_ARG, "cache_insert: bad n / emb / dtype");
+    if (n == 0) return CACHE_OK;
+    if (latents && !c->pool) return fail(CACHE_E_INVALID_ARG, "cache_insert: latents given but no pool");
+    DeviceGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const uint32_t full = (1u << c->num_k) - 1u;
+    std::vector<uint8_t> masks(n, (uint8_t)full);
+    if (present) CK(cudaMemcpy(masks.data(), present, n, cudaMemcpyDefault));
+    const size_t esz = emb_dtype == CACHE_DTYPE_BF16 ? 2 : 4;
+    const int64_t chunk = std::min<int64_t>(n, 65536);
+    CK(c->ystage.ensure((size_t)chunk * c->dim));
+    CK(c->invstage.ensure(chunk));
+    CK(c->istat.ensure(chunk));
+    std::vector<int32_t> st(n);
+    // Statuses first (rejected rows get no id / slot), then the all-or-nothing capacity check.
+    int64_t n_valid = 0, n_items = 0;
+    for (int64_t off = 0; off < n; off += chunk) {
+        const int64_t m = std::min(chunk, n - off);
+        launch_normalise((const char*)emb + off * c->dim * esz, emb_dtype, m, c->dim, c->ystage.p,
+                         c->invstage.p, c->istat.p, s);
+        c->launches++;
+        CK(cudaMemcpyAsync(st.data() + off, c->istat.p, m * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    for (int64_t r = 0; r < n; ++r) {
+        if (st[r] == CACHE_ROW_OK && (masks[r] & full) == 0) st[r] = CACHE_ROW_NO_ITEMS;
+        if (st[r] == CACHE_ROW_OK) { n_valid++; n_items += __builtin_popcount(masks[r] & full); }
+    }
+    if (n_valid > (int64_t)c->free_e.size() || n_items > (int64_t)c->free_l.size())
+        return fail(CACHE_E_FULL, "cache_insert: insufficient entry or latent capacity (evict first)");
+    if ((uint64_t)c->next_id + n_valid > 0xFFFFFFFFull)
+        return fail(CACHE_E_STATE, "cache_insert: 32-bit id space exhausted");
+    std::vector<InsertPlan> plan;
+    std::vector<CopyPlan> cp;
+    for (int64_t off = 0; off < n; off += chunk) {
+        const int64_t m = std::min(chunk, n - off);
+        if (off > 0 || n > chunk) {   // staging holds the last chunk: normalise this one again
+            launch_normalise((const char*)emb + off * c->dim * esz, emb_dtype, m, c->dim, c->ystage.p,
+                             c->invstage.p, c->istat.p, s);
+            c->launches++;
+        }
+        plan.clear();
+        cp.clear();
+        for (int64_t r = 0; r < m; ++r) {
+            const int64_t gr = off + r;
+            if (st[gr] != CACHE_ROW_OK) {
+                if (out_ids) out_ids[gr] = CACHE_NO_ID;
+                continue;
+            }
+            InsertPlan p;
+            p.src_row = r;
+            p.slot = c->free_e.back();
+            c->free_e.pop_back();
+            p.id = (uint32_t)c->next_id++;
+            p.mask = masks[gr] & full;
+            for (int j = 0; j < CACHE_MAX_K; ++j) p.lslot[j] = -1;
+            for (int j = 0; j < c->num_k; ++j) {
+                if (!((p.mask >> j) & 1u)) continue;
+                p.lslot[j] = (int32_t)c->free_l.back();
+                c->free_l.pop_back();
+                if (latents) cp.push_back(CopyPlan{gr * c->num_k + j, p.lslot[j]});
+            }
+            plan.push_back(p);
+            c->h_present[p.slot] = p.mask;
+            c->h_ids[p.slot] = p.id;
+            for (int j = 0; j < c->num_k; ++j) c->h_lslot[p.slot * c->num_k + j] = p.lslot[j];
+            c->id2slot[p.id] = p.slot;
+            c->hwm = std::max(c->hwm, p.slot + 1);
+            c->live_entries++;
+            c->live_items += __builtin_popcount(p.mask);
+            if (out_ids) out_ids[gr] = p.id;
+        }
+        CK(c->iplan.ensure(std::max<size_t>(plan.size(), 1)));
+        CK(cudaMemcpyAsync(c->iplan.p, plan.data(), plan.size() * sizeof(InsertPlan), cudaMemcpyHostToDevice, s));
+        launch_insert_commit(c->ystage.p, c->invstage.p, c->iplan.p, (int64_t)plan.size(), c->dim, c->num_k,
+                             c->emb, c->inv_e, c->ids, c->present, c->lslot, c->fcnt, s);
+        c->launches++;
+        if (!cp.empty()) {
+            CK(c->cplan.ensure(cp.size()));
+            CK(cudaMemcpyAsync(c->cplan.p, cp.data(), cp.size() * sizeof(CopyPlan), cudaMemcpyHostToDevice, s));
+            launch_copy_latents((const uint8_t*)latents, c->cplan.p, (int64_t)cp.size(), c->L, c->pool, s);
+            c->launches++;
+        }
+        CK(cudaStreamSynchronize(s));   // plans are host vectors reused by the next chunk
+        CK(cudaGetLastError());
+    }
+    if (row_status) std::memcpy(row_status, st.data(), n * 4);
+    return n_valid == n ? CACHE_OK : fail(CACHE_E_BAD_ROWS, "cache_insert: some rows rejected (row_status)");
+}
+
+static cache_status query_core(cache_t* c, int64_t b, const void* queries, int32_t q_dtype, int32_t topk,
+                               uint64_t* out_ids, float* out_scores, int32_t* out_k, void* latent_out,
+                               void** out_ptr, int32_t* row_status, cudaStream_t s) {
+    const int kmax = topk == 1 ? 1 : (topk <= 4 ? 4 : 16);
+    const int64_t bpad = (b + 127) / 128 * 128;
+    CK(c->qbuf.ensure((size_t)bpad * c->dim));
+    CK(c->invq.ensure(bpad));
+    CK(c->qstat.ensure(bpad));
+    if (c->prof_on) CK(cudaEventRecord(c->prof[0], s));
+    launch_normalise(queries, q_dtype, b, c->dim, c->qbuf.p, c->invq.p, c->qstat.p, s);
+    c->launches++;
+    const int64_t n_slots = c->hwm;
+    int parts = 0;
+    if (c->prof_on) CK(cudaEventRecord(c->prof[1], s));
+    if (n_slots > 0) {
+        bool use_tc = false;
+        TcPlan tp{};
+        if (c->scorer != CACHE_SCORER_STREAM && c->tm_e_ok && tc_supported(c->dim)) {
+            use_tc = c->scorer == CACHE_SCORER_TC || b > 4;
+        }
+        if (c->scorer == CACHE_SCORER_TC && !use_tc)
+            return fail(CACHE_E_UNSUPPORTED, "query: tensor-core scorer unavailable for this configuration");
+        if (use_tc) {
+            tp = tc_plan(b, n_slots, c->sm_count);
+            parts = tp.parts;
+            if (bpad > b) CK(cudaMemsetAsync(c->qbuf.p + b * c->dim, 0, (bpad - b) * c->dim * 2, s));
+            CUtensorMap tm_q;
+            if (!encode_rows(&tm_q, c->qbuf.p, bpad, c->dim, 128))
+                return fail(CACHE_E_CUDA, "query: cuTensorMapEncodeTiled failed");
+            CK(c->recs.ensure((size_t)parts * b * kmax));
+            if (!launch_score_tc(kmax, tp, &tm_q, &c->tm_e, c->inv_e, c->ids, c->dim, b, c->recs.p, s))
+                return fail(CACHE_E_UNSUPPORTED, "query: tensor-core scorer not built");
+            c->launches++;
+        } else {
+            parts = stream_parts(n_slots, b);
+            CK(c->recs.ensure((size_t)parts * b * kmax));
+            launch_score_stream(kmax, c->emb, c->inv_e, c->ids, n_slots, c->dim, c->qbuf.p, b, c->recs.p, parts, s);
+            c->launches++;
+        }
+    }
+    if (c->prof_on) CK(cudaEventRecord(c->prof[2], s));
+    launch_finalize(kmax, c->recs.p, parts, b, topk, c->invq.p, c->qstat.p, c->ids, c->present, c->lslot,
+                    c->fcnt, c->pool, c->L, c->km, out_ids, out_scores, out_k, (uint8_t*)latent_out, out_ptr,
+                    row_status, s);
+    c->launches++;
+    if (c->prof_on) CK(cudaEventRecord(c->prof[3], s));
+    CK(cudaGetLastError());
+    c->queries += b;
+    return CACHE_OK;
+}
+
+cache_status cache_query_batch(cache_t* c, int64_t b, const void* queries, int32_t q_dtype, int32_t topk,
+                               uint64_t* out_ids, float* out_scores, int32_t* out_k, void* latent_out,
+                               void** out_latent_ptr, int32_t* row_status, void* stream) {
+    if (!c) return fail(CACHE_E_INVALID_ARG, "cache_query_batch: null cache");
+    if (b < 0 || b > 0x7FFFFFFF || topk < 1 || topk > c->cfg.max_topk ||
+        (q_dtype != CACHE_DTYPE_F32 && q_dtype != CACHE_DTYPE_BF16))
+        return fail(CACHE_E_INVALID_ARG, "cache_query_batch: bad b / topk / dtype");
+    if (b == 0) return CACHE_OK;
+    if (!queries || !out_ids || !out_scores || !out_k)
+        return fail(CACHE_E_INVALID_ARG, "cache_query_batch: null buffer");
+    if (latent_out && !c->pool) return fail(CACHE_E_INVALID_ARG, "cache_query_batch: no latent pool");
+    DeviceGuard g(c->device);
+    return query_core(c, b, queries, q_dtype, topk, out_ids, out_scores, out_k, latent_out, out_latent_ptr,
+                      row_status, (cudaStream_t)stream);
+}
+
+cache_status cache_query_batch_host(cache_t* c, int64_t b, const void* queries, int32_t q_dtype, int32_t topk,
+                                    uint64_t* out_ids, float* out_scores, int32_t* out_k, void* latent_out,
+                                    int32_t* row_status, void* stream) {
+    if (!c) return fail(CACHE_E_INVALID_ARG, "cache_query_batch_host: null cache");
+    if (b < 0 || b > 0x7FFFFFFF || topk < 1 || topk > c->cfg.max_topk ||
+        (q_dtype != CACHE_DTYPE_F32 && q_dtype != CACHE_DTYPE_BF16))
+        return fail(CACHE_E_INVALID_ARG, "cache_query_batch_host: bad b / topk / dtype");
+    if (b == 0) return CACHE_OK;
+    if (!queries || !out_ids || !out_scores || !out_k)
+        return fail(CACHE_E_INVALID_ARG, "cache_query_batch_host: null buffer");
+    if (latent_out && !c->pool) return fail(CACHE_E_INVALID_ARG, "cache_query_batch_host: no latent pool");
+    DeviceGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t qbytes = (size_t)b * c->dim * (q_dtype == CACHE_DTYPE_BF16 ? 2 : 4);
+    CK(c->hq_in.ensure(qbytes));
+    CK(c->hq_ids.ensure((size_t)b * topk));
+    CK(c->hq_sc.ensure((size_t)b * topk));
+    CK(c->hq_k.ensure(b));
+    CK(c->hq_st.ensure(b));
+    if (latent_out) CK(c->hq_lat.ensure((size_t)b * c->L));
+    CK(cudaMemcpyAsync(c->hq_in.p, queries, qbytes, cudaMemcpyHostToDevice, s));
+    cache_status r = query_core(c, b, c->hq_in.p, q_dtype, topk, c->hq_ids.p, c->hq_sc.p, c->hq_k.p,
+                                latent_out ? c->hq_lat.p : nullptr, nullptr, c->hq_st.p, s);
+    if (r != CACHE_OK) return r;
+    CK(cudaMemcpyAsync(out_ids, c->hq_ids.p, (size_t)b * topk * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(out_scores, c->hq_sc.p, (size_t)b * topk * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(out_k, c->hq_k.p, (size_t)b * 4, cudaMemcpyDeviceToHost, s));
+    if (row_status) CK(cudaMemcpyAsync(row_status, c->hq_st.p, (size_t)b * 4, cudaMemcpyDeviceToHost, s));
+    if (latent_out) CK(cudaMemcpyAsync(latent_out, c->hq_lat.p, (size_t)b * c->L, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return CACHE_OK;
+}
+
+cache_status cache_evict(cache_t* c, int64_t n, uint64_t* out_evicted, uint64_t* out_dirty_ids,
+                         int64_t* out_n_dirty, void* stream) {
+    if (!c) return fail(CACHE_E_INVALID_ARG, "cache_evict: null cache");
+    if (n < 0) return fail(CACHE_E_INVALID_ARG, "cache_evict: n < 0");
+    if (n > c->live_items) return fail(CACHE_E_EVICT_RANGE, "cache_evict: n exceeds live items");
+    if (out_n_dirty) *out_n_dirty = 0;
+    if (n == 0) return CACHE_OK;
+    DeviceGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    CK(c->est.ensure(1));
+    CK(c->ehist.ensure(256));
+    CK(c->ekey.ensure(n));
+    CK(c->elslot.ensure(n));
+    CK(c->ecnt.ensure(2));
+    CK(c->edirty.ensure(n));
+    EvictState st0{0ull, 0ull, (unsigned long long)n};
+    CK(cudaMemcpyAsync(c->est.p, &st0, sizeof(st0), cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(c->ehist.p, 0, 256 * 4, s));
+    CK(cudaMemsetAsync(c->ecnt.p, 0, 16, s));
+    launch_evict_select(c->present, c->fcnt, c->ids, c->hwm, c->km, c->est.p, c->ehist.p, s);
+    c->launches += 16;
+    launch_evict_apply(c->present, c->fcnt, c->ids, c->lslot, c->inv_e, c->hwm, c->km, c->est.p, c->ekey.p,
+                       c->elslot.p, c->ecnt.p, c->edirty.p, s);
+    c->launches++;
+    unsigned long long cnt[2];
+    CK(cudaMemcpyAsync(cnt, c->ecnt.p, 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if ((int64_t)cnt[0] != n || (int64_t)cnt[1] > n)
+        return fail(CACHE_E_STATE, "cache_evict: selection count mismatch (internal error)");
+    std::vector<unsigned long long> keys(n);
+    std::vector<int32_t> ls(n);
+    std::vector<int64_t> dslots(cnt[1]);
+    CK(cudaMemcpy(keys.data(), c->ekey.p, n * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(ls.data(), c->elslot.p, n * 4, cudaMemcpyDeviceToHost));
+    if (cnt[1]) CK(cudaMemcpy(dslots.data(), c->edirty.p, cnt[1] * 8, cudaMemcpyDeviceToHost));
+    // host mirrors + free lists (sorted so allocation stays deterministic)
+    std::vector<size_t> order(n);
+    for (int64_t i = 0; i < n; ++i) order[i] = i;
+    std::sort(order.begin(), order.end(), [&](size_t a, size_t b2) { return keys[a] < keys[b2]; });
+    for (int64_t i = 0; i < n; ++i) {
+        const unsigned long long k = keys[order[i]];
+        const uint64_t idj = k & ((1ull << 35) - 1);
+        if (out_evicted) out_evicted[i] = idj;
+        const uint64_t id = idj >> 3;
+        const int j = (int)(idj & 7);
+        auto it = c->id2slot.find(id);
+        if (it != c->id2slot.end()) {
+            c->h_present[it->second] &= ~(1u << j);
+            c->h_lslot[it->second * c->num_k + j] = -1;
+        }
+        c->free_l.push_back(ls[order[i]]);
+    }
+    c->live_items -= n;
+    std::vector<uint64_t> dids;
+    for (int64_t ds : dslots) {
+        dids.push_back(c->h_ids[ds]);
+        c->id2slot.erase(c->h_ids[ds]);
+        c->h_present[ds] = 0;
+        c->free_e.push_back(ds);
+        c->live_entries--;
+    }
+    std::sort(dids.begin(), dids.end());
+    if (out_dirty_ids)
+        for (size_t i = 0; i < dids.size(); ++i) out_dirty_ids[i] = dids[i];
+    if (out_n_dirty) *out_n_dirty = (int64_t)dids.size();
+    std::sort(c->free_l.begin(), c->free_l.end(), std::greater<int64_t>());
+    std::sort(c->free_e.begin(), c->free_e.end(), std::greater<int64_t>());
+    // shrink the scan high-water mark past trailing empty slots
+    while (c->hwm > 0 && c->h_present[c->hwm - 1] == 0) c->hwm--;
+    return CACHE_OK;
+}
+
+cache_status cache_get_meta(cache_t* c, uint64_t id, uint64_t* f, uint32_t* present_mask) {
+    if (!c) return fail(CACHE_E_INVALID_ARG, "cache_get_meta: null cache");
+    auto it = c->id2slot.find(id);
+    if (it == c->id2slot.end()) return fail(CACHE_E_INVALID_ARG, "cache_get_meta: unknown id");
+    DeviceGuard g(c->device);
+    std::vector<uint32_t> fv(c->num_k);
+    uint32_t m = 0;
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(fv.data(), c->fcnt + it->second * c->num_k, c->num_k * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&m, c->present + it->second, 4, cudaMemcpyDeviceToHost));
+    if (f)
+        for (int j = 0; j < c->num_k; ++j) f[j] = fv[j];
+    if (present_mask) *present_mask = m;
+    return CACHE_OK;
+}
+
+cache_status cache_get_row(cache_t* c, uint64_t id, uint16_t* out_bf16) {
+    if (!c || !out_bf16) return fail(CACHE_E_INVALID_ARG, "cache_get_row: null argument");
+    auto it = c->id2slot.find(id);
+    if (it == c->id2slot.end()) return fail(CACHE_E_INVALID_ARG, "cache_get_row: unknown id");
+    DeviceGuard g(c->device);
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(out_bf16, c->emb + it->second * c->dim, c->dim * 2, cudaMemcpyDeviceToHost));
+    return CACHE_OK;
+}
+
+cache_status cache_stats(cache_t* c, cache_stats_t* out) {
+    if (!c || !out) return fail(CACHE_E_INVALID_ARG, "cache_stats: null argument");
+    DeviceGuard g(c->device);
+    CK(cudaDeviceSynchronize());
+    out->live_entries = c->live_entries;
+    out->live_items = c->live_items;
+    out->holes = c->live_entries * c->num_k - c->live_items;
+    out->entry_hwm = c->hwm;
+    out->next_id = c->next_id;
+    out->queries = c->queries;
+    return CACHE_OK;
+}
+
+cache_status cache_set_scorer(cache_t* c, int32_t scorer) {
+    if (!c || scorer < CACHE_SCORER_AUTO || scorer > CACHE_SCORER_STREAM)
+        return fail(CACHE_E_INVALID_ARG, "cache_set_scorer: bad argument");
+    c->scorer = scorer;
+    return CACHE_OK;
+}
+
+cache_status cache_set_profile_events(cache_t* c, void* const* events) {
+    if (!c) return fail(CACHE_E_INVALID_ARG, "cache_set_profile_events: null cache");
+    c->prof_on = events != nullptr;
+    for (int i = 0; i < 4; ++i) c->prof[i] = events ? (cudaEvent_t)events[i] : nullptr;
+    if (events)
+        for (int i = 0; i < 4; ++i)
+            if (!c->prof[i]) {
+                c->prof_on = false;
+                return fail(CACHE_E_INVALID_ARG, "cache_set_profile_events: null event");
+            }
+    return CACHE_OK;
+}
+
+int64_t cache_kernel_launches(const cache_t* c) { return c ? c->launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,539 @@
+// kernels.cu -- CUDA-core kernels of the NIRVANA cache lookup for sm_100a:
+//   k_normalise      query ingest / insert normalisation
+//   k_score_stream   HBM-streaming small-batch cosine scan + running top-k (a2, a3)
+//   k_finalize       cross-split merge, Fig. 11 K map, hole rule, latent gather,
+//                    LCBFU access counters (a3, a5, a6, a7, a8)
+//   k_insert_commit / k_copy_latents   LCBFU insertion (a10)
+//   k_evict_*        LCBFU eviction: radix select of the n smallest f*K keys, presence
+//                    clearing, dirty-entry removal (a9)
+#include "common.cuh"
+#include "kernels.h"
+
+namespace nv {
+
+// ---------------------------------------------------------------------------------------
+// Normalisation (reading R2).  One 128-thread CTA per row; dim <= 1024.  Thread t holds
+// elements t + 128k (k < 8) of the row zero-padded to P = next_pow2(dim).  The sum of
+// squares follows the oracle's tree exactly: stride s = P/2 ... 1, a[i] = a[i] + a[i+s],
+// so sum, sqrt and division (all correctly rounded fp64) and the direct fp64->bf16 RNE
+// conversion (cvt.rn.bf16.f64) give bit-identical stored rows.
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ double tree_sum_128x8(double v[8], int P, double* red) {
+    const int t = threadIdx.x;
+#pragma unroll
+    for (int s = 512; s >= 128; s >>= 1) {
+        if (s < P) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (128 * k < s) v[k] = __dadd_rn(v[k], v[k + s / 128]);
+        }
+    }
+    red[t] = v[0];
+    __syncthreads();
+    for (int s = min(P / 2, 64); s >= 32; s >>= 1) {
+        if (t < s) red[t] = __dadd_rn(red[t], red[t + s]);
+        __syncthreads();
+    }
+    double r = 0.0;
+    if (t < 32) {
+        r = red[t];
+        for (int s = min(P / 2, 16); s >= 1; s >>= 1) {
+            double o = __shfl_down_sync(0xFFFFFFFFu, r, s);
+            r = __dadd_rn(r, o);
+        }
+    }
+    if (t == 0) red[0] = r;
+    __syncthreads();
+    r = red[0];
+    __syncthreads();
+    return r;
+}
+
+template <typename Tin>
+__device__ __forceinline__ double load_in(const Tin* p);
+template <>
+__device__ __forceinline__ double load_in<float>(const float* p) { return (double)__ldg(p); }
+template <>
+__device__ __forceinline__ double load_in<__nv_bfloat16>(const __nv_bfloat16* p) {
+    return (double)__bfloat162float(*p);
+}
+
+template <typename Tin>
+__global__ void __launch_bounds__(128) k_normalise(const Tin* __restrict__ x, int64_t n, int dim,
+                                                   int P, __nv_bfloat16* __restrict__ y,
+                                                   float* __restrict__ inv,
+                                                   int32_t* __restrict__ status) {
+    __shared__ double red[128];
+    const int64_t r = blockIdx.x;
+    if (r >= n) return;
+    const int t = threadIdx.x;
+    const Tin* xr = x + r * (int64_t)dim;
+    double xv[8], v[8];
+    int bad = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int i = t + 128 * k;
+        xv[k] = i < dim ? load_in<Tin>(xr + i) : 0.0;
+        bad |= !isfinite(xv[k]);
+        v[k] = __dmul_rn(xv[k], xv[k]);
+    }
+    bad = __syncthreads_or(bad);
+    int st = CACHE_ROW_OK;
+    double s = 0.0;
+    if (!bad) {
+        s = tree_sum_128x8(v, P, red);
+        if (s == 0.0) st = CACHE_ROW_ZERO_NORM;
+        else if (!isfinite(s)) st = CACHE_ROW_NONFINITE;
+    } else {
+        st = CACHE_ROW_NONFINITE;
+    }
+    __nv_bfloat16* yr = y + r * (int64_t)dim;
+    if (st != CACHE_ROW_OK) {
+        for (int i = t; i < dim; i += 128) yr[i] = __float2bfloat16_rn(0.0f);
+        if (t == 0) { inv[r] = __int_as_float(0x7FC00000); status[r] = st; }
+        return;
+    }
+    const double nu = __dsqrt_rn(s);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int i = t + 128 * k;
+        __nv_bfloat16 b = __double2bfloat16(__ddiv_rn(xv[k], nu));   // cvt.rn.bf16.f64
+        if (i < dim) yr[i] = b;
+        const double yd = i < dim ? (double)__bfloat162float(b) : 0.0;
+        v[k] = __dmul_rn(yd, yd);
+    }
+    const double s2 = tree_sum_128x8(v, P, red);
+    if (t == 0) {
+        if (s2 == 0.0) {
+            inv[r] = __int_as_float(0x7FC00000);
+            status[r] = CACHE_ROW_ZERO_NORM;
+        } else {
+            inv[r] = __double2float_rn(__ddiv_rn(1.0, __dsqrt_rn(s2)));
+            status[r] = CACHE_ROW_OK;
+        }
+    }
+}
+
+void launch_normalise(const void* x, int dtype, int64_t n, int dim, __nv_bfloat16* y, float* inv,
+                      int32_t* status, cudaStream_t s) {
+    if (n <= 0) return;
+    int P = 1;
+    while (P < dim) P <<= 1;
+    if (dtype == CACHE_DTYPE_BF16)
+        k_normalise<__nv_bfloat16><<<(unsigned)n, 128, 0, s>>>((const __nv_bfloat16*)x, n, dim, P,
+                                                                 y, inv, status);
+    else
+        k_normalise<float><<<(unsigned)n, 128, 0, s>>>((const float*)x, n, dim, P, y, inv, status);
+}
+
+// ---------------------------------------------------------------------------------------
+// Streaming scan on CUDA cores (small batches, HBM bound).  Each warp owns whole entry
+// rows: lane l loads 16-byte chunks 32c+l of a 2*dim-byte row (coalesced 512 B per warp
+// instruction), multiplies them with the BQ queries held in registers (fp32 FMA on the
+// exactly widened bf16 values), reduces across the warp with shuffles, scales by the
+// entry's inv-norm and offers the result to a register top-k owned by lane b (query b).
+// CTA-level merge of the 8 warp lists -> one partial record list per (CTA, query).
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ int4 ld_stream(const int4* p) {
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+template <int BQ, int KMAX, int NCH>
+__global__ void __launch_bounds__(256, 2)
+k_score_stream(const __nv_bfloat16* __restrict__ emb, const float* __restrict__ inv_e,
+               const uint32_t* __restrict__ ids, int64_t n_slots, int dim,
+               const __nv_bfloat16* __restrict__ qbuf, int64_t b_total, Rec* __restrict__ ws) {
+    __shared__ Rec sm[8][BQ][KMAX];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int q0 = blockIdx.y * BQ;
+    const int nvec = dim / 8;   // 16-byte chunks per row
+    // queries -> registers (fp32), positions (32c + lane)*8 + [0,8)
+    float qf[BQ][NCH * 8];
+#pragma unroll
+    for (int b = 0; b < BQ; ++b) {
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            const int v = 32 * c + lane;
+            int4 w = make_int4(0, 0, 0, 0);
+            if (v < nvec && q0 + b < b_total)
+                w = *reinterpret_cast<const int4*>(qbuf + (int64_t)(q0 + b) * dim + v * 8);
+            const uint32_t ww[4] = {(uint32_t)w.x, (uint32_t)w.y, (uint32_t)w.z, (uint32_t)w.w};
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                qf[b][c * 8 + 2 * h] = __uint_as_float(ww[h] << 16);
+                qf[b][c * 8 + 2 * h + 1] = __uint_as_float(ww[h] & 0xFFFF0000u);
+            }
+        }
+    }
+    TopK<KMAX> tk;
+    tk.init();
+    const int64_t per = (n_slots + gridDim.x - 1) / gridDim.x;
+    const int64_t r0 = (int64_t)blockIdx.x * per;
+    const int64_t r1 = min(n_slots, r0 + per);
+    for (int64_t row = r0 + warp; row < r1; row += 8) {
+        const int4* rp = reinterpret_cast<const int4*>(emb + row * dim);
+        int4 e[NCH];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c)
+            e[c] = (32 * c + lane < nvec) ? ld_stream(rp + 32 * c + lane) : make_int4(0, 0, 0, 0);
+        const float ie = __ldg(inv_e + row);
+        float acc[BQ];
+#pragma unroll
+        for (int b = 0; b < BQ; ++b) acc[b] = 0.0f;
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            const uint32_t ww[4] = {(uint32_t)e[c].x, (uint32_t)e[c].y, (uint32_t)e[c].z, (uint32_t)e[c].w};
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const float lo = __uint_as_float(ww[h] << 16);
+                const float hi = __uint_as_float(ww[h] & 0xFFFF0000u);
+#pragma unroll
+                for (int b = 0; b < BQ; ++b) {
+                    acc[b] = fmaf(lo, qf[b][c * 8 + 2 * h], acc[b]);
+                    acc[b] = fmaf(hi, qf[b][c * 8 + 2 * h + 1], acc[b]);
+                }
+            }
+        }
+#pragma unroll
+        for (int b = 0; b < BQ; ++b) {
+#pragma unroll
+            for (int m = 16; m >= 1; m >>= 1) acc[b] += __shfl_xor_sync(0xFFFFFFFFu, acc[b], m);
+        }
+        float mine = 0.0f;
+#pragma unroll
+        for (int b = 0; b < BQ; ++b)
+            if (lane == b) mine = acc[b] * ie;
+        if (lane < BQ) tk.offer(mine, (uint32_t)row, ids);
+    }
+    if (lane < BQ) {
+#pragma unroll
+        for (int i = 0; i < KMAX; ++i) { sm[warp][lane][i].key = tk.k[i]; sm[warp][lane][i].slot = tk.s[i]; }
+    }
+    __syncthreads();
+    if (threadIdx.x < BQ && q0 + (int)threadIdx.x < b_total) {
+        const int b = threadIdx.x;
+        TopK<KMAX> m;
+        m.init();
+        for (int w = 0; w < 8; ++w)
+#pragma unroll
+            for (int i = 0; i < KMAX; ++i)
+                if (sm[w][b][i].key) m.offer_key(sm[w][b][i].key, sm[w][b][i].slot);
+        Rec* out = ws + ((int64_t)blockIdx.x * b_total + q0 + b) * KMAX;
+#pragma unroll
+        for (int i = 0; i < KMAX; ++i) { Rec r; r.key = m.k[i]; r.slot = m.s[i]; r.pad = 0; out[i] = r; }
+    }
+}
+
+template <int BQ, int KMAX>
+static void launch_stream_bq(int nch, dim3 g, const __nv_bfloat16* emb, const float* inv_e,
+                             const uint32_t* ids, int64_t n_slots, int dim,
+                             const __nv_bfloat16* qbuf, int64_t b, Rec* ws, cudaStream_t s) {
+    switch (nch) {
+        case 1: k_score_stream<BQ, KMAX, 1><<<g, 256, 0, s>>>(emb, inv_e, ids, n_slots, dim, qbuf, b, ws); break;
+        case 2: k_score_stream<BQ, KMAX, 2><<<g, 256, 0, s>>>(emb, inv_e, ids, n_slots, dim, qbuf, b, ws); break;
+        case 3: k_score_stream<BQ, KMAX, 3><<<g, 256, 0, s>>>(emb, inv_e, ids, n_slots, dim, qbuf, b, ws); break;
+        default: k_score_stream<BQ, KMAX, 4><<<g, 256, 0, s>>>(emb, inv_e, ids, n_slots, dim, qbuf, b, ws); break;
+    }
+}
+
+int stream_parts(int64_t n_slots, int64_t b) {
+    const int bq = b >= 4 ? 4 : (b >= 2 ? 2 : 1);
+    const int64_t groups = (b + bq - 1) / bq;
+    int64_t parts = (148 * 4 + groups - 1) / groups;
+    parts = std::max<int64_t>(1, std::min<int64_t>(parts, (n_slots + 511) / 512));
+    return (int)parts;
+}
+
+void launch_score_stream(int kmax, const __nv_bfloat16* emb, const float* inv_e, const uint32_t* ids,
+                         int64_t n_slots, int dim, const __nv_bfloat16* qbuf, int64_t b, Rec* ws,
+                         int parts, cudaStream_t s) {
+    const int bq = b >= 4 ? 4 : (b >= 2 ? 2 : 1);
+    const int nch = (dim / 8 + 31) / 32;
+    dim3 g((unsigned)parts, (unsigned)((b + bq - 1) / bq));
+#define NV_STREAM_K(BQV)                                                                              \
+    do {                                                                                              \
+        if (kmax == 1) launch_stream_bq<BQV, 1>(nch, g, emb, inv_e, ids, n_slots, dim, qbuf, b, ws, s); \
+        else if (kmax == 4) launch_stream_bq<BQV, 4>(nch, g, emb, inv_e, ids, n_slots, dim, qbuf, b, ws, s); \
+        else launch_stream_bq<BQV, 16>(nch, g, emb, inv_e, ids, n_slots, dim, qbuf, b, ws, s);      \
+    } while (0)
+    if (bq == 4) NV_STREAM_K(4);
+    else if (bq == 2) NV_STREAM_K(2);
+    else NV_STREAM_K(1);
+#undef NV_STREAM_K
+}
+
+// ---------------------------------------------------------------------------------------
+// Finalize: one 128-thread CTA per query.  Warp 0 merges the `parts` partial lists under
+// the total order (R3) -> top-k; lane 0 applies the Fig. 11 map (largest j with
+// s > thr[j], strict, compared in fp64 on the clamped fp32 score), the knob (R20) and the
+// hole rule (m = present & ((2 << j*) - 1), j = 31 - clz(m)); then the whole CTA
+// copies the selected latent (128-bit loads/stores) and one thread counts the access.
+// ---------------------------------------------------------------------------------------
+template <int KMAX>
+__global__ void __launch_bounds__(128)
+k_finalize(const Rec* __restrict__ ws, int parts, int64_t B, int topk, const float* __restrict__ inv_q,
+           const int32_t* __restrict__ qstatus, const uint32_t* __restrict__ ids,
+           const uint32_t* __restrict__ present, const int32_t* __restrict__ lslot,
+           uint32_t* __restrict__ fcnt, const uint8_t* __restrict__ pool, int64_t latent_bytes,
+           KMap km, uint64_t* __restrict__ out_ids, float* __restrict__ out_scores,
+           int32_t* __restrict__ out_k, uint8_t* __restrict__ latent_out, void** __restrict__ out_ptr,
+           int32_t* __restrict__ out_status) {
+    __shared__ unsigned long long s_key[KMAX];
+    __shared__ uint32_t s_slot[KMAX];
+    __shared__ long long s_src;
+    const int64_t b = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int st = qstatus[b];
+    if (warp == 0) {
+        TopK<KMAX> tk;
+        tk.init();
+        if (st == CACHE_ROW_OK) {
+            for (int p = lane; p < parts; p += 32) {
+                const Rec* r = ws + ((int64_t)p * B + b) * KMAX;
+                for (int i = 0; i < topk; ++i) {
+                    const Rec rr = r[i];
+                    if (rr.key == 0ull) break;
+                    tk.offer_key(rr.key, rr.slot);
+                }
+            }
+        }
+        for (int i = 0; i < topk; ++i) {
+            const unsigned long long m = warp_max_u64(tk.k[0]);
+            if (m != 0ull && tk.k[0] == m) {
+                s_key[i] = m;
+                s_slot[i] = tk.s[0];
+                tk.pop();
+            }
+            if (m == 0ull && lane == 0) s_key[i] = 0ull;
+            __syncwarp();
+        }
+        if (lane == 0) {
+            const float iq = st == CACHE_ROW_OK ? inv_q[b] : 0.0f;
+            for (int i = 0; i < topk; ++i) {
+                const unsigned long long key = s_key[i];
+                out_ids[b * topk + i] = key ? (uint64_t)key_id(key) : CACHE_NO_ID;
+                out_scores[b * topk + i] = key ? fminf(fmaxf(key_to_f32(key) * iq, -1.0f), 1.0f) : -INFINITY;
+            }
+            int K = 0;
+            long long src = -1;
+            if (s_key[0] != 0ull) {
+                const float c = fminf(fmaxf(key_to_f32(s_key[0]) * iq, -1.0f), 1.0f);
+                int jstar = -1;
+                for (int j = 0; j < km.num_k; ++j)
+                    if ((double)c > km.thr[j]) jstar = j;
+                if (jstar >= 0) {
+                    jstar = min(jstar + km.k_bias, km.num_k - 1);
+                    const uint32_t slot = s_slot[0];
+                    const uint32_t m = present[slot] & ((2u << jstar) - 1u);
+                    if (m) {
+                        const int j = 31 - __clz(m);
+                        K = km.kv[j];
+                        src = lslot[(int64_t)slot * km.num_k + j];
+                        atomicAdd(fcnt + (int64_t)slot * km.num_k + j, 1u);
+                    }
+                }
+            }
+            out_k[b] = K;
+            if (out_status) out_status[b] = st;
+            if (out_ptr) out_ptr[b] = (K > 0 && latent_out) ? (void*)(latent_out + b * latent_bytes) : nullptr;
+            s_src = src;
+        }
+    }
+    __syncthreads();
+    const long long src = s_src;
+    if (src >= 0 && latent_out && latent_bytes > 0) {
+        const int4* sp = reinterpret_cast<const int4*>(pool + src * latent_bytes);
+        int4* dp = reinterpret_cast<int4*>(latent_out + b * latent_bytes);
+        const int64_t nv = latent_bytes / 16;
+        int64_t i = threadIdx.x;
+        for (; i + 3 * 128 < nv; i += 4 * 128) {
+            int4 a0 = ld_stream(sp + i), a1 = ld_stream(sp + i + 128), a2 = ld_stream(sp + i + 256),
+                 a3 = ld_stream(sp + i + 384);
+            __stcs(dp + i, a0);
+            __stcs(dp + i + 128, a1);
+            __stcs(dp + i + 256, a2);
+            __stcs(dp + i + 384, a3);
+        }
+        for (; i < nv; i += 128) __stcs(dp + i, ld_stream(sp + i));
+    }
+}
+
+void launch_finalize(int kmax, const Rec* ws, int parts, int64_t B, int topk, const float* inv_q,
+                     const int32_t* qstatus, const uint32_t* ids, const uint32_t* present,
+                     const int32_t* lslot, uint32_t* fcnt, const uint8_t* pool, int64_t latent_bytes,
+                     const KMap& km, uint64_t* out_ids, float* out_scores, int32_t* out_k,
+                     uint8_t* latent_out, void** out_ptr, int32_t* out_status, cudaStream_t s) {
+    if (B <= 0) return;
+#define NV_FIN(KM)                                                                                \
+    k_finalize<KM><<<(unsigned)B, 128, 0, s>>>(ws, parts, B, topk, inv_q, qstatus, ids, present, \
+                                               lslot, fcnt, pool, latent_bytes, km, out_ids,     \
+                                               out_scores, out_k, latent_out, out_ptr, out_status)
+    if (kmax == 1) NV_FIN(1);
+    else if (kmax == 4) NV_FIN(4);
+    else NV_FIN(16);
+#undef NV_FIN
+}
+
+// ---------------------------------------------------------------------------------------
+// Insert: commit normalised rows into their slots and copy latent payloads.
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(128)
+k_insert_commit(const __nv_bfloat16* __restrict__ ystage, const float* __restrict__ invstage,
+                const InsertPlan* __restrict__ plan, int64_t n_valid, int dim, int num_k,
+                __nv_bfloat16* __restrict__ emb, float* __restrict__ inv_e, uint32_t* __restrict__ ids,
+                uint32_t* __restrict__ present, int32_t* __restrict__ lslot, uint32_t* __restrict__ fcnt) {
+    const int64_t i = blockIdx.x;
+    if (i >= n_valid) return;
+    const InsertPlan p = plan[i];
+    const int4* src = reinterpret_cast<const int4*>(ystage + p.src_row * (int64_t)dim);
+    int4* dst = reinterpret_cast<int4*>(emb + p.slot * (int64_t)dim);
+    for (int v = threadIdx.x; v < dim / 8; v += 128) dst[v] = src[v];
+    if (threadIdx.x < num_k) {
+        lslot[p.slot * num_k + threadIdx.x] = p.lslot[threadIdx.x];
+        fcnt[p.slot * num_k + threadIdx.x] = 0u;
+    }
+    if (threadIdx.x == 0) {
+        inv_e[p.slot] = invstage[p.src_row];
+        ids[p.slot] = p.id;
+        present[p.slot] = p.mask;
+    }
+}
+
+__global__ void __launch_bounds__(128)
+k_copy_latents(const uint8_t* __restrict__ src, const CopyPlan* __restrict__ plan, int64_t n,
+               int64_t latent_bytes, uint8_t* __restrict__ pool) {
+    const int64_t i = blockIdx.x;
+    if (i >= n) return;
+    const CopyPlan p = plan[i];
+    const int4* sp = reinterpret_cast<const int4*>(src + p.src_item * latent_bytes);
+    int4* dp = reinterpret_cast<int4*>(pool + p.dst_slot * latent_bytes);
+    for (int64_t v = threadIdx.x; v < latent_bytes / 16; v += 128) dp[v] = sp[v];
+}
+
+void launch_insert_commit(const __nv_bfloat16* ystage, const float* invstage, const InsertPlan* plan,
+                          int64_t n_valid, int dim, int num_k, __nv_bfloat16* emb, float* inv_e,
+                          uint32_t* ids, uint32_t* present, int32_t* lslot, uint32_t* fcnt, cudaStream_t s) {
+    if (n_valid > 0)
+        k_insert_commit<<<(unsigned)n_valid, 128, 0, s>>>(ystage, invstage, plan, n_valid, dim, num_k,
+                                                          emb, inv_e, ids, present, lslot, fcnt);
+}
+
+void launch_copy_latents(const uint8_t* src, const CopyPlan* plan, int64_t n, int64_t latent_bytes,
+                         uint8_t* pool, cudaStream_t s) {
+    if (n > 0) k_copy_latents<<<(unsigned)n, 128, 0, s>>>(src, plan, n, latent_bytes, pool);
+}
+
+// ---------------------------------------------------------------------------------------
+// Eviction.  Item key (reading R11): min(f*K, 2^29-1) << 35 | id << 3 | j,
+// unique per item, ascending = evicted first.  Exact selection of the n smallest keys by an
+// 8-pass MSB-first radix select (8-bit digits): histogram of keys matching the prefix ->
+// pick the digit holding the remaining-th key.  Then every key <= the selected key is
+// evicted: presence bit cleared, latent slot freed; entries left with no K are dirty and
+// are invalidated (inv_norm = NaN) in the same kernel.
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long evict_key(uint32_t f, int kval, uint32_t id, int j) {
+    unsigned long long sc = (unsigned long long)f * (unsigned long long)kval;
+    if (sc > 0x1FFFFFFFull) sc = 0x1FFFFFFFull;
+    return (sc << 35) | ((unsigned long long)id << 3) | (unsigned long long)j;
+}
+
+__global__ void __launch_bounds__(256)
+k_evict_hist(const uint32_t* __restrict__ present, const uint32_t* __restrict__ fcnt,
+             const uint32_t* __restrict__ ids, int64_t n_slots, KMap km, const EvictState* __restrict__ st,
+             int shift, unsigned int* __restrict__ hist) {
+    __shared__ unsigned int sh[256];
+    sh[threadIdx.x] = 0;
+    __syncthreads();
+    const unsigned long long prefix = st->prefix, mask = st->mask;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_slots;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t m = present[e];
+        if (!m) continue;
+        const uint32_t id = ids[e];
+        for (int j = 0; j < km.num_k; ++j) {
+            if (!((m >> j) & 1u)) continue;
+            const unsigned long long key = evict_key(fcnt[e * km.num_k + j], km.kv[j], id, j);
+            if ((key & mask) == prefix) atomicAdd(&sh[(key >> shift) & 255ull], 1u);
+        }
+    }
+    __syncthreads();
+    if (sh[threadIdx.x]) atomicAdd(&hist[threadIdx.x], sh[threadIdx.x]);
+}
+
+__global__ void k_evict_pick(unsigned int* __restrict__ hist, EvictState* __restrict__ st, int shift) {
+    if (threadIdx.x == 0) {
+        unsigned long long cum = 0;
+        const unsigned long long rem = st->remaining;
+        for (int d = 0; d < 256; ++d) {
+            if (cum + hist[d] >= rem) {
+                st->prefix |= (unsigned long long)d << shift;
+                st->remaining = rem - cum;
+                break;
+            }
+            cum += hist[d];
+        }
+        st->mask |= 255ull << shift;
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < 256; d += blockDim.x) hist[d] = 0;
+}
+
+__global__ void __launch_bounds__(256)
+k_evict_apply(uint32_t* __restrict__ present, uint32_t* __restrict__ fcnt, const uint32_t* __restrict__ ids,
+              const int32_t* __restrict__ lslot, float* __restrict__ inv_e, int64_t n_slots, KMap km,
+              const EvictState* __restrict__ st, unsigned long long* __restrict__ ev_key,
+              int32_t* __restrict__ ev_lslot, unsigned long long* __restrict__ counters,
+              int64_t* __restrict__ dirty_slot) {
+    const unsigned long long T = st->prefix;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_slots;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t m = present[e];
+        if (!m) continue;
+        const uint32_t id = ids[e];
+        uint32_t keep = m;
+        for (int j = 0; j < km.num_k; ++j) {
+            if (!((m >> j) & 1u)) continue;
+            const unsigned long long key = evict_key(fcnt[e * km.num_k + j], km.kv[j], id, j);
+            if (key <= T) {
+                keep &= ~(1u << j);
+                const unsigned long long at = atomicAdd(&counters[0], 1ull);
+                ev_key[at] = key;
+                ev_lslot[at] = lslot[e * km.num_k + j];
+                fcnt[e * km.num_k + j] = 0u;
+            }
+        }
+        if (keep != m) {
+            present[e] = keep;
+            if (keep == 0u) {
+                inv_e[e] = __int_as_float(0x7FC00000);
+                const unsigned long long at = atomicAdd(&counters[1], 1ull);
+                dirty_slot[at] = e;
+            }
+        }
+    }
+}
+
+void launch_evict_select(const uint32_t* present, const uint32_t* fcnt, const uint32_t* ids,
+                         int64_t n_slots, const KMap& km, EvictState* st, unsigned int* hist, cudaStream_t s) {
+    const int grid = (int)std::min<int64_t>(148 * 8, (n_slots + 255) / 256 + 1);
+    for (int pass = 0; pass < 8; ++pass) {
+        const int shift = 56 - 8 * pass;
+        k_evict_hist<<<grid, 256, 0, s>>>(present, fcnt, ids, n_slots, km, st, shift, hist);
+        k_evict_pick<<<1, 256, 0, s>>>(hist, st, shift);
+    }
+}
+
+void launch_evict_apply(uint32_t* present, uint32_t* fcnt, const uint32_t* ids, const int32_t* lslot,
+                        float* inv_e, int64_t n_slots, const KMap& km, const EvictState* st,
+                        unsigned long long* ev_key, int32_t* ev_lslot, unsigned long long* counters,
+                        int64_t* dirty_slot, cudaStream_t s) {
+    const int grid = (int)std::min<int64_t>(148 * 8, (n_slots + 255) / 256 + 1);
+    k_evict_apply<<<grid, 256, 0, s>>>(present, fcnt, ids, lslot, inv_e, n_slots, km, st, ev_key, ev_lslot,
+                                       counters, dirty_slot);
+}
+
+}  // namespace nv

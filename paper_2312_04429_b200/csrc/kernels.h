@@ -1,0 +1,73 @@
+// kernels.h -- launcher declarations shared by the host engine (cache.cu) and the kernels.
+#pragma once
+#include <algorithm>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace nv {
+
+struct InsertPlan {          // one accepted insert row
+    int64_t src_row;         // row index in the caller's batch / staging buffer
+    int64_t slot;            // entry slot
+    uint32_t id;             // assigned entry id
+    uint32_t mask;           // present-K bitmask
+    int32_t lslot[CACHE_MAX_K];  // latent-pool slot per K (-1 = not stored)
+};
+
+struct CopyPlan {            // one latent payload copy
+    int64_t src_item;        // (row * num_k + j) in the caller's latents buffer
+    int64_t dst_slot;        // latent-pool slot
+};
+
+struct EvictState {          // radix-select state (device)
+    unsigned long long prefix;
+    unsigned long long mask;
+    unsigned long long remaining;
+};
+
+void launch_normalise(const void* x, int dtype, int64_t n, int dim, __nv_bfloat16* y, float* inv,
+                      int32_t* status, cudaStream_t s);
+
+int stream_parts(int64_t n_slots, int64_t b);
+void launch_score_stream(int kmax, const __nv_bfloat16* emb, const float* inv_e, const uint32_t* ids,
+                         int64_t n_slots, int dim, const __nv_bfloat16* qbuf, int64_t b, Rec* ws,
+                         int parts, cudaStream_t s);
+
+// tcgen05 scorer (score_tc.cu).  Returns false if the configuration is not supported.
+struct TcPlan {
+    int m_tiles;        // ceil(B / 128)
+    int n_tiles;        // ceil(n_slots / 256)
+    int chunk_tiles;    // n-tiles per chunk (top-k segment)
+    int n_chunks;
+    int grid;           // persistent CTAs
+    int parts;          // records per query = 2 * n_chunks
+};
+bool tc_supported(int dim);
+TcPlan tc_plan(int64_t b, int64_t n_slots, int sm_count);
+bool launch_score_tc(int kmax, const TcPlan& plan, const void* tmap_q, const void* tmap_e,
+                     const float* inv_e, const uint32_t* ids, int dim, int64_t b, Rec* ws,
+                     cudaStream_t s);
+
+void launch_finalize(int kmax, const Rec* ws, int parts, int64_t B, int topk, const float* inv_q,
+                     const int32_t* qstatus, const uint32_t* ids, const uint32_t* present,
+                     const int32_t* lslot, uint32_t* fcnt, const uint8_t* pool, int64_t latent_bytes,
+                     const KMap& km, uint64_t* out_ids, float* out_scores, int32_t* out_k,
+                     uint8_t* latent_out, void** out_ptr, int32_t* out_status, cudaStream_t s);
+
+void launch_insert_commit(const __nv_bfloat16* ystage, const float* invstage, const InsertPlan* plan,
+                          int64_t n_valid, int dim, int num_k, __nv_bfloat16* emb, float* inv_e,
+                          uint32_t* ids, uint32_t* present, int32_t* lslot, uint32_t* fcnt, cudaStream_t s);
+void launch_copy_latents(const uint8_t* src, const CopyPlan* plan, int64_t n, int64_t latent_bytes,
+                         uint8_t* pool, cudaStream_t s);
+
+void launch_evict_select(const uint32_t* present, const uint32_t* fcnt, const uint32_t* ids,
+                         int64_t n_slots, const KMap& km, EvictState* st, unsigned int* hist, cudaStream_t s);
+void launch_evict_apply(uint32_t* present, uint32_t* fcnt, const uint32_t* ids, const int32_t* lslot,
+                        float* inv_e, int64_t n_slots, const KMap& km, const EvictState* st,
+                        unsigned long long* ev_key, int32_t* ev_lslot, unsigned long long* counters,
+                        int64_t* dirty_slot, cudaStream_t s);
+
+}  // namespace nv
