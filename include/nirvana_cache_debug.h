@@ -1,0 +1,29 @@
+/*
+ * nirvana_cache_debug.h -- test-only entry points of libnirvana_cache.so (not the product
+ * API).  They expose intermediate results of the lookup so each kernel can be checked on its
+ * own against a plain reference.
+ */
+#ifndef NIRVANA_CACHE_DEBUG_H
+#define NIRVANA_CACHE_DEBUG_H
+
+#include "nirvana_cache.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Dense scan values of the tensor-core main loop: out[i*ld + e] = fl(<q~_i, x~_e> *
+ * inv_norm(x~_e)) for every query i < b and entry slot e < entry_hwm (the value the fused
+ * top-k epilogue ranks; NaN for empty slots).  queries: device pointer b x dim (q_dtype);
+ * out: device pointer, b x ld floats, ld >= round_up(entry_hwm, 256).  Asynchronous.
+ * Returns CACHE_E_UNSUPPORTED when the tcgen05 kernel is unavailable. */
+cache_status cache_debug_tc_scores(cache_t *c, int64_t b, const void *queries, int32_t q_dtype,
+                                   float *out, int64_t ld, void *stream);
+
+/* Slot of entry `id` (host-synchronous), -1 if not live. */
+int64_t cache_debug_slot_of(cache_t *c, uint64_t id);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -254,3 +254,25 @@ class NirvanaCache:
     @property
     def kernel_launches(self) -> int:
         return _lib.cache_kernel_launches(self._h)
+
+
+# ------------------------------- test-only entry points -------------------------------
+_lib.cache_debug_tc_scores.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int32,
+                                       ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+_lib.cache_debug_tc_scores.restype = ctypes.c_int
+_lib.cache_debug_slot_of.argtypes = [ctypes.c_void_p, ctypes.c_uint64]
+_lib.cache_debug_slot_of.restype = ctypes.c_int64
+
+
+def debug_tc_scores(cache: NirvanaCache, q: torch.Tensor, stream=None) -> torch.Tensor:
+    """Dense fl(<q~,x~> * inv_norm(x~)) from the tcgen05 main loop, [b][round_up(hwm, 256)]."""
+    hwm = cache.stats()["entry_hwm"]
+    ld = max(256, (hwm + 255) // 256 * 256)
+    out = torch.full((q.shape[0], ld), float("nan"), dtype=torch.float32, device=q.device)
+    dt = DTYPE_BF16 if q.dtype == torch.bfloat16 else DTYPE_F32
+    _check(_lib.cache_debug_tc_scores(cache._h, q.shape[0], _ptr(q), dt, _ptr(out), ld, _stream(stream)))
+    return out
+
+
+def debug_slot_of(cache: NirvanaCache, id_: int) -> int:
+    return _lib.cache_debug_slot_of(cache._h, int(id_))

@@ -563,3 +563,39 @@ cache_status cache_set_profile_events(cache_t* c, void* const* events) {
 int64_t cache_kernel_launches(const cache_t* c) { return c ? c->launches : 0; }
 
 }  // extern "C"
+
+// ------------------------------- test-only entry points -------------------------------
+#include "../../include/nirvana_cache_debug.h"
+namespace nv {
+bool launch_score_tc_dense(const TcPlan& p, const void* tmap_q, const void* tmap_e, const float* inv_e, int dim,
+                           int64_t b, float* dense, int64_t dense_ld, cudaStream_t s);
+}
+
+extern "C" cache_status cache_debug_tc_scores(cache_t* c, int64_t b, const void* queries, int32_t q_dtype,
+                                              float* out, int64_t ld, void* stream) {
+    if (!c || b <= 0 || !queries || !out) return fail(CACHE_E_INVALID_ARG, "cache_debug_tc_scores: bad argument");
+    if (!c->tm_e_ok || !tc_supported(c->dim)) return fail(CACHE_E_UNSUPPORTED, "tcgen05 scorer unavailable");
+    const int64_t n_slots = c->hwm;
+    if (n_slots == 0) return CACHE_OK;
+    TcPlan tp = tc_plan(b, n_slots, c->sm_count);
+    if (ld < (int64_t)tp.n_tiles * 256) return fail(CACHE_E_INVALID_ARG, "cache_debug_tc_scores: ld too small");
+    DeviceGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t bpad = (b + 127) / 128 * 128;
+    CK(c->qbuf.ensure((size_t)bpad * c->dim));
+    CK(c->invq.ensure(bpad));
+    CK(c->qstat.ensure(bpad));
+    launch_normalise(queries, q_dtype, b, c->dim, c->qbuf.p, c->invq.p, c->qstat.p, s);
+    if (bpad > b) CK(cudaMemsetAsync(c->qbuf.p + b * c->dim, 0, (bpad - b) * c->dim * 2, s));
+    CUtensorMap tm_q;
+    if (!encode_rows(&tm_q, c->qbuf.p, bpad, c->dim, 128)) return fail(CACHE_E_CUDA, "tensor map encode failed");
+    if (!launch_score_tc_dense(tp, &tm_q, &c->tm_e, c->inv_e, c->dim, b, out, ld, s))
+        return fail(CACHE_E_CUDA, std::string("tc dense launch: ") + cudaGetErrorString(cudaGetLastError()));
+    return CACHE_OK;
+}
+
+extern "C" int64_t cache_debug_slot_of(cache_t* c, uint64_t id) {
+    if (!c) return -1;
+    auto it = c->id2slot.find(id);
+    return it == c->id2slot.end() ? -1 : it->second;
+}

@@ -1,11 +1,354 @@
-// score_tc.cu -- tcgen05/TMEM tensor-core scorer (placeholder until the kernel lands).
+// score_tc.cu -- tcgen05/TMEM tensor-core cosine scan with a fused top-k epilogue (sm_100a).
+//
+// The similarity of a batch of queries with every cached entry (SURVEY
+// 8(a) a2-a3) is the dense contraction S = Q~ X~^T (B x N, K = dim).  One output tile is
+// 128 queries (M, TMEM lanes) x 256 entries (N, TMEM columns) x dim:
+//
+//   warp 0 (1 lane)  TMA producer: A = Q~ tile [128 x 64] and B = X~ tile [256 x 64] per
+//                    64-wide K chunk (128-byte swizzle) into a 4-stage shared-memory ring
+//   warp 1 (1 lane)  MMA issuer: tcgen05.mma.cta_group::1.kind::f16 (bf16 x bf16 -> fp32)
+//                    M=128 N=256 K=16, accumulating in TMEM; double-buffered accumulators
+//                    (2 x 256 columns) so the epilogue of tile i overlaps the MMAs of i+1
+//   warps 4-7        epilogue: each thread owns one query row (one TMEM lane), reads its 256
+//                    fp32 dots with tcgen05.ld, scales by the entry inv-norm (NaN = empty
+//                    slot), and keeps the running top-k in registers -- no score matrix is
+//                    ever written to HBM
+//
+// Work unit = (n-chunk, m-tile): a run of `chunk_tiles` consecutive entry tiles for one
+// query tile.  Units are dealt round-robin to a persistent grid (one CTA per SM), m fastest,
+// so the CTAs running at the same time share the same entry tiles (L2 reuse).  Each unit
+// ends with one partial top-k record list per query -> ws[chunk][query][KMAX]; k_finalize
+// merges the n_chunks lists under the same total order (R3).
+#include <cuda.h>
+
 #include "kernels.h"
 
 namespace nv {
-bool tc_supported(int) { return false; }
-TcPlan tc_plan(int64_t, int64_t, int) { return TcPlan{}; }
-bool launch_score_tc(int, const TcPlan&, const void*, const void*, const float*, const uint32_t*, int,
-                     int64_t, Rec*, cudaStream_t) {
-    return false;
+namespace tc {
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;            // 16 KiB
+constexpr int B_BYTES = BN * BK * 2;            // 32 KiB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // 48 KiB
+constexpr int TMEM_COLS = 512;                  // 2 accumulators x 256 fp32 columns
+constexpr int NUM_THREADS = 256;
+constexpr int EPI_WARP0 = 4;
+// Instruction descriptor, kind::f16: D=f32 (bits 4-5 = 1), A=B=bf16 (bits 7-9, 10-12 = 1),
+// both K-major (bits 15,16 = 0), N>>3 at bits 17-22, M>>4 at bits 24-28.
+constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(BM >> 4) << 24);
+constexpr int SMEM_INV_OFF = STAGES * STAGE_BYTES;              // 2 x 256 floats
+constexpr int SMEM_BAR_OFF = SMEM_INV_OFF + 2 * BN * 4;          // 2*STAGES + 4 mbarriers
+constexpr int SMEM_TMEM_OFF = SMEM_BAR_OFF + (2 * STAGES + 4) * 8;
+constexpr int SMEM_BYTES = SMEM_TMEM_OFF + 16 + 1024;           // + alignment slack
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y)
+        : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// Shared-memory matrix descriptor: K-major, 128-byte swizzle, 8-row groups 1024 B apart.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);   // start address (bits 0-13)
+    d |= (uint64_t)1 << 16;                     // leading byte offset (unused for SW128 K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;           // stride byte offset: 8 rows x 128 B
+    d |= (uint64_t)1 << 46;                     // descriptor version 1 (sm_100)
+    d |= (uint64_t)2 << 61;                     // layout: SWIZZLE_128B
+    return d;
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %3, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %4, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(accum), "r"(IDESC)
+        : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// kDense = true: debug/test variant that stores the scan values t = dot * inv_e densely
+// (out[q][col]) instead of reducing them -- used to check the tcgen05 main loop on its own.
+template <int KMAX, bool kDense>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+k_score_tc(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_e,
+           const float* __restrict__ inv_e, const uint32_t* __restrict__ ids, int dim, int64_t B,
+           int m_tiles, int n_tiles, int chunk_tiles, int n_units, Rec* __restrict__ ws,
+           float* __restrict__ dense, int64_t dense_ld) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    float* inv_s = reinterpret_cast<float*>(smem + SMEM_INV_OFF);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SMEM_BAR_OFF);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SMEM_TMEM_OFF);
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t bar_full = smem_u32(bars), bar_empty = bar_full + STAGES * 8;
+    const uint32_t bar_tfull = bar_empty + STAGES * 8, bar_tempty = bar_tfull + 2 * 8;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int kch = dim / BK;
+
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_q)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_e)) : "memory");
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(bar_full + 8 * s, 1);
+            mbar_init(bar_empty + 8 * s, 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(bar_tfull + 8 * a, 1);
+            mbar_init(bar_tempty + 8 * a, 4);   // one arrive per epilogue warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------- TMA producer -------------------------------
+        if (lane == 0) {
+            uint32_t stage = 0, phase = 0;
+            for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+                const int chunk = u / m_tiles, m = u - chunk * m_tiles;
+                const int n0 = chunk * chunk_tiles, n1 = min(n_tiles, n0 + chunk_tiles);
+                for (int n = n0; n < n1; ++n) {
+                    for (int kc = 0; kc < kch; ++kc) {
+                        mbar_wait(bar_empty + 8 * stage, phase ^ 1);
+                        const uint32_t sa = sbase + stage * STAGE_BYTES;
+                        mbar_expect_tx(bar_full + 8 * stage, STAGE_BYTES);
+                        tma_load_2d(sa, &tmap_q, bar_full + 8 * stage, kc * BK, m * BM);
+                        tma_load_2d(sa + A_BYTES, &tmap_e, bar_full + 8 * stage, kc * BK, n * BN);
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------- MMA issuer ---------------------------------
+        if (lane == 0) {
+            uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+            for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+                const int chunk = u / m_tiles;
+                const int n0 = chunk * chunk_tiles, n1 = min(n_tiles, n0 + chunk_tiles);
+                for (int n = n0; n < n1; ++n) {
+                    mbar_wait(bar_tempty + 8 * acc, acc_phase ^ 1);
+                    tc_fence_after();
+                    const uint32_t d = tmem_base + acc * BN;
+                    for (int kc = 0; kc < kch; ++kc) {
+                        mbar_wait(bar_full + 8 * stage, phase);
+                        tc_fence_after();
+                        const uint32_t sa = sbase + stage * STAGE_BYTES;
+                        const uint64_t ad = sw128_desc(sa), bd = sw128_desc(sa + A_BYTES);
+#pragma unroll
+                        for (int k = 0; k < BK / 16; ++k)   // +32 B along K inside the swizzle atom
+                            umma_bf16(d, ad + 2 * k, bd + 2 * k, (kc | k) != 0);
+                        umma_commit(bar_empty + 8 * stage);  // frees the smem stage when done
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    }
+                    umma_commit(bar_tfull + 8 * acc);        // accumulator ready
+                    acc ^= 1;
+                    if (acc == 0) acc_phase ^= 1;
+                }
+            }
+        }
+    } else if (warp >= EPI_WARP0) {
+        // ------------------------------- epilogue -----------------------------------
+        const int ew = warp - EPI_WARP0;            // == warp % 4: TMEM lanes 32*ew .. +31
+        const int et = threadIdx.x - EPI_WARP0 * 32; // 0..127
+        const int row = 32 * ew + lane;
+        uint32_t acc = 0, acc_phase = 0;
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+            const int chunk = u / m_tiles, m = u - chunk * m_tiles;
+            const int n0 = chunk * chunk_tiles, n1 = min(n_tiles, n0 + chunk_tiles);
+            const int64_t q = (int64_t)m * BM + row;
+            TopK<KMAX> tk;
+            tk.init();
+            for (int n = n0; n < n1; ++n) {
+                float* iv = inv_s + acc * BN;
+                iv[et] = __ldg(inv_e + (int64_t)n * BN + et);
+                iv[et + 128] = __ldg(inv_e + (int64_t)n * BN + 128 + et);
+                epi_bar();
+                mbar_wait(bar_tfull + 8 * acc, acc_phase);
+                tc_fence_after();
+                const uint32_t taddr = tmem_base + ((uint32_t)(32 * ew) << 16) + acc * BN;
+#pragma unroll 1
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t r[32];
+                    tmem_ld32(taddr + c * 32, r);
+                    tmem_ld_wait();
+                    float t[32];
+                    float mx = -INFINITY;
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        t[i] = __uint_as_float(r[i]) * iv[c * 32 + i];
+                        mx = fmaxf(mx, t[i]);
+                    }
+                    if (kDense) {
+                        if (q < B) {
+                            float* o = dense + q * dense_ld + (int64_t)n * BN + c * 32;
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) o[i] = t[i];
+                        }
+                    } else if (mx >= tk.thr) {
+                        const uint32_t col0 = (uint32_t)(n * BN + c * 32);
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) tk.offer(t[i], col0 + i, ids);
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar_tempty + 8 * acc);
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+            }
+            if (!kDense && q < B) {
+                Rec* o = ws + ((int64_t)chunk * B + q) * KMAX;
+#pragma unroll
+                for (int i = 0; i < KMAX; ++i) {
+                    Rec rr;
+                    rr.key = tk.k[i];
+                    rr.slot = tk.s[i];
+                    rr.pad = 0;
+                    o[i] = rr;
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 1) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
+                     : "memory");
+    }
+}
+
+template <int KMAX, bool kDense>
+static bool launch(const TcPlan& p, const CUtensorMap* tq, const CUtensorMap* te, const float* inv_e,
+                   const uint32_t* ids, int dim, int64_t b, Rec* ws, float* dense, int64_t dense_ld,
+                   cudaStream_t s) {
+    auto kern = k_score_tc<KMAX, kDense>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess)
+            return false;
+        attr_set = true;
+    }
+    const int n_units = p.n_chunks * p.m_tiles;
+    kern<<<p.grid, NUM_THREADS, SMEM_BYTES, s>>>(*tq, *te, inv_e, ids, dim, b, p.m_tiles, p.n_tiles,
+                                                 p.chunk_tiles, n_units, ws, dense, dense_ld);
+    return cudaPeekAtLastError() == cudaSuccess;
+}
+
+}  // namespace tc
+
+bool tc_supported(int dim) { return dim % tc::BK == 0 && dim >= tc::BK && dim <= kMaxDim; }
+
+// Chunk size: minimise the round-robin makespan (in tiles, + a small per-unit cost for the
+// record flush / pipeline refill); ties -> larger chunks (fewer partial records to merge).
+TcPlan tc_plan(int64_t b, int64_t n_slots, int sm_count) {
+    TcPlan p{};
+    p.m_tiles = (int)((b + tc::BM - 1) / tc::BM);
+    p.n_tiles = (int)((n_slots + tc::BN - 1) / tc::BN);
+    double best = 1e30;
+    for (int nc = 1; nc <= std::min(p.n_tiles, 64); ++nc) {
+        const int nch = (p.n_tiles + nc - 1) / nc;
+        const int64_t units = (int64_t)nch * p.m_tiles;
+        const int g = (int)std::min<int64_t>(sm_count, units);
+        // CTA j takes units j, j+g, ...; unit u has chunk u / m_tiles
+        double mk = 0;
+        for (int j = 0; j < g; ++j) {
+            double t = 0;
+            for (int64_t u = j; u < units; u += g) {
+                const int c = (int)(u / p.m_tiles);
+                t += std::min(nc, p.n_tiles - c * nc) + 0.15;
+            }
+            mk = std::max(mk, t);
+        }
+        if (mk < best - 1e-9 || (mk <= best + 1e-9 && nc > p.chunk_tiles)) {
+            best = mk;
+            p.chunk_tiles = nc;
+        }
+    }
+    p.n_chunks = (p.n_tiles + p.chunk_tiles - 1) / p.chunk_tiles;
+    p.grid = (int)std::min<int64_t>(sm_count, (int64_t)p.n_chunks * p.m_tiles);
+    p.parts = p.n_chunks;
+    return p;
+}
+
+bool launch_score_tc(int kmax, const TcPlan& p, const void* tmap_q, const void* tmap_e, const float* inv_e,
+                     const uint32_t* ids, int dim, int64_t b, Rec* ws, cudaStream_t s) {
+    const CUtensorMap* tq = static_cast<const CUtensorMap*>(tmap_q);
+    const CUtensorMap* te = static_cast<const CUtensorMap*>(tmap_e);
+    if (kmax == 1) return tc::launch<1, false>(p, tq, te, inv_e, ids, dim, b, ws, nullptr, 0, s);
+    if (kmax == 4) return tc::launch<4, false>(p, tq, te, inv_e, ids, dim, b, ws, nullptr, 0, s);
+    return tc::launch<16, false>(p, tq, te, inv_e, ids, dim, b, ws, nullptr, 0, s);
+}
+
+bool launch_score_tc_dense(const TcPlan& p, const void* tmap_q, const void* tmap_e, const float* inv_e, int dim,
+                           int64_t b, float* dense, int64_t dense_ld, cudaStream_t s) {
+    return tc::launch<1, true>(p, static_cast<const CUtensorMap*>(tmap_q), static_cast<const CUtensorMap*>(tmap_e),
+                               inv_e, nullptr, dim, b, nullptr, dense, dense_ld, s);
+}
+
 }  // namespace nv
