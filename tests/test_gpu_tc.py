@@ -23,7 +23,7 @@ def _stored(cache, n):
                                      (2048, 300, 1024), (513, 257, 128)])
 def test_tc_dense_matches_torch_fp32(B, oracle_mod, n, b, dim):
     emb, cl = synth.entries(n, seed=n, dim=dim)
-    g = B.NirvanaCache(entry_capacity=n, dim=dim, latent_bytes=0, latent_capacity=0)
+    g = B.NirvanaCache(entry_capacity=n, dim=dim, latent_bytes=0, latent_capacity=5 * n)
     g.insert(torch.from_numpy(emb).cuda())
     q, _, _ = synth.queries(emb, cl, b, seed=b, )
     dense = B.debug_tc_scores(g, torch.from_numpy(q).cuda()).cpu()
@@ -46,7 +46,7 @@ def test_tc_single_tile_exact_on_dyadic_data(B):
     e = rng.integers(-3, 4, size=(n, dim)).astype(np.float32)
     q = rng.integers(-3, 4, size=(b, dim)).astype(np.float32)
     e[:, 0] = 64.0   # dominant component so the normalised row is a power-of-two scale of e
-    g = B.NirvanaCache(entry_capacity=n, dim=dim, latent_bytes=0, latent_capacity=0)
+    g = B.NirvanaCache(entry_capacity=n, dim=dim, latent_bytes=0, latent_capacity=5 * n)
     g.insert(torch.from_numpy(e).cuda())
     dense = B.debug_tc_scores(g, torch.from_numpy(q).cuda()).cpu().double()
     x = _stored(g, n).double()
