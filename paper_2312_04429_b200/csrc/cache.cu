@@ -342,7 +342,7 @@ static cache_status query_core(cache_t* c, int64_t b, const void* queries, int32
     c->launches++;
     const int64_t n_slots = c->hwm;
     int parts = 0;
-    if (c->prof_on) CK(cudaEventRecord(c->prof[1], s));
+    bool prof1 = false;   // prof[1] is recorded right before the scoring launch (after host planning)
     if (n_slots > 0) {
         bool use_tc = false;
         TcPlan tp{};
@@ -359,16 +359,19 @@ static cache_status query_core(cache_t* c, int64_t b, const void* queries, int32
             if (!encode_rows(&tm_q, c->qbuf.p, bpad, c->dim, 128))
                 return fail(CACHE_E_CUDA, "query: cuTensorMapEncodeTiled failed");
             CK(c->recs.ensure((size_t)parts * b * kmax));
+            if (c->prof_on) { CK(cudaEventRecord(c->prof[1], s)); prof1 = true; }
             if (!launch_score_tc(kmax, tp, &tm_q, &c->tm_e, c->inv_e, c->ids, c->dim, b, c->recs.p, s))
                 return fail(CACHE_E_UNSUPPORTED, "query: tensor-core scorer not built");
             c->launches++;
         } else {
             parts = stream_parts(n_slots, b);
             CK(c->recs.ensure((size_t)parts * b * kmax));
+            if (c->prof_on) { CK(cudaEventRecord(c->prof[1], s)); prof1 = true; }
             launch_score_stream(kmax, c->emb, c->inv_e, c->ids, n_slots, c->dim, c->qbuf.p, b, c->recs.p, parts, s);
             c->launches++;
         }
     }
+    if (c->prof_on && !prof1) CK(cudaEventRecord(c->prof[1], s));
     if (c->prof_on) CK(cudaEventRecord(c->prof[2], s));
     launch_finalize(kmax, c->recs.p, parts, b, topk, c->invq.p, c->qstat.p, c->ids, c->present, c->lslot,
                     c->fcnt, c->pool, c->L, c->km, out_ids, out_scores, out_k, (uint8_t*)latent_out, out_ptr,

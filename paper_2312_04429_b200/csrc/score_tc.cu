@@ -31,7 +31,6 @@ constexpr int A_BYTES = BM * BK * 2;            // 16 KiB
 constexpr int B_BYTES = BN * BK * 2;            // 32 KiB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // 48 KiB
 constexpr int TMEM_COLS = 512;                  // 2 accumulators x 256 fp32 columns
-constexpr int NUM_THREADS = 256;
 constexpr int EPI_WARP0 = 4;
 // Instruction descriptor, kind::f16: D=f32 (bits 4-5 = 1), A=B=bf16 (bits 7-9, 10-12 = 1),
 // both K-major (bits 15,16 = 0), N>>3 at bits 17-22, M>>4 at bits 24-28.
@@ -40,7 +39,8 @@ constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >
 constexpr int SMEM_INV_OFF = STAGES * STAGE_BYTES;              // 2 x 256 floats
 constexpr int SMEM_BAR_OFF = SMEM_INV_OFF + 2 * BN * 4;          // 2*STAGES + 4 mbarriers
 constexpr int SMEM_TMEM_OFF = SMEM_BAR_OFF + (2 * STAGES + 4) * 8;
-constexpr int SMEM_BYTES = SMEM_TMEM_OFF + 16 + 1024;           // + alignment slack
+constexpr int SMEM_XCH_OFF = SMEM_TMEM_OFF + 16;                  // half-merge exchange (128 x 16 x 12 B)
+constexpr int SMEM_BYTES = SMEM_XCH_OFF + BM * 16 * 12 + 1024;   // + alignment slack
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -121,21 +121,69 @@ __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
+// Wait for this thread's outstanding tcgen05.ld; the registers are tied as in/out operands
+// so the compiler cannot schedule their uses above the wait.
+__device__ __forceinline__ void tmem_ld_wait_regs(uint32_t (&r)[32]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]),
+                   "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]),
+                   "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]),
+                   "+r"(r[21]), "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]),
+                   "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+                 :
+                 : "memory");
+}
+
+__device__ __forceinline__ float4 lds_f4(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+    return v;
+}
+
+// Scale one 32-column chunk by the entry inv-norms, gate on its max, offer survivors.
+template <int KMAX, bool kDense>
+__device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], uint32_t inv_addr, uint32_t col0, TopK<KMAX>& tk,
+                                          const uint32_t* __restrict__ ids, float* dense_row) {
+    float t[32];
+    float mx = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+        const float4 iv = lds_f4(inv_addr + 4 * i);
+        t[i] = __uint_as_float(r[i]) * iv.x;
+        t[i + 1] = __uint_as_float(r[i + 1]) * iv.y;
+        t[i + 2] = __uint_as_float(r[i + 2]) * iv.z;
+        t[i + 3] = __uint_as_float(r[i + 3]) * iv.w;
+        mx = fmaxf(mx, fmaxf(fmaxf(t[i], t[i + 1]), fmaxf(t[i + 2], t[i + 3])));
+    }
+    if (kDense) {
+        if (dense_row) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4)
+                *reinterpret_cast<float4*>(dense_row + col0 + i) = make_float4(t[i], t[i + 1], t[i + 2], t[i + 3]);
+        }
+    } else if (mx >= tk.thr) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) tk.offer(t[i], col0 + i, ids);
+    }
+}
+
+constexpr int EPI_WARPS = 8;                       // 2 per SM sub-partition: column halves
+constexpr int NUM_THREADS_TC = (EPI_WARP0 + EPI_WARPS) * 32;   // 384
+
 // kDense = true: debug/test variant that stores the scan values t = dot * inv_e densely
 // (out[q][col]) instead of reducing them -- used to check the tcgen05 main loop on its own.
 template <int KMAX, bool kDense>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+__global__ void __launch_bounds__(NUM_THREADS_TC, 1)
 k_score_tc(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_e,
            const float* __restrict__ inv_e, const uint32_t* __restrict__ ids, int dim, int64_t B,
            int m_tiles, int n_tiles, int chunk_tiles, int n_units, Rec* __restrict__ ws,
            float* __restrict__ dense, int64_t dense_ld) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-    float* inv_s = reinterpret_cast<float*>(smem + SMEM_INV_OFF);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SMEM_BAR_OFF);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SMEM_TMEM_OFF);
     const uint32_t sbase = smem_u32(smem);
-    const uint32_t bar_full = smem_u32(bars), bar_empty = bar_full + STAGES * 8;
+    const uint32_t inv_base = sbase + SMEM_INV_OFF;
+    const uint32_t bar_full = sbase + SMEM_BAR_OFF, bar_empty = bar_full + STAGES * 8;
     const uint32_t bar_tfull = bar_empty + STAGES * 8, bar_tempty = bar_tfull + 2 * 8;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int kch = dim / BK;
@@ -149,7 +197,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ C
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(bar_tfull + 8 * a, 1);
-            mbar_init(bar_tempty + 8 * a, 4);   // one arrive per epilogue warp
+            mbar_init(bar_tempty + 8 * a, EPI_WARPS);   // one arrive per epilogue warp
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -213,64 +261,77 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ C
         }
     } else if (warp >= EPI_WARP0) {
         // ------------------------------- epilogue -----------------------------------
-        const int ew = warp - EPI_WARP0;            // == warp % 4: TMEM lanes 32*ew .. +31
-        const int et = threadIdx.x - EPI_WARP0 * 32; // 0..127
+        // warp w: TMEM lane quarter w % 4 (rows 32*(w%4)..+31), column half h = (w-4)/4.
+        const int ew = warp & 3;
+        const int h = (warp - EPI_WARP0) >> 2;
+        const int et = threadIdx.x - EPI_WARP0 * 32;        // 0..255
         const int row = 32 * ew + lane;
         uint32_t acc = 0, acc_phase = 0;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             const int chunk = u / m_tiles, m = u - chunk * m_tiles;
             const int n0 = chunk * chunk_tiles, n1 = min(n_tiles, n0 + chunk_tiles);
             const int64_t q = (int64_t)m * BM + row;
+            float* dense_row = (kDense && q < B) ? dense + q * dense_ld : nullptr;
             TopK<KMAX> tk;
             tk.init();
             for (int n = n0; n < n1; ++n) {
-                float* iv = inv_s + acc * BN;
-                iv[et] = __ldg(inv_e + (int64_t)n * BN + et);
-                iv[et + 128] = __ldg(inv_e + (int64_t)n * BN + 128 + et);
-                epi_bar();
+                // entry inv-norms of this tile -> smem (double-buffered by accumulator)
+                const uint32_t ivb = inv_base + acc * BN * 4;
+                {
+                    const float v = __ldg(inv_e + (int64_t)n * BN + et);
+                    asm volatile("st.shared.f32 [%0], %1;" ::"r"(ivb + 4 * et), "f"(v) : "memory");
+                }
+                asm volatile("bar.sync 1, 256;" ::: "memory");
                 mbar_wait(bar_tfull + 8 * acc, acc_phase);
                 tc_fence_after();
-                const uint32_t taddr = tmem_base + ((uint32_t)(32 * ew) << 16) + acc * BN;
-#pragma unroll 1
-                for (int c = 0; c < BN / 32; ++c) {
-                    uint32_t r[32];
-                    tmem_ld32(taddr + c * 32, r);
-                    tmem_ld_wait();
-                    float t[32];
-                    float mx = -INFINITY;
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        t[i] = __uint_as_float(r[i]) * iv[c * 32 + i];
-                        mx = fmaxf(mx, t[i]);
-                    }
-                    if (kDense) {
-                        if (q < B) {
-                            float* o = dense + q * dense_ld + (int64_t)n * BN + c * 32;
-#pragma unroll
-                            for (int i = 0; i < 32; ++i) o[i] = t[i];
-                        }
-                    } else if (mx >= tk.thr) {
-                        const uint32_t col0 = (uint32_t)(n * BN + c * 32);
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) tk.offer(t[i], col0 + i, ids);
-                    }
-                }
+                const uint32_t taddr = tmem_base + ((uint32_t)(32 * ew) << 16) + acc * BN + h * 128;
+                const uint32_t col_base = (uint32_t)(n * BN + h * 128);
+                uint32_t ra[32], rb[32];
+                tmem_ld32(taddr, ra);
+                tmem_ld_wait_regs(ra);
+                tmem_ld32(taddr + 32, rb);
+                epi_chunk<KMAX, kDense>(ra, ivb + 4 * (h * 128), col_base, tk, ids, dense_row);
+                tmem_ld_wait_regs(rb);
+                tmem_ld32(taddr + 64, ra);
+                epi_chunk<KMAX, kDense>(rb, ivb + 4 * (h * 128 + 32), col_base + 32, tk, ids, dense_row);
+                tmem_ld_wait_regs(ra);
+                tmem_ld32(taddr + 96, rb);
+                epi_chunk<KMAX, kDense>(ra, ivb + 4 * (h * 128 + 64), col_base + 64, tk, ids, dense_row);
+                tmem_ld_wait_regs(rb);
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(bar_tempty + 8 * acc);
+                if (lane == 0) mbar_arrive(bar_tempty + 8 * acc);   // TMEM columns free again
+                epi_chunk<KMAX, kDense>(rb, ivb + 4 * (h * 128 + 96), col_base + 96, tk, ids, dense_row);
                 acc ^= 1;
                 if (acc == 0) acc_phase ^= 1;
             }
-            if (!kDense && q < B) {
-                Rec* o = ws + ((int64_t)chunk * B + q) * KMAX;
+            if (!kDense) {
+                // merge the two column halves of each row through shared memory (the inv buffer
+                // region is free: every thread has passed this unit's last bar.sync)
+                unsigned long long* mk = reinterpret_cast<unsigned long long*>(smem + SMEM_XCH_OFF);
+                uint32_t* ms = reinterpret_cast<uint32_t*>(smem + SMEM_XCH_OFF + BM * KMAX * 8);
+                if (h == 1) {
 #pragma unroll
-                for (int i = 0; i < KMAX; ++i) {
-                    Rec rr;
-                    rr.key = tk.k[i];
-                    rr.slot = tk.s[i];
-                    rr.pad = 0;
-                    o[i] = rr;
+                    for (int i = 0; i < KMAX; ++i) { mk[row * KMAX + i] = tk.k[i]; ms[row * KMAX + i] = tk.s[i]; }
                 }
+                asm volatile("bar.sync 2, 256;" ::: "memory");
+                if (h == 0) {
+#pragma unroll
+                    for (int i = 0; i < KMAX; ++i)
+                        if (mk[row * KMAX + i]) tk.offer_key(mk[row * KMAX + i], ms[row * KMAX + i]);
+                    if (q < B) {
+                        Rec* o = ws + ((int64_t)chunk * B + q) * KMAX;
+#pragma unroll
+                        for (int i = 0; i < KMAX; ++i) {
+                            Rec rr;
+                            rr.key = tk.k[i];
+                            rr.slot = tk.s[i];
+                            rr.pad = 0;
+                            o[i] = rr;
+                        }
+                    }
+                }
+                asm volatile("bar.sync 2, 256;" ::: "memory");
             }
         }
     }
@@ -295,7 +356,7 @@ static bool launch(const TcPlan& p, const CUtensorMap* tq, const CUtensorMap* te
         attr_set = true;
     }
     const int n_units = p.n_chunks * p.m_tiles;
-    kern<<<p.grid, NUM_THREADS, SMEM_BYTES, s>>>(*tq, *te, inv_e, ids, dim, b, p.m_tiles, p.n_tiles,
+    kern<<<p.grid, NUM_THREADS_TC, SMEM_BYTES, s>>>(*tq, *te, inv_e, ids, dim, b, p.m_tiles, p.n_tiles,
                                                  p.chunk_tiles, n_units, ws, dense, dense_ld);
     return cudaPeekAtLastError() == cudaSuccess;
 }
@@ -304,9 +365,13 @@ static bool launch(const TcPlan& p, const CUtensorMap* tq, const CUtensorMap* te
 
 bool tc_supported(int dim) { return dim % tc::BK == 0 && dim >= tc::BK && dim <= kMaxDim; }
 
-// Chunk size: minimise the round-robin makespan (in tiles, + a small per-unit cost for the
+// Chunk size: minimise the round-robin makespan (memoised per (b, n_slots, sm_count)) (in tiles, + a small per-unit cost for the
 // record flush / pipeline refill); ties -> larger chunks (fewer partial records to merge).
 TcPlan tc_plan(int64_t b, int64_t n_slots, int sm_count) {
+    static thread_local int64_t mb = -1, mn = -1;
+    static thread_local int ms = -1;
+    static thread_local TcPlan memo{};
+    if (b == mb && n_slots == mn && sm_count == ms) return memo;
     TcPlan p{};
     p.m_tiles = (int)((b + tc::BM - 1) / tc::BM);
     p.n_tiles = (int)((n_slots + tc::BN - 1) / tc::BN);
@@ -333,6 +398,10 @@ TcPlan tc_plan(int64_t b, int64_t n_slots, int sm_count) {
     p.n_chunks = (p.n_tiles + p.chunk_tiles - 1) / p.chunk_tiles;
     p.grid = (int)std::min<int64_t>(sm_count, (int64_t)p.n_chunks * p.m_tiles);
     p.parts = p.n_chunks;
+    mb = b;
+    mn = n_slots;
+    ms = sm_count;
+    memo = p;
     return p;
 }
 
