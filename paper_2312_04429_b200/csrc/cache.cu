@@ -123,6 +123,7 @@ struct cache_t {
     DevBuf<__nv_bfloat16> qbuf, ystage;
     DevBuf<float> invq, invstage;
     DevBuf<int32_t> qstat, istat;
+    DevBuf<uint32_t> gk;   // per-query global k-th-best gate of the tcgen05 scorer
     DevBuf<Rec> recs;
     DevBuf<InsertPlan> iplan;
     DevBuf<CopyPlan> cplan;
@@ -227,7 +228,7 @@ cache_status cache_destroy(cache_t* c) {
     cudaFree(c->emb); cudaFree(c->inv_e); cudaFree(c->ids); cudaFree(c->present);
     cudaFree(c->lslot); cudaFree(c->fcnt); cudaFree(c->pool);
     c->qbuf.release(); c->ystage.release(); c->invq.release(); c->invstage.release();
-    c->qstat.release(); c->istat.release(); c->recs.release(); c->iplan.release(); c->cplan.release();
+    c->qstat.release(); c->istat.release(); c->gk.release(); c->recs.release(); c->iplan.release(); c->cplan.release();
     c->hq_in.release(); c->hq_lat.release(); c->hq_ids.release(); c->hq_sc.release(); c->hq_k.release();
     c->hq_st.release(); c->est.release(); c->ehist.release(); c->ekey.release(); c->ecnt.release();
     c->elslot.release(); c->edirty.release();
@@ -337,8 +338,9 @@ static cache_status query_core(cache_t* c, int64_t b, const void* queries, int32
     CK(c->qbuf.ensure((size_t)bpad * c->dim));
     CK(c->invq.ensure(bpad));
     CK(c->qstat.ensure(bpad));
+    CK(c->gk.ensure(bpad));
     if (c->prof_on) CK(cudaEventRecord(c->prof[0], s));
-    launch_normalise(queries, q_dtype, b, c->dim, c->qbuf.p, c->invq.p, c->qstat.p, s);
+    launch_normalise(queries, q_dtype, b, c->dim, c->qbuf.p, c->invq.p, c->qstat.p, s, c->gk.p);
     c->launches++;
     const int64_t n_slots = c->hwm;
     int parts = 0;
@@ -360,7 +362,7 @@ static cache_status query_core(cache_t* c, int64_t b, const void* queries, int32
                 return fail(CACHE_E_CUDA, "query: cuTensorMapEncodeTiled failed");
             CK(c->recs.ensure((size_t)parts * b * kmax));
             if (c->prof_on) { CK(cudaEventRecord(c->prof[1], s)); prof1 = true; }
-            if (!launch_score_tc(kmax, tp, &tm_q, &c->tm_e, c->inv_e, c->ids, c->dim, b, c->recs.p, s))
+            if (!launch_score_tc(kmax, tp, &tm_q, &c->tm_e, c->inv_e, c->ids, c->dim, b, c->recs.p, c->gk.p, s))
                 return fail(CACHE_E_UNSUPPORTED, "query: tensor-core scorer not built");
             c->launches++;
         } else {

@@ -62,10 +62,12 @@ template <typename Tin>
 __global__ void __launch_bounds__(128) k_normalise(const Tin* __restrict__ x, int64_t n, int dim,
                                                    int P, __nv_bfloat16* __restrict__ y,
                                                    float* __restrict__ inv,
-                                                   int32_t* __restrict__ status) {
+                                                   int32_t* __restrict__ status,
+                                                   uint32_t* __restrict__ gk) {
     __shared__ double red[128];
     const int64_t r = blockIdx.x;
     if (r >= n) return;
+    if (gk != nullptr && threadIdx.x == 0) gk[r] = 0u;
     const int t = threadIdx.x;
     const Tin* xr = x + r * (int64_t)dim;
     double xv[8], v[8];
@@ -115,15 +117,15 @@ __global__ void __launch_bounds__(128) k_normalise(const Tin* __restrict__ x, in
 }
 
 void launch_normalise(const void* x, int dtype, int64_t n, int dim, __nv_bfloat16* y, float* inv,
-                      int32_t* status, cudaStream_t s) {
+                      int32_t* status, cudaStream_t s, uint32_t* gk) {
     if (n <= 0) return;
     int P = 1;
     while (P < dim) P <<= 1;
     if (dtype == CACHE_DTYPE_BF16)
         k_normalise<__nv_bfloat16><<<(unsigned)n, 128, 0, s>>>((const __nv_bfloat16*)x, n, dim, P,
-                                                                 y, inv, status);
+                                                                 y, inv, status, gk);
     else
-        k_normalise<float><<<(unsigned)n, 128, 0, s>>>((const float*)x, n, dim, P, y, inv, status);
+        k_normalise<float><<<(unsigned)n, 128, 0, s>>>((const float*)x, n, dim, P, y, inv, status, gk);
 }
 
 // ---------------------------------------------------------------------------------------

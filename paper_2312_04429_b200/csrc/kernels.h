@@ -28,8 +28,9 @@ struct EvictState {          // radix-select state (device)
     unsigned long long remaining;
 };
 
+// gk (optional): per-row u32 reset to 0 (the scorer's global k-th-best gate, see score_tc.cu)
 void launch_normalise(const void* x, int dtype, int64_t n, int dim, __nv_bfloat16* y, float* inv,
-                      int32_t* status, cudaStream_t s);
+                      int32_t* status, cudaStream_t s, uint32_t* gk = nullptr);
 
 int stream_parts(int64_t n_slots, int64_t b);
 void launch_score_stream(int kmax, const __nv_bfloat16* emb, const float* inv_e, const uint32_t* ids,
@@ -49,7 +50,7 @@ bool tc_supported(int dim);
 TcPlan tc_plan(int64_t b, int64_t n_slots, int sm_count);
 bool launch_score_tc(int kmax, const TcPlan& plan, const void* tmap_q, const void* tmap_e,
                      const float* inv_e, const uint32_t* ids, int dim, int64_t b, Rec* ws,
-                     cudaStream_t s);
+                     uint32_t* gk, cudaStream_t s);
 
 void launch_finalize(int kmax, const Rec* ws, int parts, int64_t B, int topk, const float* inv_q,
                      const int32_t* qstatus, const uint32_t* ids, const uint32_t* present,

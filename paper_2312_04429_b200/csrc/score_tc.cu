@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(NUM_THREADS_TC, 1)
 k_score_tc(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_e,
            const float* __restrict__ inv_e, const uint32_t* __restrict__ ids, int dim, int64_t B,
            int m_tiles, int n_tiles, int chunk_tiles, int n_units, Rec* __restrict__ ws,
-           float* __restrict__ dense, int64_t dense_ld) {
+           uint32_t* __restrict__ gk, float* __restrict__ dense, int64_t dense_ld) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SMEM_TMEM_OFF);
@@ -274,6 +274,14 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ C
             float* dense_row = (kDense && q < B) ? dense + q * dense_ld : nullptr;
             TopK<KMAX> tk;
             tk.init();
+            // Seed the gate with a global lower bound on this query's k-th best scan value:
+            // the best k-th value of any finished unit (every member of the final top-k has
+            // t >= it, so nothing that can reach the final top-k is ever gated out).
+            if (!kDense && gk != nullptr && q < B) {
+                const uint32_t g = *reinterpret_cast<volatile const uint32_t*>(gk + q);
+                if (g != 0u) tk.thr = key_to_f32((unsigned long long)g << 32);
+            }
+#pragma unroll 1
             for (int n = n0; n < n1; ++n) {
                 // entry inv-norms of this tile -> smem (double-buffered by accumulator)
                 const uint32_t ivb = inv_base + acc * BN * 4;
@@ -286,22 +294,24 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ C
                 tc_fence_after();
                 const uint32_t taddr = tmem_base + ((uint32_t)(32 * ew) << 16) + acc * BN + h * 128;
                 const uint32_t col_base = (uint32_t)(n * BN + h * 128);
+                const uint32_t ivh = ivb + 4 * (h * 128);
                 uint32_t ra[32], rb[32];
                 tmem_ld32(taddr, ra);
                 tmem_ld_wait_regs(ra);
-                tmem_ld32(taddr + 32, rb);
-                epi_chunk<KMAX, kDense>(ra, ivb + 4 * (h * 128), col_base, tk, ids, dense_row);
-                tmem_ld_wait_regs(rb);
-                tmem_ld32(taddr + 64, ra);
-                epi_chunk<KMAX, kDense>(rb, ivb + 4 * (h * 128 + 32), col_base + 32, tk, ids, dense_row);
-                tmem_ld_wait_regs(ra);
-                tmem_ld32(taddr + 96, rb);
-                epi_chunk<KMAX, kDense>(ra, ivb + 4 * (h * 128 + 64), col_base + 64, tk, ids, dense_row);
-                tmem_ld_wait_regs(rb);
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(bar_tempty + 8 * acc);   // TMEM columns free again
-                epi_chunk<KMAX, kDense>(rb, ivb + 4 * (h * 128 + 96), col_base + 96, tk, ids, dense_row);
+#pragma unroll 1
+                for (int c = 0; c < 128; c += 64) {
+                    tmem_ld32(taddr + c + 32, rb);
+                    epi_chunk<KMAX, kDense>(ra, ivh + 4 * c, col_base + c, tk, ids, dense_row);
+                    tmem_ld_wait_regs(rb);
+                    if (c + 64 < 128) tmem_ld32(taddr + c + 64, ra);
+                    else {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(bar_tempty + 8 * acc);   // TMEM columns free again
+                    }
+                    epi_chunk<KMAX, kDense>(rb, ivh + 4 * (c + 32), col_base + c + 32, tk, ids, dense_row);
+                    if (c + 64 < 128) tmem_ld_wait_regs(ra);
+                }
                 acc ^= 1;
                 if (acc == 0) acc_phase ^= 1;
             }
@@ -320,6 +330,8 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ C
                     for (int i = 0; i < KMAX; ++i)
                         if (mk[row * KMAX + i]) tk.offer_key(mk[row * KMAX + i], ms[row * KMAX + i]);
                     if (q < B) {
+                        if (gk != nullptr && tk.k[KMAX - 1] != 0ull)
+                            atomicMax(gk + q, (uint32_t)(tk.k[KMAX - 1] >> 32));
                         Rec* o = ws + ((int64_t)chunk * B + q) * KMAX;
 #pragma unroll
                         for (int i = 0; i < KMAX; ++i) {
@@ -346,8 +358,8 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ C
 
 template <int KMAX, bool kDense>
 static bool launch(const TcPlan& p, const CUtensorMap* tq, const CUtensorMap* te, const float* inv_e,
-                   const uint32_t* ids, int dim, int64_t b, Rec* ws, float* dense, int64_t dense_ld,
-                   cudaStream_t s) {
+                   const uint32_t* ids, int dim, int64_t b, Rec* ws, uint32_t* gk, float* dense,
+                   int64_t dense_ld, cudaStream_t s) {
     auto kern = k_score_tc<KMAX, kDense>;
     static bool attr_set = false;
     if (!attr_set) {
@@ -357,7 +369,7 @@ static bool launch(const TcPlan& p, const CUtensorMap* tq, const CUtensorMap* te
     }
     const int n_units = p.n_chunks * p.m_tiles;
     kern<<<p.grid, NUM_THREADS_TC, SMEM_BYTES, s>>>(*tq, *te, inv_e, ids, dim, b, p.m_tiles, p.n_tiles,
-                                                 p.chunk_tiles, n_units, ws, dense, dense_ld);
+                                                 p.chunk_tiles, n_units, ws, gk, dense, dense_ld);
     return cudaPeekAtLastError() == cudaSuccess;
 }
 
@@ -406,18 +418,18 @@ TcPlan tc_plan(int64_t b, int64_t n_slots, int sm_count) {
 }
 
 bool launch_score_tc(int kmax, const TcPlan& p, const void* tmap_q, const void* tmap_e, const float* inv_e,
-                     const uint32_t* ids, int dim, int64_t b, Rec* ws, cudaStream_t s) {
+                     const uint32_t* ids, int dim, int64_t b, Rec* ws, uint32_t* gk, cudaStream_t s) {
     const CUtensorMap* tq = static_cast<const CUtensorMap*>(tmap_q);
     const CUtensorMap* te = static_cast<const CUtensorMap*>(tmap_e);
-    if (kmax == 1) return tc::launch<1, false>(p, tq, te, inv_e, ids, dim, b, ws, nullptr, 0, s);
-    if (kmax == 4) return tc::launch<4, false>(p, tq, te, inv_e, ids, dim, b, ws, nullptr, 0, s);
-    return tc::launch<16, false>(p, tq, te, inv_e, ids, dim, b, ws, nullptr, 0, s);
+    if (kmax == 1) return tc::launch<1, false>(p, tq, te, inv_e, ids, dim, b, ws, gk, nullptr, 0, s);
+    if (kmax == 4) return tc::launch<4, false>(p, tq, te, inv_e, ids, dim, b, ws, gk, nullptr, 0, s);
+    return tc::launch<16, false>(p, tq, te, inv_e, ids, dim, b, ws, gk, nullptr, 0, s);
 }
 
 bool launch_score_tc_dense(const TcPlan& p, const void* tmap_q, const void* tmap_e, const float* inv_e, int dim,
                            int64_t b, float* dense, int64_t dense_ld, cudaStream_t s) {
     return tc::launch<1, true>(p, static_cast<const CUtensorMap*>(tmap_q), static_cast<const CUtensorMap*>(tmap_e),
-                               inv_e, nullptr, dim, b, nullptr, dense, dense_ld, s);
+                               inv_e, nullptr, dim, b, nullptr, nullptr, dense, dense_ld, s);
 }
 
 }  // namespace nv
