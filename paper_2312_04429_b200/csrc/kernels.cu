@@ -12,41 +12,29 @@
 namespace nv {
 
 // ---------------------------------------------------------------------------------------
-// Normalisation (reading R2).  One 128-thread CTA per row; dim <= 1024.  Thread t holds
-// elements t + 128k (k < 8) of the row zero-padded to P = next_pow2(dim).  The sum of
-// squares follows the oracle's tree exactly: stride s = P/2 ... 1, a[i] = a[i] + a[i+s],
-// so sum, sqrt and division (all correctly rounded fp64) and the direct fp64->bf16 RNE
-// conversion (cvt.rn.bf16.f64) give bit-identical stored rows.
+// Normalisation (reading R2).  One warp per row (8 rows per 256-thread CTA); dim <= 1024.
+// Lane l holds elements l + 32k (k < 32) of the row zero-padded to P = next_pow2(dim).
+// The sum of squares follows the oracle's halving tree exactly -- stride s = P/2 ... 1,
+// a[i] = a[i] + a[i+s]: strides >= 32 pair slots inside a lane, strides < 32 pair lanes
+// (shfl_down) -- so the sum, the correctly rounded fp64 sqrt and division and the direct
+// fp64->bf16 RNE conversion (cvt.rn.bf16.f64) give bit-identical stored rows.
 // ---------------------------------------------------------------------------------------
-__device__ __forceinline__ double tree_sum_128x8(double v[8], int P, double* red) {
-    const int t = threadIdx.x;
+__device__ __forceinline__ double warp_tree_sum(double (&v)[32], int P) {
 #pragma unroll
-    for (int s = 512; s >= 128; s >>= 1) {
+    for (int s = 512; s >= 32; s >>= 1) {
         if (s < P) {
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
-                if (128 * k < s) v[k] = __dadd_rn(v[k], v[k + s / 128]);
+            for (int k = 0; k < 16; ++k)
+                if (32 * k < s) v[k] = __dadd_rn(v[k], v[k + s / 32]);
         }
     }
-    red[t] = v[0];
-    __syncthreads();
-    for (int s = min(P / 2, 64); s >= 32; s >>= 1) {
-        if (t < s) red[t] = __dadd_rn(red[t], red[t + s]);
-        __syncthreads();
+    double r = v[0];
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+        const double o = __shfl_down_sync(0xFFFFFFFFu, r, s);
+        if (s < P) r = __dadd_rn(r, o);
     }
-    double r = 0.0;
-    if (t < 32) {
-        r = red[t];
-        for (int s = min(P / 2, 16); s >= 1; s >>= 1) {
-            double o = __shfl_down_sync(0xFFFFFFFFu, r, s);
-            r = __dadd_rn(r, o);
-        }
-    }
-    if (t == 0) red[0] = r;
-    __syncthreads();
-    r = red[0];
-    __syncthreads();
-    return r;
+    return __shfl_sync(0xFFFFFFFFu, r, 0);
 }
 
 template <typename Tin>
@@ -59,53 +47,50 @@ __device__ __forceinline__ double load_in<__nv_bfloat16>(const __nv_bfloat16* p)
 }
 
 template <typename Tin>
-__global__ void __launch_bounds__(128) k_normalise(const Tin* __restrict__ x, int64_t n, int dim,
-                                                   int P, __nv_bfloat16* __restrict__ y,
-                                                   float* __restrict__ inv,
-                                                   int32_t* __restrict__ status,
-                                                   uint32_t* __restrict__ gk) {
-    __shared__ double red[128];
-    const int64_t r = blockIdx.x;
-    if (r >= n) return;
-    if (gk != nullptr && threadIdx.x == 0) gk[r] = 0u;
-    const int t = threadIdx.x;
+__global__ void __launch_bounds__(256) k_normalise(const Tin* __restrict__ x, int64_t n, int dim, int P,
+                                                   __nv_bfloat16* __restrict__ y, float* __restrict__ inv,
+                                                   int32_t* __restrict__ status, uint32_t* __restrict__ gk) {
+    const int lane = threadIdx.x & 31;
+    const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (r >= n) return;   // warp-uniform
+    if (gk != nullptr && lane == 0) gk[r] = 0u;
     const Tin* xr = x + r * (int64_t)dim;
-    double xv[8], v[8];
+    __nv_bfloat16* yr = y + r * (int64_t)dim;
+    double v[32];
     int bad = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        const int i = t + 128 * k;
-        xv[k] = i < dim ? load_in<Tin>(xr + i) : 0.0;
-        bad |= !isfinite(xv[k]);
-        v[k] = __dmul_rn(xv[k], xv[k]);
+    for (int k = 0; k < 32; ++k) {
+        const int i = lane + 32 * k;
+        const double xv = i < dim ? load_in<Tin>(xr + i) : 0.0;
+        bad |= !isfinite(xv);
+        v[k] = __dmul_rn(xv, xv);
     }
-    bad = __syncthreads_or(bad);
-    int st = CACHE_ROW_OK;
+    bad = __any_sync(0xFFFFFFFFu, bad);
+    int st = CACHE_ROW_NONFINITE;
     double s = 0.0;
     if (!bad) {
-        s = tree_sum_128x8(v, P, red);
-        if (s == 0.0) st = CACHE_ROW_ZERO_NORM;
-        else if (!isfinite(s)) st = CACHE_ROW_NONFINITE;
-    } else {
-        st = CACHE_ROW_NONFINITE;
+        s = warp_tree_sum(v, P);
+        st = s == 0.0 ? CACHE_ROW_ZERO_NORM : (!isfinite(s) ? CACHE_ROW_NONFINITE : CACHE_ROW_OK);
     }
-    __nv_bfloat16* yr = y + r * (int64_t)dim;
     if (st != CACHE_ROW_OK) {
-        for (int i = t; i < dim; i += 128) yr[i] = __float2bfloat16_rn(0.0f);
-        if (t == 0) { inv[r] = __int_as_float(0x7FC00000); status[r] = st; }
+        for (int i = lane; i < dim; i += 32) yr[i] = __float2bfloat16_rn(0.0f);
+        if (lane == 0) { inv[r] = __int_as_float(0x7FC00000); status[r] = st; }
         return;
     }
     const double nu = __dsqrt_rn(s);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        const int i = t + 128 * k;
-        __nv_bfloat16 b = __double2bfloat16(__ddiv_rn(xv[k], nu));   // cvt.rn.bf16.f64
-        if (i < dim) yr[i] = b;
-        const double yd = i < dim ? (double)__bfloat162float(b) : 0.0;
+    for (int k = 0; k < 32; ++k) {
+        const int i = lane + 32 * k;
+        double yd = 0.0;
+        if (i < dim) {
+            const __nv_bfloat16 b = __double2bfloat16(__ddiv_rn(load_in<Tin>(xr + i), nu));  // cvt.rn.bf16.f64
+            yr[i] = b;
+            yd = (double)__bfloat162float(b);
+        }
         v[k] = __dmul_rn(yd, yd);
     }
-    const double s2 = tree_sum_128x8(v, P, red);
-    if (t == 0) {
+    const double s2 = warp_tree_sum(v, P);
+    if (lane == 0) {
         if (s2 == 0.0) {
             inv[r] = __int_as_float(0x7FC00000);
             status[r] = CACHE_ROW_ZERO_NORM;
@@ -121,11 +106,11 @@ void launch_normalise(const void* x, int dtype, int64_t n, int dim, __nv_bfloat1
     if (n <= 0) return;
     int P = 1;
     while (P < dim) P <<= 1;
+    const unsigned grid = (unsigned)((n + 7) / 8);
     if (dtype == CACHE_DTYPE_BF16)
-        k_normalise<__nv_bfloat16><<<(unsigned)n, 128, 0, s>>>((const __nv_bfloat16*)x, n, dim, P,
-                                                                 y, inv, status, gk);
+        k_normalise<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)x, n, dim, P, y, inv, status, gk);
     else
-        k_normalise<float><<<(unsigned)n, 128, 0, s>>>((const float*)x, n, dim, P, y, inv, status, gk);
+        k_normalise<float><<<grid, 256, 0, s>>>((const float*)x, n, dim, P, y, inv, status, gk);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -209,7 +194,7 @@ k_score_stream(const __nv_bfloat16* __restrict__ emb, const float* __restrict__ 
 #pragma unroll
         for (int b = 0; b < BQ; ++b)
             if (lane == b) mine = acc[b] * ie;
-        if (lane < BQ) tk.offer(mine, (uint32_t)row, ids);
+        if (lane < BQ && q0 + lane < b_total) tk.offer(mine, (uint32_t)row, ids);
     }
     if (lane < BQ) {
 #pragma unroll

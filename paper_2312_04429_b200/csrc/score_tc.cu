@@ -281,6 +281,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ C
                 const uint32_t g = *reinterpret_cast<volatile const uint32_t*>(gk + q);
                 if (g != 0u) tk.thr = key_to_f32((unsigned long long)g << 32);
             }
+            if (q >= B) tk.thr = INFINITY;   // padding rows of the last query tile: never offer
 #pragma unroll 1
             for (int n = n0; n < n1; ++n) {
                 // entry inv-norms of this tile -> smem (double-buffered by accumulator)
