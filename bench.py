@@ -233,10 +233,11 @@ def main():
     hbm, tflops, peak_src = _peaks()
     n = cfg["n"]
     sc_ms = statistics.mean(score_ms)
-    scorer_used = "tc" if (args.scorer == "tc" or (args.scorer == "auto" and b > 4)) else "stream"
+    scorer_used = "stream" if args.scorer == "stream" else "tc"
     flops = 2.0 * b * n * D
-    bytes_scan = n * (2 * D + 4)
-    if scorer_used == "tc":
+    bytes_scan = n * (2 * D + 4) + b * D * 2          # entry rows + inv-norms + the query tile
+    # the binding resource: tensor if flops / peak_tensor > bytes / peak_hbm (C2), else HBM (C3)
+    if scorer_used == "tc" and flops / (tflops * 1e12) >= bytes_scan / (hbm * 1e9):
         achieved = flops / (sc_ms / 1e3) / 1e12
         roof = dict(bound="tensor", achieved=achieved, peak=tflops, unit="TFLOP/s", frac=achieved / tflops)
     else:
@@ -245,7 +246,7 @@ def main():
     roof["kernel"] = f"score_{scorer_used}"
     roof["peak_source"] = peak_src
     roof["traffic"] = _ncu_traffic(scorer_used, args.config)
-    roof["algorithmic_per_launch"] = flops if scorer_used == "tc" else bytes_scan
+    roof["algorithmic_per_launch"] = flops if roof["bound"] == "tensor" else bytes_scan
     # end-to-end through the public host-buffer API (H2D queries + D2H results incl. latents)
     e2e = None
     if not args.no_e2e:

@@ -85,6 +85,10 @@ typedef struct {
     int32_t k_bias;           /* quality-vs-savings knob (R20): on a hit the
                                  bucket moves up by k_bias (clamped); 0 = Fig. 11 verbatim */
     int32_t max_topk;         /* largest topk a query may request (<= CACHE_MAX_TOPK)      */
+    int32_t shard_rank;       /* entry sharding over shard_world GPUs: every  */
+    int32_t shard_world;      /* rank receives the same insert batches; accepted rows get
+                                 global ids 0,1,2,... and rank r stores the rows with
+                                 id % shard_world == r.  Default 0 / 1 = unsharded.         */
 } cache_config;
 
 typedef struct {
@@ -94,7 +98,39 @@ typedef struct {
     int64_t entry_hwm;        /* high-water mark of entry slots (the scan length)          */
     uint64_t next_id;         /* id the next inserted entry receives                       */
     int64_t queries;          /* queries answered so far                                   */
+    int64_t free_entries;     /* free entry slots on this rank                              */
+    int64_t free_items;       /* free latent-pool slots on this rank                        */
 } cache_stats_t;
+
+/* One partial top-k record of a shard (16 bytes): the ranking key of an entry,
+ * key = orderable_f32(t) << 32 | (2^32 - 1 - id) with t = fl(<q~,x~> * inv_norm(x~)) (a larger
+ * key is a better candidate, 0 = none), the entry's slot and presence mask on its owner rank. */
+typedef struct {
+    uint64_t key;
+    uint32_t slot;
+    uint8_t present_mask;
+    uint8_t owner;
+    uint16_t reserved;
+} cache_shard_rec;
+
+/* Radix-select state of a (possibly distributed) LCBFU eviction; lives in device memory. */
+typedef struct {
+    uint64_t prefix;     /* selected high digits of the n-th smallest item key so far  */
+    uint64_t mask;       /* which digits of prefix are decided                         */
+    uint64_t remaining;  /* rank of the target key among keys matching prefix (1-based) */
+} cache_evict_state;
+
+/* What a rank shares with its peers so their merge kernels can read its latent pool and
+ * slot tables and count accesses on its counters directly over NVLink (P2P loads/atomics). */
+typedef struct {
+    int32_t device;
+    int32_t pid;
+    int32_t num_k;
+    int32_t reserved;
+    int64_t latent_bytes;
+    void *lslot, *fcnt, *pool;                     /* raw device pointers (same process)   */
+    unsigned char ipc_lslot[64], ipc_fcnt[64], ipc_pool[64]; /* cudaIpcMemHandle_t bytes */
+} cache_peer_desc;
 
 /* Fill *cfg with the paper's defaults: dim 768, K = {5,10,15,20,25}, Fig. 11
  * thresholds, k_bias 0, max_topk 16, latent_bytes 32768. Capacities are set to 0
@@ -167,6 +203,45 @@ cache_status cache_query_batch_host(cache_t *c, int64_t b, const void *queries, 
  * n > live items -> CACHE_E_EVICT_RANGE.  Synchronises `stream`. */
 cache_status cache_evict(cache_t *c, int64_t n, uint64_t *out_evicted, uint64_t *out_dirty_ids,
                          int64_t *out_n_dirty, void *stream);
+
+/* ---- distributed eviction building blocks (cache_evict = these three with no exchange) ----
+ * The n lowest LCBFU keys across all shards are found by an 8-pass MSB-first radix select
+ * over 8-bit digits of the 64-bit item key (R11).  Per pass: cache_evict_hist computes this
+ * rank's 256-bin histogram of keys matching st->prefix (hist: device, 256 u32, overwritten);
+ * the caller sums the histograms over ranks (e.g. an NCCL all-reduce); cache_evict_pick then
+ * fixes the pass's digit in st (identically on every rank).  st starts as {0, 0, n}.
+ * cache_evict_apply evicts this rank's items with key <= st->prefix (the n-th smallest key)
+ * and removes its dirty entries.  Outputs are host arrays of capacity `cap`: evicted items
+ * (id << 3 | j) in key order, removed entry ids ascending; counts in *out_n / *out_n_dirty.
+ * Synchronises `stream`. */
+cache_status cache_evict_hist(cache_t *c, const cache_evict_state *st, int32_t pass,
+                              uint32_t *hist, void *stream);
+cache_status cache_evict_pick(cache_t *c, uint32_t *hist, cache_evict_state *st, int32_t pass,
+                              void *stream);
+cache_status cache_evict_apply(cache_t *c, const cache_evict_state *st, int64_t cap,
+                               uint64_t *out_evicted, int64_t *out_n, uint64_t *out_dirty_ids,
+                               int64_t *out_n_dirty, void *stream);
+/* Live items on this rank (host-synchronous). */
+int64_t cache_live_items(const cache_t *c);
+
+/* ---- sharded lookup ----
+ * 1. every rank gathers the global batch of b queries (caller's all-gather);
+ * 2. cache_query_local: ingest + tcgen05 scan of this rank's shard + local top-k ->
+ *    out_recs (device, b x topk cache_shard_rec, owner = shard_rank);
+ * 3. the caller all-gathers the records of all ranks -> recs (device, world x b x topk);
+ * 4. cache_query_merge: for global rows [row0, row0 + nb) merge the world lists under the
+ *    total order (R3), apply Fig. 11 + holes, copy the winning state straight from the
+ *    owner's latent pool (P2P over NVLink) into latent_out and count the access on the
+ *    owner's counters (P2P atomics).  Outputs as in cache_query_batch, nb rows each.
+ * cache_attach_peers must have been called with every rank's cache_export_peer(). */
+cache_status cache_query_local(cache_t *c, int64_t b, const void *queries, int32_t q_dtype,
+                               int32_t topk, cache_shard_rec *out_recs, void *stream);
+cache_status cache_query_merge(cache_t *c, int64_t b, int64_t row0, int64_t nb, int32_t topk,
+                               const cache_shard_rec *recs, uint64_t *out_ids, float *out_scores,
+                               int32_t *out_k, void *latent_out, void **out_latent_ptr,
+                               int32_t *row_status, void *stream);
+cache_status cache_export_peer(cache_t *c, cache_peer_desc *out);
+cache_status cache_attach_peers(cache_t *c, int32_t world, const cache_peer_desc *descs);
 
 /* Counters: read the LCBFU access counts and presence mask of entry `id` (host outputs,
  * f has num_k slots).  Host-synchronous; intended for tests and maintenance tools. */

@@ -38,17 +38,31 @@ class CacheConfig(ctypes.Structure):
                 ("latent_capacity", ctypes.c_int64), ("latent_bytes", ctypes.c_int64),
                 ("num_k", ctypes.c_int32), ("k_values", ctypes.c_int32 * MAX_K),
                 ("thresholds", ctypes.c_double * MAX_K), ("k_bias", ctypes.c_int32),
-                ("max_topk", ctypes.c_int32)]
+                ("max_topk", ctypes.c_int32), ("shard_rank", ctypes.c_int32), ("shard_world", ctypes.c_int32)]
 
 
 class CacheStats(ctypes.Structure):
     _fields_ = [("live_entries", ctypes.c_int64), ("live_items", ctypes.c_int64), ("holes", ctypes.c_int64),
-                ("entry_hwm", ctypes.c_int64), ("next_id", ctypes.c_uint64), ("queries", ctypes.c_int64)]
+                ("entry_hwm", ctypes.c_int64), ("next_id", ctypes.c_uint64), ("queries", ctypes.c_int64),
+                ("free_entries", ctypes.c_int64), ("free_items", ctypes.c_int64)]
+
+
+class PeerDesc(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int32), ("pid", ctypes.c_int32), ("num_k", ctypes.c_int32),
+                ("reserved", ctypes.c_int32), ("latent_bytes", ctypes.c_int64), ("lslot", ctypes.c_void_p),
+                ("fcnt", ctypes.c_void_p), ("pool", ctypes.c_void_p), ("ipc_lslot", ctypes.c_ubyte * 64),
+                ("ipc_fcnt", ctypes.c_ubyte * 64), ("ipc_pool", ctypes.c_ubyte * 64)]
+
+
+SHARD_REC_BYTES = 16   # cache_shard_rec
+EVICT_STATE_BYTES = 24  # cache_evict_state
 
 
 EXPORTS = ("cache_default_config", "cache_create", "cache_destroy", "cache_insert", "cache_query_batch",
            "cache_query_batch_host", "cache_evict", "cache_get_meta", "cache_get_row", "cache_stats",
-           "cache_set_scorer", "cache_set_profile_events", "cache_kernel_launches", "cache_last_error")
+           "cache_set_scorer", "cache_set_profile_events", "cache_kernel_launches", "cache_last_error",
+           "cache_evict_hist", "cache_evict_pick", "cache_evict_apply", "cache_live_items", "cache_query_local",
+           "cache_query_merge", "cache_export_peer", "cache_attach_peers")
 
 
 def load_library(path: str = LIB_PATH):
@@ -69,6 +83,18 @@ def load_library(path: str = LIB_PATH):
     L.cache_stats.argtypes = [P, ctypes.POINTER(CacheStats)]
     L.cache_set_scorer.argtypes = [P, I32]
     L.cache_set_profile_events.argtypes = [P, P]
+    L.cache_evict_hist.argtypes = [P, P, I32, P, P]
+    L.cache_evict_pick.argtypes = [P, P, P, I32, P]
+    L.cache_evict_apply.argtypes = [P, P, I64, P, P, P, P, P]
+    L.cache_live_items.argtypes = [P]
+    L.cache_live_items.restype = I64
+    L.cache_query_local.argtypes = [P, I64, P, I32, I32, P, P]
+    L.cache_query_merge.argtypes = [P, I64, I64, I64, I32, P, P, P, P, P, P, P, P]
+    L.cache_export_peer.argtypes = [P, ctypes.POINTER(PeerDesc)]
+    L.cache_attach_peers.argtypes = [P, I32, P]
+    for fn in ("cache_evict_hist", "cache_evict_pick", "cache_evict_apply", "cache_query_local",
+               "cache_query_merge", "cache_export_peer", "cache_attach_peers"):
+        getattr(L, fn).restype = ctypes.c_int
     L.cache_kernel_launches.argtypes = [P]
     L.cache_kernel_launches.restype = I64
     L.cache_last_error.restype = ctypes.c_char_p
@@ -126,7 +152,7 @@ class NirvanaCache:
     def __init__(self, entry_capacity: int, latent_capacity: int | None = None, dim: int = 768,
                  latent_bytes: int = 32768, k_values=(5, 10, 15, 20, 25),
                  thresholds=(0.65, 0.75, 0.85, 0.90, 0.95), k_bias: int = 0, max_topk: int = MAX_TOPK,
-                 device: int | None = None):
+                 device: int | None = None, shard_rank: int = 0, shard_world: int = 1):
         if device is None:
             device = torch.cuda.current_device()
         self.device = device
@@ -134,7 +160,9 @@ class NirvanaCache:
             latent_capacity = entry_capacity * len(k_values)
         self.cfg = default_config(dim=dim, entry_capacity=entry_capacity, latent_capacity=latent_capacity,
                                   latent_bytes=latent_bytes, k_values=tuple(k_values),
-                                  thresholds=tuple(thresholds), k_bias=k_bias, max_topk=max_topk)
+                                  thresholds=tuple(thresholds), k_bias=k_bias, max_topk=max_topk,
+                                  shard_rank=shard_rank, shard_world=shard_world)
+        self.shard_rank, self.shard_world = shard_rank, shard_world
         self.dim, self.latent_bytes, self.num_k = dim, latent_bytes, len(k_values)
         self.k_values = tuple(k_values)
         h = ctypes.c_void_p()
@@ -237,6 +265,49 @@ class NirvanaCache:
 
     def set_scorer(self, scorer: int):
         _check(_lib.cache_set_scorer(self._h, scorer))
+
+    # ------------------------- sharded-path building blocks --------------------------
+    def query_local(self, q: torch.Tensor, topk: int, out_recs: torch.Tensor, stream=None):
+        """Ingest + scan of this shard for the global batch q -> out_recs [b][topk] records
+        (a uint8 tensor of b*topk*16 bytes)."""
+        dt = DTYPE_BF16 if q.dtype == torch.bfloat16 else DTYPE_F32
+        _check(_lib.cache_query_local(self._h, q.shape[0], _ptr(q), dt, topk, _ptr(out_recs), _stream(stream)))
+        return out_recs
+
+    def query_merge(self, b: int, row0: int, nb: int, topk: int, recs_all: torch.Tensor, out: dict, stream=None):
+        """Merge the world x b x topk records for global rows [row0, row0+nb) into out."""
+        _check(_lib.cache_query_merge(self._h, b, row0, nb, topk, _ptr(recs_all), _ptr(out["ids"]),
+                                      _ptr(out["scores"]), _ptr(out["k"]), _ptr(out.get("latents")),
+                                      _ptr(out.get("ptrs")), _ptr(out.get("status")), _stream(stream)))
+        return out
+
+    def export_peer(self) -> PeerDesc:
+        d = PeerDesc()
+        _check(_lib.cache_export_peer(self._h, ctypes.byref(d)))
+        return d
+
+    def attach_peers(self, descs):
+        arr = (PeerDesc * len(descs))(*descs)
+        _check(_lib.cache_attach_peers(self._h, len(descs), arr))
+
+    def evict_hist(self, state: torch.Tensor, pass_: int, hist: torch.Tensor, stream=None):
+        _check(_lib.cache_evict_hist(self._h, _ptr(state), pass_, _ptr(hist), _stream(stream)))
+
+    def evict_pick(self, hist: torch.Tensor, state: torch.Tensor, pass_: int, stream=None):
+        _check(_lib.cache_evict_pick(self._h, _ptr(hist), _ptr(state), pass_, _stream(stream)))
+
+    def evict_apply(self, state: torch.Tensor, cap: int, stream=None):
+        ev = np.empty(max(cap, 1), dtype=np.uint64)
+        dirty = np.empty(max(cap, 1), dtype=np.uint64)
+        n = np.zeros(1, dtype=np.int64)
+        nd = np.zeros(1, dtype=np.int64)
+        _check(_lib.cache_evict_apply(self._h, _ptr(state), cap, _ptr(ev), _ptr(n), _ptr(dirty), _ptr(nd),
+                                      _stream(stream)))
+        return ev[: int(n[0])].copy(), dirty[: int(nd[0])].copy()
+
+    @property
+    def live_items(self) -> int:
+        return _lib.cache_live_items(self._h)
 
     def set_profile_events(self, events):
         """events: 4 torch.cuda.Event(enable_timing=True) (recorded around ingest / score /

@@ -12,6 +12,8 @@
 #include <unordered_map>
 #include <vector>
 
+#include <unistd.h>
+
 #include "kernels.h"
 
 using namespace nv;
@@ -136,6 +138,11 @@ struct cache_t {
     DevBuf<unsigned long long> ekey, ecnt;
     DevBuf<int32_t> elslot;
     DevBuf<int64_t> edirty;
+    // sharding
+    int rank = 0, world = 1;
+    PeerPtrs peers{};
+    bool peers_ok = false;
+    std::vector<void*> ipc_opened;   // peer allocations opened through CUDA IPC
 };
 
 extern "C" {
@@ -153,6 +160,8 @@ void cache_default_config(cache_config* cfg) {
     for (int j = 0; j < 5; ++j) { cfg->k_values[j] = kv[j]; cfg->thresholds[j] = th[j]; }
     cfg->k_bias = 0;
     cfg->max_topk = CACHE_MAX_TOPK;
+    cfg->shard_rank = 0;
+    cfg->shard_world = 1;
 }
 
 cache_status cache_create(const cache_config* cfg, int device, cache_t** out) {
@@ -171,6 +180,9 @@ cache_status cache_create(const cache_config* cfg, int device, cache_t** out) {
         if (cfg->k_values[j] <= cfg->k_values[j - 1] || !(cfg->thresholds[j] >= cfg->thresholds[j - 1]))
             return fail(CACHE_E_INVALID_ARG,
                         "cache_create: K values must increase and thresholds must not decrease (R6)");
+    if (cfg->shard_world < 1 || cfg->shard_world > kMaxWorld || cfg->shard_rank < 0 ||
+        cfg->shard_rank >= cfg->shard_world)
+        return fail(CACHE_E_INVALID_ARG, "cache_create: bad shard_rank / shard_world (world <= 16)");
     int ndev = 0;
     CK(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev) return fail(CACHE_E_INVALID_ARG, "cache_create: bad device");
@@ -187,6 +199,8 @@ cache_status cache_create(const cache_config* cfg, int device, cache_t** out) {
     for (int j = 0; j < c->num_k; ++j) { c->km.thr[j] = cfg->thresholds[j]; c->km.kv[j] = cfg->k_values[j]; }
     c->km.num_k = c->num_k;
     c->km.k_bias = cfg->k_bias;
+    c->rank = cfg->shard_rank;
+    c->world = cfg->shard_world;
     cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
     auto bail = [&](cudaError_t e, const char* what) {
         cache_destroy(c);
@@ -225,6 +239,7 @@ cache_status cache_destroy(cache_t* c) {
     if (!c) return CACHE_OK;
     DeviceGuard g(c->device);
     cudaDeviceSynchronize();
+    for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
     cudaFree(c->emb); cudaFree(c->inv_e); cudaFree(c->ids); cudaFree(c->present);
     cudaFree(c->lslot); cudaFree(c->fcnt); cudaFree(c->pool);
     c->qbuf.release(); c->ystage.release(); c->invq.release(); c->invstage.release();
@@ -264,13 +279,19 @@ cache_status cache_insert(cache_t* c, int64_t n, const void* emb, int32_t emb_dt
         CK(cudaMemcpyAsync(st.data() + off, c->istat.p, m * 4, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
     }
+    // Accepted rows get consecutive global ids; with sharding this rank keeps id % world == rank.
+    int64_t n_accepted = 0;
     for (int64_t r = 0; r < n; ++r) {
         if (st[r] == CACHE_ROW_OK && (masks[r] & full) == 0) st[r] = CACHE_ROW_NO_ITEMS;
-        if (st[r] == CACHE_ROW_OK) { n_valid++; n_items += __builtin_popcount(masks[r] & full); }
+        if (st[r] != CACHE_ROW_OK) continue;
+        const uint64_t id = c->next_id + n_accepted++;
+        if ((int64_t)(id % (uint64_t)c->world) != c->rank) continue;
+        n_valid++;
+        n_items += __builtin_popcount(masks[r] & full);
     }
     if (n_valid > (int64_t)c->free_e.size() || n_items > (int64_t)c->free_l.size())
         return fail(CACHE_E_FULL, "cache_insert: insufficient entry or latent capacity (evict first)");
-    if ((uint64_t)c->next_id + n_valid > 0xFFFFFFFFull)
+    if ((uint64_t)c->next_id + n_accepted > 0xFFFFFFFFull)
         return fail(CACHE_E_STATE, "cache_insert: 32-bit id space exhausted");
     std::vector<InsertPlan> plan;
     std::vector<CopyPlan> cp;
@@ -290,10 +311,12 @@ cache_status cache_insert(cache_t* c, int64_t n, const void* emb, int32_t emb_dt
                 continue;
             }
             InsertPlan p;
+            p.id = (uint32_t)c->next_id++;
+            if (out_ids) out_ids[gr] = p.id;
+            if ((int64_t)(p.id % (uint32_t)c->world) != c->rank) continue;   // another shard's row
             p.src_row = r;
             p.slot = c->free_e.back();
             c->free_e.pop_back();
-            p.id = (uint32_t)c->next_id++;
             p.mask = masks[gr] & full;
             for (int j = 0; j < CACHE_MAX_K; ++j) p.lslot[j] = -1;
             for (int j = 0; j < c->num_k; ++j) {
@@ -310,7 +333,6 @@ cache_status cache_insert(cache_t* c, int64_t n, const void* emb, int32_t emb_dt
             c->hwm = std::max(c->hwm, p.slot + 1);
             c->live_entries++;
             c->live_items += __builtin_popcount(p.mask);
-            if (out_ids) out_ids[gr] = p.id;
         }
         CK(c->iplan.ensure(std::max<size_t>(plan.size(), 1)));
         CK(cudaMemcpyAsync(c->iplan.p, plan.data(), plan.size() * sizeof(InsertPlan), cudaMemcpyHostToDevice, s));
@@ -327,13 +349,13 @@ cache_status cache_insert(cache_t* c, int64_t n, const void* emb, int32_t emb_dt
         CK(cudaGetLastError());
     }
     if (row_status) std::memcpy(row_status, st.data(), n * 4);
-    return n_valid == n ? CACHE_OK : fail(CACHE_E_BAD_ROWS, "cache_insert: some rows rejected (row_status)");
+    return n_accepted == n ? CACHE_OK : fail(CACHE_E_BAD_ROWS, "cache_insert: some rows rejected (row_status)");
 }
 
-static cache_status query_core(cache_t* c, int64_t b, const void* queries, int32_t q_dtype, int32_t topk,
-                               uint64_t* out_ids, float* out_scores, int32_t* out_k, void* latent_out,
-                               void** out_ptr, int32_t* row_status, cudaStream_t s) {
-    const int kmax = topk == 1 ? 1 : (topk <= 4 ? 4 : 16);
+// Query ingest + scan of this cache's entries: partial top-k record lists in c->recs
+// ([parts][b][kmax]); *parts_out = number of lists per query (0 for an empty cache).
+static cache_status scan_core(cache_t* c, int64_t b, const void* queries, int32_t q_dtype, int kmax,
+                              cudaStream_t s, int* parts_out) {
     const int64_t bpad = (b + 127) / 128 * 128;
     CK(c->qbuf.ensure((size_t)bpad * c->dim));
     CK(c->invq.ensure(bpad));
@@ -349,7 +371,9 @@ static cache_status query_core(cache_t* c, int64_t b, const void* queries, int32
         bool use_tc = false;
         TcPlan tp{};
         if (c->scorer != CACHE_SCORER_STREAM && c->tm_e_ok && tc_supported(c->dim)) {
-            use_tc = c->scorer == CACHE_SCORER_TC || b > 4;
+            // measured (round 1): the tcgen05 scan is at 97-98% of HBM bandwidth for every
+            // b <= 128 on 1M entries and tensor-bound above, so AUTO always takes it
+            use_tc = true;
         }
         if (c->scorer == CACHE_SCORER_TC && !use_tc)
             return fail(CACHE_E_UNSUPPORTED, "query: tensor-core scorer unavailable for this configuration");
@@ -374,6 +398,17 @@ static cache_status query_core(cache_t* c, int64_t b, const void* queries, int32
         }
     }
     if (c->prof_on && !prof1) CK(cudaEventRecord(c->prof[1], s));
+    *parts_out = parts;
+    return CACHE_OK;
+}
+
+static cache_status query_core(cache_t* c, int64_t b, const void* queries, int32_t q_dtype, int32_t topk,
+                               uint64_t* out_ids, float* out_scores, int32_t* out_k, void* latent_out,
+                               void** out_ptr, int32_t* row_status, cudaStream_t s) {
+    const int kmax = topk == 1 ? 1 : (topk <= 4 ? 4 : 16);
+    int parts = 0;
+    cache_status r = scan_core(c, b, queries, q_dtype, kmax, s, &parts);
+    if (r != CACHE_OK) return r;
     if (c->prof_on) CK(cudaEventRecord(c->prof[2], s));
     launch_finalize(kmax, c->recs.p, parts, b, topk, c->invq.p, c->qstat.p, c->ids, c->present, c->lslot,
                     c->fcnt, c->pool, c->L, c->km, out_ids, out_scores, out_k, (uint8_t*)latent_out, out_ptr,
@@ -399,6 +434,108 @@ cache_status cache_query_batch(cache_t* c, int64_t b, const void* queries, int32
     DeviceGuard g(c->device);
     return query_core(c, b, queries, q_dtype, topk, out_ids, out_scores, out_k, latent_out, out_latent_ptr,
                       row_status, (cudaStream_t)stream);
+}
+
+cache_status cache_query_local(cache_t* c, int64_t b, const void* queries, int32_t q_dtype, int32_t topk,
+                               cache_shard_rec* out_recs, void* stream) {
+    if (!c) return fail(CACHE_E_INVALID_ARG, "cache_query_local: null cache");
+    if (b < 0 || b > 0x7FFFFFFF || topk < 1 || topk > c->cfg.max_topk ||
+        (q_dtype != CACHE_DTYPE_F32 && q_dtype != CACHE_DTYPE_BF16))
+        return fail(CACHE_E_INVALID_ARG, "cache_query_local: bad b / topk / dtype");
+    if (b == 0) return CACHE_OK;
+    if (!queries || !out_recs) return fail(CACHE_E_INVALID_ARG, "cache_query_local: null buffer");
+    DeviceGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int kmax = topk == 1 ? 1 : (topk <= 4 ? 4 : 16);
+    int parts = 0;
+    cache_status r = scan_core(c, b, queries, q_dtype, kmax, s, &parts);
+    if (r != CACHE_OK) return r;
+    launch_local_merge(kmax, c->recs.p, parts, b, topk, c->qstat.p, c->present, c->rank, out_recs, s);
+    c->launches++;
+    CK(cudaGetLastError());
+    return CACHE_OK;
+}
+
+cache_status cache_query_merge(cache_t* c, int64_t b, int64_t row0, int64_t nb, int32_t topk,
+                               const cache_shard_rec* recs, uint64_t* out_ids, float* out_scores, int32_t* out_k,
+                               void* latent_out, void** out_latent_ptr, int32_t* row_status, void* stream) {
+    if (!c) return fail(CACHE_E_INVALID_ARG, "cache_query_merge: null cache");
+    if (b < 0 || row0 < 0 || nb < 0 || row0 + nb > b || topk < 1 || topk > c->cfg.max_topk)
+        return fail(CACHE_E_INVALID_ARG, "cache_query_merge: bad b / row range / topk");
+    if (nb == 0) return CACHE_OK;
+    if (!recs || !out_ids || !out_scores || !out_k) return fail(CACHE_E_INVALID_ARG, "cache_query_merge: null buffer");
+    if (!c->peers_ok) return fail(CACHE_E_STATE, "cache_query_merge: cache_attach_peers not called");
+    if (c->qstat.n < (size_t)b) return fail(CACHE_E_STATE, "cache_query_merge: no matching cache_query_local batch");
+    DeviceGuard g(c->device);
+    const int kmax = topk == 1 ? 1 : (topk <= 4 ? 4 : 16);
+    launch_merge_sharded(kmax, recs, c->world, b, row0, nb, topk, c->invq.p, c->qstat.p, c->peers, c->L, c->km,
+                         out_ids, out_scores, out_k, (uint8_t*)latent_out, out_latent_ptr, row_status,
+                         (cudaStream_t)stream);
+    c->launches++;
+    CK(cudaGetLastError());
+    c->queries += nb;
+    return CACHE_OK;
+}
+
+cache_status cache_export_peer(cache_t* c, cache_peer_desc* out) {
+    if (!c || !out) return fail(CACHE_E_INVALID_ARG, "cache_export_peer: null argument");
+    DeviceGuard g(c->device);
+    std::memset(out, 0, sizeof(*out));
+    out->device = c->device;
+    out->pid = (int32_t)getpid();
+    out->num_k = c->num_k;
+    out->latent_bytes = c->L;
+    out->lslot = c->lslot;
+    out->fcnt = c->fcnt;
+    out->pool = c->pool;
+    cudaIpcMemHandle_t h;
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    CK(cudaIpcGetMemHandle(&h, c->lslot));
+    std::memcpy(out->ipc_lslot, &h, 64);
+    CK(cudaIpcGetMemHandle(&h, c->fcnt));
+    std::memcpy(out->ipc_fcnt, &h, 64);
+    if (c->pool) {
+        CK(cudaIpcGetMemHandle(&h, c->pool));
+        std::memcpy(out->ipc_pool, &h, 64);
+    }
+    return CACHE_OK;
+}
+
+cache_status cache_attach_peers(cache_t* c, int32_t world, const cache_peer_desc* descs) {
+    if (!c || !descs || world != c->world) return fail(CACHE_E_INVALID_ARG, "cache_attach_peers: bad argument");
+    DeviceGuard g(c->device);
+    const int32_t me = (int32_t)getpid();
+    PeerPtrs p{};
+    for (int r = 0; r < world; ++r) {
+        const cache_peer_desc& d = descs[r];
+        if (d.num_k != c->num_k || d.latent_bytes != c->L)
+            return fail(CACHE_E_INVALID_ARG, "cache_attach_peers: peer configuration differs");
+        if (d.pid == me) {   // same process (own rank, or virtual ranks sharing one GPU)
+            p.lslot[r] = (const int32_t*)d.lslot;
+            p.fcnt[r] = (uint32_t*)d.fcnt;
+            p.pool[r] = (const uint8_t*)d.pool;
+            continue;
+        }
+        void* ptr = nullptr;
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, d.ipc_lslot, 64);
+        CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+        c->ipc_opened.push_back(ptr);
+        p.lslot[r] = (const int32_t*)ptr;
+        std::memcpy(&h, d.ipc_fcnt, 64);
+        CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+        c->ipc_opened.push_back(ptr);
+        p.fcnt[r] = (uint32_t*)ptr;
+        if (d.pool) {
+            std::memcpy(&h, d.ipc_pool, 64);
+            CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+            c->ipc_opened.push_back(ptr);
+            p.pool[r] = (const uint8_t*)ptr;
+        }
+    }
+    c->peers = p;
+    c->peers_ok = true;
+    return CACHE_OK;
 }
 
 cache_status cache_query_batch_host(cache_t* c, int64_t b, const void* queries, int32_t q_dtype, int32_t topk,
@@ -434,6 +571,30 @@ cache_status cache_query_batch_host(cache_t* c, int64_t b, const void* queries, 
     return CACHE_OK;
 }
 
+cache_status cache_evict_hist(cache_t* c, const cache_evict_state* st, int32_t pass, uint32_t* hist,
+                              void* stream) {
+    if (!c || !st || !hist || pass < 0 || pass > 7) return fail(CACHE_E_INVALID_ARG, "cache_evict_hist: bad argument");
+    DeviceGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    CK(cudaMemsetAsync(hist, 0, 256 * 4, s));
+    launch_evict_hist(c->present, c->fcnt, c->ids, c->hwm, c->km, reinterpret_cast<const EvictState*>(st), pass,
+                      hist, s);
+    c->launches++;
+    CK(cudaGetLastError());
+    return CACHE_OK;
+}
+
+cache_status cache_evict_pick(cache_t* c, uint32_t* hist, cache_evict_state* st, int32_t pass, void* stream) {
+    if (!c || !st || !hist || pass < 0 || pass > 7) return fail(CACHE_E_INVALID_ARG, "cache_evict_pick: bad argument");
+    DeviceGuard g(c->device);
+    launch_evict_pick(hist, reinterpret_cast<EvictState*>(st), pass, (cudaStream_t)stream);
+    c->launches++;
+    CK(cudaGetLastError());
+    return CACHE_OK;
+}
+
+int64_t cache_live_items(const cache_t* c) { return c ? c->live_items : 0; }
+
 cache_status cache_evict(cache_t* c, int64_t n, uint64_t* out_evicted, uint64_t* out_dirty_ids,
                          int64_t* out_n_dirty, void* stream) {
     if (!c) return fail(CACHE_E_INVALID_ARG, "cache_evict: null cache");
@@ -445,24 +606,42 @@ cache_status cache_evict(cache_t* c, int64_t n, uint64_t* out_evicted, uint64_t*
     cudaStream_t s = (cudaStream_t)stream;
     CK(c->est.ensure(1));
     CK(c->ehist.ensure(256));
-    CK(c->ekey.ensure(n));
-    CK(c->elslot.ensure(n));
-    CK(c->ecnt.ensure(2));
-    CK(c->edirty.ensure(n));
     EvictState st0{0ull, 0ull, (unsigned long long)n};
     CK(cudaMemcpyAsync(c->est.p, &st0, sizeof(st0), cudaMemcpyHostToDevice, s));
-    CK(cudaMemsetAsync(c->ehist.p, 0, 256 * 4, s));
+    cache_evict_state* st = reinterpret_cast<cache_evict_state*>(c->est.p);
+    for (int pass = 0; pass < 8; ++pass) {
+        cache_status r = cache_evict_hist(c, st, pass, c->ehist.p, stream);
+        if (r != CACHE_OK) return r;
+        if ((r = cache_evict_pick(c, c->ehist.p, st, pass, stream)) != CACHE_OK) return r;
+    }
+    int64_t got = 0;
+    cache_status r = cache_evict_apply(c, st, n, out_evicted, &got, out_dirty_ids, out_n_dirty, stream);
+    if (r != CACHE_OK) return r;
+    if (got != n) return fail(CACHE_E_STATE, "cache_evict: selection count mismatch (internal error)");
+    return CACHE_OK;
+}
+
+cache_status cache_evict_apply(cache_t* c, const cache_evict_state* st, int64_t cap, uint64_t* out_evicted,
+                               int64_t* out_n, uint64_t* out_dirty_ids, int64_t* out_n_dirty, void* stream) {
+    if (!c || !st || cap < 0) return fail(CACHE_E_INVALID_ARG, "cache_evict_apply: bad argument");
+    DeviceGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t bound = std::max<int64_t>(1, c->live_items);
+    CK(c->ekey.ensure(bound));
+    CK(c->elslot.ensure(bound));
+    CK(c->ecnt.ensure(2));
+    CK(c->edirty.ensure(std::max<int64_t>(1, c->live_entries)));
     CK(cudaMemsetAsync(c->ecnt.p, 0, 16, s));
-    launch_evict_select(c->present, c->fcnt, c->ids, c->hwm, c->km, c->est.p, c->ehist.p, s);
-    c->launches += 16;
-    launch_evict_apply(c->present, c->fcnt, c->ids, c->lslot, c->inv_e, c->hwm, c->km, c->est.p, c->ekey.p,
-                       c->elslot.p, c->ecnt.p, c->edirty.p, s);
+    launch_evict_apply(c->present, c->fcnt, c->ids, c->lslot, c->inv_e, c->hwm, c->km,
+                       reinterpret_cast<const EvictState*>(st), c->ekey.p, c->elslot.p, c->ecnt.p, c->edirty.p, s);
     c->launches++;
     unsigned long long cnt[2];
     CK(cudaMemcpyAsync(cnt, c->ecnt.p, 16, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    if ((int64_t)cnt[0] != n || (int64_t)cnt[1] > n)
-        return fail(CACHE_E_STATE, "cache_evict: selection count mismatch (internal error)");
+    const int64_t n = (int64_t)cnt[0];
+    if (out_n) *out_n = n;
+    if (n > cap || (int64_t)cnt[1] > cap)
+        return fail(CACHE_E_STATE, "cache_evict_apply: more evictions than the output capacity");
     std::vector<unsigned long long> keys(n);
     std::vector<int32_t> ls(n);
     std::vector<int64_t> dslots(cnt[1]);
@@ -542,6 +721,8 @@ cache_status cache_stats(cache_t* c, cache_stats_t* out) {
     out->entry_hwm = c->hwm;
     out->next_id = c->next_id;
     out->queries = c->queries;
+    out->free_entries = (int64_t)c->free_e.size();
+    out->free_items = (int64_t)c->free_l.size();
     return CACHE_OK;
 }
 

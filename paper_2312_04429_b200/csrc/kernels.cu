@@ -504,14 +504,187 @@ k_evict_apply(uint32_t* __restrict__ present, uint32_t* __restrict__ fcnt, const
     }
 }
 
-void launch_evict_select(const uint32_t* present, const uint32_t* fcnt, const uint32_t* ids,
-                         int64_t n_slots, const KMap& km, EvictState* st, unsigned int* hist, cudaStream_t s) {
+void launch_evict_hist(const uint32_t* present, const uint32_t* fcnt, const uint32_t* ids, int64_t n_slots,
+                       const KMap& km, const EvictState* st, int pass, unsigned int* hist, cudaStream_t s) {
     const int grid = (int)std::min<int64_t>(148 * 8, (n_slots + 255) / 256 + 1);
-    for (int pass = 0; pass < 8; ++pass) {
-        const int shift = 56 - 8 * pass;
-        k_evict_hist<<<grid, 256, 0, s>>>(present, fcnt, ids, n_slots, km, st, shift, hist);
-        k_evict_pick<<<1, 256, 0, s>>>(hist, st, shift);
+    k_evict_hist<<<grid, 256, 0, s>>>(present, fcnt, ids, n_slots, km, st, 56 - 8 * pass, hist);
+}
+
+void launch_evict_pick(unsigned int* hist, EvictState* st, int pass, cudaStream_t s) {
+    k_evict_pick<<<1, 256, 0, s>>>(hist, st, 56 - 8 * pass);
+}
+
+// ---------------------------------------------------------------------------------------
+// Sharded lookup.
+// k_local_merge: one warp per query merges the scorer's partial lists of this shard into
+// one top-k list of 16-byte shard records (key, slot, presence mask, owner rank).
+// k_merge_sharded: one CTA per local query merges the world lists, applies Fig. 11 + the
+// hole rule with the record's presence mask, then reads the winner's latent-slot table
+// entry and the 32 KiB state directly from the OWNER's memory (peer pointers over NVLink,
+// or local pointers for the own rank) and counts the access with an atomic on the owner's
+// counter -- the fetch is fused into the merge kernel, no second collective.
+// ---------------------------------------------------------------------------------------
+template <int KMAX>
+__global__ void __launch_bounds__(256)
+k_local_merge(const Rec* __restrict__ ws, int parts, int64_t B, int topk, const int32_t* __restrict__ qstatus,
+              const uint32_t* __restrict__ present, int owner, cache_shard_rec* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t b = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (b >= B) return;
+    TopK<KMAX> tk;
+    tk.init();
+    if (qstatus[b] == CACHE_ROW_OK) {
+        for (int p = lane; p < parts; p += 32) {
+            const Rec* r = ws + ((int64_t)p * B + b) * KMAX;
+            for (int i = 0; i < topk; ++i) {
+                const Rec rr = r[i];
+                if (rr.key == 0ull) break;
+                tk.offer_key(rr.key, rr.slot);
+            }
+        }
     }
+    for (int i = 0; i < topk; ++i) {
+        const unsigned long long m = warp_max_u64(tk.k[0]);
+        if (m != 0ull && tk.k[0] == m) {
+            cache_shard_rec o;
+            o.key = m;
+            o.slot = tk.s[0];
+            o.present_mask = (uint8_t)(present[tk.s[0]] & 0xFFu);
+            o.owner = (uint8_t)owner;
+            o.reserved = 0;
+            out[b * topk + i] = o;
+            tk.pop();
+        }
+        if (m == 0ull && lane == 0) {
+            cache_shard_rec o{};
+            out[b * topk + i] = o;
+        }
+    }
+}
+
+void launch_local_merge(int kmax, const Rec* ws, int parts, int64_t B, int topk, const int32_t* qstatus,
+                        const uint32_t* present, int owner, cache_shard_rec* out, cudaStream_t s) {
+    if (B <= 0) return;
+    const unsigned grid = (unsigned)((B + 7) / 8);
+    if (kmax == 1) k_local_merge<1><<<grid, 256, 0, s>>>(ws, parts, B, topk, qstatus, present, owner, out);
+    else if (kmax == 4) k_local_merge<4><<<grid, 256, 0, s>>>(ws, parts, B, topk, qstatus, present, owner, out);
+    else k_local_merge<16><<<grid, 256, 0, s>>>(ws, parts, B, topk, qstatus, present, owner, out);
+}
+
+template <int KMAX>
+__global__ void __launch_bounds__(128)
+k_merge_sharded(const cache_shard_rec* __restrict__ recs, int world, int64_t B, int64_t row0, int topk,
+                const float* __restrict__ inv_q, const int32_t* __restrict__ qstatus, PeerPtrs peers,
+                int64_t latent_bytes, KMap km, uint64_t* __restrict__ out_ids, float* __restrict__ out_scores,
+                int32_t* __restrict__ out_k, uint8_t* __restrict__ latent_out, void** __restrict__ out_ptr,
+                int32_t* __restrict__ out_status) {
+    __shared__ unsigned long long s_key[KMAX];
+    __shared__ uint32_t s_slot[KMAX];
+    __shared__ long long s_src;
+    __shared__ int s_owner;
+    const int64_t i = blockIdx.x;          // local output row
+    const int64_t g = row0 + i;            // global query row
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int st = qstatus[g];
+    if (warp == 0) {
+        // candidate = (key, slot, owner << 8 | mask) -- keys are unique across shards (ids are)
+        unsigned long long ck[KMAX];
+        uint32_t cs[KMAX], cm[KMAX];
+#pragma unroll
+        for (int t = 0; t < KMAX; ++t) { ck[t] = 0ull; cs[t] = 0u; cm[t] = 0u; }
+        if (st == CACHE_ROW_OK) {
+            for (int idx = lane; idx < world * topk; idx += 32) {
+                const int r = idx / topk, t = idx - r * topk;
+                const cache_shard_rec rec = recs[((int64_t)r * B + g) * topk + t];
+                if (rec.key == 0ull || rec.key <= ck[KMAX - 1]) continue;
+                const uint32_t meta = ((uint32_t)rec.owner << 8) | rec.present_mask;
+#pragma unroll
+                for (int u = KMAX - 1; u > 0; --u) {
+                    if (rec.key > ck[u - 1]) { ck[u] = ck[u - 1]; cs[u] = cs[u - 1]; cm[u] = cm[u - 1]; }
+                    else if (rec.key > ck[u]) { ck[u] = rec.key; cs[u] = rec.slot; cm[u] = meta; }
+                }
+                if (rec.key > ck[0]) { ck[0] = rec.key; cs[0] = rec.slot; cm[0] = meta; }
+            }
+        }
+        __shared__ uint32_t s_meta0;
+        for (int t = 0; t < topk; ++t) {
+            const unsigned long long m = warp_max_u64(ck[0]);
+            if (m != 0ull && ck[0] == m) {
+                s_key[t] = m;
+                s_slot[t] = cs[0];
+                if (t == 0) s_meta0 = cm[0];
+#pragma unroll
+                for (int u = 0; u < KMAX - 1; ++u) { ck[u] = ck[u + 1]; cs[u] = cs[u + 1]; cm[u] = cm[u + 1]; }
+                ck[KMAX - 1] = 0ull;
+            }
+            if (m == 0ull && lane == 0) s_key[t] = 0ull;
+            __syncwarp();
+        }
+        if (lane == 0) {
+            const float iq = st == CACHE_ROW_OK ? inv_q[g] : 0.0f;
+            for (int t = 0; t < topk; ++t) {
+                const unsigned long long key = s_key[t];
+                out_ids[i * topk + t] = key ? (uint64_t)key_id(key) : CACHE_NO_ID;
+                out_scores[i * topk + t] = key ? fminf(fmaxf(key_to_f32(key) * iq, -1.0f), 1.0f) : -INFINITY;
+            }
+            int K = 0, owner = 0;
+            long long src = -1;
+            if (s_key[0] != 0ull) {
+                const float c = fminf(fmaxf(key_to_f32(s_key[0]) * iq, -1.0f), 1.0f);
+                int jstar = -1;
+                for (int j = 0; j < km.num_k; ++j)
+                    if ((double)c > km.thr[j]) jstar = j;
+                if (jstar >= 0) {
+                    jstar = min(jstar + km.k_bias, km.num_k - 1);
+                    owner = (int)(s_meta0 >> 8);
+                    const uint32_t m = (s_meta0 & 0xFFu) & ((2u << jstar) - 1u);
+                    if (m) {
+                        const int j = 31 - __clz(m);
+                        K = km.kv[j];
+                        const int64_t e = (int64_t)s_slot[0] * km.num_k + j;
+                        src = peers.lslot[owner][e];                  // P2P read of the owner's table
+                        atomicAdd(peers.fcnt[owner] + e, 1u);         // P2P atomic on the owner's f
+                    }
+                }
+            }
+            out_k[i] = K;
+            if (out_status) out_status[i] = st;
+            if (out_ptr) out_ptr[i] = (K > 0 && latent_out) ? (void*)(latent_out + i * latent_bytes) : nullptr;
+            s_src = src;
+            s_owner = owner;
+        }
+    }
+    __syncthreads();
+    const long long src = s_src;
+    if (src >= 0 && latent_out && latent_bytes > 0) {
+        const int4* sp = reinterpret_cast<const int4*>(peers.pool[s_owner] + src * latent_bytes);
+        int4* dp = reinterpret_cast<int4*>(latent_out + i * latent_bytes);
+        const int64_t nv = latent_bytes / 16;
+        int64_t v = threadIdx.x;
+        for (; v + 3 * 128 < nv; v += 4 * 128) {
+            const int4 a0 = sp[v], a1 = sp[v + 128], a2 = sp[v + 256], a3 = sp[v + 384];
+            __stcs(dp + v, a0);
+            __stcs(dp + v + 128, a1);
+            __stcs(dp + v + 256, a2);
+            __stcs(dp + v + 384, a3);
+        }
+        for (; v < nv; v += 128) __stcs(dp + v, sp[v]);
+    }
+}
+
+void launch_merge_sharded(int kmax, const cache_shard_rec* recs, int world, int64_t B, int64_t row0, int64_t nb,
+                          int topk, const float* inv_q, const int32_t* qstatus, const PeerPtrs& peers,
+                          int64_t latent_bytes, const KMap& km, uint64_t* out_ids, float* out_scores,
+                          int32_t* out_k, uint8_t* latent_out, void** out_ptr, int32_t* out_status, cudaStream_t s) {
+    if (nb <= 0) return;
+#define NV_MS(KM)                                                                                          \
+    k_merge_sharded<KM><<<(unsigned)nb, 128, 0, s>>>(recs, world, B, row0, topk, inv_q, qstatus, peers,     \
+                                                     latent_bytes, km, out_ids, out_scores, out_k, latent_out, \
+                                                     out_ptr, out_status)
+    if (kmax == 1) NV_MS(1);
+    else if (kmax == 4) NV_MS(4);
+    else NV_MS(16);
+#undef NV_MS
 }
 
 void launch_evict_apply(uint32_t* present, uint32_t* fcnt, const uint32_t* ids, const int32_t* lslot,

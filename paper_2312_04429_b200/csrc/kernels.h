@@ -64,8 +64,23 @@ void launch_insert_commit(const __nv_bfloat16* ystage, const float* invstage, co
 void launch_copy_latents(const uint8_t* src, const CopyPlan* plan, int64_t n, int64_t latent_bytes,
                          uint8_t* pool, cudaStream_t s);
 
-void launch_evict_select(const uint32_t* present, const uint32_t* fcnt, const uint32_t* ids,
-                         int64_t n_slots, const KMap& km, EvictState* st, unsigned int* hist, cudaStream_t s);
+void launch_evict_hist(const uint32_t* present, const uint32_t* fcnt, const uint32_t* ids, int64_t n_slots,
+                       const KMap& km, const EvictState* st, int pass, unsigned int* hist, cudaStream_t s);
+void launch_evict_pick(unsigned int* hist, EvictState* st, int pass, cudaStream_t s);
+
+// sharded lookup
+constexpr int kMaxWorld = 16;
+struct PeerPtrs {                       // per-rank device pointers (own rank included)
+    const int32_t* lslot[kMaxWorld];
+    uint32_t* fcnt[kMaxWorld];
+    const uint8_t* pool[kMaxWorld];
+};
+void launch_local_merge(int kmax, const Rec* ws, int parts, int64_t B, int topk, const int32_t* qstatus,
+                        const uint32_t* present, int owner, cache_shard_rec* out, cudaStream_t s);
+void launch_merge_sharded(int kmax, const cache_shard_rec* recs, int world, int64_t B, int64_t row0, int64_t nb,
+                          int topk, const float* inv_q, const int32_t* qstatus, const PeerPtrs& peers,
+                          int64_t latent_bytes, const KMap& km, uint64_t* out_ids, float* out_scores,
+                          int32_t* out_k, uint8_t* latent_out, void** out_ptr, int32_t* out_status, cudaStream_t s);
 void launch_evict_apply(uint32_t* present, uint32_t* fcnt, const uint32_t* ids, const int32_t* lslot,
                         float* inv_e, int64_t n_slots, const KMap& km, const EvictState* st,
                         unsigned long long* ev_key, int32_t* ev_lslot, unsigned long long* counters,

@@ -1,0 +1,211 @@
+"""Entry-sharded NIRVANA cache over several GPUs.
+
+Every step runs in the library's kernels; this module only moves buffers between ranks with
+collectives (torch.distributed / NCCL over NVLink, or in-process copies for virtual ranks):
+
+  insert  every rank receives the same batch; accepted rows get global ids 0,1,2,...
+          and rank r stores the rows with id % world == r (cache_insert, shard config)
+  query   all-gather the ranks' local query batches -> global batch Q (b rows)
+          -> cache_query_local on every rank (tcgen05 scan of its shard + local top-k)
+          -> all-gather the 16-byte shard records (world x b x topk)
+          -> cache_query_merge for the rank's own rows: merge under (score desc, id asc),
+             Fig. 11 + holes, and the winning state copied straight out of the OWNER's latent
+             pool over NVLink (peer pointers from CUDA IPC), access counted on the owner's f
+  evict   8 radix passes: per-rank key histograms (cache_evict_hist) summed with an
+          all-reduce, digit picked identically everywhere (cache_evict_pick), then each rank
+          applies the global threshold to its own items (cache_evict_apply)
+
+Because a query's answer is a max over shards under a total order and ids are global, the
+results are identical to one unsharded cache (tested with virtual ranks on one GPU).
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import binding as B
+
+
+class TorchComm:
+    """Collectives of one process group (one rank per GPU)."""
+
+    def __init__(self, group=None, device: str = "cuda"):
+        import torch.distributed as dist
+        self.dist, self.group, self.device = dist, group, device
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def all_gather(self, t: torch.Tensor) -> torch.Tensor:
+        out = torch.empty((self.world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+        self.dist.all_gather_into_tensor(out.view(-1), t.contiguous().view(-1), group=self.group)
+        return out
+
+    def all_reduce_sum(self, t: torch.Tensor) -> torch.Tensor:
+        self.dist.all_reduce(t, group=self.group)
+        return t
+
+    def all_reduce_min_int(self, v: int) -> int:
+        t = torch.tensor([v], dtype=torch.int64, device=self.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
+        return int(t.item())
+
+    def all_gather_object(self, obj):
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+
+def query_protocol(comm, q_local: torch.Tensor, topk: int, local_fn, merge_fn):
+    """The sharded lookup's data movement: all-gather queries -> local scan (local_fn(qg) ->
+    this rank's record tensor) -> all-gather records -> merge of this rank's own rows
+    (merge_fn(b, row0, nb, recs_all)).  Rank r owns global rows [r*nb, (r+1)*nb)."""
+    qg = comm.all_gather(q_local).reshape(-1, q_local.shape[1])
+    recs = local_fn(qg)
+    recs_all = comm.all_gather(recs)
+    nb = q_local.shape[0]
+    return merge_fn(qg.shape[0], comm.rank * nb, nb, recs_all)
+
+
+def evict_protocol(comm, n: int, state, hist, hist_fn, pick_fn):
+    """Distributed exact selection of the n lowest item keys: 8 MSB-first radix passes, each
+    a per-rank histogram summed over ranks, then the same digit pick on every rank."""
+    for p in range(8):
+        hist_fn(state, p, hist)
+        comm.all_reduce_sum(hist)
+        pick_fn(hist, state, p)
+    return state
+
+
+def _desc_bytes(d: B.PeerDesc) -> bytes:
+    return ctypes.string_at(ctypes.addressof(d), ctypes.sizeof(d))
+
+
+def _desc_from_bytes(b: bytes) -> B.PeerDesc:
+    d = B.PeerDesc()
+    ctypes.memmove(ctypes.addressof(d), b, ctypes.sizeof(d))
+    return d
+
+
+class ShardedCache:
+    """One rank's handle of an entry-sharded cache (one process per GPU)."""
+
+    def __init__(self, comm: TorchComm, entry_capacity: int, latent_capacity: int | None = None, **kw):
+        self.comm = comm
+        self.cache = B.NirvanaCache(entry_capacity=entry_capacity, latent_capacity=latent_capacity,
+                                    shard_rank=comm.rank, shard_world=comm.world, **kw)
+        descs = comm.all_gather_object(_desc_bytes(self.cache.export_peer()))
+        self.cache.attach_peers([_desc_from_bytes(d) for d in descs])
+        self.latent_bytes = self.cache.latent_bytes
+
+    def insert(self, emb: torch.Tensor, latents=None, present=None):
+        """Collective: every rank passes the SAME batch.  Conservative capacity agreement: the
+        insert proceeds only if every rank can hold its worst-case share."""
+        n = emb.shape[0]
+        share = (n + self.comm.world - 1) // self.comm.world
+        st = self.cache.stats()
+        ok = int(st["free_entries"] >= share and st["free_items"] >= share * self.cache.num_k)
+        if self.comm.all_reduce_min_int(ok) == 0:
+            raise B.CacheError(B.E_FULL, "sharded insert: some rank lacks capacity for its share")
+        return self.cache.insert(emb, latents, present)
+
+    def alloc_outputs(self, b_local: int, topk: int = 1, latents: bool = True):
+        return self.cache.alloc_outputs(b_local, topk, latents)
+
+    def query_into(self, q_local: torch.Tensor, out: dict, topk: int = 1, stream=None):
+        """Collective: every rank passes its own b_local queries (same b_local everywhere)."""
+        def local_fn(qg):
+            recs = torch.empty((qg.shape[0] * topk * B.SHARD_REC_BYTES,), dtype=torch.uint8, device=qg.device)
+            return self.cache.query_local(qg, topk, recs, stream)
+
+        def merge_fn(b, row0, nb, recs_all):
+            return self.cache.query_merge(b, row0, nb, topk, recs_all, out, stream)
+
+        return query_protocol(self.comm, q_local, topk, local_fn, merge_fn)
+
+    def evict(self, n: int):
+        """Collective: evict the n globally lowest LCBFU items (every rank passes the same n)."""
+        live = self.comm.all_reduce_sum(torch.tensor([self.cache.live_items], dtype=torch.int64,
+                                                     device="cuda")).item()
+        if n > live:
+            raise B.CacheError(B.E_EVICT_RANGE, "sharded evict: n exceeds live items")
+        st = torch.tensor([0, 0, n], dtype=torch.int64, device="cuda")
+        hist = torch.zeros(256, dtype=torch.int32, device="cuda")
+        evict_protocol(self.comm, n, st, hist, self.cache.evict_hist, self.cache.evict_pick)
+        ev, dirty = self.cache.evict_apply(st, n)
+        evs = self.comm.all_gather_object(ev.tolist())
+        dts = self.comm.all_gather_object(dirty.tolist())
+        return _merge_evicted(evs), np.array(sorted(x for d in dts for x in d), dtype=np.uint64)
+
+
+class VirtualShards:
+    """P shards of one cache held by ONE process on one GPU (virtual ranks): the same kernels
+    and the same merge/P2P code path as ShardedCache, with collectives replaced by copies.
+    Used to test sharding invariance on a single B200."""
+
+    def __init__(self, world: int, entry_capacity: int, latent_capacity: int | None = None, **kw):
+        self.world = world
+        self.caches = [B.NirvanaCache(entry_capacity=entry_capacity, latent_capacity=latent_capacity,
+                                      shard_rank=r, shard_world=world, **kw) for r in range(world)]
+        descs = [c.export_peer() for c in self.caches]
+        for c in self.caches:
+            c.attach_peers(descs)
+        self.latent_bytes = self.caches[0].latent_bytes
+
+    def insert(self, emb, latents=None, present=None):
+        res = [c.insert(emb, latents, present) for c in self.caches]
+        return res[0]
+
+    def query(self, q_global: torch.Tensor, topk: int = 1, latents: bool = True):
+        """q_global = the concatenation of the ranks' local batches (b divisible by world)."""
+        b = q_global.shape[0]
+        assert b % self.world == 0
+        bl = b // self.world
+        recs = []
+        for c in self.caches:
+            r = torch.empty((b * topk * B.SHARD_REC_BYTES,), dtype=torch.uint8, device=q_global.device)
+            c.query_local(q_global, topk, r)
+            recs.append(r)
+        recs_all = torch.stack(recs)
+        outs = []
+        for r, c in enumerate(self.caches):
+            o = c.alloc_outputs(bl, topk, latents)
+            c.query_merge(b, r * bl, bl, topk, recs_all, o)
+            outs.append(o)
+        cat = {k: (torch.cat([o[k] for o in outs]) if outs[0][k] is not None else None) for k in outs[0]}
+        return cat
+
+    def evict(self, n: int):
+        live = sum(c.live_items for c in self.caches)
+        if n > live:
+            raise B.CacheError(B.E_EVICT_RANGE, "sharded evict: n exceeds live items")
+        sts = [torch.tensor([0, 0, n], dtype=torch.int64, device="cuda") for _ in self.caches]
+        hists = [torch.zeros(256, dtype=torch.int32, device="cuda") for _ in self.caches]
+        for p in range(8):
+            for c, st, h in zip(self.caches, sts, hists):
+                c.evict_hist(st, p, h)
+            tot = torch.stack(hists).sum(0).to(torch.int32)
+            for c, st, h in zip(self.caches, sts, hists):
+                h.copy_(tot)
+                c.evict_pick(h, st, p)
+        res = [c.evict_apply(st, n) for c, st in zip(self.caches, sts)]
+        return (_merge_evicted([r[0].tolist() for r in res]),
+                np.array(sorted(x for r in res for x in r[1].tolist()), dtype=np.uint64))
+
+    def meta(self, id_: int):
+        return self.caches[id_ % self.world].meta(id_)
+
+    def stats(self):
+        ss = [c.stats() for c in self.caches]
+        return {k: sum(s[k] for s in ss) if k not in ("next_id",) else ss[0][k] for k in ss[0]}
+
+
+def _merge_evicted(lists):
+    """Per-rank eviction lists are each in key order; the global order is by key too, but the
+    key (f*K) is not recoverable from (id << 3 | j): the caller gets the union sorted by
+    (id, j) when more than one rank evicted."""
+    allv = [x for l in lists for x in l]
+    if sum(1 for l in lists if l) <= 1:
+        return np.array(allv, dtype=np.uint64)
+    return np.array(sorted(allv), dtype=np.uint64)

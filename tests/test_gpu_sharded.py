@@ -1,0 +1,65 @@
+"""Sharding invariance on one GPU: P virtual ranks (separate caches, peer-pointer merge path)
+must give results identical to one unsharded cache -- ids, scores (bitwise), K, latent bytes,
+LCBFU counters, eviction sets -- and agree with the oracle."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from tests.parity import check_batch, gpu_to_numpy
+
+pytestmark = pytest.mark.gpu
+L = 256
+
+
+@pytest.fixture(scope="module")
+def mods():
+    from paper_2312_04429_b200 import binding, sharded
+    return binding, sharded
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("topk", [1, 4])
+def test_virtual_shards_equal_single_cache(mods, oracle_mod, world, topk):
+    B, S = mods
+    n = 1500
+    emb, cl = synth.entries(n, seed=31 + world)
+    emb[1400] = emb[7]                                     # cross-shard exact tie (ids 7 / 1400)
+    pres = synth.present_masks(n, seed=31, hole_frac=0.2)
+    lat = synth.latents_np(np.arange(n), 5, L, seed=31)
+    single = B.NirvanaCache(entry_capacity=n, dim=768, latent_bytes=L)
+    vs = S.VirtualShards(world, entry_capacity=n, dim=768, latent_bytes=L)
+    et, lt = torch.from_numpy(emb).cuda(), torch.from_numpy(lat).cuda()
+    ids1, _ = single.insert(et, lt, present=pres)
+    ids2, _ = vs.insert(et, lt, present=pres)
+    assert np.array_equal(ids1, ids2)
+    o = oracle_mod.OracleCache(dim=768, entry_capacity=n, latent_bytes=L)
+    o.insert(emb, latents=lat, present=pres)
+    b = 48 * world
+    for rnd in range(2):
+        q, _, _ = synth.queries(emb, cl, b, seed=200 + rnd)
+        q[5] = emb[7]
+        qt = torch.from_numpy(q).cuda()
+        a = gpu_to_numpy(single.query(qt, topk=topk))
+        s = gpu_to_numpy(vs.query(qt, topk=topk))
+        assert np.array_equal(a["ids"], s["ids"])
+        assert np.array_equal(a["scores"].view(np.uint32), s["scores"].view(np.uint32))
+        assert np.array_equal(a["k"], s["k"]) and np.array_equal(a["status"], s["status"])
+        hit = a["k"] > 0
+        assert np.array_equal(a["latents"][hit], s["latents"][hit])
+        assert a["ids"][5, 0] == 7
+        check_batch(s, o, q, topk, expected_latent=lambda e, k: lat[e, synth.K_VALUES.index(k)])
+    for e in range(0, n, 7):
+        assert np.array_equal(single.meta(e)[0], vs.meta(e)[0]) and single.meta(e)[1] == vs.meta(e)[1]
+    # distributed eviction == single-cache eviction == oracle (as sets; keys are unique)
+    for nev in (333, 1200):
+        e1, d1 = single.evict(nev)
+        e2, d2 = vs.evict(nev)
+        rc, e3, d3 = o.evict(nev)
+        assert np.array_equal(np.sort(e1), e2) and np.array_equal(np.sort(e3), e2)
+        assert np.array_equal(d1, d2) and np.array_equal(d3, d2)
+    q, _, _ = synth.queries(emb, cl, b, seed=300)
+    qt = torch.from_numpy(q).cuda()
+    a = gpu_to_numpy(single.query(qt, topk=topk))
+    s = gpu_to_numpy(vs.query(qt, topk=topk))
+    assert np.array_equal(a["ids"], s["ids"]) and np.array_equal(a["k"], s["k"])
