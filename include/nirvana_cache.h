@@ -89,7 +89,18 @@ typedef struct {
     int32_t shard_world;      /* rank receives the same insert batches; accepted rows get
                                  global ids 0,1,2,... and rank r stores the rows with
                                  id % shard_world == r.  Default 0 / 1 = unsharded.         */
+    int32_t latent_alias;     /* 0: every stored (entry, K) owns a pool slot (default).
+                                 1: declared aliasing for caches whose full per-K state
+                                 store exceeds HBM: item (id, j) reads
+                                 pool slot CACHE_ALIAS_SLOT(id, j, latent_capacity); inserts
+                                 take no payload (latents must be NULL) and consume no pool
+                                 capacity; the pool is filled with cache_pool_write and is
+                                 never freed by eviction.                                  */
 } cache_config;
+
+/* The declared aliasing map of latent_alias = 1 (a plain, documented function of the id). */
+#define CACHE_ALIAS_SLOT(id, j, cap) \
+    ((int64_t)(((uint32_t)(id) * 8u + (uint32_t)(j)) * 2654435761u) % (int64_t)(cap))
 
 typedef struct {
     int64_t live_entries;     /* prompt embeddings present in the index                   */
@@ -242,6 +253,10 @@ cache_status cache_query_merge(cache_t *c, int64_t b, int64_t row0, int64_t nb, 
                                int32_t *row_status, void *stream);
 cache_status cache_export_peer(cache_t *c, cache_peer_desc *out);
 cache_status cache_attach_peers(cache_t *c, int32_t world, const cache_peer_desc *descs);
+
+/* Write n consecutive latent-pool slots starting at slot0 from `src` (device pointer,
+ * n x latent_bytes).  Asynchronous.  Used to pre-fill an aliased pool (latent_alias = 1). */
+cache_status cache_pool_write(cache_t *c, int64_t slot0, int64_t n, const void *src, void *stream);
 
 /* Counters: read the LCBFU access counts and presence mask of entry `id` (host outputs,
  * f has num_k slots).  Host-synchronous; intended for tests and maintenance tools. */

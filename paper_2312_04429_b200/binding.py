@@ -38,7 +38,13 @@ class CacheConfig(ctypes.Structure):
                 ("latent_capacity", ctypes.c_int64), ("latent_bytes", ctypes.c_int64),
                 ("num_k", ctypes.c_int32), ("k_values", ctypes.c_int32 * MAX_K),
                 ("thresholds", ctypes.c_double * MAX_K), ("k_bias", ctypes.c_int32),
-                ("max_topk", ctypes.c_int32), ("shard_rank", ctypes.c_int32), ("shard_world", ctypes.c_int32)]
+                ("max_topk", ctypes.c_int32), ("shard_rank", ctypes.c_int32), ("shard_world", ctypes.c_int32),
+                ("latent_alias", ctypes.c_int32)]
+
+
+def alias_slot(id_: int, j: int, cap: int) -> int:
+    """CACHE_ALIAS_SLOT of include/nirvana_cache.h (the declared aliasing map)."""
+    return ((((int(id_) & 0xFFFFFFFF) * 8 + j) * 2654435761) & 0xFFFFFFFF) % cap
 
 
 class CacheStats(ctypes.Structure):
@@ -62,7 +68,7 @@ EXPORTS = ("cache_default_config", "cache_create", "cache_destroy", "cache_inser
            "cache_query_batch_host", "cache_evict", "cache_get_meta", "cache_get_row", "cache_stats",
            "cache_set_scorer", "cache_set_profile_events", "cache_kernel_launches", "cache_last_error",
            "cache_evict_hist", "cache_evict_pick", "cache_evict_apply", "cache_live_items", "cache_query_local",
-           "cache_query_merge", "cache_export_peer", "cache_attach_peers")
+           "cache_query_merge", "cache_export_peer", "cache_attach_peers", "cache_pool_write")
 
 
 def load_library(path: str = LIB_PATH):
@@ -91,6 +97,8 @@ def load_library(path: str = LIB_PATH):
     L.cache_query_local.argtypes = [P, I64, P, I32, I32, P, P]
     L.cache_query_merge.argtypes = [P, I64, I64, I64, I32, P, P, P, P, P, P, P, P]
     L.cache_export_peer.argtypes = [P, ctypes.POINTER(PeerDesc)]
+    L.cache_pool_write.argtypes = [P, I64, I64, P, P]
+    L.cache_pool_write.restype = ctypes.c_int
     L.cache_attach_peers.argtypes = [P, I32, P]
     for fn in ("cache_evict_hist", "cache_evict_pick", "cache_evict_apply", "cache_query_local",
                "cache_query_merge", "cache_export_peer", "cache_attach_peers"):
@@ -152,7 +160,7 @@ class NirvanaCache:
     def __init__(self, entry_capacity: int, latent_capacity: int | None = None, dim: int = 768,
                  latent_bytes: int = 32768, k_values=(5, 10, 15, 20, 25),
                  thresholds=(0.65, 0.75, 0.85, 0.90, 0.95), k_bias: int = 0, max_topk: int = MAX_TOPK,
-                 device: int | None = None, shard_rank: int = 0, shard_world: int = 1):
+                 device: int | None = None, shard_rank: int = 0, shard_world: int = 1, latent_alias: bool = False):
         if device is None:
             device = torch.cuda.current_device()
         self.device = device
@@ -161,7 +169,8 @@ class NirvanaCache:
         self.cfg = default_config(dim=dim, entry_capacity=entry_capacity, latent_capacity=latent_capacity,
                                   latent_bytes=latent_bytes, k_values=tuple(k_values),
                                   thresholds=tuple(thresholds), k_bias=k_bias, max_topk=max_topk,
-                                  shard_rank=shard_rank, shard_world=shard_world)
+                                  shard_rank=shard_rank, shard_world=shard_world, latent_alias=int(latent_alias))
+        self.latent_capacity = latent_capacity
         self.shard_rank, self.shard_world = shard_rank, shard_world
         self.dim, self.latent_bytes, self.num_k = dim, latent_bytes, len(k_values)
         self.k_values = tuple(k_values)
@@ -265,6 +274,11 @@ class NirvanaCache:
 
     def set_scorer(self, scorer: int):
         _check(_lib.cache_set_scorer(self._h, scorer))
+
+    def pool_write(self, slot0: int, src: torch.Tensor, stream=None):
+        """Fill pool slots [slot0, slot0 + n) from a [n][latent_bytes] uint8 device tensor."""
+        n = src.numel() // self.latent_bytes
+        _check(_lib.cache_pool_write(self._h, slot0, n, _ptr(src), _stream(stream)))
 
     # ------------------------- sharded-path building blocks --------------------------
     def query_local(self, q: torch.Tensor, topk: int, out_recs: torch.Tensor, stream=None):

@@ -140,6 +140,7 @@ struct cache_t {
     DevBuf<int64_t> edirty;
     // sharding
     int rank = 0, world = 1;
+    bool alias = false;   // declared latent aliasing (cache_config.latent_alias)
     PeerPtrs peers{};
     bool peers_ok = false;
     std::vector<void*> ipc_opened;   // peer allocations opened through CUDA IPC
@@ -201,6 +202,11 @@ cache_status cache_create(const cache_config* cfg, int device, cache_t** out) {
     c->km.k_bias = cfg->k_bias;
     c->rank = cfg->shard_rank;
     c->world = cfg->shard_world;
+    c->alias = cfg->latent_alias != 0;
+    if (c->alias && c->lcap <= 0) {
+        delete c;
+        return fail(CACHE_E_INVALID_ARG, "cache_create: latent_alias needs latent_capacity > 0");
+    }
     cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
     auto bail = [&](cudaError_t e, const char* what) {
         cache_destroy(c);
@@ -258,6 +264,8 @@ cache_status cache_insert(cache_t* c, int64_t n, const void* emb, int32_t emb_dt
         return fail(CACHE_E_INVALID_ARG, "cache_insert: bad n / emb / dtype");
     if (n == 0) return CACHE_OK;
     if (latents && !c->pool) return fail(CACHE_E_INVALID_ARG, "cache_insert: latents given but no pool");
+    if (latents && c->alias)
+        return fail(CACHE_E_INVALID_ARG, "cache_insert: an aliased pool takes no payload (use cache_pool_write)");
     DeviceGuard g(c->device);
     cudaStream_t s = (cudaStream_t)stream;
     const uint32_t full = (1u << c->num_k) - 1u;
@@ -289,7 +297,7 @@ cache_status cache_insert(cache_t* c, int64_t n, const void* emb, int32_t emb_dt
         n_valid++;
         n_items += __builtin_popcount(masks[r] & full);
     }
-    if (n_valid > (int64_t)c->free_e.size() || n_items > (int64_t)c->free_l.size())
+    if (n_valid > (int64_t)c->free_e.size() || (!c->alias && n_items > (int64_t)c->free_l.size()))
         return fail(CACHE_E_FULL, "cache_insert: insufficient entry or latent capacity (evict first)");
     if ((uint64_t)c->next_id + n_accepted > 0xFFFFFFFFull)
         return fail(CACHE_E_STATE, "cache_insert: 32-bit id space exhausted");
@@ -321,6 +329,10 @@ cache_status cache_insert(cache_t* c, int64_t n, const void* emb, int32_t emb_dt
             for (int j = 0; j < CACHE_MAX_K; ++j) p.lslot[j] = -1;
             for (int j = 0; j < c->num_k; ++j) {
                 if (!((p.mask >> j) & 1u)) continue;
+                if (c->alias) {
+                    p.lslot[j] = (int32_t)CACHE_ALIAS_SLOT(p.id, j, c->lcap);
+                    continue;
+                }
                 p.lslot[j] = (int32_t)c->free_l.back();
                 c->free_l.pop_back();
                 if (latents) cp.push_back(CopyPlan{gr * c->num_k + j, p.lslot[j]});
@@ -398,6 +410,7 @@ static cache_status scan_core(cache_t* c, int64_t b, const void* queries, int32_
         }
     }
     if (c->prof_on && !prof1) CK(cudaEventRecord(c->prof[1], s));
+    if (c->prof_on) CK(cudaEventRecord(c->prof[2], s));   // end of the scan
     *parts_out = parts;
     return CACHE_OK;
 }
@@ -474,6 +487,15 @@ cache_status cache_query_merge(cache_t* c, int64_t b, int64_t row0, int64_t nb, 
     c->launches++;
     CK(cudaGetLastError());
     c->queries += nb;
+    return CACHE_OK;
+}
+
+cache_status cache_pool_write(cache_t* c, int64_t slot0, int64_t n, const void* src, void* stream) {
+    if (!c || slot0 < 0 || n < 0 || slot0 + n > c->lcap || (n > 0 && !src) || !c->pool)
+        return fail(CACHE_E_INVALID_ARG, "cache_pool_write: bad slot range / source / no pool");
+    if (n == 0) return CACHE_OK;
+    DeviceGuard g(c->device);
+    CK(cudaMemcpyAsync(c->pool + slot0 * c->L, src, (size_t)n * c->L, cudaMemcpyDefault, (cudaStream_t)stream));
     return CACHE_OK;
 }
 
@@ -663,7 +685,7 @@ cache_status cache_evict_apply(cache_t* c, const cache_evict_state* st, int64_t 
             c->h_present[it->second] &= ~(1u << j);
             c->h_lslot[it->second * c->num_k + j] = -1;
         }
-        c->free_l.push_back(ls[order[i]]);
+        if (!c->alias) c->free_l.push_back(ls[order[i]]);   // aliased slots are shared, never freed
     }
     c->live_items -= n;
     std::vector<uint64_t> dids;

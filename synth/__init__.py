@@ -157,6 +157,69 @@ def _mix_t(x):
     return x
 
 
+def _normal_t(rows, cols, salt: int):
+    """Counter-based standard normals N[row][col] (Box-Muller on two hashed uniforms): a pure
+    function of (row, col, salt), so any subset of rows can be regenerated anywhere."""
+    import torch
+    r = (rows & _M32)[:, None]
+    c = (cols & _M32)[None, :]
+    h1 = _mix_t((_mix_t(r ^ (salt & _M32)) * 0x9E3779B1 + c) & _M32)
+    h2 = _mix_t((h1 ^ 0x85EBCA6B) & _M32)
+    u1 = (h1.to(torch.float64) + 0.5) / 4294967296.0
+    u2 = (h2.to(torch.float64) + 0.5) / 4294967296.0
+    return (torch.sqrt(-2.0 * torch.log(u1)) * torch.cos(6.283185307179586 * u2)).to(torch.float32)
+
+
+class TorchEntries:
+    """On-device variant of ``entries`` for caches too large to draw on the host (C4/C5):
+    the same recipe (cluster centres + noise at cos 0.85, Zipf-popular anchors, the Fig. 11
+    similarity buckets for queries) but every number is a counter-based hash of (row, dim,
+    seed), so row r is identical on every rank and in every call."""
+
+    def __init__(self, n_total: int, seed: int, device, dim: int = D, cos_centre: float = 0.85):
+        import torch
+        self.n, self.seed, self.device, self.dim = n_total, seed, device, dim
+        self.n_c = max(1, n_total // 64)
+        cols = torch.arange(dim, dtype=torch.int64, device=device)
+        self.cols = cols
+        cen = []
+        for s in range(0, self.n_c, 65536):
+            rr = torch.arange(s, min(self.n_c, s + 65536), dtype=torch.int64, device=device)
+            cen.append(_normal_t(rr, cols, seed * 7 + 1))
+        c = torch.cat(cen)
+        self.centres = c / c.norm(dim=1, keepdim=True)
+        self.sigma = float(np.sqrt((1.0 / cos_centre ** 2 - 1.0) / dim))
+
+    def cluster(self, rows):
+        return _mix_t((rows & _M32) ^ (self.seed & _M32)) % self.n_c
+
+    def rows(self, rows):
+        """fp32 unit rows [len(rows)][dim] for an int64 tensor of row indices."""
+        x = self.centres[self.cluster(rows)] + self.sigma * _normal_t(rows, self.cols, self.seed * 7 + 2)
+        return x / x.norm(dim=1, keepdim=True)
+
+    def queries(self, b: int, qseed: int, zipf_s: float = 1.0):
+        """b queries around Zipf(zipf_s)-popular anchor rows with the bucket mixture of
+        ``queries``.  Returns (q [b][dim] fp32, anchor rows, target cos)."""
+        import torch
+        rng = np.random.default_rng(qseed)
+        # bounded Zipf(1) over the n rows by inverse CDF: P(rank <= k) ~ ln k / ln n
+        ranks = np.floor(np.exp(rng.random(b) * np.log(self.n))).astype(np.int64) if zipf_s > 0 \
+            else rng.integers(1, self.n, b)
+        perm_a = np.uint64(rng.integers(1, 2 ** 31) | 1)
+        anchor = ((ranks.astype(np.uint64) * perm_a) % np.uint64(self.n)).astype(np.int64)
+        probs = np.array([w for _, _, w in BUCKETS])
+        bk = rng.choice(len(BUCKETS), size=b, p=probs / probs.sum())
+        lo = np.maximum(np.array([BUCKETS[i][0] for i in bk]), 0.40)
+        hi = np.array([BUCKETS[i][1] for i in bk])
+        t = np.clip(lo + (hi - lo) * rng.random(b), 0.40, 0.999)
+        sig = torch.from_numpy(np.sqrt((1.0 / t ** 2 - 1.0) / self.dim)).to(self.device, torch.float32)
+        a = torch.from_numpy(anchor).to(self.device)
+        qrows = torch.arange(b, dtype=torch.int64, device=self.device) + (qseed * 1_000_003) % (1 << 30)
+        q = self.rows(a) + sig[:, None] * _normal_t(qrows, self.cols, self.seed * 7 + 3)
+        return q / q.norm(dim=1, keepdim=True), anchor, t
+
+
 def latents_torch(row0: int, n: int, num_k: int, latent_bytes: int, seed: int, device):
     """Same bytes as ``latents_np(range(row0, row0+n), ...)`` generated with torch int64 ops
     on ``device``: returns a uint8 tensor [n][num_k][latent_bytes]."""

@@ -256,3 +256,26 @@ def test_full_size_sampled_parity_c2(B, oracle_mod):
     rows = list(np.random.default_rng(3).choice(b, 24, replace=False))
     rep = check_batch(out, o, q, 1, rows=rows, adopt=False)
     assert rep["max_dscore"] < 1e-4
+
+
+def test_aliased_latent_pool(B, oracle_mod):
+    """latent_alias = 1 (SURVEY 8(d) capacity decision for C4/C5): items read the declared
+    slot CACHE_ALIAS_SLOT(id, j, cap) of a pre-filled pool; entries/K unaffected."""
+    n, cap, L2 = 700, 37, 512
+    emb, cl = synth.entries(n, seed=41)
+    pres = synth.present_masks(n, seed=41, hole_frac=0.3)
+    pool = synth.latents_np(np.arange(cap) + 90_000, 1, L2, seed=41)[:, 0]     # [cap][L]
+    g = B.NirvanaCache(entry_capacity=n, latent_capacity=cap, dim=768, latent_bytes=L2, latent_alias=True)
+    g.pool_write(0, torch.from_numpy(pool).cuda())
+    g.insert(torch.from_numpy(emb).cuda(), None, present=pres)
+    per_item = np.stack([np.stack([pool[B.alias_slot(e, j, cap)] for j in range(5)]) for e in range(n)])
+    o = oracle_mod.OracleCache(dim=768, entry_capacity=n, latent_bytes=L2)
+    o.insert(emb, latents=per_item, present=pres)
+    q, _, _ = synth.queries(emb, cl, 130, seed=42)
+    out = gpu_to_numpy(g.query(torch.from_numpy(q).cuda(), topk=2))
+    check_batch(out, o, q, 2, expected_latent=lambda e, k: per_item[e, synth.K_VALUES.index(k)])
+    ev, d = g.evict(900)
+    rc, oev, od = o.evict(900)
+    assert np.array_equal(ev, oev) and np.array_equal(d, od)
+    with pytest.raises(B.CacheError):
+        g.insert(torch.from_numpy(emb[:2]).cuda(), torch.zeros((2, 5, L2), dtype=torch.uint8, device="cuda"))
