@@ -105,7 +105,8 @@ class ShardedCache:
         n = emb.shape[0]
         share = (n + self.comm.world - 1) // self.comm.world
         st = self.cache.stats()
-        ok = int(st["free_entries"] >= share and st["free_items"] >= share * self.cache.num_k)
+        items_ok = bool(self.cache.cfg.latent_alias) or st["free_items"] >= share * self.cache.num_k
+        ok = int(st["free_entries"] >= share and items_ok)
         if self.comm.all_reduce_min_int(ok) == 0:
             raise B.CacheError(B.E_FULL, "sharded insert: some rank lacks capacity for its share")
         return self.cache.insert(emb, latents, present)
