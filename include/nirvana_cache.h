@@ -196,10 +196,13 @@ cache_status cache_query_batch(cache_t *c, int64_t b, const void *queries, int32
                                int32_t *out_k, void *latent_out, void **out_latent_ptr,
                                int32_t *row_status, void *stream);
 
-/* Same lookup with HOST buffers (the end-to-end call a serving process makes): queries,
- * out_ids, out_scores, out_k, latent_out and row_status are host pointers (pinned memory
- * recommended); the library stages them through its own device buffers, copies the results
- * back and synchronises `stream` before returning.  latent_out / row_status may be NULL. */
+/* Same lookup called from the host (the end-to-end call a serving process makes): queries,
+ * out_ids, out_scores, out_k and row_status are host pointers (pinned memory recommended);
+ * the library copies the queries in, runs the lookup, copies ids/scores/K/status back in one
+ * transfer and synchronises `stream` before returning.  latent_out may be a DEVICE pointer
+ * (the denoiser's input buffer on this GPU: states are gathered there directly, nothing
+ * crosses PCIe) or a HOST pointer (staged on the device, then copied back); it may be NULL.
+ * row_status may be NULL. */
 cache_status cache_query_batch_host(cache_t *c, int64_t b, const void *queries, int32_t q_dtype,
                                     int32_t topk, uint64_t *out_ids, float *out_scores,
                                     int32_t *out_k, void *latent_out, int32_t *row_status,

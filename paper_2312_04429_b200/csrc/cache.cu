@@ -129,7 +129,9 @@ struct cache_t {
     DevBuf<Rec> recs;
     DevBuf<InsertPlan> iplan;
     DevBuf<CopyPlan> cplan;
-    DevBuf<uint8_t> hq_in, hq_lat;
+    DevBuf<uint8_t> hq_in, hq_lat, hq_out;
+    void* h_out = nullptr;   // pinned staging of the packed host-call results
+    size_t h_out_n = 0;
     DevBuf<uint64_t> hq_ids;
     DevBuf<float> hq_sc;
     DevBuf<int32_t> hq_k, hq_st;
@@ -246,6 +248,8 @@ cache_status cache_destroy(cache_t* c) {
     DeviceGuard g(c->device);
     cudaDeviceSynchronize();
     for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+    if (c->h_out) cudaFreeHost(c->h_out);
+    c->hq_out.release();
     cudaFree(c->emb); cudaFree(c->inv_e); cudaFree(c->ids); cudaFree(c->present);
     cudaFree(c->lslot); cudaFree(c->fcnt); cudaFree(c->pool);
     c->qbuf.release(); c->ystage.release(); c->invq.release(); c->invstage.release();
@@ -574,22 +578,44 @@ cache_status cache_query_batch_host(cache_t* c, int64_t b, const void* queries, 
     DeviceGuard g(c->device);
     cudaStream_t s = (cudaStream_t)stream;
     const size_t qbytes = (size_t)b * c->dim * (q_dtype == CACHE_DTYPE_BF16 ? 2 : 4);
+    // latent_out may be device memory (the denoiser's input buffer on this GPU: gathered in
+    // place, no host copy) or host memory (staged on the device, then copied back).
+    bool lat_dev = false;
+    if (latent_out) {
+        cudaPointerAttributes pa;
+        if (cudaPointerGetAttributes(&pa, latent_out) == cudaSuccess &&
+            (pa.type == cudaMemoryTypeDevice || pa.type == cudaMemoryTypeManaged))
+            lat_dev = true;
+        cudaGetLastError();
+    }
     CK(c->hq_in.ensure(qbytes));
-    CK(c->hq_ids.ensure((size_t)b * topk));
-    CK(c->hq_sc.ensure((size_t)b * topk));
-    CK(c->hq_k.ensure(b));
-    CK(c->hq_st.ensure(b));
-    if (latent_out) CK(c->hq_lat.ensure((size_t)b * c->L));
+    // ids | scores | K | status packed in one buffer -> one device-to-host copy
+    const size_t o_ids = 0, o_sc = (size_t)b * topk * 8, o_k = o_sc + (size_t)b * topk * 4, o_st = o_k + (size_t)b * 4;
+    const size_t obytes = o_st + (size_t)b * 4;
+    CK(c->hq_out.ensure(obytes));
+    if (c->h_out_n < obytes) {
+        if (c->h_out) cudaFreeHost(c->h_out);
+        c->h_out = nullptr;
+        c->h_out_n = 0;
+        CK(cudaHostAlloc(&c->h_out, obytes, cudaHostAllocDefault));
+        c->h_out_n = obytes;
+    }
+    if (latent_out && !lat_dev) CK(c->hq_lat.ensure((size_t)b * c->L));
     CK(cudaMemcpyAsync(c->hq_in.p, queries, qbytes, cudaMemcpyHostToDevice, s));
-    cache_status r = query_core(c, b, c->hq_in.p, q_dtype, topk, c->hq_ids.p, c->hq_sc.p, c->hq_k.p,
-                                latent_out ? c->hq_lat.p : nullptr, nullptr, c->hq_st.p, s);
+    uint8_t* ob = c->hq_out.p;
+    cache_status r = query_core(c, b, c->hq_in.p, q_dtype, topk, (uint64_t*)(ob + o_ids), (float*)(ob + o_sc),
+                                (int32_t*)(ob + o_k), latent_out ? (lat_dev ? latent_out : (void*)c->hq_lat.p) : nullptr,
+                                nullptr, (int32_t*)(ob + o_st), s);
     if (r != CACHE_OK) return r;
-    CK(cudaMemcpyAsync(out_ids, c->hq_ids.p, (size_t)b * topk * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(out_scores, c->hq_sc.p, (size_t)b * topk * 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(out_k, c->hq_k.p, (size_t)b * 4, cudaMemcpyDeviceToHost, s));
-    if (row_status) CK(cudaMemcpyAsync(row_status, c->hq_st.p, (size_t)b * 4, cudaMemcpyDeviceToHost, s));
-    if (latent_out) CK(cudaMemcpyAsync(latent_out, c->hq_lat.p, (size_t)b * c->L, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(c->h_out, ob, obytes, cudaMemcpyDeviceToHost, s));
+    if (latent_out && !lat_dev)
+        CK(cudaMemcpyAsync(latent_out, c->hq_lat.p, (size_t)b * c->L, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    const uint8_t* hb = static_cast<const uint8_t*>(c->h_out);
+    std::memcpy(out_ids, hb + o_ids, (size_t)b * topk * 8);
+    std::memcpy(out_scores, hb + o_sc, (size_t)b * topk * 4);
+    std::memcpy(out_k, hb + o_k, (size_t)b * 4);
+    if (row_status) std::memcpy(row_status, hb + o_st, (size_t)b * 4);
     return CACHE_OK;
 }
 
