@@ -106,7 +106,8 @@ def build_cache(B, torch, cfg, seed, dev):
     emb, cl = __import__("synth").entries(n, seed=seed)
     import synth
     pres = synth.present_masks(n, seed=seed)
-    g = B.NirvanaCache(entry_capacity=n, dim=D, latent_bytes=L, device=dev)
+    # 2% entry headroom so the maintenance leg can re-insert after evicting 1% of the states
+    g = B.NirvanaCache(entry_capacity=n + n // 50 + 64, latent_capacity=5 * n, dim=D, latent_bytes=L, device=dev)
     chunk = 8192
     for s in range(0, n, chunk):
         m = min(chunk, n - s)
