@@ -381,6 +381,7 @@ def main():
     maint = None
     if not args.no_maintenance:
         import synth as _s
+        g.evict(5)                       # warm-up: lazy module load + first workspace allocations
         st = g.stats()
         nev = max(5, st["live_items"] // 100)
         torch.cuda.synchronize()
