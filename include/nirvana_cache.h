@@ -96,7 +96,18 @@ typedef struct {
                                  take no payload (latents must be NULL) and consume no pool
                                  capacity; the pool is filled with cache_pool_write and is
                                  never freed by eviction.                                  */
+    int32_t evict_policy;     /* CACHE_POLICY_*: which item score cache_evict minimises     */
 } cache_config;
+
+/* Eviction policies: the item score minimised by cache_evict (ties by (id, K) ascending).
+ * LCBFU is the paper's policy; the others are the baselines it is compared with. */
+enum {
+    CACHE_POLICY_LCBFU = 0, /* f_i x K_i: access frequency x computation saved   */
+    CACHE_POLICY_LRU = 1,   /* batch clock of the last access; insert clock until accessed
+                                                                       */
+    CACHE_POLICY_LFU = 2,   /* f_i                                               */
+    CACHE_POLICY_FIFO = 3   /* insertion order: the id alone                     */
+};
 
 /* The declared aliasing map of latent_alias = 1 (a plain, documented function of the id). */
 #define CACHE_ALIAS_SLOT(id, j, cap) \
@@ -139,8 +150,8 @@ typedef struct {
     int32_t num_k;
     int32_t reserved;
     int64_t latent_bytes;
-    void *lslot, *fcnt, *pool;                     /* raw device pointers (same process)   */
-    unsigned char ipc_lslot[64], ipc_fcnt[64], ipc_pool[64]; /* cudaIpcMemHandle_t bytes */
+    void *lslot, *fcnt, *pool, *lastacc;           /* raw device pointers (same process)   */
+    unsigned char ipc_lslot[64], ipc_fcnt[64], ipc_pool[64], ipc_lastacc[64]; /* IPC handles */
 } cache_peer_desc;
 
 /* Fill *cfg with the paper's defaults: dim 768, K = {5,10,15,20,25}, Fig. 11
@@ -270,6 +281,9 @@ cache_status cache_get_row(cache_t *c, uint64_t id, uint16_t *out_bf16);
 
 /* Host-synchronous statistics. */
 cache_status cache_stats(cache_t *c, cache_stats_t *out);
+
+/* Select the eviction policy (CACHE_POLICY_*) used by later cache_evict calls. */
+cache_status cache_set_evict_policy(cache_t *c, int32_t policy);
 
 /* Force a scoring kernel (CACHE_SCORER_*); AUTO by default. */
 cache_status cache_set_scorer(cache_t *c, int32_t scorer);

@@ -20,6 +20,7 @@ _SRC = os.path.join(_HERE, "nirvana_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 OK, E_INVALID_ARG, E_FULL, E_EVICT_RANGE, E_BAD_ROWS, E_OOM = 0, 1, 3, 4, 5, 8
+LCBFU, LRU, LFU, FIFO = 0, 1, 2, 3   # eviction policies
 ROW_OK, ROW_NONFINITE, ROW_ZERO_NORM, ROW_NO_ITEMS = 0, 1, 2, 3
 NO_ID = np.uint64(0xFFFFFFFFFFFFFFFF)
 
@@ -54,6 +55,12 @@ def lib():
         L.oracle_score_id.argtypes = [P, P, I32, U64]
         L.oracle_score_id.restype = D
         L.oracle_evict.argtypes = [P, I64, P, P, P]
+        L.oracle_evict_policy.argtypes = [P, I64, I32, P, P, P]
+        L.oracle_tick.argtypes = [P]
+        L.oracle_tick.restype = None
+        L.oracle_clock.argtypes = [P]
+        L.oracle_clock.restype = U64
+        L.oracle_get_last.argtypes = [P, U64, P]
         L.oracle_live_entries.argtypes = [P]
         L.oracle_live_entries.restype = I64
         L.oracle_live_items.argtypes = [P]
@@ -144,12 +151,26 @@ class OracleCache:
         q = np.ascontiguousarray(qrow, dtype=np.uint16 if q_is_bf16 else np.float32)
         return lib().oracle_score_id(self._h, _p(q), int(q_is_bf16), int(id_))
 
-    def evict(self, n):
+    def evict(self, n, policy=0):
+        """policy: 0 LCBFU, 1 LRU, 2 LFU, 3 FIFO."""
         ev = np.empty(max(n, 1), dtype=np.uint64)
         dirty = np.empty(max(n, 1), dtype=np.uint64)
         nd = np.zeros(1, dtype=np.int64)
-        rc = lib().oracle_evict(self._h, n, _p(ev), _p(dirty), _p(nd))
+        rc = lib().oracle_evict_policy(self._h, n, policy, _p(ev), _p(dirty), _p(nd))
         return rc, ev[:n].copy(), dirty[: int(nd[0])].copy()
+
+    def tick(self):
+        lib().oracle_tick(self._h)
+
+    @property
+    def clock(self):
+        return lib().oracle_clock(self._h)
+
+    def last(self, id_):
+        out = np.empty(self.num_k, dtype=np.uint64)
+        if lib().oracle_get_last(self._h, int(id_), _p(out)) != 0:
+            raise KeyError(id_)
+        return out
 
     def select_k(self, s):
         return lib().oracle_select_k(self._h, float(s))

@@ -57,6 +57,7 @@ typedef struct {
     double nrm;           /* sqrt(sum x_i^2), index order */
     int present[ORC_MAX_K];
     uint64_t f[ORC_MAX_K];            /* LCBFU access frequency per K */
+    uint64_t last[ORC_MAX_K];         /* batch clock of the last access (LRU), insert clock at first */
     unsigned char *lat[ORC_MAX_K];    /* stored latent bytes per present K, or NULL (no payload) */
 } oentry;
 
@@ -74,6 +75,7 @@ typedef struct {
     int64_t live_entries;
     int64_t live_items;
     uint64_t next_id;
+    uint64_t clock;       /* number of query batches so far (the LRU logical clock) */
 } oracle_cache;
 
 /* ---------------------------------------------------------------------------------------
@@ -271,6 +273,7 @@ int oracle_insert(oracle_cache *c, int64_t n, const void *emb, int emb_is_bf16,
         for (j = 0; j < c->num_k; j++) {
             e->present[j] = (m >> j) & 1u;
             e->f[j] = 0;
+            e->last[j] = c->clock;
             e->lat[j] = NULL;
             if (e->present[j] && latents && c->latent_bytes > 0) {
                 e->lat[j] = (unsigned char *)malloc((size_t)c->latent_bytes);
@@ -422,9 +425,14 @@ int oracle_query(oracle_cache *c, int64_t b, const void *queries, int q_is_bf16,
             memcpy(latent_out + (size_t)r * c->latent_bytes, c->e[all[0].idx].lat[jused],
                    (size_t)c->latent_bytes);
     }
-    if (apply_counters)
+    if (apply_counters) {
+        c->clock++;   /* one query batch = one tick of the LRU clock */
         for (r = 0; r < b; r++)
-            if (hit_idx[r] >= 0) c->e[hit_idx[r]].f[hit_j[r]] += 1;
+            if (hit_idx[r] >= 0) {
+                c->e[hit_idx[r]].f[hit_j[r]] += 1;
+                c->e[hit_idx[r]].last[hit_j[r]] = c->clock;
+            }
+    }
     free(x); free(q); free(all); free(hit_idx); free(hit_j);
     return any_bad ? ORC_E_BAD_ROWS : ORC_OK;
 }
@@ -437,11 +445,13 @@ static oentry *find_id(oracle_cache *c, uint64_t id)
     return NULL;
 }
 
-/* Record accesses chosen elsewhere (the parity harness adopts an accepted GPU choice for
- * queries whose top-1 is within tolerance, so multi-round counter state stays comparable). */
+/* Record the accesses of one query batch chosen elsewhere (the parity harness adopts an
+ * accepted GPU choice for queries whose top-1 is within tolerance, so multi-round counter
+ * state stays comparable).  Like a query with apply_counters, it ticks the LRU clock once. */
 int oracle_record_access(oracle_cache *c, int64_t n, const uint64_t *ids, const int32_t *ks)
 {
     int64_t r;
+    c->clock++;
     for (r = 0; r < n; r++) {
         oentry *e;
         int j, jj = -1;
@@ -452,9 +462,13 @@ int oracle_record_access(oracle_cache *c, int64_t n, const uint64_t *ids, const 
             if (c->k_values[j] == ks[r]) jj = j;
         if (jj < 0 || !e->present[jj]) return ORC_E_INVALID_ARG;
         e->f[jj] += 1;
+        e->last[jj] = c->clock;
     }
     return ORC_OK;
 }
+
+/* Advance the LRU clock by one batch without accesses (a query batch with no hits). */
+void oracle_tick(oracle_cache *c) { c->clock++; }
 
 /* fp64 cosine of the (normalised, bf16-rounded) query row with a given live entry id. */
 double oracle_score_id(oracle_cache *c, const void *query, int q_is_bf16, uint64_t id)
@@ -490,6 +504,24 @@ static int cmp_item(const void *a, const void *b)
     return x->j < y->j ? -1 : (x->j > y->j ? 1 : 0);
 }
 
+/* Policy scores (ascending = evicted first; ties by (id, K), reading R11 / SPEC S:341):
+ *   0 LCBFU  f_i x K_i
+ *   1 LRU    clock of the last access (insert clock if never accessed)
+ *   2 LFU    f_i
+ *   3 FIFO   0 -- the id (insertion sequence) decides */
+static uint64_t policy_score(const oracle_cache *c, const oentry *e, int j, int policy)
+{
+    switch (policy) {
+    case 1: return e->last[j];
+    case 2: return e->f[j];
+    case 3: return 0;
+    default: return e->f[j] * (uint64_t)c->k_values[j];
+    }
+}
+
+int oracle_evict_policy(oracle_cache *c, int64_t n, int policy, uint64_t *out_evicted,
+                        uint64_t *out_dirty_ids, int64_t *out_n_dirty);
+
 /* LCBFU eviction of the n lowest-scored items, then dirty-prompt removal.
  *   out_evicted[n]  : (id << 3 | j) in eviction order (ascending key); may be NULL
  *   out_dirty_ids   : ids of removed entries, ascending; capacity n (a dirty entry needs at
@@ -498,9 +530,16 @@ static int cmp_item(const void *a, const void *b)
 int oracle_evict(oracle_cache *c, int64_t n, uint64_t *out_evicted, uint64_t *out_dirty_ids,
                  int64_t *out_n_dirty)
 {
+    return oracle_evict_policy(c, n, 0, out_evicted, out_dirty_ids, out_n_dirty);
+}
+
+/* Eviction of the n items with the smallest policy score (see policy_score). */
+int oracle_evict_policy(oracle_cache *c, int64_t n, int policy, uint64_t *out_evicted,
+                        uint64_t *out_dirty_ids, int64_t *out_n_dirty)
+{
     item *it;
     int64_t i, m = 0, nd = 0;
-    if (n < 0) return ORC_E_INVALID_ARG;
+    if (n < 0 || policy < 0 || policy > 3) return ORC_E_INVALID_ARG;
     if (n > c->live_items) return ORC_E_EVICT_RANGE;
     it = (item *)malloc(sizeof(item) * (c->live_items > 0 ? c->live_items : 1));
     if (!it) return ORC_E_OOM;
@@ -509,7 +548,7 @@ int oracle_evict(oracle_cache *c, int64_t n, uint64_t *out_evicted, uint64_t *ou
         if (!c->e[i].live) continue;
         for (j = 0; j < c->num_k; j++) {
             if (!c->e[i].present[j]) continue;
-            it[m].score = c->e[i].f[j] * (uint64_t)c->k_values[j];
+            it[m].score = policy_score(c, &c->e[i], j, policy);
             it[m].id = c->e[i].id;
             it[m].j = j;
             it[m].idx = i;
@@ -570,6 +609,18 @@ int oracle_get_meta(oracle_cache *c, uint64_t id, uint64_t *f, uint32_t *present
         m |= (uint32_t)(e->present[j] ? 1u : 0u) << j;
     }
     if (present_mask) *present_mask = m;
+    return ORC_OK;
+}
+
+uint64_t oracle_clock(const oracle_cache *c) { return c->clock; }
+
+/* last-access clocks of entry id (num_k values) */
+int oracle_get_last(oracle_cache *c, uint64_t id, uint64_t *last)
+{
+    int j;
+    oentry *e = find_id(c, id);
+    if (!e) return ORC_E_INVALID_ARG;
+    for (j = 0; j < c->num_k; j++) last[j] = e->last[j];
     return ORC_OK;
 }
 

@@ -39,7 +39,10 @@ class CacheConfig(ctypes.Structure):
                 ("num_k", ctypes.c_int32), ("k_values", ctypes.c_int32 * MAX_K),
                 ("thresholds", ctypes.c_double * MAX_K), ("k_bias", ctypes.c_int32),
                 ("max_topk", ctypes.c_int32), ("shard_rank", ctypes.c_int32), ("shard_world", ctypes.c_int32),
-                ("latent_alias", ctypes.c_int32)]
+                ("latent_alias", ctypes.c_int32), ("evict_policy", ctypes.c_int32)]
+
+
+POLICY_LCBFU, POLICY_LRU, POLICY_LFU, POLICY_FIFO = 0, 1, 2, 3
 
 
 def alias_slot(id_: int, j: int, cap: int) -> int:
@@ -56,8 +59,9 @@ class CacheStats(ctypes.Structure):
 class PeerDesc(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("pid", ctypes.c_int32), ("num_k", ctypes.c_int32),
                 ("reserved", ctypes.c_int32), ("latent_bytes", ctypes.c_int64), ("lslot", ctypes.c_void_p),
-                ("fcnt", ctypes.c_void_p), ("pool", ctypes.c_void_p), ("ipc_lslot", ctypes.c_ubyte * 64),
-                ("ipc_fcnt", ctypes.c_ubyte * 64), ("ipc_pool", ctypes.c_ubyte * 64)]
+                ("fcnt", ctypes.c_void_p), ("pool", ctypes.c_void_p), ("lastacc", ctypes.c_void_p),
+                ("ipc_lslot", ctypes.c_ubyte * 64), ("ipc_fcnt", ctypes.c_ubyte * 64),
+                ("ipc_pool", ctypes.c_ubyte * 64), ("ipc_lastacc", ctypes.c_ubyte * 64)]
 
 
 SHARD_REC_BYTES = 16   # cache_shard_rec
@@ -68,7 +72,8 @@ EXPORTS = ("cache_default_config", "cache_create", "cache_destroy", "cache_inser
            "cache_query_batch_host", "cache_evict", "cache_get_meta", "cache_get_row", "cache_stats",
            "cache_set_scorer", "cache_set_profile_events", "cache_kernel_launches", "cache_last_error",
            "cache_evict_hist", "cache_evict_pick", "cache_evict_apply", "cache_live_items", "cache_query_local",
-           "cache_query_merge", "cache_export_peer", "cache_attach_peers", "cache_pool_write")
+           "cache_query_merge", "cache_export_peer", "cache_attach_peers", "cache_pool_write",
+           "cache_set_evict_policy")
 
 
 def load_library(path: str = LIB_PATH):
@@ -88,6 +93,8 @@ def load_library(path: str = LIB_PATH):
     L.cache_get_row.argtypes = [P, U64, P]
     L.cache_stats.argtypes = [P, ctypes.POINTER(CacheStats)]
     L.cache_set_scorer.argtypes = [P, I32]
+    L.cache_set_evict_policy.argtypes = [P, I32]
+    L.cache_set_evict_policy.restype = ctypes.c_int
     L.cache_set_profile_events.argtypes = [P, P]
     L.cache_evict_hist.argtypes = [P, P, I32, P, P]
     L.cache_evict_pick.argtypes = [P, P, P, I32, P]
@@ -271,6 +278,10 @@ class NirvanaCache:
         s = CacheStats()
         _check(_lib.cache_stats(self._h, ctypes.byref(s)))
         return {k: getattr(s, k) for k, _ in CacheStats._fields_}
+
+    def set_evict_policy(self, policy: int):
+        """POLICY_LCBFU (paper), POLICY_LRU, POLICY_LFU, POLICY_FIFO (its baselines)."""
+        _check(_lib.cache_set_evict_policy(self._h, policy))
 
     def set_scorer(self, scorer: int):
         _check(_lib.cache_set_scorer(self._h, scorer))

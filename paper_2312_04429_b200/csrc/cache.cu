@@ -107,6 +107,7 @@ struct cache_t {
     uint32_t* present = nullptr;    // [cap_pad]       bit j = K_j stored
     int32_t* lslot = nullptr;       // [cap_pad][num_k] latent-pool slot (-1 = hole)
     uint32_t* fcnt = nullptr;       // [cap_pad][num_k] LCBFU access counts f
+    uint32_t* lastacc = nullptr;    // [cap_pad][num_k] batch clock of the last access (LRU)
     uint8_t* pool = nullptr;        // [lcap][L]       intermediate states
     CUtensorMap tm_e;               // TMA map of emb (box 64 x 256)
     bool tm_e_ok = false;
@@ -117,6 +118,7 @@ struct cache_t {
     std::unordered_map<uint64_t, int64_t> id2slot;
     int64_t hwm = 0, live_entries = 0, live_items = 0, queries = 0;
     uint64_t next_id = 0;
+    uint32_t clock = 0;             // query batches so far (the LRU logical clock)
     int scorer = CACHE_SCORER_AUTO;
     int64_t launches = 0;
     cudaEvent_t prof[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -202,6 +204,11 @@ cache_status cache_create(const cache_config* cfg, int device, cache_t** out) {
     for (int j = 0; j < c->num_k; ++j) { c->km.thr[j] = cfg->thresholds[j]; c->km.kv[j] = cfg->k_values[j]; }
     c->km.num_k = c->num_k;
     c->km.k_bias = cfg->k_bias;
+    c->km.policy = cfg->evict_policy;
+    if (cfg->evict_policy < CACHE_POLICY_LCBFU || cfg->evict_policy > CACHE_POLICY_FIFO) {
+        delete c;
+        return fail(CACHE_E_INVALID_ARG, "cache_create: bad evict_policy");
+    }
     c->rank = cfg->shard_rank;
     c->world = cfg->shard_world;
     c->alias = cfg->latent_alias != 0;
@@ -222,6 +229,7 @@ cache_status cache_create(const cache_config* cfg, int device, cache_t** out) {
     if ((e = cudaMalloc(&c->present, (size_t)c->cap_pad * 4)) != cudaSuccess) return bail(e, "present");
     if ((e = cudaMalloc(&c->lslot, (size_t)c->cap_pad * c->num_k * 4)) != cudaSuccess) return bail(e, "lslot");
     if ((e = cudaMalloc(&c->fcnt, (size_t)c->cap_pad * c->num_k * 4)) != cudaSuccess) return bail(e, "f");
+    if ((e = cudaMalloc(&c->lastacc, (size_t)c->cap_pad * c->num_k * 4)) != cudaSuccess) return bail(e, "lastacc");
     if (c->lcap > 0 && c->L > 0 && (e = cudaMalloc(&c->pool, (size_t)c->lcap * c->L)) != cudaSuccess)
         return bail(e, "latent pool");
     cudaMemset(c->emb, 0, (size_t)c->cap_pad * c->dim * 2);
@@ -230,6 +238,7 @@ cache_status cache_create(const cache_config* cfg, int device, cache_t** out) {
     cudaMemset(c->present, 0, (size_t)c->cap_pad * 4);
     cudaMemset(c->lslot, 0xFF, (size_t)c->cap_pad * c->num_k * 4);
     cudaMemset(c->fcnt, 0, (size_t)c->cap_pad * c->num_k * 4);
+    cudaMemset(c->lastacc, 0, (size_t)c->cap_pad * c->num_k * 4);
     if ((e = cudaDeviceSynchronize()) != cudaSuccess) return bail(e, "init");
     c->tm_e_ok = encode_rows(&c->tm_e, c->emb, c->cap_pad, c->dim, 256);
     c->h_present.assign(c->cap_pad, 0);
@@ -251,7 +260,7 @@ cache_status cache_destroy(cache_t* c) {
     if (c->h_out) cudaFreeHost(c->h_out);
     c->hq_out.release();
     cudaFree(c->emb); cudaFree(c->inv_e); cudaFree(c->ids); cudaFree(c->present);
-    cudaFree(c->lslot); cudaFree(c->fcnt); cudaFree(c->pool);
+    cudaFree(c->lslot); cudaFree(c->fcnt); cudaFree(c->lastacc); cudaFree(c->pool);
     c->qbuf.release(); c->ystage.release(); c->invq.release(); c->invstage.release();
     c->qstat.release(); c->istat.release(); c->gk.release(); c->recs.release(); c->iplan.release(); c->cplan.release();
     c->hq_in.release(); c->hq_lat.release(); c->hq_ids.release(); c->hq_sc.release(); c->hq_k.release();
@@ -353,7 +362,7 @@ cache_status cache_insert(cache_t* c, int64_t n, const void* emb, int32_t emb_dt
         CK(c->iplan.ensure(std::max<size_t>(plan.size(), 1)));
         CK(cudaMemcpyAsync(c->iplan.p, plan.data(), plan.size() * sizeof(InsertPlan), cudaMemcpyHostToDevice, s));
         launch_insert_commit(c->ystage.p, c->invstage.p, c->iplan.p, (int64_t)plan.size(), c->dim, c->num_k,
-                             c->emb, c->inv_e, c->ids, c->present, c->lslot, c->fcnt, s);
+                             c->emb, c->inv_e, c->ids, c->present, c->lslot, c->fcnt, c->lastacc, c->clock, s);
         c->launches++;
         if (!cp.empty()) {
             CK(c->cplan.ensure(cp.size()));
@@ -427,9 +436,10 @@ static cache_status query_core(cache_t* c, int64_t b, const void* queries, int32
     cache_status r = scan_core(c, b, queries, q_dtype, kmax, s, &parts);
     if (r != CACHE_OK) return r;
     if (c->prof_on) CK(cudaEventRecord(c->prof[2], s));
+    c->clock++;   // one query batch = one tick of the LRU clock
     launch_finalize(kmax, c->recs.p, parts, b, topk, c->invq.p, c->qstat.p, c->ids, c->present, c->lslot,
-                    c->fcnt, c->pool, c->L, c->km, out_ids, out_scores, out_k, (uint8_t*)latent_out, out_ptr,
-                    row_status, s);
+                    c->fcnt, c->lastacc, c->clock, c->pool, c->L, c->km, out_ids, out_scores, out_k,
+                    (uint8_t*)latent_out, out_ptr, row_status, s);
     c->launches++;
     if (c->prof_on) CK(cudaEventRecord(c->prof[3], s));
     CK(cudaGetLastError());
@@ -485,7 +495,9 @@ cache_status cache_query_merge(cache_t* c, int64_t b, int64_t row0, int64_t nb, 
     if (c->qstat.n < (size_t)b) return fail(CACHE_E_STATE, "cache_query_merge: no matching cache_query_local batch");
     DeviceGuard g(c->device);
     const int kmax = topk == 1 ? 1 : (topk <= 4 ? 4 : 16);
-    launch_merge_sharded(kmax, recs, c->world, b, row0, nb, topk, c->invq.p, c->qstat.p, c->peers, c->L, c->km,
+    c->clock++;   // every rank merges once per global batch -> the clocks agree across ranks
+    launch_merge_sharded(kmax, recs, c->world, b, row0, nb, topk, c->invq.p, c->qstat.p, c->peers, c->clock, c->L,
+                         c->km,
                          out_ids, out_scores, out_k, (uint8_t*)latent_out, out_latent_ptr, row_status,
                          (cudaStream_t)stream);
     c->launches++;
@@ -513,6 +525,7 @@ cache_status cache_export_peer(cache_t* c, cache_peer_desc* out) {
     out->latent_bytes = c->L;
     out->lslot = c->lslot;
     out->fcnt = c->fcnt;
+    out->lastacc = c->lastacc;
     out->pool = c->pool;
     cudaIpcMemHandle_t h;
     static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
@@ -520,6 +533,8 @@ cache_status cache_export_peer(cache_t* c, cache_peer_desc* out) {
     std::memcpy(out->ipc_lslot, &h, 64);
     CK(cudaIpcGetMemHandle(&h, c->fcnt));
     std::memcpy(out->ipc_fcnt, &h, 64);
+    CK(cudaIpcGetMemHandle(&h, c->lastacc));
+    std::memcpy(out->ipc_lastacc, &h, 64);
     if (c->pool) {
         CK(cudaIpcGetMemHandle(&h, c->pool));
         std::memcpy(out->ipc_pool, &h, 64);
@@ -539,6 +554,7 @@ cache_status cache_attach_peers(cache_t* c, int32_t world, const cache_peer_desc
         if (d.pid == me) {   // same process (own rank, or virtual ranks sharing one GPU)
             p.lslot[r] = (const int32_t*)d.lslot;
             p.fcnt[r] = (uint32_t*)d.fcnt;
+            p.lastacc[r] = (uint32_t*)d.lastacc;
             p.pool[r] = (const uint8_t*)d.pool;
             continue;
         }
@@ -552,6 +568,10 @@ cache_status cache_attach_peers(cache_t* c, int32_t world, const cache_peer_desc
         CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
         c->ipc_opened.push_back(ptr);
         p.fcnt[r] = (uint32_t*)ptr;
+        std::memcpy(&h, d.ipc_lastacc, 64);
+        CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+        c->ipc_opened.push_back(ptr);
+        p.lastacc[r] = (uint32_t*)ptr;
         if (d.pool) {
             std::memcpy(&h, d.ipc_pool, 64);
             CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
@@ -625,7 +645,7 @@ cache_status cache_evict_hist(cache_t* c, const cache_evict_state* st, int32_t p
     DeviceGuard g(c->device);
     cudaStream_t s = (cudaStream_t)stream;
     CK(cudaMemsetAsync(hist, 0, 256 * 4, s));
-    launch_evict_hist(c->present, c->fcnt, c->ids, c->hwm, c->km, reinterpret_cast<const EvictState*>(st), pass,
+    launch_evict_hist(c->present, c->fcnt, c->lastacc, c->ids, c->hwm, c->km, reinterpret_cast<const EvictState*>(st), pass,
                       hist, s);
     c->launches++;
     CK(cudaGetLastError());
@@ -680,7 +700,7 @@ cache_status cache_evict_apply(cache_t* c, const cache_evict_state* st, int64_t 
     CK(c->ecnt.ensure(2));
     CK(c->edirty.ensure(std::max<int64_t>(1, c->live_entries)));
     CK(cudaMemsetAsync(c->ecnt.p, 0, 16, s));
-    launch_evict_apply(c->present, c->fcnt, c->ids, c->lslot, c->inv_e, c->hwm, c->km,
+    launch_evict_apply(c->present, c->fcnt, c->lastacc, c->ids, c->lslot, c->inv_e, c->hwm, c->km,
                        reinterpret_cast<const EvictState*>(st), c->ekey.p, c->elslot.p, c->ecnt.p, c->edirty.p, s);
     c->launches++;
     unsigned long long cnt[2];
@@ -771,6 +791,13 @@ cache_status cache_stats(cache_t* c, cache_stats_t* out) {
     out->queries = c->queries;
     out->free_entries = (int64_t)c->free_e.size();
     out->free_items = (int64_t)c->free_l.size();
+    return CACHE_OK;
+}
+
+cache_status cache_set_evict_policy(cache_t* c, int32_t policy) {
+    if (!c || policy < CACHE_POLICY_LCBFU || policy > CACHE_POLICY_FIFO)
+        return fail(CACHE_E_INVALID_ARG, "cache_set_evict_policy: bad argument");
+    c->km.policy = policy;
     return CACHE_OK;
 }
 

@@ -115,6 +115,7 @@ struct KMap {
     int32_t kv[CACHE_MAX_K];
     int32_t num_k;
     int32_t k_bias;
+    int32_t policy;   // CACHE_POLICY_* (eviction kernels)
 };
 
 }  // namespace nv

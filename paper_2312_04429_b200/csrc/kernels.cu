@@ -265,7 +265,8 @@ __global__ void __launch_bounds__(128)
 k_finalize(const Rec* __restrict__ ws, int parts, int64_t B, int topk, const float* __restrict__ inv_q,
            const int32_t* __restrict__ qstatus, const uint32_t* __restrict__ ids,
            const uint32_t* __restrict__ present, const int32_t* __restrict__ lslot,
-           uint32_t* __restrict__ fcnt, const uint8_t* __restrict__ pool, int64_t latent_bytes,
+           uint32_t* __restrict__ fcnt, uint32_t* __restrict__ lastacc, uint32_t clock,
+           const uint8_t* __restrict__ pool, int64_t latent_bytes,
            KMap km, uint64_t* __restrict__ out_ids, float* __restrict__ out_scores,
            int32_t* __restrict__ out_k, uint8_t* __restrict__ latent_out, void** __restrict__ out_ptr,
            int32_t* __restrict__ out_status) {
@@ -321,6 +322,7 @@ k_finalize(const Rec* __restrict__ ws, int parts, int64_t B, int topk, const flo
                         K = km.kv[j];
                         src = lslot[(int64_t)slot * km.num_k + j];
                         atomicAdd(fcnt + (int64_t)slot * km.num_k + j, 1u);
+                        lastacc[(int64_t)slot * km.num_k + j] = clock;   // LRU clock (same value for all hits)
                     }
                 }
             }
@@ -351,14 +353,16 @@ k_finalize(const Rec* __restrict__ ws, int parts, int64_t B, int topk, const flo
 
 void launch_finalize(int kmax, const Rec* ws, int parts, int64_t B, int topk, const float* inv_q,
                      const int32_t* qstatus, const uint32_t* ids, const uint32_t* present,
-                     const int32_t* lslot, uint32_t* fcnt, const uint8_t* pool, int64_t latent_bytes,
+                     const int32_t* lslot, uint32_t* fcnt, uint32_t* lastacc, uint32_t clock,
+                     const uint8_t* pool, int64_t latent_bytes,
                      const KMap& km, uint64_t* out_ids, float* out_scores, int32_t* out_k,
                      uint8_t* latent_out, void** out_ptr, int32_t* out_status, cudaStream_t s) {
     if (B <= 0) return;
 #define NV_FIN(KM)                                                                                \
     k_finalize<KM><<<(unsigned)B, 128, 0, s>>>(ws, parts, B, topk, inv_q, qstatus, ids, present, \
-                                               lslot, fcnt, pool, latent_bytes, km, out_ids,     \
-                                               out_scores, out_k, latent_out, out_ptr, out_status)
+                                               lslot, fcnt, lastacc, clock, pool, latent_bytes,   \
+                                               km, out_ids, out_scores, out_k, latent_out, out_ptr, \
+                                               out_status)
     if (kmax == 1) NV_FIN(1);
     else if (kmax == 4) NV_FIN(4);
     else NV_FIN(16);
@@ -372,7 +376,8 @@ __global__ void __launch_bounds__(128)
 k_insert_commit(const __nv_bfloat16* __restrict__ ystage, const float* __restrict__ invstage,
                 const InsertPlan* __restrict__ plan, int64_t n_valid, int dim, int num_k,
                 __nv_bfloat16* __restrict__ emb, float* __restrict__ inv_e, uint32_t* __restrict__ ids,
-                uint32_t* __restrict__ present, int32_t* __restrict__ lslot, uint32_t* __restrict__ fcnt) {
+                uint32_t* __restrict__ present, int32_t* __restrict__ lslot, uint32_t* __restrict__ fcnt,
+                uint32_t* __restrict__ lastacc, uint32_t clock) {
     const int64_t i = blockIdx.x;
     if (i >= n_valid) return;
     const InsertPlan p = plan[i];
@@ -382,6 +387,7 @@ k_insert_commit(const __nv_bfloat16* __restrict__ ystage, const float* __restric
     if (threadIdx.x < num_k) {
         lslot[p.slot * num_k + threadIdx.x] = p.lslot[threadIdx.x];
         fcnt[p.slot * num_k + threadIdx.x] = 0u;
+        lastacc[p.slot * num_k + threadIdx.x] = clock;   // LRU: a fresh item counts as just used
     }
     if (threadIdx.x == 0) {
         inv_e[p.slot] = invstage[p.src_row];
@@ -403,10 +409,11 @@ k_copy_latents(const uint8_t* __restrict__ src, const CopyPlan* __restrict__ pla
 
 void launch_insert_commit(const __nv_bfloat16* ystage, const float* invstage, const InsertPlan* plan,
                           int64_t n_valid, int dim, int num_k, __nv_bfloat16* emb, float* inv_e,
-                          uint32_t* ids, uint32_t* present, int32_t* lslot, uint32_t* fcnt, cudaStream_t s) {
+                          uint32_t* ids, uint32_t* present, int32_t* lslot, uint32_t* fcnt, uint32_t* lastacc,
+                          uint32_t clock, cudaStream_t s) {
     if (n_valid > 0)
         k_insert_commit<<<(unsigned)n_valid, 128, 0, s>>>(ystage, invstage, plan, n_valid, dim, num_k,
-                                                          emb, inv_e, ids, present, lslot, fcnt);
+                                                          emb, inv_e, ids, present, lslot, fcnt, lastacc, clock);
 }
 
 void launch_copy_latents(const uint8_t* src, const CopyPlan* plan, int64_t n, int64_t latent_bytes,
@@ -422,16 +429,27 @@ void launch_copy_latents(const uint8_t* src, const CopyPlan* plan, int64_t n, in
 // evicted: presence bit cleared, latent slot freed; entries left with no K are dirty and
 // are invalidated (inv_norm = NaN) in the same kernel.
 // ---------------------------------------------------------------------------------------
-__device__ __forceinline__ unsigned long long evict_key(uint32_t f, int kval, uint32_t id, int j) {
-    unsigned long long sc = (unsigned long long)f * (unsigned long long)kval;
+// Policy score of item (e, j) (CACHE_POLICY_*): LCBFU f*K, LRU last-access clock,
+// LFU f, FIFO 0 (the id decides).  Saturated at 2^29-1 to fit the 64-bit key.
+__device__ __forceinline__ unsigned long long evict_key(const KMap& km, const uint32_t* __restrict__ fcnt,
+                                                        const uint32_t* __restrict__ lastacc, int64_t e, int j,
+                                                        uint32_t id) {
+    const int64_t it = e * km.num_k + j;
+    unsigned long long sc;
+    switch (km.policy) {
+        case CACHE_POLICY_LRU: sc = lastacc[it]; break;
+        case CACHE_POLICY_LFU: sc = fcnt[it]; break;
+        case CACHE_POLICY_FIFO: sc = 0ull; break;
+        default: sc = (unsigned long long)fcnt[it] * (unsigned long long)km.kv[j]; break;
+    }
     if (sc > 0x1FFFFFFFull) sc = 0x1FFFFFFFull;
     return (sc << 35) | ((unsigned long long)id << 3) | (unsigned long long)j;
 }
 
 __global__ void __launch_bounds__(256)
 k_evict_hist(const uint32_t* __restrict__ present, const uint32_t* __restrict__ fcnt,
-             const uint32_t* __restrict__ ids, int64_t n_slots, KMap km, const EvictState* __restrict__ st,
-             int shift, unsigned int* __restrict__ hist) {
+             const uint32_t* __restrict__ lastacc, const uint32_t* __restrict__ ids, int64_t n_slots, KMap km,
+             const EvictState* __restrict__ st, int shift, unsigned int* __restrict__ hist) {
     __shared__ unsigned int sh[256];
     sh[threadIdx.x] = 0;
     __syncthreads();
@@ -443,7 +461,7 @@ k_evict_hist(const uint32_t* __restrict__ present, const uint32_t* __restrict__ 
         const uint32_t id = ids[e];
         for (int j = 0; j < km.num_k; ++j) {
             if (!((m >> j) & 1u)) continue;
-            const unsigned long long key = evict_key(fcnt[e * km.num_k + j], km.kv[j], id, j);
+            const unsigned long long key = evict_key(km, fcnt, lastacc, e, j, id);
             if ((key & mask) == prefix) atomicAdd(&sh[(key >> shift) & 255ull], 1u);
         }
     }
@@ -470,8 +488,9 @@ __global__ void k_evict_pick(unsigned int* __restrict__ hist, EvictState* __rest
 }
 
 __global__ void __launch_bounds__(256)
-k_evict_apply(uint32_t* __restrict__ present, uint32_t* __restrict__ fcnt, const uint32_t* __restrict__ ids,
-              const int32_t* __restrict__ lslot, float* __restrict__ inv_e, int64_t n_slots, KMap km,
+k_evict_apply(uint32_t* __restrict__ present, uint32_t* __restrict__ fcnt, const uint32_t* __restrict__ lastacc,
+              const uint32_t* __restrict__ ids, const int32_t* __restrict__ lslot, float* __restrict__ inv_e,
+              int64_t n_slots, KMap km,
               const EvictState* __restrict__ st, unsigned long long* __restrict__ ev_key,
               int32_t* __restrict__ ev_lslot, unsigned long long* __restrict__ counters,
               int64_t* __restrict__ dirty_slot) {
@@ -484,7 +503,7 @@ k_evict_apply(uint32_t* __restrict__ present, uint32_t* __restrict__ fcnt, const
         uint32_t keep = m;
         for (int j = 0; j < km.num_k; ++j) {
             if (!((m >> j) & 1u)) continue;
-            const unsigned long long key = evict_key(fcnt[e * km.num_k + j], km.kv[j], id, j);
+            const unsigned long long key = evict_key(km, fcnt, lastacc, e, j, id);
             if (key <= T) {
                 keep &= ~(1u << j);
                 const unsigned long long at = atomicAdd(&counters[0], 1ull);
@@ -504,10 +523,11 @@ k_evict_apply(uint32_t* __restrict__ present, uint32_t* __restrict__ fcnt, const
     }
 }
 
-void launch_evict_hist(const uint32_t* present, const uint32_t* fcnt, const uint32_t* ids, int64_t n_slots,
-                       const KMap& km, const EvictState* st, int pass, unsigned int* hist, cudaStream_t s) {
+void launch_evict_hist(const uint32_t* present, const uint32_t* fcnt, const uint32_t* lastacc, const uint32_t* ids,
+                       int64_t n_slots, const KMap& km, const EvictState* st, int pass, unsigned int* hist,
+                       cudaStream_t s) {
     const int grid = (int)std::min<int64_t>(148 * 8, (n_slots + 255) / 256 + 1);
-    k_evict_hist<<<grid, 256, 0, s>>>(present, fcnt, ids, n_slots, km, st, 56 - 8 * pass, hist);
+    k_evict_hist<<<grid, 256, 0, s>>>(present, fcnt, lastacc, ids, n_slots, km, st, 56 - 8 * pass, hist);
 }
 
 void launch_evict_pick(unsigned int* hist, EvictState* st, int pass, cudaStream_t s) {
@@ -575,7 +595,8 @@ template <int KMAX>
 __global__ void __launch_bounds__(128)
 k_merge_sharded(const cache_shard_rec* __restrict__ recs, int world, int64_t B, int64_t row0, int topk,
                 const float* __restrict__ inv_q, const int32_t* __restrict__ qstatus, PeerPtrs peers,
-                int64_t latent_bytes, KMap km, uint64_t* __restrict__ out_ids, float* __restrict__ out_scores,
+                uint32_t clock, int64_t latent_bytes, KMap km, uint64_t* __restrict__ out_ids,
+                float* __restrict__ out_scores,
                 int32_t* __restrict__ out_k, uint8_t* __restrict__ latent_out, void** __restrict__ out_ptr,
                 int32_t* __restrict__ out_status) {
     __shared__ unsigned long long s_key[KMAX];
@@ -644,6 +665,7 @@ k_merge_sharded(const cache_shard_rec* __restrict__ recs, int world, int64_t B, 
                         const int64_t e = (int64_t)s_slot[0] * km.num_k + j;
                         src = peers.lslot[owner][e];                  // P2P read of the owner's table
                         atomicAdd(peers.fcnt[owner] + e, 1u);         // P2P atomic on the owner's f
+                        peers.lastacc[owner][e] = clock;              // P2P store of the LRU clock
                     }
                 }
             }
@@ -674,26 +696,27 @@ k_merge_sharded(const cache_shard_rec* __restrict__ recs, int world, int64_t B, 
 
 void launch_merge_sharded(int kmax, const cache_shard_rec* recs, int world, int64_t B, int64_t row0, int64_t nb,
                           int topk, const float* inv_q, const int32_t* qstatus, const PeerPtrs& peers,
-                          int64_t latent_bytes, const KMap& km, uint64_t* out_ids, float* out_scores,
-                          int32_t* out_k, uint8_t* latent_out, void** out_ptr, int32_t* out_status, cudaStream_t s) {
+                          uint32_t clock, int64_t latent_bytes, const KMap& km, uint64_t* out_ids,
+                          float* out_scores, int32_t* out_k, uint8_t* latent_out, void** out_ptr,
+                          int32_t* out_status, cudaStream_t s) {
     if (nb <= 0) return;
 #define NV_MS(KM)                                                                                          \
     k_merge_sharded<KM><<<(unsigned)nb, 128, 0, s>>>(recs, world, B, row0, topk, inv_q, qstatus, peers,     \
-                                                     latent_bytes, km, out_ids, out_scores, out_k, latent_out, \
-                                                     out_ptr, out_status)
+                                                     clock, latent_bytes, km, out_ids, out_scores, out_k,   \
+                                                     latent_out, out_ptr, out_status)
     if (kmax == 1) NV_MS(1);
     else if (kmax == 4) NV_MS(4);
     else NV_MS(16);
 #undef NV_MS
 }
 
-void launch_evict_apply(uint32_t* present, uint32_t* fcnt, const uint32_t* ids, const int32_t* lslot,
-                        float* inv_e, int64_t n_slots, const KMap& km, const EvictState* st,
+void launch_evict_apply(uint32_t* present, uint32_t* fcnt, const uint32_t* lastacc, const uint32_t* ids,
+                        const int32_t* lslot, float* inv_e, int64_t n_slots, const KMap& km, const EvictState* st,
                         unsigned long long* ev_key, int32_t* ev_lslot, unsigned long long* counters,
                         int64_t* dirty_slot, cudaStream_t s) {
     const int grid = (int)std::min<int64_t>(148 * 8, (n_slots + 255) / 256 + 1);
-    k_evict_apply<<<grid, 256, 0, s>>>(present, fcnt, ids, lslot, inv_e, n_slots, km, st, ev_key, ev_lslot,
-                                       counters, dirty_slot);
+    k_evict_apply<<<grid, 256, 0, s>>>(present, fcnt, lastacc, ids, lslot, inv_e, n_slots, km, st, ev_key,
+                                       ev_lslot, counters, dirty_slot);
 }
 
 }  // namespace nv

@@ -22,7 +22,7 @@ struct CopyPlan {            // one latent payload copy
     int64_t dst_slot;        // latent-pool slot
 };
 
-struct EvictState {          // radix-select state (device)
+struct EvictState {          // radix-select state (device); layout = cache_evict_state
     unsigned long long prefix;
     unsigned long long mask;
     unsigned long long remaining;
@@ -44,7 +44,7 @@ struct TcPlan {
     int chunk_tiles;    // n-tiles per chunk (top-k segment)
     int n_chunks;
     int grid;           // persistent CTAs
-    int parts;          // records per query = 2 * n_chunks
+    int parts;          // records per query = n_chunks
 };
 bool tc_supported(int dim);
 TcPlan tc_plan(int64_t b, int64_t n_slots, int sm_count);
@@ -52,38 +52,44 @@ bool launch_score_tc(int kmax, const TcPlan& plan, const void* tmap_q, const voi
                      const float* inv_e, const uint32_t* ids, int dim, int64_t b, Rec* ws,
                      uint32_t* gk, cudaStream_t s);
 
+// lastacc / clock: the LRU last-access clock of every hit item is set to `clock`
 void launch_finalize(int kmax, const Rec* ws, int parts, int64_t B, int topk, const float* inv_q,
                      const int32_t* qstatus, const uint32_t* ids, const uint32_t* present,
-                     const int32_t* lslot, uint32_t* fcnt, const uint8_t* pool, int64_t latent_bytes,
+                     const int32_t* lslot, uint32_t* fcnt, uint32_t* lastacc, uint32_t clock,
+                     const uint8_t* pool, int64_t latent_bytes,
                      const KMap& km, uint64_t* out_ids, float* out_scores, int32_t* out_k,
                      uint8_t* latent_out, void** out_ptr, int32_t* out_status, cudaStream_t s);
 
 void launch_insert_commit(const __nv_bfloat16* ystage, const float* invstage, const InsertPlan* plan,
                           int64_t n_valid, int dim, int num_k, __nv_bfloat16* emb, float* inv_e,
-                          uint32_t* ids, uint32_t* present, int32_t* lslot, uint32_t* fcnt, cudaStream_t s);
+                          uint32_t* ids, uint32_t* present, int32_t* lslot, uint32_t* fcnt, uint32_t* lastacc,
+                          uint32_t clock, cudaStream_t s);
 void launch_copy_latents(const uint8_t* src, const CopyPlan* plan, int64_t n, int64_t latent_bytes,
                          uint8_t* pool, cudaStream_t s);
 
-void launch_evict_hist(const uint32_t* present, const uint32_t* fcnt, const uint32_t* ids, int64_t n_slots,
-                       const KMap& km, const EvictState* st, int pass, unsigned int* hist, cudaStream_t s);
+void launch_evict_hist(const uint32_t* present, const uint32_t* fcnt, const uint32_t* lastacc, const uint32_t* ids,
+                       int64_t n_slots, const KMap& km, const EvictState* st, int pass, unsigned int* hist,
+                       cudaStream_t s);
 void launch_evict_pick(unsigned int* hist, EvictState* st, int pass, cudaStream_t s);
+void launch_evict_apply(uint32_t* present, uint32_t* fcnt, const uint32_t* lastacc, const uint32_t* ids,
+                        const int32_t* lslot, float* inv_e, int64_t n_slots, const KMap& km, const EvictState* st,
+                        unsigned long long* ev_key, int32_t* ev_lslot, unsigned long long* counters,
+                        int64_t* dirty_slot, cudaStream_t s);
 
 // sharded lookup
 constexpr int kMaxWorld = 16;
 struct PeerPtrs {                       // per-rank device pointers (own rank included)
     const int32_t* lslot[kMaxWorld];
     uint32_t* fcnt[kMaxWorld];
+    uint32_t* lastacc[kMaxWorld];
     const uint8_t* pool[kMaxWorld];
 };
 void launch_local_merge(int kmax, const Rec* ws, int parts, int64_t B, int topk, const int32_t* qstatus,
                         const uint32_t* present, int owner, cache_shard_rec* out, cudaStream_t s);
 void launch_merge_sharded(int kmax, const cache_shard_rec* recs, int world, int64_t B, int64_t row0, int64_t nb,
                           int topk, const float* inv_q, const int32_t* qstatus, const PeerPtrs& peers,
-                          int64_t latent_bytes, const KMap& km, uint64_t* out_ids, float* out_scores,
-                          int32_t* out_k, uint8_t* latent_out, void** out_ptr, int32_t* out_status, cudaStream_t s);
-void launch_evict_apply(uint32_t* present, uint32_t* fcnt, const uint32_t* ids, const int32_t* lslot,
-                        float* inv_e, int64_t n_slots, const KMap& km, const EvictState* st,
-                        unsigned long long* ev_key, int32_t* ev_lslot, unsigned long long* counters,
-                        int64_t* dirty_slot, cudaStream_t s);
+                          uint32_t clock, int64_t latent_bytes, const KMap& km, uint64_t* out_ids,
+                          float* out_scores, int32_t* out_k, uint8_t* latent_out, void** out_ptr,
+                          int32_t* out_status, cudaStream_t s);
 
 }  // namespace nv

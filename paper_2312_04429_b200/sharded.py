@@ -111,6 +111,9 @@ class ShardedCache:
             raise B.CacheError(B.E_FULL, "sharded insert: some rank lacks capacity for its share")
         return self.cache.insert(emb, latents, present)
 
+    def set_evict_policy(self, policy: int):
+        self.cache.set_evict_policy(policy)
+
     def alloc_outputs(self, b_local: int, topk: int = 1, latents: bool = True):
         return self.cache.alloc_outputs(b_local, topk, latents)
 
@@ -196,6 +199,10 @@ class VirtualShards:
 
     def meta(self, id_: int):
         return self.caches[id_ % self.world].meta(id_)
+
+    def set_evict_policy(self, policy: int):
+        for c in self.caches:
+            c.set_evict_policy(policy)
 
     def stats(self):
         ss = [c.stats() for c in self.caches]

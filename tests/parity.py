@@ -78,7 +78,7 @@ def check_batch(gpu: dict, orc, q: np.ndarray, topk: int, expected_latent=None, 
                 assert np.array_equal(gpu["latents"][i], exp), f"row {i}: latent bytes differ"
         acc_ids.append(gid)
         acc_k.append(gk)
-    if adopt and acc_ids:
+    if adopt:   # one GPU query batch = one record_access call = one tick of the LRU clock
         assert orc.record_access(np.array(acc_ids, np.uint64), np.array(acc_k, np.int32)) == 0
     return rep
 
