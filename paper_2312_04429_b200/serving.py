@@ -1,0 +1,158 @@
+"""Alg. 1 serving loop over a request stream + the paper's analytic accounting.
+
+Per batch of prompt embeddings (batched):
+  lookup      cache_query_batch -> K_used per request (0 = generate from scratch)
+  hit         the diffusion model runs N - K_used steps from the retrieved state
+  miss        it runs all N steps; LCBFU insertion then admits the prompt's embedding and
+              all |K| intermediate states, evicting the policy's lowest-scored
+              items first when the cache is full ("every insertion is preceded by an
+              eviction")
+Accounting:
+  latency     hit  l_s + C (N - K)/N + l_r   (Eq. eq:latency)
+              miss l_s + C
+  f_C         sum_K hits(K) K / (requests N)  (Eq. eq:compute_saving, per K h(K) K/N)
+  h_opt(K)    fraction of requests served at exactly K; h(K) = sum_{K' >= K} h_opt(K');
+              overall hit-rate h(min K) = sum_K h_opt(K) (Eq. eq:overall_hit)
+The loop only orchestrates library calls; every lookup, eviction and insertion runs in the
+CUDA library through the cache object it is given.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+
+@dataclass
+class LatencyParams:
+    """Paper constants: C ~ 8.59 s for N = 50 DDIM steps on an A10g, l_s of
+    the order of 100 ms; l_r is not given numerically (SPEC's default 50 ms)."""
+    C: float = 8.59
+    l_s: float = 0.1
+    l_r: float = 0.05
+    N: int = 50
+
+
+@dataclass
+class RunReport:
+    k_values: tuple
+    requests: int = 0
+    hits_at: dict = field(default_factory=dict)      # K -> count
+    latencies: list = field(default_factory=list)
+    steps: int = 0
+    evicted_items: int = 0
+    admitted_prompts: int = 0
+    dirty_removed: int = 0
+
+    def h_opt(self):
+        return {k: self.hits_at.get(k, 0) / max(1, self.requests) for k in self.k_values}
+
+    def h(self):
+        ho = self.h_opt()
+        return {k: sum(v for kk, v in ho.items() if kk >= k) for k in self.k_values}
+
+    @property
+    def hit_rate(self):
+        return sum(self.h_opt().values())
+
+    def f_c(self, N):
+        return sum(k * c for k, c in self.hits_at.items()) / (max(1, self.requests) * N)
+
+    def summary(self, lat: LatencyParams):
+        L = np.asarray(self.latencies)
+        return dict(requests=self.requests, hit_rate=self.hit_rate, h_opt=self.h_opt(), h=self.h(),
+                    f_c=self.f_c(lat.N), f_c_from_steps=1.0 - self.steps / (max(1, self.requests) * lat.N),
+                    per_k_savings={k: v * k / lat.N for k, v in self.h_opt().items()},
+                    mean_latency_s=float(L.mean()) if len(L) else 0.0,
+                    p50_latency_s=float(np.percentile(L, 50)) if len(L) else 0.0,
+                    p99_latency_s=float(np.percentile(L, 99)) if len(L) else 0.0,
+                    latency_reduction_vs_scratch=1.0 - float(L.mean()) / (lat.C) if len(L) else 0.0,
+                    evicted_items=self.evicted_items, admitted_prompts=self.admitted_prompts,
+                    dirty_removed=self.dirty_removed)
+
+
+def request_latency(k_used: int, lat: LatencyParams) -> float:
+    """Eq. eq:latency for a hit at K; l_s + C for a miss."""
+    if k_used > 0:
+        return lat.l_s + lat.C * (lat.N - k_used) / lat.N + lat.l_r
+    return lat.l_s + lat.C
+
+
+class ServingLoop:
+    """cache: an object with lookup(q) -> (ids, K), admit(emb, latents), evict(n) -> (evicted,
+    dirty), free() -> (free entries, free items); see GpuCache for the library adapter."""
+
+    def __init__(self, cache, k_values, lat: LatencyParams = LatencyParams(), make_latents=None):
+        self.cache, self.k_values, self.lat = cache, tuple(k_values), lat
+        self.make_latents = make_latents
+        self.report = RunReport(k_values=self.k_values)
+        self._admitted = 0
+
+    def step(self, q: np.ndarray):
+        ids, ks = self.cache.lookup(q)
+        r = self.report
+        for k in ks.tolist():
+            r.requests += 1
+            if k > 0:
+                r.hits_at[k] = r.hits_at.get(k, 0) + 1
+            r.steps += self.lat.N - k
+            r.latencies.append(request_latency(k, self.lat))
+        miss = np.nonzero(ks == 0)[0]
+        if len(miss):
+            self._admit(q[miss])
+        return ids, ks
+
+    def _admit(self, emb: np.ndarray):
+        nk = len(self.k_values)
+        need_e, need_i = len(emb), len(emb) * nk
+        fe, fi = self.cache.free()
+        short = max(0, need_i - fi)
+        if fe < need_e:          # entries only come back when all of an entry's K are evicted
+            short = max(short, (need_e - fe) * nk)
+        if short:
+            ev, dirty = self.cache.evict(short)
+            self.report.evicted_items += len(ev)
+            self.report.dirty_removed += len(dirty)
+            fe, fi = self.cache.free()
+        m = min(len(emb), fe, fi // nk)
+        if m <= 0:
+            return
+        lat = self.make_latents(self._admitted, m) if self.make_latents else None
+        self.cache.admit(emb[:m], lat)
+        self._admitted += m
+        self.report.admitted_prompts += m
+
+
+class GpuCache:
+    """ServingLoop adapter over binding.NirvanaCache (device buffers, CUDA library calls)."""
+
+    def __init__(self, cache, device="cuda"):
+        import torch
+        self.c, self.torch, self.device = cache, torch, device
+
+    def lookup(self, q):
+        out = self.c.query(self.torch.from_numpy(np.ascontiguousarray(q)).to(self.device), topk=1)
+        return out["ids"][:, 0].cpu().numpy().view(np.uint64), out["k"].cpu().numpy()
+
+    def admit(self, emb, latents):
+        self.c.insert(self.torch.from_numpy(np.ascontiguousarray(emb)).to(self.device), latents)
+
+    def evict(self, n):
+        return self.c.evict(n)
+
+    def free(self):
+        s = self.c.stats()
+        return s["free_entries"], s["free_items"]
+
+
+# ------------------------- footnote closed forms ------------------------------
+def k_opt_linear(K_T: float, N: float):
+    """h(K) = 1 - K/K_T  =>  f_C(K) = h(K) K/N is maximal at K_OPT = K_T/2 with
+    f_C^max = K_T/(4N)."""
+    return K_T / 2.0, K_T / (4.0 * N)
+
+
+def k_opt_quadratic(K_T: float, N: float):
+    """h(K) = 1 - (K/K_T)^2  =>  K_OPT = K_T/sqrt(3), f_C^max = 2 K_T/(3 sqrt(3) N)."""
+    return K_T / math.sqrt(3.0), 2.0 * K_T / (3.0 * math.sqrt(3.0) * N)

@@ -1,0 +1,34 @@
+"""NEXT-1 on the GPU: the serving loop driving the CUDA library agrees with the same loop
+driving the fp64 oracle (aggregate decisions; individual near-threshold decisions may differ
+within the parity tolerance and then cascade through admission), and is deterministic."""
+import numpy as np
+import pytest
+
+import synth
+from paper_2312_04429_b200.serving import GpuCache, LatencyParams, ServingLoop
+from tests.test_serving import OracleAdapter
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(cache, universe, cl, n_batches=15, b=64):
+    loop = ServingLoop(cache, synth.K_VALUES, LatencyParams())
+    for i in range(n_batches):
+        q, _, _ = synth.queries(universe, cl, b, seed=300 + i)
+        loop.step(q)
+    return loop.report.summary(loop.lat)
+
+
+def test_gpu_serving_loop_matches_oracle_loop(oracle_mod):
+    from paper_2312_04429_b200 import binding as B
+    universe, cl = synth.entries(3000, seed=77)
+    runs = []
+    for _ in range(2):
+        g = B.NirvanaCache(entry_capacity=300, latent_capacity=1200, dim=768, latent_bytes=0)
+        runs.append(_run(GpuCache(g), universe, cl))
+    assert runs[0] == runs[1]
+    o = _run(OracleAdapter(oracle_mod, 768, entries=300, items=1200), universe, cl)
+    g = runs[0]
+    assert g["requests"] == o["requests"]
+    assert abs(g["hit_rate"] - o["hit_rate"]) <= 0.02 and abs(g["f_c"] - o["f_c"]) <= 0.01, (g, o)
+    assert g["evicted_items"] > 0
