@@ -348,6 +348,14 @@ def main():
     roof["peak_source"] = peak_src
     roof["traffic"] = _ncu_traffic(scorer_used, args.config)
     roof["algorithmic_per_launch"] = flops if roof["bound"] == "tensor" else bytes_scan
+    # the gather (finalize) kernel is HBM-bound: 2 x 32 KiB per hit (pool read + denoiser-buffer
+    # write) + the partial records it merges; reported beside the dominant kernel
+    fin_ms = statistics.mean(fin_ms)
+    hits = int((out["k"] > 0).sum().item())
+    g_bytes = 2 * L * hits + b * 16 * 64
+    gather_roof = dict(bound="hbm", achieved=g_bytes / (fin_ms / 1e3) / 1e9, peak=hbm, unit="GB/s",
+                       frac=g_bytes / (fin_ms / 1e3) / 1e9 / hbm, kernel="finalize_gather",
+                       algorithmic_per_launch=g_bytes)
     # end-to-end through the public host-buffer API (H2D queries + D2H results incl. latents)
     e2e = None
     if not args.no_e2e:
@@ -414,8 +422,9 @@ def main():
                                 scorer=scorer_used, l2="flushed between timed steps (512 MiB write)",
                                 parallelism=f"replicas x{world}" if world > 1 else "single GPU",
                                 hit_rate=float((k_np > 0).mean())),
-                    kernel_ms=dict(ingest=statistics.mean(prep_ms), score=sc_ms, finalize_gather=statistics.mean(fin_ms)),
-                    roofline=roof, cpu_baseline=cpu, e2e=e2e, gpu_launches=launches, clocks=clk.summary(),
+                    kernel_ms=dict(ingest=statistics.mean(prep_ms), score=sc_ms, finalize_gather=fin_ms),
+                    roofline=roof, roofline_gather=gather_roof, cpu_baseline=cpu, e2e=e2e, gpu_launches=launches,
+                    clocks=clk.summary(),
                     maintenance=maint)
         print(json.dumps(line), flush=True)
     if world > 1:

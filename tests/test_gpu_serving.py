@@ -32,3 +32,21 @@ def test_gpu_serving_loop_matches_oracle_loop(oracle_mod):
     assert g["requests"] == o["requests"]
     assert abs(g["hit_rate"] - o["hit_rate"]) <= 0.02 and abs(g["f_c"] - o["f_c"]) <= 0.01, (g, o)
     assert g["evicted_items"] > 0
+
+
+def test_policy_direction_lcbfu_first():
+    """SPEC acceptance #6 / Table 3(b) direction: on a skewed-similarity stream at
+    two capacities LCBFU saves at least as much compute as LFU and FIFO, and >= LRU - 0.01."""
+    from paper_2312_04429_b200 import binding as B
+    universe, cl = synth.entries(50_000, seed=2024)
+    streams = [synth.queries(universe, cl, 256, seed=9000 + i)[0] for i in range(60)]
+    for cap in (2000, 8000):
+        fc = {}
+        for policy in (0, 1, 2, 3):
+            g = B.NirvanaCache(entry_capacity=cap, latent_capacity=5 * cap, dim=768, latent_bytes=0)
+            g.set_evict_policy(policy)
+            loop = ServingLoop(GpuCache(g), synth.K_VALUES, LatencyParams())
+            for q in streams:
+                loop.step(q)
+            fc[policy] = loop.report.f_c(50)
+        assert fc[0] >= fc[2] - 1e-12 and fc[0] >= fc[3] - 1e-12 and fc[0] >= fc[1] - 0.01, (cap, fc)
