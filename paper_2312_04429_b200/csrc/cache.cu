@@ -128,6 +128,7 @@ struct cache_t {
     DevBuf<float> invq, invstage;
     DevBuf<int32_t> qstat, istat;
     DevBuf<uint32_t> gk;   // per-query global k-th-best gate of the tcgen05 scorer
+    DevBuf<long long> gsrc;   // per-query pool slot to gather (-1 = none)
     DevBuf<Rec> recs;
     DevBuf<InsertPlan> iplan;
     DevBuf<CopyPlan> cplan;
@@ -386,6 +387,7 @@ static cache_status scan_core(cache_t* c, int64_t b, const void* queries, int32_
     CK(c->invq.ensure(bpad));
     CK(c->qstat.ensure(bpad));
     CK(c->gk.ensure(bpad));
+    CK(c->gsrc.ensure(bpad));
     if (c->prof_on) CK(cudaEventRecord(c->prof[0], s));
     launch_normalise(queries, q_dtype, b, c->dim, c->qbuf.p, c->invq.p, c->qstat.p, s, c->gk.p);
     c->launches++;
@@ -438,9 +440,13 @@ static cache_status query_core(cache_t* c, int64_t b, const void* queries, int32
     if (c->prof_on) CK(cudaEventRecord(c->prof[2], s));
     c->clock++;   // one query batch = one tick of the LRU clock
     launch_finalize(kmax, c->recs.p, parts, b, topk, c->invq.p, c->qstat.p, c->ids, c->present, c->lslot,
-                    c->fcnt, c->lastacc, c->clock, c->pool, c->L, c->km, out_ids, out_scores, out_k,
+                    c->fcnt, c->lastacc, c->clock, c->gsrc.p, c->L, c->km, out_ids, out_scores, out_k,
                     (uint8_t*)latent_out, out_ptr, row_status, s);
     c->launches++;
+    if (latent_out && c->pool && c->L > 0) {
+        launch_gather(c->gsrc.p, b, c->pool, c->L, (uint8_t*)latent_out, s);
+        c->launches++;
+    }
     if (c->prof_on) CK(cudaEventRecord(c->prof[3], s));
     CK(cudaGetLastError());
     c->queries += b;

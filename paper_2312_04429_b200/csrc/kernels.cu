@@ -78,12 +78,23 @@ __global__ void __launch_bounds__(256) k_normalise(const Tin* __restrict__ x, in
         return;
     }
     const double nu = __dsqrt_rn(s);
+    // bf16_RNE(x / nu) without a division per element: y = x * rcp(nu) is within ~2 fp64 ulps
+    // of x / nu, so both round to the same bf16 unless y lies within a few ulps of a bf16
+    // rounding midpoint (the 45 fp64 mantissa bits below the bf16 LSB == 2^44) or in the bf16
+    // subnormal range -- then the exact correctly rounded division is used.  Bit-identical
+    // to bf16_RNE(__ddiv_rn(x, nu)) by construction.
+    const double rnu = __drcp_rn(nu);
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
         const int i = lane + 32 * k;
         double yd = 0.0;
         if (i < dim) {
-            const __nv_bfloat16 b = __double2bfloat16(__ddiv_rn(load_in<Tin>(xr + i), nu));  // cvt.rn.bf16.f64
+            const double x = load_in<Tin>(xr + i);
+            double y = __dmul_rn(x, rnu);
+            const long long low = (long long)((unsigned long long)__double_as_longlong(y) & ((1ull << 45) - 1));
+            const long long dm = low - (1ll << 44);
+            if ((dm <= 16 && dm >= -16) || fabs(y) < 0x1p-120) y = __ddiv_rn(x, nu);
+            const __nv_bfloat16 b = __double2bfloat16(y);   // cvt.rn.bf16.f64
             yr[i] = b;
             yd = (double)__bfloat162float(b);
         }
@@ -254,11 +265,11 @@ void launch_score_stream(int kmax, const __nv_bfloat16* emb, const float* inv_e,
 }
 
 // ---------------------------------------------------------------------------------------
-// Finalize: one 128-thread CTA per query.  Warp 0 merges the `parts` partial lists under
+// Finalize: one warp per query (4 per CTA).  The warp merges the `parts` partial lists under
 // the total order (R3) -> top-k; lane 0 applies the Fig. 11 map (largest j with
 // s > thr[j], strict, compared in fp64 on the clamped fp32 score), the knob (R20) and the
-// hole rule (m = present & ((2 << j*) - 1), j = 31 - clz(m)); then the whole CTA
-// copies the selected latent (128-bit loads/stores) and one thread counts the access.
+// hole rule (m = present & ((2 << j*) - 1), j = 31 - clz(m)), counts the access
+// and emits the pool slot to gather (gsrc[b], -1 = none).  k_gather then moves the states.
 // ---------------------------------------------------------------------------------------
 template <int KMAX>
 __global__ void __launch_bounds__(128)
@@ -266,17 +277,19 @@ k_finalize(const Rec* __restrict__ ws, int parts, int64_t B, int topk, const flo
            const int32_t* __restrict__ qstatus, const uint32_t* __restrict__ ids,
            const uint32_t* __restrict__ present, const int32_t* __restrict__ lslot,
            uint32_t* __restrict__ fcnt, uint32_t* __restrict__ lastacc, uint32_t clock,
-           const uint8_t* __restrict__ pool, int64_t latent_bytes,
+           long long* __restrict__ gsrc, int64_t latent_bytes,
            KMap km, uint64_t* __restrict__ out_ids, float* __restrict__ out_scores,
            int32_t* __restrict__ out_k, uint8_t* __restrict__ latent_out, void** __restrict__ out_ptr,
            int32_t* __restrict__ out_status) {
-    __shared__ unsigned long long s_key[KMAX];
-    __shared__ uint32_t s_slot[KMAX];
-    __shared__ long long s_src;
-    const int64_t b = blockIdx.x;
+    __shared__ unsigned long long s_keys[4][KMAX];
+    __shared__ uint32_t s_slots[4][KMAX];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t b = (int64_t)blockIdx.x * 4 + warp;
+    if (b >= B) return;   // warp-uniform
+    unsigned long long* s_key = s_keys[warp];
+    uint32_t* s_slot = s_slots[warp];
     const int st = qstatus[b];
-    if (warp == 0) {
+    {
         TopK<KMAX> tk;
         tk.init();
         if (st == CACHE_ROW_OK) {
@@ -329,44 +342,57 @@ k_finalize(const Rec* __restrict__ ws, int parts, int64_t B, int topk, const flo
             out_k[b] = K;
             if (out_status) out_status[b] = st;
             if (out_ptr) out_ptr[b] = (K > 0 && latent_out) ? (void*)(latent_out + b * latent_bytes) : nullptr;
-            s_src = src;
+            gsrc[b] = src;
         }
     }
-    __syncthreads();
-    const long long src = s_src;
-    if (src >= 0 && latent_out && latent_bytes > 0) {
-        const int4* sp = reinterpret_cast<const int4*>(pool + src * latent_bytes);
-        int4* dp = reinterpret_cast<int4*>(latent_out + b * latent_bytes);
-        const int64_t nv = latent_bytes / 16;
-        int64_t i = threadIdx.x;
-        for (; i + 3 * 128 < nv; i += 4 * 128) {
-            int4 a0 = ld_stream(sp + i), a1 = ld_stream(sp + i + 128), a2 = ld_stream(sp + i + 256),
-                 a3 = ld_stream(sp + i + 384);
-            __stcs(dp + i, a0);
-            __stcs(dp + i + 128, a1);
-            __stcs(dp + i + 256, a2);
-            __stcs(dp + i + 384, a3);
-        }
-        for (; i < nv; i += 128) __stcs(dp + i, ld_stream(sp + i));
+}
+
+// Latent gather: one 256-thread CTA per query row; each thread issues all of its
+// 16-byte loads of the 32 KiB state before storing them (8 in flight per thread, 32 KiB per
+// CTA), streaming cache hints on both sides.  Rows with no hit exit at once.
+__global__ void __launch_bounds__(256)
+k_gather(const long long* __restrict__ gsrc, const uint8_t* __restrict__ pool, int64_t latent_bytes,
+         uint8_t* __restrict__ latent_out) {
+    const int64_t b = blockIdx.x;
+    const long long src = gsrc[b];
+    if (src < 0) return;
+    const int4* sp = reinterpret_cast<const int4*>(pool + src * latent_bytes);
+    int4* dp = reinterpret_cast<int4*>(latent_out + b * latent_bytes);
+    const int64_t nv = latent_bytes / 16;
+    int64_t i = threadIdx.x;
+    for (; i + 7 * 256 < nv; i += 8 * 256) {
+        int4 a[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] = ld_stream(sp + i + u * 256);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) __stcs(dp + i + u * 256, a[u]);
     }
+    for (; i < nv; i += 256) __stcs(dp + i, ld_stream(sp + i));
 }
 
 void launch_finalize(int kmax, const Rec* ws, int parts, int64_t B, int topk, const float* inv_q,
                      const int32_t* qstatus, const uint32_t* ids, const uint32_t* present,
                      const int32_t* lslot, uint32_t* fcnt, uint32_t* lastacc, uint32_t clock,
-                     const uint8_t* pool, int64_t latent_bytes,
+                     long long* gsrc, int64_t latent_bytes,
                      const KMap& km, uint64_t* out_ids, float* out_scores, int32_t* out_k,
                      uint8_t* latent_out, void** out_ptr, int32_t* out_status, cudaStream_t s) {
     if (B <= 0) return;
+    const unsigned grid = (unsigned)((B + 3) / 4);
 #define NV_FIN(KM)                                                                                \
-    k_finalize<KM><<<(unsigned)B, 128, 0, s>>>(ws, parts, B, topk, inv_q, qstatus, ids, present, \
-                                               lslot, fcnt, lastacc, clock, pool, latent_bytes,   \
-                                               km, out_ids, out_scores, out_k, latent_out, out_ptr, \
-                                               out_status)
+    k_finalize<KM><<<grid, 128, 0, s>>>(ws, parts, B, topk, inv_q, qstatus, ids, present,         \
+                                        lslot, fcnt, lastacc, clock, gsrc, latent_bytes,          \
+                                        km, out_ids, out_scores, out_k, latent_out, out_ptr,      \
+                                        out_status)
     if (kmax == 1) NV_FIN(1);
     else if (kmax == 4) NV_FIN(4);
     else NV_FIN(16);
 #undef NV_FIN
+}
+
+void launch_gather(const long long* gsrc, int64_t B, const uint8_t* pool, int64_t latent_bytes,
+                   uint8_t* latent_out, cudaStream_t s) {
+    if (B > 0 && latent_out && pool && latent_bytes > 0)
+        k_gather<<<(unsigned)B, 256, 0, s>>>(gsrc, pool, latent_bytes, latent_out);
 }
 
 // ---------------------------------------------------------------------------------------
