@@ -440,13 +440,9 @@ static cache_status query_core(cache_t* c, int64_t b, const void* queries, int32
     if (c->prof_on) CK(cudaEventRecord(c->prof[2], s));
     c->clock++;   // one query batch = one tick of the LRU clock
     launch_finalize(kmax, c->recs.p, parts, b, topk, c->invq.p, c->qstat.p, c->ids, c->present, c->lslot,
-                    c->fcnt, c->lastacc, c->clock, c->gsrc.p, c->L, c->km, out_ids, out_scores, out_k,
+                    c->fcnt, c->lastacc, c->clock, c->pool, c->L, c->km, out_ids, out_scores, out_k,
                     (uint8_t*)latent_out, out_ptr, row_status, s);
     c->launches++;
-    if (latent_out && c->pool && c->L > 0) {
-        launch_gather(c->gsrc.p, b, c->pool, c->L, (uint8_t*)latent_out, s);
-        c->launches++;
-    }
     if (c->prof_on) CK(cudaEventRecord(c->prof[3], s));
     CK(cudaGetLastError());
     c->queries += b;

@@ -19,57 +19,64 @@ namespace nv {
 // (shfl_down) -- so the sum, the correctly rounded fp64 sqrt and division and the direct
 // fp64->bf16 RNE conversion (cvt.rn.bf16.f64) give bit-identical stored rows.
 // ---------------------------------------------------------------------------------------
-__device__ __forceinline__ double warp_tree_sum(double (&v)[32], int P) {
+// NS = dim / 32 slots per lane (slot k of lane l = element l + 32k); the zero padding up to
+// P = next_pow2(dim) is implicit: an addition of a padded +0.0 to a non-negative partial sum
+// is an identity, so it is skipped at compile time without changing a single bit.
+template <int NS>
+__device__ __forceinline__ double warp_tree_sum(double (&v)[NS]) {
+    // element stride 32h pairs slot k with slot k + h of the same lane (i < s <=> k < h);
+    // slots >= NS are padding zeros and stay zero, strides >= P pair nothing
 #pragma unroll
-    for (int s = 512; s >= 32; s >>= 1) {
-        if (s < P) {
+    for (int h = 16; h >= 1; h >>= 1) {
 #pragma unroll
-            for (int k = 0; k < 16; ++k)
-                if (32 * k < s) v[k] = __dadd_rn(v[k], v[k + s / 32]);
-        }
+        for (int k = 0; k < 16; ++k)
+            if (k < h && k + h < NS) v[k] = __dadd_rn(v[k], v[k + h]);
     }
     double r = v[0];
 #pragma unroll
     for (int s = 16; s >= 1; s >>= 1) {
         const double o = __shfl_down_sync(0xFFFFFFFFu, r, s);
-        if (s < P) r = __dadd_rn(r, o);
+        r = __dadd_rn(r, o);
     }
     return __shfl_sync(0xFFFFFFFFu, r, 0);
 }
 
 template <typename Tin>
-__device__ __forceinline__ double load_in(const Tin* p);
+__device__ __forceinline__ float load_in(const Tin* p);
 template <>
-__device__ __forceinline__ double load_in<float>(const float* p) { return (double)__ldg(p); }
+__device__ __forceinline__ float load_in<float>(const float* p) { return __ldg(p); }
 template <>
-__device__ __forceinline__ double load_in<__nv_bfloat16>(const __nv_bfloat16* p) {
-    return (double)__bfloat162float(*p);
+__device__ __forceinline__ float load_in<__nv_bfloat16>(const __nv_bfloat16* p) {
+    return __bfloat162float(*p);
 }
 
-template <typename Tin>
-__global__ void __launch_bounds__(256) k_normalise(const Tin* __restrict__ x, int64_t n, int dim, int P,
+template <typename Tin, int NS>
+__global__ void __launch_bounds__(256) k_normalise(const Tin* __restrict__ x, int64_t n,
                                                    __nv_bfloat16* __restrict__ y, float* __restrict__ inv,
                                                    int32_t* __restrict__ status, uint32_t* __restrict__ gk) {
+    constexpr int dim = NS * 32;
     const int lane = threadIdx.x & 31;
     const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     if (r >= n) return;   // warp-uniform
     if (gk != nullptr && lane == 0) gk[r] = 0u;
     const Tin* xr = x + r * (int64_t)dim;
     __nv_bfloat16* yr = y + r * (int64_t)dim;
-    double v[32];
+    float xf[NS];
+    double v[NS];
     int bad = 0;
 #pragma unroll
-    for (int k = 0; k < 32; ++k) {
-        const int i = lane + 32 * k;
-        const double xv = i < dim ? load_in<Tin>(xr + i) : 0.0;
-        bad |= !isfinite(xv);
+    for (int k = 0; k < NS; ++k) xf[k] = load_in<Tin>(xr + lane + 32 * k);
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+        const double xv = (double)xf[k];
+        bad |= !isfinite(xf[k]);
         v[k] = __dmul_rn(xv, xv);
     }
     bad = __any_sync(0xFFFFFFFFu, bad);
     int st = CACHE_ROW_NONFINITE;
     double s = 0.0;
     if (!bad) {
-        s = warp_tree_sum(v, P);
+        s = warp_tree_sum<NS>(v);
         st = s == 0.0 ? CACHE_ROW_ZERO_NORM : (!isfinite(s) ? CACHE_ROW_NONFINITE : CACHE_ROW_OK);
     }
     if (st != CACHE_ROW_OK) {
@@ -85,22 +92,18 @@ __global__ void __launch_bounds__(256) k_normalise(const Tin* __restrict__ x, in
     // to bf16_RNE(__ddiv_rn(x, nu)) by construction.
     const double rnu = __drcp_rn(nu);
 #pragma unroll
-    for (int k = 0; k < 32; ++k) {
-        const int i = lane + 32 * k;
-        double yd = 0.0;
-        if (i < dim) {
-            const double x = load_in<Tin>(xr + i);
-            double y = __dmul_rn(x, rnu);
-            const long long low = (long long)((unsigned long long)__double_as_longlong(y) & ((1ull << 45) - 1));
-            const long long dm = low - (1ll << 44);
-            if ((dm <= 16 && dm >= -16) || fabs(y) < 0x1p-120) y = __ddiv_rn(x, nu);
-            const __nv_bfloat16 b = __double2bfloat16(y);   // cvt.rn.bf16.f64
-            yr[i] = b;
-            yd = (double)__bfloat162float(b);
-        }
+    for (int k = 0; k < NS; ++k) {
+        const double x = (double)xf[k];
+        double y = __dmul_rn(x, rnu);
+        const long long low = (long long)((unsigned long long)__double_as_longlong(y) & ((1ull << 45) - 1));
+        const long long dm = low - (1ll << 44);
+        if ((dm <= 16 && dm >= -16) || fabs(y) < 0x1p-120) y = __ddiv_rn(x, nu);
+        const __nv_bfloat16 b = __double2bfloat16(y);   // cvt.rn.bf16.f64
+        yr[lane + 32 * k] = b;
+        const double yd = (double)__bfloat162float(b);
         v[k] = __dmul_rn(yd, yd);
     }
-    const double s2 = warp_tree_sum(v, P);
+    const double s2 = warp_tree_sum<NS>(v);
     if (lane == 0) {
         if (s2 == 0.0) {
             inv[r] = __int_as_float(0x7FC00000);
@@ -115,13 +118,21 @@ __global__ void __launch_bounds__(256) k_normalise(const Tin* __restrict__ x, in
 void launch_normalise(const void* x, int dtype, int64_t n, int dim, __nv_bfloat16* y, float* inv,
                       int32_t* status, cudaStream_t s, uint32_t* gk) {
     if (n <= 0) return;
-    int P = 1;
-    while (P < dim) P <<= 1;
     const unsigned grid = (unsigned)((n + 7) / 8);
-    if (dtype == CACHE_DTYPE_BF16)
-        k_normalise<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)x, n, dim, P, y, inv, status, gk);
-    else
-        k_normalise<float><<<grid, 256, 0, s>>>((const float*)x, n, dim, P, y, inv, status, gk);
+#define NV_NORM_NS(NSV)                                                                                   \
+    case NSV:                                                                                             \
+        if (dtype == CACHE_DTYPE_BF16)                                                                    \
+            k_normalise<__nv_bfloat16, NSV><<<grid, 256, 0, s>>>((const __nv_bfloat16*)x, n, y, inv, status, gk); \
+        else                                                                                              \
+            k_normalise<float, NSV><<<grid, 256, 0, s>>>((const float*)x, n, y, inv, status, gk);        \
+        break;
+    switch (dim / 32) {   // dim is a multiple of 64, <= 1024
+        NV_NORM_NS(2) NV_NORM_NS(4) NV_NORM_NS(6) NV_NORM_NS(8) NV_NORM_NS(10) NV_NORM_NS(12)
+        NV_NORM_NS(14) NV_NORM_NS(16) NV_NORM_NS(18) NV_NORM_NS(20) NV_NORM_NS(22) NV_NORM_NS(24)
+        NV_NORM_NS(26) NV_NORM_NS(28) NV_NORM_NS(30) NV_NORM_NS(32)
+        default: break;
+    }
+#undef NV_NORM_NS
 }
 
 // ---------------------------------------------------------------------------------------
@@ -265,31 +276,36 @@ void launch_score_stream(int kmax, const __nv_bfloat16* emb, const float* inv_e,
 }
 
 // ---------------------------------------------------------------------------------------
-// Finalize: one warp per query (4 per CTA).  The warp merges the `parts` partial lists under
-// the total order (R3) -> top-k; lane 0 applies the Fig. 11 map (largest j with
-// s > thr[j], strict, compared in fp64 on the clamped fp32 score), the knob (R20) and the
-// hole rule (m = present & ((2 << j*) - 1), j = 31 - clz(m)), counts the access
-// and emits the pool slot to gather (gsrc[b], -1 = none).  k_gather then moves the states.
+// Finalize + gather: 8 queries per 256-thread CTA.  Warp w merges query b0+w's `parts`
+// partial lists under the total order (R3) -> top-k; its lane 0 applies the Fig. 11 map
+// (largest j with s > thr[j], strict, compared in fp64 on the clamped fp32
+// score), the knob (R20) and the hole rule (m = present & ((2 << j*) - 1),
+// j = 31 - clz(m)) and counts the access.  Then the whole CTA streams the (up to 8) selected
+// 32 KiB states into latent_out with 8 16-byte loads in flight per thread, so the
+// merges of one CTA overlap the copies of the others.
 // ---------------------------------------------------------------------------------------
+constexpr int kFinQ = 8;
 template <int KMAX>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(256)
 k_finalize(const Rec* __restrict__ ws, int parts, int64_t B, int topk, const float* __restrict__ inv_q,
            const int32_t* __restrict__ qstatus, const uint32_t* __restrict__ ids,
            const uint32_t* __restrict__ present, const int32_t* __restrict__ lslot,
            uint32_t* __restrict__ fcnt, uint32_t* __restrict__ lastacc, uint32_t clock,
-           long long* __restrict__ gsrc, int64_t latent_bytes,
+           const uint8_t* __restrict__ pool, int64_t latent_bytes,
            KMap km, uint64_t* __restrict__ out_ids, float* __restrict__ out_scores,
            int32_t* __restrict__ out_k, uint8_t* __restrict__ latent_out, void** __restrict__ out_ptr,
            int32_t* __restrict__ out_status) {
-    __shared__ unsigned long long s_keys[4][KMAX];
-    __shared__ uint32_t s_slots[4][KMAX];
+    __shared__ unsigned long long s_keys[kFinQ][KMAX];
+    __shared__ uint32_t s_slots[kFinQ][KMAX];
+    __shared__ long long s_src[kFinQ];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t b = (int64_t)blockIdx.x * 4 + warp;
-    if (b >= B) return;   // warp-uniform
+    const int64_t b0 = (int64_t)blockIdx.x * kFinQ;
+    const int64_t b = b0 + warp;
+    if (lane == 0) s_src[warp] = -1;
     unsigned long long* s_key = s_keys[warp];
     uint32_t* s_slot = s_slots[warp];
-    const int st = qstatus[b];
-    {
+    const int st = b < B ? qstatus[b] : CACHE_ROW_ZERO_NORM;
+    if (b < B) {
         TopK<KMAX> tk;
         tk.init();
         if (st == CACHE_ROW_OK) {
@@ -342,57 +358,46 @@ k_finalize(const Rec* __restrict__ ws, int parts, int64_t B, int topk, const flo
             out_k[b] = K;
             if (out_status) out_status[b] = st;
             if (out_ptr) out_ptr[b] = (K > 0 && latent_out) ? (void*)(latent_out + b * latent_bytes) : nullptr;
-            gsrc[b] = src;
+            s_src[warp] = src;
         }
     }
-}
-
-// Latent gather: one 256-thread CTA per query row; each thread issues all of its
-// 16-byte loads of the 32 KiB state before storing them (8 in flight per thread, 32 KiB per
-// CTA), streaming cache hints on both sides.  Rows with no hit exit at once.
-__global__ void __launch_bounds__(256)
-k_gather(const long long* __restrict__ gsrc, const uint8_t* __restrict__ pool, int64_t latent_bytes,
-         uint8_t* __restrict__ latent_out) {
-    const int64_t b = blockIdx.x;
-    const long long src = gsrc[b];
-    if (src < 0) return;
-    const int4* sp = reinterpret_cast<const int4*>(pool + src * latent_bytes);
-    int4* dp = reinterpret_cast<int4*>(latent_out + b * latent_bytes);
+    __syncthreads();
+    if (!latent_out || !pool || latent_bytes <= 0) return;
     const int64_t nv = latent_bytes / 16;
-    int64_t i = threadIdx.x;
-    for (; i + 7 * 256 < nv; i += 8 * 256) {
-        int4 a[8];
+    for (int w = 0; w < kFinQ; ++w) {
+        const long long src = s_src[w];
+        if (src < 0) continue;   // CTA-uniform
+        const int4* sp = reinterpret_cast<const int4*>(pool + src * latent_bytes);
+        int4* dp = reinterpret_cast<int4*>(latent_out + (b0 + w) * latent_bytes);
+        int64_t i = threadIdx.x;
+        for (; i + 7 * 256 < nv; i += 8 * 256) {
+            int4 a[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) a[u] = ld_stream(sp + i + u * 256);
+            for (int u = 0; u < 8; ++u) a[u] = ld_stream(sp + i + u * 256);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) __stcs(dp + i + u * 256, a[u]);
+            for (int u = 0; u < 8; ++u) __stcs(dp + i + u * 256, a[u]);
+        }
+        for (; i < nv; i += 256) __stcs(dp + i, ld_stream(sp + i));
     }
-    for (; i < nv; i += 256) __stcs(dp + i, ld_stream(sp + i));
 }
 
 void launch_finalize(int kmax, const Rec* ws, int parts, int64_t B, int topk, const float* inv_q,
                      const int32_t* qstatus, const uint32_t* ids, const uint32_t* present,
                      const int32_t* lslot, uint32_t* fcnt, uint32_t* lastacc, uint32_t clock,
-                     long long* gsrc, int64_t latent_bytes,
+                     const uint8_t* pool, int64_t latent_bytes,
                      const KMap& km, uint64_t* out_ids, float* out_scores, int32_t* out_k,
                      uint8_t* latent_out, void** out_ptr, int32_t* out_status, cudaStream_t s) {
     if (B <= 0) return;
-    const unsigned grid = (unsigned)((B + 3) / 4);
+    const unsigned grid = (unsigned)((B + kFinQ - 1) / kFinQ);
 #define NV_FIN(KM)                                                                                \
-    k_finalize<KM><<<grid, 128, 0, s>>>(ws, parts, B, topk, inv_q, qstatus, ids, present,         \
-                                        lslot, fcnt, lastacc, clock, gsrc, latent_bytes,          \
+    k_finalize<KM><<<grid, 256, 0, s>>>(ws, parts, B, topk, inv_q, qstatus, ids, present,         \
+                                        lslot, fcnt, lastacc, clock, pool, latent_bytes,          \
                                         km, out_ids, out_scores, out_k, latent_out, out_ptr,      \
                                         out_status)
     if (kmax == 1) NV_FIN(1);
     else if (kmax == 4) NV_FIN(4);
     else NV_FIN(16);
 #undef NV_FIN
-}
-
-void launch_gather(const long long* gsrc, int64_t B, const uint8_t* pool, int64_t latent_bytes,
-                   uint8_t* latent_out, cudaStream_t s) {
-    if (B > 0 && latent_out && pool && latent_bytes > 0)
-        k_gather<<<(unsigned)B, 256, 0, s>>>(gsrc, pool, latent_bytes, latent_out);
 }
 
 // ---------------------------------------------------------------------------------------

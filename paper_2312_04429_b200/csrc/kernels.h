@@ -56,12 +56,9 @@ bool launch_score_tc(int kmax, const TcPlan& plan, const void* tmap_q, const voi
 void launch_finalize(int kmax, const Rec* ws, int parts, int64_t B, int topk, const float* inv_q,
                      const int32_t* qstatus, const uint32_t* ids, const uint32_t* present,
                      const int32_t* lslot, uint32_t* fcnt, uint32_t* lastacc, uint32_t clock,
-                     long long* gsrc, int64_t latent_bytes,
+                     const uint8_t* pool, int64_t latent_bytes,
                      const KMap& km, uint64_t* out_ids, float* out_scores, int32_t* out_k,
                      uint8_t* latent_out, void** out_ptr, int32_t* out_status, cudaStream_t s);
-// copies pool[gsrc[b]] -> latent_out[b] for every row with gsrc[b] >= 0
-void launch_gather(const long long* gsrc, int64_t B, const uint8_t* pool, int64_t latent_bytes,
-                   uint8_t* latent_out, cudaStream_t s);
 
 void launch_insert_commit(const __nv_bfloat16* ystage, const float* invstage, const InsertPlan* plan,
                           int64_t n_valid, int dim, int num_k, __nv_bfloat16* emb, float* inv_e,
