@@ -20,7 +20,11 @@ rows = page("source", ["--print-source", "sass"])
 h = rows[1]
 si = h.index("Warp Stall Sampling (All Samples)"); ei = h.index("Instructions Executed")
 stall_cols = [i for i, n in enumerate(h) if n.startswith("stall_") and "Not Issued" not in n]
-data = [r for r in rows[2:] if len(r) == len(h)]
+data = []
+for r in rows[2:]:          # first kernel of the report only (a new header starts the next)
+    if len(r) != len(h) or r[0] in ("Address", "Kernel Name"):
+        break
+    data.append(r)
 tot = sum(float(r[si]) for r in data) or 1
 print("--- top stall lines")
 for r in sorted(data, key=lambda r: -float(r[si]))[:int(sys.argv[2]) if len(sys.argv) > 2 else 15]:
