@@ -159,7 +159,8 @@ def run_reference(args, cfg):
     line = dict(impl="reference", metric=METRIC, value=v, unit=UNIT, n_gpus=args.gpus, steps=args.steps,
                 warmup=args.warmup, ms_per_step=1e3 * statistics.mean(times), higher_is_better=True,
                 scaling="weak", vs_baseline=None, dtype="f64", data="synthetic",
-                config=dict(workload=cfg["workload"], entries=n, batch=cfg["b"]),
+                config=dict(workload=cfg["workload"], entries=n, batch=cfg["b"], dim=D, latent_bytes=L, topk=1,
+                            parallelism="single host thread (fp64 oracle)"),
                 cpu_baseline=dict(value=v, unit=UNIT, cores=1, kind="oracle",
                                   sample=f"{per_step} queries per step of the {cfg['b']}-query batch, "
                                          f"full {n}-entry scan, 1 thread"),

@@ -268,6 +268,21 @@ cache_status cache_query_merge(cache_t *c, int64_t b, int64_t row0, int64_t nb, 
 cache_status cache_export_peer(cache_t *c, cache_peer_desc *out);
 cache_status cache_attach_peers(cache_t *c, int32_t world, const cache_peer_desc *descs);
 
+/* ---- match predictor ----
+ * A linear one-class SVM f(x) = <w, x> - rho over the cached embeddings (unit-scaled stored
+ * values), "trained by utilizing all prompt embeddings stored in the VDB" with
+ * nu (0.001 in the paper).  Training (reading R22): rho is set each epoch to the
+ * ceil(nu n)-th smallest margin (the exact minimiser of the one-class objective in rho) and w
+ * takes a subgradient step w <- w - eta_t (nu w - (1/n) sum_{<w,x_i> < rho} x_i) / nu with
+ * eta_t = lr0 / sqrt(1 + t), from w = mean(x_i); `epochs` steps.  Synchronises `stream`.
+ * cache_predict: out_flags[i] = 1 iff f(q~_i / ||q~_i||) >= 0 ("a close match is likely",
+ * P:465-468), out_margin[i] = f (device pointers; either may be NULL; rejected rows get 0 /
+ * -inf).  Asynchronous.  cache_predictor_get copies w (dim floats) and rho to the host. */
+cache_status cache_predictor_train(cache_t *c, double nu, int32_t epochs, double lr0, void *stream);
+cache_status cache_predict(cache_t *c, int64_t b, const void *queries, int32_t q_dtype,
+                           uint8_t *out_flags, float *out_margin, void *stream);
+cache_status cache_predictor_get(cache_t *c, float *w, float *rho);
+
 /* Write n consecutive latent-pool slots starting at slot0 from `src` (device pointer,
  * n x latent_bytes).  Asynchronous.  Used to pre-fill an aliased pool (latent_alias = 1). */
 cache_status cache_pool_write(cache_t *c, int64_t slot0, int64_t n, const void *src, void *stream);

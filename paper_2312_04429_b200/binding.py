@@ -73,7 +73,7 @@ EXPORTS = ("cache_default_config", "cache_create", "cache_destroy", "cache_inser
            "cache_set_scorer", "cache_set_profile_events", "cache_kernel_launches", "cache_last_error",
            "cache_evict_hist", "cache_evict_pick", "cache_evict_apply", "cache_live_items", "cache_query_local",
            "cache_query_merge", "cache_export_peer", "cache_attach_peers", "cache_pool_write",
-           "cache_set_evict_policy")
+           "cache_set_evict_policy", "cache_predictor_train", "cache_predict", "cache_predictor_get")
 
 
 def load_library(path: str = LIB_PATH):
@@ -106,6 +106,11 @@ def load_library(path: str = LIB_PATH):
     L.cache_export_peer.argtypes = [P, ctypes.POINTER(PeerDesc)]
     L.cache_pool_write.argtypes = [P, I64, I64, P, P]
     L.cache_pool_write.restype = ctypes.c_int
+    L.cache_predictor_train.argtypes = [P, ctypes.c_double, I32, ctypes.c_double, P]
+    L.cache_predict.argtypes = [P, I64, P, I32, P, P, P]
+    L.cache_predictor_get.argtypes = [P, P, P]
+    for fn in ("cache_predictor_train", "cache_predict", "cache_predictor_get"):
+        getattr(L, fn).restype = ctypes.c_int
     L.cache_attach_peers.argtypes = [P, I32, P]
     for fn in ("cache_evict_hist", "cache_evict_pick", "cache_evict_apply", "cache_query_local",
                "cache_query_merge", "cache_export_peer", "cache_attach_peers"):
@@ -285,6 +290,25 @@ class NirvanaCache:
 
     def set_scorer(self, scorer: int):
         _check(_lib.cache_set_scorer(self._h, scorer))
+
+    # ------------------------- match predictor (NEXT-3) --------------------------------
+    def train_predictor(self, nu: float = 0.001, epochs: int = 50, lr0: float = 0.5, stream=None):
+        _check(_lib.cache_predictor_train(self._h, nu, epochs, lr0, _stream(stream)))
+
+    def predict(self, q: torch.Tensor, stream=None):
+        """-> (flags uint8 [b], margins float32 [b]) device tensors."""
+        b = q.shape[0]
+        flags = torch.empty(b, dtype=torch.uint8, device=q.device)
+        margin = torch.empty(b, dtype=torch.float32, device=q.device)
+        dt = DTYPE_BF16 if q.dtype == torch.bfloat16 else DTYPE_F32
+        _check(_lib.cache_predict(self._h, b, _ptr(q), dt, _ptr(flags), _ptr(margin), _stream(stream)))
+        return flags, margin
+
+    def predictor(self):
+        w = np.empty(self.dim, dtype=np.float32)
+        rho = np.empty(1, dtype=np.float32)
+        _check(_lib.cache_predictor_get(self._h, _ptr(w), _ptr(rho)))
+        return w, float(rho[0])
 
     def pool_write(self, slot0: int, src: torch.Tensor, stream=None):
         """Fill pool slots [slot0, slot0 + n) from a [n][latent_bytes] uint8 device tensor."""

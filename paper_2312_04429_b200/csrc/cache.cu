@@ -143,6 +143,12 @@ struct cache_t {
     DevBuf<unsigned long long> ekey, ecnt;
     DevBuf<int32_t> elslot;
     DevBuf<int64_t> edirty;
+    // match predictor (NEXT-3)
+    DevBuf<float> pw, prho, pgpart;
+    DevBuf<uint32_t> pkeys;
+    DevBuf<unsigned int> pcpart, phist;
+    DevBuf<EvictState> pst;
+    bool pred_ok = false;
     // sharding
     int rank = 0, world = 1;
     bool alias = false;   // declared latent aliasing (cache_config.latent_alias)
@@ -505,6 +511,78 @@ cache_status cache_query_merge(cache_t* c, int64_t b, int64_t row0, int64_t nb, 
     c->launches++;
     CK(cudaGetLastError());
     c->queries += nb;
+    return CACHE_OK;
+}
+
+cache_status cache_predictor_train(cache_t* c, double nu, int32_t epochs, double lr0, void* stream) {
+    if (!c || !(nu > 0.0 && nu < 1.0) || epochs < 0 || !(lr0 > 0.0))
+        return fail(CACHE_E_INVALID_ARG, "cache_predictor_train: bad nu / epochs / lr0");
+    if (c->live_entries <= 0) return fail(CACHE_E_STATE, "cache_predictor_train: empty cache");
+    DeviceGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t n_slots = c->hwm, n = c->live_entries;
+    const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>(296, n_slots));
+    CK(c->pw.ensure(c->dim));
+    CK(c->prho.ensure(1));
+    CK(c->pkeys.ensure(n_slots));
+    CK(c->pgpart.ensure((size_t)nblk * c->dim));
+    CK(c->pcpart.ensure(nblk));
+    CK(c->phist.ensure(256));
+    CK(c->pst.ensure(1));
+    const unsigned long long k = (unsigned long long)std::max<double>(1.0, std::ceil(nu * (double)n));
+    // w0 = mean of the unit-scaled cached embeddings (keys of live rows first, w = 0)
+    CK(cudaMemsetAsync(c->pst.p, 0, sizeof(EvictState), s));
+    CK(cudaMemsetAsync(c->pw.p, 0, c->dim * 4, s));
+    CK(cudaMemsetAsync(c->phist.p, 0, 256 * 4, s));
+    pred_margins(c->emb, c->inv_e, n_slots, c->dim, c->pw.p, c->pkeys.p, s);
+    pred_viol(c->emb, c->inv_e, c->pkeys.p, n_slots, c->dim, c->pst.p, 1, c->pgpart.p, c->pcpart.p, nblk, s);
+    pred_update(c->pgpart.p, c->pcpart.p, nblk, c->dim, c->pw.p, nu, 0.0, n, 0, s);
+    c->launches += 3;
+    for (int t = 0; t <= epochs; ++t) {
+        EvictState st0{0ull, 0ull, k};
+        CK(cudaMemcpyAsync(c->pst.p, &st0, sizeof(st0), cudaMemcpyHostToDevice, s));
+        pred_margins(c->emb, c->inv_e, n_slots, c->dim, c->pw.p, c->pkeys.p, s);
+        pred_select(c->pkeys.p, n_slots, c->pst.p, c->phist.p, s);   // rho = k-th smallest margin
+        c->launches += 9;
+        if (t == epochs) break;
+        pred_viol(c->emb, c->inv_e, c->pkeys.p, n_slots, c->dim, c->pst.p, 0, c->pgpart.p, c->pcpart.p, nblk, s);
+        pred_update(c->pgpart.p, c->pcpart.p, nblk, c->dim, c->pw.p, nu, lr0 / std::sqrt(1.0 + t), n, 1, s);
+        c->launches += 2;
+    }
+    pred_finish(c->pst.p, c->prho.p, s);
+    c->launches++;
+    CK(cudaStreamSynchronize(s));
+    CK(cudaGetLastError());
+    c->pred_ok = true;
+    return CACHE_OK;
+}
+
+cache_status cache_predict(cache_t* c, int64_t b, const void* queries, int32_t q_dtype, uint8_t* out_flags,
+                           float* out_margin, void* stream) {
+    if (!c || b < 0 || (b > 0 && !queries) || (q_dtype != CACHE_DTYPE_F32 && q_dtype != CACHE_DTYPE_BF16))
+        return fail(CACHE_E_INVALID_ARG, "cache_predict: bad argument");
+    if (!c->pred_ok) return fail(CACHE_E_STATE, "cache_predict: predictor not trained");
+    if (b == 0) return CACHE_OK;
+    DeviceGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t bpad = (b + 127) / 128 * 128;
+    CK(c->qbuf.ensure((size_t)bpad * c->dim));
+    CK(c->invq.ensure(bpad));
+    CK(c->qstat.ensure(bpad));
+    launch_normalise(queries, q_dtype, b, c->dim, c->qbuf.p, c->invq.p, c->qstat.p, s);
+    pred_predict(c->qbuf.p, c->invq.p, c->qstat.p, b, c->dim, c->pw.p, c->prho.p, out_flags, out_margin, s);
+    c->launches += 2;
+    CK(cudaGetLastError());
+    return CACHE_OK;
+}
+
+cache_status cache_predictor_get(cache_t* c, float* w, float* rho) {
+    if (!c || !w || !rho) return fail(CACHE_E_INVALID_ARG, "cache_predictor_get: null argument");
+    if (!c->pred_ok) return fail(CACHE_E_STATE, "cache_predictor_get: predictor not trained");
+    DeviceGuard g(c->device);
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(w, c->pw.p, c->dim * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(rho, c->prho.p, 4, cudaMemcpyDeviceToHost));
     return CACHE_OK;
 }
 

@@ -76,6 +76,18 @@ void launch_evict_apply(uint32_t* present, uint32_t* fcnt, const uint32_t* lasta
                         unsigned long long* ev_key, int32_t* ev_lslot, unsigned long long* counters,
                         int64_t* dirty_slot, cudaStream_t s);
 
+// match predictor (predictor.cu)
+void pred_margins(const __nv_bfloat16* emb, const float* inv_e, int64_t n_slots, int dim, const float* w,
+                  uint32_t* keys, cudaStream_t s);
+void pred_select(const uint32_t* keys, int64_t n, EvictState* st, unsigned int* hist, cudaStream_t s);
+void pred_viol(const __nv_bfloat16* emb, const float* inv_e, const uint32_t* keys, int64_t n_slots, int dim,
+               const EvictState* st, int all_rows, float* gpart, unsigned int* cpart, int nblk, cudaStream_t s);
+void pred_update(const float* gpart, const unsigned int* cpart, int nblk, int dim, float* w, double nu, double eta,
+                 int64_t n, int mode, cudaStream_t s);
+void pred_finish(const EvictState* st, float* rho, cudaStream_t s);
+void pred_predict(const __nv_bfloat16* qbuf, const float* inv_q, const int32_t* qstatus, int64_t b, int dim,
+                  const float* w, const float* rho, uint8_t* flags, float* margin, cudaStream_t s);
+
 // sharded lookup
 constexpr int kMaxWorld = 16;
 struct PeerPtrs {                       // per-rank device pointers (own rank included)
