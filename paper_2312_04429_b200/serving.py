@@ -81,19 +81,58 @@ def request_latency(k_used: int, lat: LatencyParams) -> float:
 
 class ServingLoop:
     """cache: an object with lookup(q) -> (ids, K), admit(emb, latents), evict(n) -> (evicted,
-    dirty), free() -> (free entries, free items); see GpuCache for the library adapter."""
+    dirty), free() -> (free entries, free items) and, with use_predictor, train_predictor()
+    and predict(q) -> bool flags; see GpuCache for the library adapter.
 
-    def __init__(self, cache, k_values, lat: LatencyParams = LatencyParams(), make_latents=None):
+    With the match predictor (Alg. 1 line 2) a predicted miss goes straight
+    to scratch generation without the search (latency C, arrow 1 of the overview); it
+    is retrained when more than 5% of the cached entries changed since the last training
+    (P:485-486)."""
+
+    def __init__(self, cache, k_values, lat: LatencyParams = LatencyParams(), make_latents=None,
+                 use_predictor: bool = False, retrain_threshold: float = 0.05):
         self.cache, self.k_values, self.lat = cache, tuple(k_values), lat
         self.make_latents = make_latents
         self.report = RunReport(k_values=self.k_values)
         self._admitted = 0
+        self.use_predictor, self.retrain_threshold = use_predictor, retrain_threshold
+        self._changed = 0          # entries admitted + removed since the last training
+        self._trained_on = 0
+        self.pred_stats = dict(predicted_true=0, predicted_true_hit=0, predicted_false=0,
+                               predicted_false_would_hit=0, searched_missed=0, retrains=0)
+
+    def _maybe_retrain(self):
+        fe, _ = self.cache.free()
+        live = self.cache.capacity_entries - fe
+        if live <= 0:
+            return False
+        if self._trained_on == 0 or self._changed > self.retrain_threshold * max(1, self._trained_on):
+            self.cache.train_predictor()
+            self._trained_on, self._changed = live, 0
+            self.pred_stats["retrains"] += 1
+        return True
 
     def step(self, q: np.ndarray):
         ids, ks = self.cache.lookup(q)
+        gate = None
+        if self.use_predictor and self._maybe_retrain():
+            gate = self.cache.predict(q)
         r = self.report
-        for k in ks.tolist():
+        for i, k in enumerate(ks.tolist()):
             r.requests += 1
+            if gate is not None:
+                ps = self.pred_stats
+                if gate[i]:
+                    ps["predicted_true"] += 1
+                    ps["predicted_true_hit"] += int(k > 0)
+                    ps["searched_missed"] += int(k == 0)
+                else:                       # arrow 1: scratch without searching
+                    ps["predicted_false"] += 1
+                    ps["predicted_false_would_hit"] += int(k > 0)
+                    r.steps += self.lat.N
+                    r.latencies.append(self.lat.C)
+                    ks[i] = 0
+                    continue
             if k > 0:
                 r.hits_at[k] = r.hits_at.get(k, 0) + 1
             r.steps += self.lat.N - k
@@ -102,6 +141,14 @@ class ServingLoop:
         if len(miss):
             self._admit(q[miss])
         return ids, ks
+
+    def predictor_summary(self):
+        ps = dict(self.pred_stats)
+        n = max(1, self.report.requests)
+        ps["precision_c_p"] = ps["predicted_true_hit"] / max(1, ps["predicted_true"])
+        ps["recall"] = ps["predicted_true_hit"] / max(1, ps["predicted_true_hit"] + ps["predicted_false_would_hit"])
+        ps["wasted_search_fraction"] = ps["searched_missed"] / n
+        return ps
 
     def _admit(self, emb: np.ndarray):
         nk = len(self.k_values)
@@ -114,6 +161,7 @@ class ServingLoop:
             ev, dirty = self.cache.evict(short)
             self.report.evicted_items += len(ev)
             self.report.dirty_removed += len(dirty)
+            self._changed += len(dirty)
             fe, fi = self.cache.free()
         m = min(len(emb), fe, fi // nk)
         if m <= 0:
@@ -121,15 +169,24 @@ class ServingLoop:
         lat = self.make_latents(self._admitted, m) if self.make_latents else None
         self.cache.admit(emb[:m], lat)
         self._admitted += m
+        self._changed += m
         self.report.admitted_prompts += m
 
 
 class GpuCache:
     """ServingLoop adapter over binding.NirvanaCache (device buffers, CUDA library calls)."""
 
-    def __init__(self, cache, device="cuda"):
+    def __init__(self, cache, device="cuda", nu: float = 0.001):
         import torch
-        self.c, self.torch, self.device = cache, torch, device
+        self.c, self.torch, self.device, self.nu = cache, torch, device, nu
+        self.capacity_entries = cache.cfg.entry_capacity
+
+    def train_predictor(self):
+        self.c.train_predictor(nu=self.nu)
+
+    def predict(self, q):
+        flags, _ = self.c.predict(self.torch.from_numpy(np.ascontiguousarray(q)).to(self.device))
+        return flags.cpu().numpy().astype(bool)
 
     def lookup(self, q):
         out = self.c.query(self.torch.from_numpy(np.ascontiguousarray(q)).to(self.device), topk=1)

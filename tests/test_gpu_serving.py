@@ -34,6 +34,25 @@ def test_gpu_serving_loop_matches_oracle_loop(oracle_mod):
     assert g["evicted_items"] > 0
 
 
+def test_serving_with_match_predictor():
+    """Alg. 1 with the predictor: predicted misses cost exactly C and take
+    no search; the predictor is retrained on > 5% change; its precision c_p and
+    the wasted-search fraction are reported."""
+    from paper_2312_04429_b200 import binding as B
+    universe, cl = synth.entries(20_000, seed=5)
+    g = B.NirvanaCache(entry_capacity=2000, latent_capacity=10_000, dim=768, latent_bytes=0)
+    loop = ServingLoop(GpuCache(g), synth.K_VALUES, LatencyParams(), use_predictor=True)
+    for i in range(20):
+        q, _, _ = synth.queries(universe, cl, 128, seed=700 + i)
+        loop.step(q)
+    ps = loop.predictor_summary()
+    s = loop.report.summary(loop.lat)
+    assert ps["retrains"] >= 2 and ps["predicted_true"] + ps["predicted_false"] <= s["requests"]
+    assert 0.0 <= ps["precision_c_p"] <= 1.0 and s["f_c"] == pytest.approx(s["f_c_from_steps"], abs=1e-12)
+    n_scratch_pred = sum(1 for x in loop.report.latencies if x == loop.lat.C)
+    assert n_scratch_pred >= ps["predicted_false"]
+
+
 def test_policy_direction_lcbfu_first():
     """SPEC acceptance #6 / Table 3(b) direction: on a skewed-similarity stream at
     two capacities LCBFU saves at least as much compute as LFU and FIFO, and >= LRU - 0.01."""
