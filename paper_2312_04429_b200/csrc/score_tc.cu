@@ -282,12 +282,15 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ C
                 if (g != 0u) tk.thr = key_to_f32((unsigned long long)g << 32);
             }
             if (q >= B) tk.thr = INFINITY;   // padding rows of the last query tile: never offer
+            float inv_next = __ldg(inv_e + (int64_t)n0 * BN + et);
 #pragma unroll 1
             for (int n = n0; n < n1; ++n) {
-                // entry inv-norms of this tile -> smem (double-buffered by accumulator)
+                // entry inv-norms of this tile -> smem (double-buffered by accumulator); the
+                // next tile's value is fetched now so its L2 latency hides behind this tile
                 const uint32_t ivb = inv_base + acc * BN * 4;
                 {
-                    const float v = __ldg(inv_e + (int64_t)n * BN + et);
+                    const float v = inv_next;
+                    if (n + 1 < n1) inv_next = __ldg(inv_e + (int64_t)(n + 1) * BN + et);
                     asm volatile("st.shared.f32 [%0], %1;" ::"r"(ivb + 4 * et), "f"(v) : "memory");
                 }
                 asm volatile("bar.sync 1, 256;" ::: "memory");
