@@ -62,7 +62,9 @@ enum { CACHE_DTYPE_F32 = 0, CACHE_DTYPE_BF16 = 1 };
 enum {
     CACHE_SCORER_AUTO = 0,   /* library picks by batch size                                */
     CACHE_SCORER_TC = 1,     /* tcgen05/TMEM tensor-core scan with fused top-k epilogue    */
-    CACHE_SCORER_STREAM = 2  /* CUDA-core HBM-streaming scan (small batches)               */
+    CACHE_SCORER_STREAM = 2, /* CUDA-core HBM-streaming scan (small batches)               */
+    CACHE_SCORER_TC_SINGLE = 3 /* tcgen05 scan with single-CTA tiles only (no CTA pairs);
+                                  AUTO / TC use CTA pairs (cta_group::2) when b > 128       */
 };
 
 #define CACHE_MAX_K 8      /* max |K| (the paper uses 5: {5,10,15,20,25})           */

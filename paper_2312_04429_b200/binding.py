@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libnirvana_cache.so")
 OK, E_INVALID_ARG, E_DIM, E_FULL, E_EVICT_RANGE, E_BAD_ROWS, E_CUDA, E_NCCL, E_OOM, E_STATE, E_UNSUPPORTED = range(11)
 ROW_OK, ROW_NONFINITE, ROW_ZERO_NORM, ROW_NO_ITEMS = range(4)
 DTYPE_F32, DTYPE_BF16 = 0, 1
-SCORER_AUTO, SCORER_TC, SCORER_STREAM = 0, 1, 2
+SCORER_AUTO, SCORER_TC, SCORER_STREAM, SCORER_TC_SINGLE = 0, 1, 2, 3
 MAX_K, MAX_TOPK = 8, 16
 NO_ID = 0xFFFFFFFFFFFFFFFF
 

@@ -109,7 +109,8 @@ struct cache_t {
     uint32_t* fcnt = nullptr;       // [cap_pad][num_k] LCBFU access counts f
     uint32_t* lastacc = nullptr;    // [cap_pad][num_k] batch clock of the last access (LRU)
     uint8_t* pool = nullptr;        // [lcap][L]       intermediate states
-    CUtensorMap tm_e;               // TMA map of emb (box 64 x 256)
+    CUtensorMap tm_e;               // TMA map of emb (box 64 x 256): single-CTA scan
+    CUtensorMap tm_e128;            // TMA map of emb (box 64 x 128): CTA-pair scan (half a tile per CTA)
     bool tm_e_ok = false;
     // host mirrors / allocators
     std::vector<uint32_t> h_present, h_ids;
@@ -247,7 +248,8 @@ cache_status cache_create(const cache_config* cfg, int device, cache_t** out) {
     cudaMemset(c->fcnt, 0, (size_t)c->cap_pad * c->num_k * 4);
     cudaMemset(c->lastacc, 0, (size_t)c->cap_pad * c->num_k * 4);
     if ((e = cudaDeviceSynchronize()) != cudaSuccess) return bail(e, "init");
-    c->tm_e_ok = encode_rows(&c->tm_e, c->emb, c->cap_pad, c->dim, 256);
+    c->tm_e_ok = encode_rows(&c->tm_e, c->emb, c->cap_pad, c->dim, 256) &&
+                 encode_rows(&c->tm_e128, c->emb, c->cap_pad, c->dim, 128);
     c->h_present.assign(c->cap_pad, 0);
     c->h_ids.assign(c->cap_pad, 0);
     c->h_lslot.assign((size_t)c->cap_pad * c->num_k, -1);
@@ -408,10 +410,12 @@ static cache_status scan_core(cache_t* c, int64_t b, const void* queries, int32_
             // b <= 128 on 1M entries and tensor-bound above, so AUTO always takes it
             use_tc = true;
         }
-        if (c->scorer == CACHE_SCORER_TC && !use_tc)
+        if ((c->scorer == CACHE_SCORER_TC || c->scorer == CACHE_SCORER_TC_SINGLE) && !use_tc)
             return fail(CACHE_E_UNSUPPORTED, "query: tensor-core scorer unavailable for this configuration");
         if (use_tc) {
-            tp = tc_plan(b, n_slots, c->sm_count);
+            // more than one 128-query tile: the CTA-pair kernel (half the operand traffic per SM)
+            const bool pair = b > 128 && c->scorer != CACHE_SCORER_TC_SINGLE;
+            tp = tc_plan(b, n_slots, c->sm_count, pair);
             parts = tp.parts;
             if (bpad > b) CK(cudaMemsetAsync(c->qbuf.p + b * c->dim, 0, (bpad - b) * c->dim * 2, s));
             CUtensorMap tm_q;
@@ -419,7 +423,8 @@ static cache_status scan_core(cache_t* c, int64_t b, const void* queries, int32_
                 return fail(CACHE_E_CUDA, "query: cuTensorMapEncodeTiled failed");
             CK(c->recs.ensure((size_t)parts * b * kmax));
             if (c->prof_on) { CK(cudaEventRecord(c->prof[1], s)); prof1 = true; }
-            if (!launch_score_tc(kmax, tp, &tm_q, &c->tm_e, c->inv_e, c->ids, c->dim, b, c->recs.p, c->gk.p, s))
+            if (!launch_score_tc(kmax, tp, &tm_q, pair ? &c->tm_e128 : &c->tm_e, c->inv_e, c->ids, c->dim, b,
+                                 c->recs.p, c->gk.p, s))
                 return fail(CACHE_E_UNSUPPORTED, "query: tensor-core scorer not built");
             c->launches++;
         } else {
@@ -882,7 +887,7 @@ cache_status cache_set_evict_policy(cache_t* c, int32_t policy) {
 }
 
 cache_status cache_set_scorer(cache_t* c, int32_t scorer) {
-    if (!c || scorer < CACHE_SCORER_AUTO || scorer > CACHE_SCORER_STREAM)
+    if (!c || scorer < CACHE_SCORER_AUTO || scorer > CACHE_SCORER_TC_SINGLE)
         return fail(CACHE_E_INVALID_ARG, "cache_set_scorer: bad argument");
     c->scorer = scorer;
     return CACHE_OK;
@@ -918,7 +923,8 @@ extern "C" cache_status cache_debug_tc_scores(cache_t* c, int64_t b, const void*
     if (!c->tm_e_ok || !tc_supported(c->dim)) return fail(CACHE_E_UNSUPPORTED, "tcgen05 scorer unavailable");
     const int64_t n_slots = c->hwm;
     if (n_slots == 0) return CACHE_OK;
-    TcPlan tp = tc_plan(b, n_slots, c->sm_count);
+    const bool pair = b > 128 && c->scorer != CACHE_SCORER_TC_SINGLE;
+    TcPlan tp = tc_plan(b, n_slots, c->sm_count, pair);
     if (ld < (int64_t)tp.n_tiles * 256) return fail(CACHE_E_INVALID_ARG, "cache_debug_tc_scores: ld too small");
     DeviceGuard g(c->device);
     cudaStream_t s = (cudaStream_t)stream;
@@ -930,7 +936,7 @@ extern "C" cache_status cache_debug_tc_scores(cache_t* c, int64_t b, const void*
     if (bpad > b) CK(cudaMemsetAsync(c->qbuf.p + b * c->dim, 0, (bpad - b) * c->dim * 2, s));
     CUtensorMap tm_q;
     if (!encode_rows(&tm_q, c->qbuf.p, bpad, c->dim, 128)) return fail(CACHE_E_CUDA, "tensor map encode failed");
-    if (!launch_score_tc_dense(tp, &tm_q, &c->tm_e, c->inv_e, c->dim, b, out, ld, s))
+    if (!launch_score_tc_dense(tp, &tm_q, pair ? &c->tm_e128 : &c->tm_e, c->inv_e, c->dim, b, out, ld, s))
         return fail(CACHE_E_CUDA, std::string("tc dense launch: ") + cudaGetErrorString(cudaGetLastError()));
     return CACHE_OK;
 }

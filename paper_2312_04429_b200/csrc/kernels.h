@@ -43,11 +43,12 @@ struct TcPlan {
     int n_tiles;        // ceil(n_slots / 256)
     int chunk_tiles;    // n-tiles per chunk (top-k segment)
     int n_chunks;
-    int grid;           // persistent CTAs
+    int grid;           // persistent CTAs (clusters for the CTA-pair kernel)
     int parts;          // records per query = n_chunks
+    bool pair;          // cta_group::2 kernel: m_tiles counts 256-query tile pairs
 };
 bool tc_supported(int dim);
-TcPlan tc_plan(int64_t b, int64_t n_slots, int sm_count);
+TcPlan tc_plan(int64_t b, int64_t n_slots, int sm_count, bool pair);
 bool launch_score_tc(int kmax, const TcPlan& plan, const void* tmap_q, const void* tmap_e,
                      const float* inv_e, const uint32_t* ids, int dim, int64_t b, Rec* ws,
                      uint32_t* gk, cudaStream_t s);

@@ -360,6 +360,291 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ C
     }
 }
 
+// =========================================================================================
+// CTA-pair variant (cta_group::2).  A cluster of 2 CTAs on one TPC computes a 256-query x
+// 256-entry tile per MMA: CTA r holds query rows [128r, 128r+128) of the pair's A tile and
+// entry rows [128r, 128r+128) of the B tile; the leader (rank 0) issues
+// tcgen05.mma.cta_group::2 M256 N256 K16, whose result lands in both CTAs' TMEM (each its own
+// 128 query rows x 256 entries).  Per SM and K chunk the TMA fill drops from 48 KiB to 32 KiB
+// and the tensor core's shared-memory reads from 12 KiB to 8 KiB per MMA.  Both TMA halves
+// signal the leader's full barrier (the peer-bit trick), MMA completion is multicast to both
+// CTAs' empty / tfull barriers, and both CTAs' epilogue warps release the accumulator on the
+// leader's tempty barrier.  The epilogue is the single-CTA one.
+// =========================================================================================
+namespace pair {
+constexpr int STAGES = 6;
+constexpr int A_BYTES = BM * BK * 2;            // 16 KiB: own 128 query rows
+constexpr int B_BYTES = (BN / 2) * BK * 2;      // 16 KiB: own 128 entry rows
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // 32 KiB
+constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(256 >> 4) << 24);   // M = 256 (the pair), N = 256
+constexpr int SMEM_INV_OFF = STAGES * STAGE_BYTES;
+constexpr int SMEM_BAR_OFF = SMEM_INV_OFF + 2 * BN * 4;
+constexpr int SMEM_TMEM_OFF = SMEM_BAR_OFF + (2 * STAGES + 4) * 8;
+constexpr int SMEM_XCH_OFF = SMEM_TMEM_OFF + 16;
+constexpr int SMEM_BYTES = SMEM_XCH_OFF + BM * 16 * 12 + 1024;
+}  // namespace pair
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y) {
+    // both CTAs of the pair signal the leader's barrier (clear the peer bit of the address)
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar & 0xFEFFFFFFu), "r"(x), "r"(y)
+        : "memory");
+}
+__device__ __forceinline__ void umma_bf16_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %3, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %4, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(accum), "r"(pair::IDESC)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit_pair(uint32_t bar) {
+    asm volatile(
+        "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+            bar)
+        : "memory");
+}
+
+namespace pair {   // (unqualified layout constants below resolve to pair::)
+template <int KMAX, bool kDense>
+__global__ void __launch_bounds__(NUM_THREADS_TC, 1)
+k_score_tc2(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_e,
+            const float* __restrict__ inv_e, const uint32_t* __restrict__ ids, int dim, int64_t B,
+            int m_pairs, int n_tiles, int chunk_tiles, int n_units, Rec* __restrict__ ws,
+            uint32_t* __restrict__ gk, float* __restrict__ dense, int64_t dense_ld) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SMEM_TMEM_OFF);
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t inv_base = sbase + SMEM_INV_OFF;
+    const uint32_t bar_full = sbase + SMEM_BAR_OFF, bar_empty = bar_full + STAGES * 8;
+    const uint32_t bar_tfull = bar_empty + STAGES * 8, bar_tempty = bar_tfull + 2 * 8;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int kch = dim / BK;
+    const uint32_t rank = cluster_rank();
+    const int cid = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
+
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_q)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_e)) : "memory");
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(bar_full + 8 * s, 1);
+            mbar_init(bar_empty + 8 * s, 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(bar_tfull + 8 * a, 1);
+            mbar_init(bar_tempty + 8 * a, 2 * EPI_WARPS);   // both CTAs' epilogue warps (leader's copy)
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();   // peer barriers initialised, TMEM allocated in both CTAs
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------- TMA producer (both CTAs) ---------------------
+        if (lane == 0) {
+            uint32_t stage = 0, phase = 0;
+            for (int u = cid; u < n_units; u += n_clusters) {
+                const int chunk = u / m_pairs, mp = u - chunk * m_pairs;
+                const int n0 = chunk * chunk_tiles, n1 = min(n_tiles, n0 + chunk_tiles);
+                const int qrow = (2 * mp + (int)rank) * BM;
+                for (int n = n0; n < n1; ++n) {
+                    for (int kc = 0; kc < kch; ++kc) {
+                        mbar_wait(bar_empty + 8 * stage, phase ^ 1);
+                        const uint32_t sa = sbase + stage * STAGE_BYTES;
+                        if (rank == 0) mbar_expect_tx(bar_full + 8 * stage, 2 * STAGE_BYTES);
+                        tma_load_2d_pair(sa, &tmap_q, bar_full + 8 * stage, kc * BK, qrow);
+                        tma_load_2d_pair(sa + A_BYTES, &tmap_e, bar_full + 8 * stage, kc * BK,
+                                         n * BN + (int)rank * (BN / 2));
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------- MMA issuer (leader only) --------------------
+        if (lane == 0 && rank == 0) {
+            uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+            for (int u = cid; u < n_units; u += n_clusters) {
+                const int chunk = u / m_pairs;
+                const int n0 = chunk * chunk_tiles, n1 = min(n_tiles, n0 + chunk_tiles);
+                for (int n = n0; n < n1; ++n) {
+                    mbar_wait(bar_tempty + 8 * acc, acc_phase ^ 1);
+                    tc_fence_after();
+                    const uint32_t d = tmem_base + acc * BN;
+                    for (int kc = 0; kc < kch; ++kc) {
+                        mbar_wait(bar_full + 8 * stage, phase);
+                        tc_fence_after();
+                        const uint32_t sa = sbase + stage * STAGE_BYTES;
+                        const uint64_t ad = sw128_desc(sa), bd = sw128_desc(sa + A_BYTES);
+#pragma unroll
+                        for (int k = 0; k < BK / 16; ++k)
+                            umma_bf16_pair(d, ad + 2 * k, bd + 2 * k, (kc | k) != 0);
+                        umma_commit_pair(bar_empty + 8 * stage);   // frees the stage in both CTAs
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    }
+                    umma_commit_pair(bar_tfull + 8 * acc);         // both CTAs' accumulators ready
+                    acc ^= 1;
+                    if (acc == 0) acc_phase ^= 1;
+                }
+            }
+        }
+    } else if (warp >= EPI_WARP0) {
+        // ------------------------------- epilogue (both CTAs) ------------------------
+        const int ew = warp & 3;
+        const int h = (warp - EPI_WARP0) >> 2;
+        const int et = threadIdx.x - EPI_WARP0 * 32;
+        const int row = 32 * ew + lane;
+        const uint32_t tempty_leader = map_to_rank(bar_tempty, 0);
+        uint32_t acc = 0, acc_phase = 0;
+        for (int u = cid; u < n_units; u += n_clusters) {
+            const int chunk = u / m_pairs, mp = u - chunk * m_pairs;
+            const int n0 = chunk * chunk_tiles, n1 = min(n_tiles, n0 + chunk_tiles);
+            const int64_t q = (int64_t)(2 * mp + (int)rank) * BM + row;
+            float* dense_row = (kDense && q < B) ? dense + q * dense_ld : nullptr;
+            TopK<KMAX> tk;
+            tk.init();
+            if (!kDense && gk != nullptr && q < B) {
+                const uint32_t g = *reinterpret_cast<volatile const uint32_t*>(gk + q);
+                if (g != 0u) tk.thr = key_to_f32((unsigned long long)g << 32);
+            }
+            if (q >= B) tk.thr = INFINITY;
+            float inv_next = __ldg(inv_e + (int64_t)n0 * BN + et);
+#pragma unroll 1
+            for (int n = n0; n < n1; ++n) {
+                const uint32_t ivb = inv_base + acc * BN * 4;
+                {
+                    const float v = inv_next;
+                    if (n + 1 < n1) inv_next = __ldg(inv_e + (int64_t)(n + 1) * BN + et);
+                    asm volatile("st.shared.f32 [%0], %1;" ::"r"(ivb + 4 * et), "f"(v) : "memory");
+                }
+                asm volatile("bar.sync 1, 256;" ::: "memory");
+                mbar_wait(bar_tfull + 8 * acc, acc_phase);
+                tc_fence_after();
+                const uint32_t taddr = tmem_base + ((uint32_t)(32 * ew) << 16) + acc * BN + h * 128;
+                const uint32_t col_base = (uint32_t)(n * BN + h * 128);
+                const uint32_t ivh = ivb + 4 * (h * 128);
+                uint32_t ra[32], rb[32];
+                tmem_ld32(taddr, ra);
+                tmem_ld_wait_regs(ra);
+#pragma unroll 1
+                for (int c = 0; c < 128; c += 64) {
+                    tmem_ld32(taddr + c + 32, rb);
+                    epi_chunk<KMAX, kDense>(ra, ivh + 4 * c, col_base + c, tk, ids, dense_row);
+                    tmem_ld_wait_regs(rb);
+                    if (c + 64 < 128) tmem_ld32(taddr + c + 64, ra);
+                    else {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_cluster(tempty_leader + 8 * acc);
+                    }
+                    epi_chunk<KMAX, kDense>(rb, ivh + 4 * (c + 32), col_base + c + 32, tk, ids, dense_row);
+                    if (c + 64 < 128) tmem_ld_wait_regs(ra);
+                }
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+            }
+            if (!kDense) {
+                unsigned long long* mk = reinterpret_cast<unsigned long long*>(smem + SMEM_XCH_OFF);
+                uint32_t* ms = reinterpret_cast<uint32_t*>(smem + SMEM_XCH_OFF + BM * KMAX * 8);
+                if (h == 1) {
+#pragma unroll
+                    for (int i = 0; i < KMAX; ++i) { mk[row * KMAX + i] = tk.k[i]; ms[row * KMAX + i] = tk.s[i]; }
+                }
+                asm volatile("bar.sync 2, 256;" ::: "memory");
+                if (h == 0) {
+#pragma unroll
+                    for (int i = 0; i < KMAX; ++i)
+                        if (mk[row * KMAX + i]) tk.offer_key(mk[row * KMAX + i], ms[row * KMAX + i]);
+                    if (q < B) {
+                        if (gk != nullptr && tk.k[KMAX - 1] != 0ull)
+                            atomicMax(gk + q, (uint32_t)(tk.k[KMAX - 1] >> 32));
+                        Rec* o = ws + ((int64_t)chunk * B + q) * KMAX;
+#pragma unroll
+                        for (int i = 0; i < KMAX; ++i) {
+                            Rec rr;
+                            rr.key = tk.k[i];
+                            rr.slot = tk.s[i];
+                            rr.pad = 0;
+                            o[i] = rr;
+                        }
+                    }
+                }
+                asm volatile("bar.sync 2, 256;" ::: "memory");
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();   // both CTAs finished with TMEM and with the leader's barriers
+    tc_fence_after();
+    if (warp == 1) {
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
+                     : "memory");
+    }
+}
+}  // namespace pair
+
+template <int KMAX, bool kDense>
+static bool launch_pair(const TcPlan& p, const CUtensorMap* tq, const CUtensorMap* te, const float* inv_e,
+                        const uint32_t* ids, int dim, int64_t b, Rec* ws, uint32_t* gk, float* dense,
+                        int64_t dense_ld, cudaStream_t s) {
+    auto kern = pair::k_score_tc2<KMAX, kDense>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pair::SMEM_BYTES) != cudaSuccess)
+            return false;
+        attr_set = true;
+    }
+    const int n_units = p.n_chunks * p.m_tiles;   // m_tiles of a pair plan = query-tile pairs
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(2 * p.grid));
+    cfg.blockDim = dim3(NUM_THREADS_TC);
+    cfg.dynamicSmemBytes = pair::SMEM_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const CUtensorMap q = *tq, e = *te;
+    if (cudaLaunchKernelEx(&cfg, kern, q, e, inv_e, ids, dim, b, p.m_tiles, p.n_tiles, p.chunk_tiles, n_units,
+                           ws, gk, dense, dense_ld) != cudaSuccess)
+        return false;
+    return cudaPeekAtLastError() == cudaSuccess;
+}
+
 template <int KMAX, bool kDense>
 static bool launch(const TcPlan& p, const CUtensorMap* tq, const CUtensorMap* te, const float* inv_e,
                    const uint32_t* ids, int dim, int64_t b, Rec* ws, uint32_t* gk, float* dense,
@@ -383,13 +668,18 @@ bool tc_supported(int dim) { return dim % tc::BK == 0 && dim >= tc::BK && dim <=
 
 // Chunk size: minimise the round-robin makespan (memoised per (b, n_slots, sm_count)) (in tiles, + a small per-unit cost for the
 // record flush / pipeline refill); ties -> larger chunks (fewer partial records to merge).
-TcPlan tc_plan(int64_t b, int64_t n_slots, int sm_count) {
+// pair = true: CTA-pair kernel; m_tiles then counts 256-query tile pairs and the "CTAs" of
+// the makespan model are clusters (sm_count / 2).
+TcPlan tc_plan(int64_t b, int64_t n_slots, int sm_count, bool pair) {
     static thread_local int64_t mb = -1, mn = -1;
     static thread_local int ms = -1;
+    static thread_local bool mp = false;
     static thread_local TcPlan memo{};
-    if (b == mb && n_slots == mn && sm_count == ms) return memo;
+    if (b == mb && n_slots == mn && sm_count == ms && pair == mp) return memo;
     TcPlan p{};
-    p.m_tiles = (int)((b + tc::BM - 1) / tc::BM);
+    p.pair = pair;
+    if (pair) sm_count = std::max(1, sm_count / 2);
+    p.m_tiles = (int)((b + (pair ? 2 * tc::BM : tc::BM) - 1) / (pair ? 2 * tc::BM : tc::BM));
     p.n_tiles = (int)((n_slots + tc::BN - 1) / tc::BN);
     double best = 1e30;
     for (int nc = 1; nc <= std::min(p.n_tiles, 64); ++nc) {
@@ -416,15 +706,22 @@ TcPlan tc_plan(int64_t b, int64_t n_slots, int sm_count) {
     p.parts = p.n_chunks;
     mb = b;
     mn = n_slots;
-    ms = sm_count;
+    ms = pair ? 2 * sm_count : sm_count;
+    mp = pair;
     memo = p;
     return p;
 }
 
+// tmap_e: box of 256 entry rows for the single-CTA kernel, 128 rows for the CTA pair.
 bool launch_score_tc(int kmax, const TcPlan& p, const void* tmap_q, const void* tmap_e, const float* inv_e,
                      const uint32_t* ids, int dim, int64_t b, Rec* ws, uint32_t* gk, cudaStream_t s) {
     const CUtensorMap* tq = static_cast<const CUtensorMap*>(tmap_q);
     const CUtensorMap* te = static_cast<const CUtensorMap*>(tmap_e);
+    if (p.pair) {
+        if (kmax == 1) return tc::launch_pair<1, false>(p, tq, te, inv_e, ids, dim, b, ws, gk, nullptr, 0, s);
+        if (kmax == 4) return tc::launch_pair<4, false>(p, tq, te, inv_e, ids, dim, b, ws, gk, nullptr, 0, s);
+        return tc::launch_pair<16, false>(p, tq, te, inv_e, ids, dim, b, ws, gk, nullptr, 0, s);
+    }
     if (kmax == 1) return tc::launch<1, false>(p, tq, te, inv_e, ids, dim, b, ws, gk, nullptr, 0, s);
     if (kmax == 4) return tc::launch<4, false>(p, tq, te, inv_e, ids, dim, b, ws, gk, nullptr, 0, s);
     return tc::launch<16, false>(p, tq, te, inv_e, ids, dim, b, ws, gk, nullptr, 0, s);
@@ -432,8 +729,10 @@ bool launch_score_tc(int kmax, const TcPlan& p, const void* tmap_q, const void* 
 
 bool launch_score_tc_dense(const TcPlan& p, const void* tmap_q, const void* tmap_e, const float* inv_e, int dim,
                            int64_t b, float* dense, int64_t dense_ld, cudaStream_t s) {
-    return tc::launch<1, true>(p, static_cast<const CUtensorMap*>(tmap_q), static_cast<const CUtensorMap*>(tmap_e),
-                               inv_e, nullptr, dim, b, nullptr, nullptr, dense, dense_ld, s);
+    const CUtensorMap* tq = static_cast<const CUtensorMap*>(tmap_q);
+    const CUtensorMap* te = static_cast<const CUtensorMap*>(tmap_e);
+    if (p.pair) return tc::launch_pair<1, true>(p, tq, te, inv_e, nullptr, dim, b, nullptr, nullptr, dense, dense_ld, s);
+    return tc::launch<1, true>(p, tq, te, inv_e, nullptr, dim, b, nullptr, nullptr, dense, dense_ld, s);
 }
 
 }  // namespace nv
