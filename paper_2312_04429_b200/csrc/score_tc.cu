@@ -399,7 +399,10 @@ __device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
     return r;
 }
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+    // default (.release.cta) semantics like CUTLASS's ClusterBarrier::arrive(cta_id): the
+    // TMEM reads it publishes are ordered by tcgen05.wait::ld + fence::before_thread_sync;
+    // a .cluster-scope release would add a cluster-wide memory barrier per tile
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y) {
     // both CTAs of the pair signal the leader's barrier (clear the peer bit of the address)
@@ -565,7 +568,10 @@ k_score_tc2(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ 
                     else {
                         tc_fence_before();
                         __syncwarp();
-                        if (lane == 0) mbar_arrive_cluster(tempty_leader + 8 * acc);
+                        if (lane == 0) {
+                            if (rank == 0) mbar_arrive(bar_tempty + 8 * acc);   // own barrier
+                            else mbar_arrive_cluster(tempty_leader + 8 * acc);
+                        }
                     }
                     epi_chunk<KMAX, kDense>(rb, ivh + 4 * (c + 32), col_base + c + 32, tk, ids, dense_row);
                     if (c + 64 < 128) tmem_ld_wait_regs(ra);
