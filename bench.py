@@ -269,7 +269,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=list(CONFIGS))
     ap.add_argument("--batch", type=int, default=None)
-    ap.add_argument("--scorer", default="auto", choices=["auto", "tc", "stream"])
+    ap.add_argument("--scorer", default="auto", choices=["auto", "tc", "tc1", "stream"],
+                    help="tc1 = single-CTA tensor-core scan (auto/tc use CTA pairs for > 128 queries)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-maintenance", action="store_true")
@@ -295,7 +296,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = local
     g, emb, cl, pres = build_cache(B, torch, cfg, seed=1000, dev=dev)
-    g.set_scorer({"auto": B.SCORER_AUTO, "tc": B.SCORER_TC, "stream": B.SCORER_STREAM}[args.scorer])
+    g.set_scorer({"auto": B.SCORER_AUTO, "tc": B.SCORER_TC, "tc1": B.SCORER_TC_SINGLE,
+                  "stream": B.SCORER_STREAM}[args.scorer])
     b = cfg["b"]
     q_np, _, _ = synth.queries(emb, cl, b, seed=1001 + 7919 * rank)
     q = torch.from_numpy(q_np).cuda()

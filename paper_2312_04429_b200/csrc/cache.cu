@@ -21,6 +21,11 @@ using namespace nv;
 namespace {
 thread_local std::string g_err = "no error";
 
+// cache_query_batch_host: batches of >= kHostSplitMin queries are uploaded in kHostSplit
+// slices so the copy overlaps the scan (see cache_query_batch_host)
+constexpr int kHostSplit = 4;
+constexpr int64_t kHostSplitMin = 2048;
+
 cache_status fail(cache_status st, const std::string& msg) {
     g_err = msg;
     return st;
@@ -136,6 +141,9 @@ struct cache_t {
     DevBuf<uint8_t> hq_in, hq_lat, hq_out;
     void* h_out = nullptr;   // pinned staging of the packed host-call results
     size_t h_out_n = 0;
+    // host-call pipeline: query H2D copies on their own stream, one event per sub-batch
+    cudaStream_t hcopy = nullptr;
+    cudaEvent_t hev[kHostSplit + 1] = {};
     DevBuf<uint64_t> hq_ids;
     DevBuf<float> hq_sc;
     DevBuf<int32_t> hq_k, hq_st;
@@ -267,6 +275,9 @@ cache_status cache_destroy(cache_t* c) {
     cudaDeviceSynchronize();
     for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
     if (c->h_out) cudaFreeHost(c->h_out);
+    for (cudaEvent_t e : c->hev)
+        if (e) cudaEventDestroy(e);
+    if (c->hcopy) cudaStreamDestroy(c->hcopy);
     c->hq_out.release();
     cudaFree(c->emb); cudaFree(c->inv_e); cudaFree(c->ids); cudaFree(c->present);
     cudaFree(c->lslot); cudaFree(c->fcnt); cudaFree(c->lastacc); cudaFree(c->pool);
@@ -441,15 +452,16 @@ static cache_status scan_core(cache_t* c, int64_t b, const void* queries, int32_
     return CACHE_OK;
 }
 
+// tick = false: a later sub-batch of the same host batch (same LRU clock value).
 static cache_status query_core(cache_t* c, int64_t b, const void* queries, int32_t q_dtype, int32_t topk,
                                uint64_t* out_ids, float* out_scores, int32_t* out_k, void* latent_out,
-                               void** out_ptr, int32_t* row_status, cudaStream_t s) {
+                               void** out_ptr, int32_t* row_status, cudaStream_t s, bool tick = true) {
     const int kmax = topk == 1 ? 1 : (topk <= 4 ? 4 : 16);
     int parts = 0;
     cache_status r = scan_core(c, b, queries, q_dtype, kmax, s, &parts);
     if (r != CACHE_OK) return r;
     if (c->prof_on) CK(cudaEventRecord(c->prof[2], s));
-    c->clock++;   // one query batch = one tick of the LRU clock
+    if (tick) c->clock++;   // one query batch = one tick of the LRU clock
     launch_finalize(kmax, c->recs.p, parts, b, topk, c->invq.p, c->qstat.p, c->ids, c->present, c->lslot,
                     c->fcnt, c->lastacc, c->clock, c->pool, c->L, c->km, out_ids, out_scores, out_k,
                     (uint8_t*)latent_out, out_ptr, row_status, s);
@@ -706,12 +718,43 @@ cache_status cache_query_batch_host(cache_t* c, int64_t b, const void* queries, 
         c->h_out_n = obytes;
     }
     if (latent_out && !lat_dev) CK(c->hq_lat.ensure((size_t)b * c->L));
-    CK(cudaMemcpyAsync(c->hq_in.p, queries, qbytes, cudaMemcpyHostToDevice, s));
     uint8_t* ob = c->hq_out.p;
-    cache_status r = query_core(c, b, c->hq_in.p, q_dtype, topk, (uint64_t*)(ob + o_ids), (float*)(ob + o_sc),
-                                (int32_t*)(ob + o_k), latent_out ? (lat_dev ? latent_out : (void*)c->hq_lat.p) : nullptr,
-                                nullptr, (int32_t*)(ob + o_st), s);
-    if (r != CACHE_OK) return r;
+    uint8_t* lat = latent_out ? (uint8_t*)(lat_dev ? latent_out : (void*)c->hq_lat.p) : nullptr;
+    // Large batches: the query upload is split into kHostSplit slices on a copy stream and
+    // slice i's ingest/scan/finalize waits only for slice i, so the host-to-device copy of
+    // the rest of the batch overlaps the scan (the scan is tensor-bound at these sizes, so a
+    // quarter batch runs at the same rate per query).  One LRU clock tick for the whole batch.
+    const int64_t sub = b >= kHostSplitMin ? (((b + kHostSplit - 1) / kHostSplit + 255) / 256) * 256 : b;
+    if (sub >= b) {
+        CK(cudaMemcpyAsync(c->hq_in.p, queries, qbytes, cudaMemcpyHostToDevice, s));
+        cache_status r = query_core(c, b, c->hq_in.p, q_dtype, topk, (uint64_t*)(ob + o_ids), (float*)(ob + o_sc),
+                                    (int32_t*)(ob + o_k), lat, nullptr, (int32_t*)(ob + o_st), s);
+        if (r != CACHE_OK) return r;
+    } else {
+        if (!c->hcopy) CK(cudaStreamCreateWithFlags(&c->hcopy, cudaStreamNonBlocking));
+        for (cudaEvent_t& e : c->hev)
+            if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        const size_t row = qbytes / (size_t)b;
+        CK(cudaEventRecord(c->hev[kHostSplit], s));   // hq_in is free once earlier work on s is done
+        CK(cudaStreamWaitEvent(c->hcopy, c->hev[kHostSplit], 0));
+        int ns = 0;
+        for (int64_t off = 0; off < b; off += sub, ++ns) {
+            const int64_t nb = std::min(sub, b - off);
+            CK(cudaMemcpyAsync(c->hq_in.p + off * row, static_cast<const uint8_t*>(queries) + off * row, nb * row,
+                               cudaMemcpyHostToDevice, c->hcopy));
+            CK(cudaEventRecord(c->hev[ns], c->hcopy));
+        }
+        ns = 0;
+        for (int64_t off = 0; off < b; off += sub, ++ns) {
+            const int64_t nb = std::min(sub, b - off);
+            CK(cudaStreamWaitEvent(s, c->hev[ns], 0));
+            cache_status r = query_core(
+                c, nb, c->hq_in.p + off * row, q_dtype, topk, (uint64_t*)(ob + o_ids) + off * topk,
+                (float*)(ob + o_sc) + off * topk, (int32_t*)(ob + o_k) + off, lat ? lat + off * c->L : nullptr,
+                nullptr, (int32_t*)(ob + o_st) + off, s, off == 0);
+            if (r != CACHE_OK) return r;
+        }
+    }
     CK(cudaMemcpyAsync(c->h_out, ob, obytes, cudaMemcpyDeviceToHost, s));
     if (latent_out && !lat_dev)
         CK(cudaMemcpyAsync(latent_out, c->hq_lat.p, (size_t)b * c->L, cudaMemcpyDeviceToHost, s));

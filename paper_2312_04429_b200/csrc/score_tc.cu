@@ -77,6 +77,15 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
         : "memory");
 }
 
+// One lane of a converged warp (elect.sync): the rest of the warp stays in uniform control flow.
+__device__ __forceinline__ bool elect_one() {
+    uint32_t e;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(e));
+    return e != 0;
+}
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -233,30 +242,37 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ C
         }
     } else if (warp == 1) {
         // ------------------------------- MMA issuer ---------------------------------
-        if (lane == 0) {
-            uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
-            for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-                const int chunk = u / m_tiles;
-                const int n0 = chunk * chunk_tiles, n1 = min(n_tiles, n0 + chunk_tiles);
-                for (int n = n0; n < n1; ++n) {
-                    mbar_wait(bar_tempty + 8 * acc, acc_phase ^ 1);
+        // The whole warp runs the loop (warp-uniform control flow keeps the descriptor
+        // arithmetic in uniform registers); one elected lane issues.  Issued from a single
+        // divergent lane, every tcgen05.mma got an ELECT/R2UR.BROADCAST wrapper and the
+        // ~110-instruction k-chunk loop took about as long as the 512 tensor cycles it feeds.
+        const uint64_t desc0 = sw128_desc(sbase);
+        uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+            const int chunk = u / m_tiles;
+            const int n0 = chunk * chunk_tiles, n1 = min(n_tiles, n0 + chunk_tiles);
+            for (int n = n0; n < n1; ++n) {
+                mbar_wait(bar_tempty + 8 * acc, acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem_base + acc * BN;
+                for (int kc = 0; kc < kch; ++kc) {
+                    mbar_wait(bar_full + 8 * stage, phase);
                     tc_fence_after();
-                    const uint32_t d = tmem_base + acc * BN;
-                    for (int kc = 0; kc < kch; ++kc) {
-                        mbar_wait(bar_full + 8 * stage, phase);
-                        tc_fence_after();
-                        const uint32_t sa = sbase + stage * STAGE_BYTES;
-                        const uint64_t ad = sw128_desc(sa), bd = sw128_desc(sa + A_BYTES);
+                    const uint64_t ad = desc0 + (uint64_t)(stage * (STAGE_BYTES >> 4));
+                    const uint64_t bd = ad + (uint64_t)(A_BYTES >> 4);
+                    if (elect_one()) {
 #pragma unroll
                         for (int k = 0; k < BK / 16; ++k)   // +32 B along K inside the swizzle atom
                             umma_bf16(d, ad + 2 * k, bd + 2 * k, (kc | k) != 0);
                         umma_commit(bar_empty + 8 * stage);  // frees the smem stage when done
-                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
-                    umma_commit(bar_tfull + 8 * acc);        // accumulator ready
-                    acc ^= 1;
-                    if (acc == 0) acc_phase ^= 1;
+                    __syncwarp();
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
+                if (elect_one()) umma_commit(bar_tfull + 8 * acc);   // accumulator ready
+                __syncwarp();
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
             }
         }
     } else if (warp >= EPI_WARP0) {
@@ -495,7 +511,9 @@ k_score_tc2(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ 
         }
     } else if (warp == 1) {
         // ------------------------------- MMA issuer (leader only) --------------------
-        if (lane == 0 && rank == 0) {
+        // whole warp in the loop, one elected lane issues (see the single-CTA kernel)
+        if (rank == 0) {
+            const uint64_t desc0 = sw128_desc(sbase);
             uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
             for (int u = cid; u < n_units; u += n_clusters) {
                 const int chunk = u / m_pairs;
@@ -507,15 +525,19 @@ k_score_tc2(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ 
                     for (int kc = 0; kc < kch; ++kc) {
                         mbar_wait(bar_full + 8 * stage, phase);
                         tc_fence_after();
-                        const uint32_t sa = sbase + stage * STAGE_BYTES;
-                        const uint64_t ad = sw128_desc(sa), bd = sw128_desc(sa + A_BYTES);
+                        const uint64_t ad = desc0 + (uint64_t)(stage * (STAGE_BYTES >> 4));
+                        const uint64_t bd = ad + (uint64_t)(A_BYTES >> 4);
+                        if (elect_one()) {
 #pragma unroll
-                        for (int k = 0; k < BK / 16; ++k)
-                            umma_bf16_pair(d, ad + 2 * k, bd + 2 * k, (kc | k) != 0);
-                        umma_commit_pair(bar_empty + 8 * stage);   // frees the stage in both CTAs
+                            for (int k = 0; k < BK / 16; ++k)
+                                umma_bf16_pair(d, ad + 2 * k, bd + 2 * k, (kc | k) != 0);
+                            umma_commit_pair(bar_empty + 8 * stage);   // frees the stage in both CTAs
+                        }
+                        __syncwarp();
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
-                    umma_commit_pair(bar_tfull + 8 * acc);         // both CTAs' accumulators ready
+                    if (elect_one()) umma_commit_pair(bar_tfull + 8 * acc);   // both CTAs' accumulators ready
+                    __syncwarp();
                     acc ^= 1;
                     if (acc == 0) acc_phase ^= 1;
                 }

@@ -6,7 +6,7 @@ import pytest
 import torch
 
 import synth
-from tests.parity import gpu_to_numpy
+from tests.parity import check_batch, gpu_to_numpy
 
 pytestmark = pytest.mark.gpu
 
@@ -32,3 +32,41 @@ def test_host_call_with_device_latent_buffer():
     assert np.array_equal(got[hit], d["latents"][hit]) and not got[~hit].any()
     h = g.query_host(np.ascontiguousarray(q), topk=2)            # host latent buffer
     assert np.array_equal(h["latents"][hit], d["latents"][hit])
+
+
+@pytest.mark.parametrize("b", [2048, 3000])
+def test_host_call_split_upload_equals_device(oracle_mod, b):
+    """b >= 2048: the upload is split into 4 slices (ragged last slice at b=3000) that overlap
+    the scan.  Results equal the device call's, and the batch is ONE tick of the LRU clock
+    (R13): LRU eviction after the call matches the oracle's, which ticks once per batch."""
+    from paper_2312_04429_b200 import binding as B
+    n, L = 1500, 256
+    emb, cl = synth.entries(n, seed=b)
+    lat = synth.latents_np(np.arange(n), 5, L, seed=b)
+    mk = lambda: B.NirvanaCache(entry_capacity=n, latent_capacity=5 * n, dim=768, latent_bytes=L)
+    g, gd = mk(), mk()
+    for c in (g, gd):
+        c.set_evict_policy(B.POLICY_LRU)
+        c.insert(torch.from_numpy(emb).cuda(), torch.from_numpy(lat).cuda())
+    o = oracle_mod.OracleCache(dim=768, entry_capacity=n, latent_capacity=5 * n, latent_bytes=L)
+    o.insert(emb, latents=lat)
+    q, _, _ = synth.queries(emb, cl, b, seed=b + 1)
+    d = gpu_to_numpy(gd.query(torch.from_numpy(q).cuda(), topk=4))
+    dev_lat = torch.zeros((b, L), dtype=torch.uint8, device="cuda")
+    out = dict(ids=np.empty((b, 4), np.uint64), scores=np.empty((b, 4), np.float32), k=np.empty(b, np.int32),
+               status=np.empty(b, np.int32), latents=dev_lat)
+    g.query_host(torch.from_numpy(q).pin_memory(), topk=4, out=out)
+    for key in ("ids", "scores", "k", "status"):
+        assert np.array_equal(out[key], d[key]), key
+    hit = d["k"] > 0
+    assert np.array_equal(dev_lat.cpu().numpy()[hit], d["latents"][hit])
+    check_batch(d, o, q, 4, expected_latent=None)            # oracle: same access, one clock tick
+    q2, _, _ = synth.queries(emb, cl, 64, seed=b + 2)        # a second (unsplit) batch on all three
+    check_batch(gpu_to_numpy(g.query(torch.from_numpy(q2).cuda(), topk=1, latents=False)), o, q2, 1,
+                expected_latent=None)
+    gd.query(torch.from_numpy(q2).cuda(), topk=1, latents=False)
+    ev, dirty = g.evict(900)
+    rc, oev, od = o.evict(900, policy=oracle_mod.LRU)
+    assert rc == 0 and np.array_equal(ev, oev) and np.array_equal(dirty, od)
+    evd, _ = gd.evict(900)
+    assert np.array_equal(ev, evd)
