@@ -99,7 +99,17 @@ typedef struct {
                                  capacity; the pool is filled with cache_pool_write and is
                                  never freed by eviction.                                  */
     int32_t evict_policy;     /* CACHE_POLICY_*: which item score cache_evict minimises     */
+    int32_t evict_granularity; /* CACHE_EVICT_ITEM (default, the paper's) or CACHE_EVICT_ENTRY */
 } cache_config;
+
+/* Eviction granularity (SURVEY 8(b) / reading c10, DESIGN R24).
+ * ITEM:  cache_evict(n) removes the n (entry, K) items with the smallest policy score
+ *        (P:602-611); entries left with no K are dirty and removed too.
+ * ENTRY: cache_evict(n) removes n whole entries, those with the smallest ENTRY score = the
+ *        policy score aggregated over the entry's stored items -- LCBFU sum f_j x K_j (the
+ *        segmented reduction), LFU sum f_j, LRU max of the items' last-access clocks, FIFO 0 --
+ *        ties by id ascending; every stored state of an evicted entry is freed. */
+enum { CACHE_EVICT_ITEM = 0, CACHE_EVICT_ENTRY = 1 };
 
 /* Eviction policies: the item score minimised by cache_evict (ties by (id, K) ascending).
  * LCBFU is the paper's policy; the others are the baselines it is compared with. */
@@ -227,7 +237,10 @@ cache_status cache_query_batch_host(cache_t *c, int64_t b, const void *queries, 
  *   out_evicted    host pointer, n u64 (id << 3 | j) in eviction order; may be NULL
  *   out_dirty_ids  host pointer, capacity n, ids of removed entries ascending; may be NULL
  *   out_n_dirty    host pointer, number of entries removed; may be NULL
- * n > live items -> CACHE_E_EVICT_RANGE.  Synchronises `stream`. */
+ * n > live items -> CACHE_E_EVICT_RANGE.  Synchronises `stream`.
+ * With evict_granularity = CACHE_EVICT_ENTRY, n counts entries (n > live entries ->
+ * CACHE_E_EVICT_RANGE), out_evicted receives the n entry ids in eviction order (ascending
+ * entry score, then id) and out_dirty_ids the same ids ascending (*out_n_dirty = n). */
 cache_status cache_evict(cache_t *c, int64_t n, uint64_t *out_evicted, uint64_t *out_dirty_ids,
                          int64_t *out_n_dirty, void *stream);
 
@@ -250,6 +263,8 @@ cache_status cache_evict_apply(cache_t *c, const cache_evict_state *st, int64_t 
                                int64_t *out_n_dirty, void *stream);
 /* Live items on this rank (host-synchronous). */
 int64_t cache_live_items(const cache_t *c);
+/* Live entries on this rank (host-synchronous). */
+int64_t cache_live_entries(const cache_t *c);
 
 /* ---- sharded lookup ----
  * 1. every rank gathers the global batch of b queries (caller's all-gather);
@@ -301,6 +316,8 @@ cache_status cache_stats(cache_t *c, cache_stats_t *out);
 
 /* Select the eviction policy (CACHE_POLICY_*) used by later cache_evict calls. */
 cache_status cache_set_evict_policy(cache_t *c, int32_t policy);
+/* Select the eviction granularity (CACHE_EVICT_ITEM / CACHE_EVICT_ENTRY) of later evictions. */
+cache_status cache_set_evict_granularity(cache_t *c, int32_t granularity);
 
 /* Force a scoring kernel (CACHE_SCORER_*); AUTO by default. */
 cache_status cache_set_scorer(cache_t *c, int32_t scorer);

@@ -56,6 +56,7 @@ def lib():
         L.oracle_score_id.restype = D
         L.oracle_evict.argtypes = [P, I64, P, P, P]
         L.oracle_evict_policy.argtypes = [P, I64, I32, P, P, P]
+        L.oracle_evict_entries.argtypes = [P, I64, I32, P]
         L.oracle_tick.argtypes = [P]
         L.oracle_tick.restype = None
         L.oracle_clock.argtypes = [P]
@@ -158,6 +159,13 @@ class OracleCache:
         nd = np.zeros(1, dtype=np.int64)
         rc = lib().oracle_evict_policy(self._h, n, policy, _p(ev), _p(dirty), _p(nd))
         return rc, ev[:n].copy(), dirty[: int(nd[0])].copy()
+
+    def evict_entries(self, n, policy=0):
+        """Entry granularity (R24): remove the n entries with the smallest aggregated policy
+        score (LCBFU sum f*K, LRU max last, LFU sum f, FIFO 0), ties by id.  Returns (rc, ids)."""
+        ids = np.empty(max(n, 1), dtype=np.uint64)
+        rc = lib().oracle_evict_entries(self._h, n, policy, _p(ids))
+        return rc, ids[:n].copy()
 
     def tick(self):
         lib().oracle_tick(self._h)

@@ -583,6 +583,72 @@ int oracle_evict_policy(oracle_cache *c, int64_t n, int policy, uint64_t *out_ev
     return ORC_OK;
 }
 
+/* Entry-granularity eviction (SURVEY 8(b) evict_granularity = entry, reading c10 / DESIGN R24):
+ * the score of a live entry is its items' policy scores aggregated over its PRESENT K --
+ *   0 LCBFU  sum_j f_j x K_j   (the "segmented reduction" of the north_star)
+ *   1 LRU    max_j last_j      (an entry is as recent as its most recently used state)
+ *   2 LFU    sum_j f_j
+ *   3 FIFO   0                 (the id decides)
+ * Entries are ordered by (score, id) ascending and the first n are removed whole: every
+ * stored state freed, the prompt gone from the index.
+ *   out_ids[n] : removed entry ids in eviction order; may be NULL
+ * n > live entries -> ORC_E_EVICT_RANGE. */
+typedef struct {
+    uint64_t score;
+    uint64_t id;
+    int64_t idx;
+} entry_rank;
+
+static int cmp_entry(const void *a, const void *b)
+{
+    const entry_rank *x = (const entry_rank *)a, *y = (const entry_rank *)b;
+    if (x->score != y->score) return x->score < y->score ? -1 : 1;
+    return x->id < y->id ? -1 : (x->id > y->id ? 1 : 0);
+}
+
+int oracle_evict_entries(oracle_cache *c, int64_t n, int policy, uint64_t *out_ids)
+{
+    entry_rank *er;
+    int64_t i, m = 0;
+    if (n < 0 || policy < 0 || policy > 3) return ORC_E_INVALID_ARG;
+    if (n > c->live_entries) return ORC_E_EVICT_RANGE;
+    er = (entry_rank *)malloc(sizeof(entry_rank) * (c->live_entries > 0 ? c->live_entries : 1));
+    if (!er) return ORC_E_OOM;
+    for (i = 0; i < c->n_e; i++) {
+        int j;
+        uint64_t sc = 0;
+        const oentry *e = &c->e[i];
+        if (!e->live) continue;
+        for (j = 0; j < c->num_k; j++) {
+            uint64_t v;
+            if (!e->present[j]) continue;
+            v = policy_score(c, e, j, policy);
+            if (policy == 1) sc = v > sc ? v : sc;
+            else sc += v;
+        }
+        er[m].score = sc;
+        er[m].id = e->id;
+        er[m].idx = i;
+        m++;
+    }
+    qsort(er, (size_t)m, sizeof(entry_rank), cmp_entry);
+    for (i = 0; i < n; i++) {
+        int j;
+        oentry *e = &c->e[er[i].idx];
+        for (j = 0; j < c->num_k; j++) {
+            if (!e->present[j]) continue;
+            e->present[j] = 0;
+            c->live_items--;
+        }
+        e->live = 0;
+        free_entry_payload(c, e);
+        c->live_entries--;
+        if (out_ids) out_ids[i] = er[i].id;
+    }
+    free(er);
+    return ORC_OK;
+}
+
 /* ---- inspection helpers for tests ---- */
 int64_t oracle_live_entries(const oracle_cache *c) { return c->live_entries; }
 int64_t oracle_live_items(const oracle_cache *c) { return c->live_items; }

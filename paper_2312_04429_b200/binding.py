@@ -39,10 +39,12 @@ class CacheConfig(ctypes.Structure):
                 ("num_k", ctypes.c_int32), ("k_values", ctypes.c_int32 * MAX_K),
                 ("thresholds", ctypes.c_double * MAX_K), ("k_bias", ctypes.c_int32),
                 ("max_topk", ctypes.c_int32), ("shard_rank", ctypes.c_int32), ("shard_world", ctypes.c_int32),
-                ("latent_alias", ctypes.c_int32), ("evict_policy", ctypes.c_int32)]
+                ("latent_alias", ctypes.c_int32), ("evict_policy", ctypes.c_int32),
+                ("evict_granularity", ctypes.c_int32)]
 
 
 POLICY_LCBFU, POLICY_LRU, POLICY_LFU, POLICY_FIFO = 0, 1, 2, 3
+EVICT_ITEM, EVICT_ENTRY = 0, 1   # eviction granularity (CACHE_EVICT_*)
 
 
 def alias_slot(id_: int, j: int, cap: int) -> int:
@@ -73,7 +75,8 @@ EXPORTS = ("cache_default_config", "cache_create", "cache_destroy", "cache_inser
            "cache_set_scorer", "cache_set_profile_events", "cache_kernel_launches", "cache_last_error",
            "cache_evict_hist", "cache_evict_pick", "cache_evict_apply", "cache_live_items", "cache_query_local",
            "cache_query_merge", "cache_export_peer", "cache_attach_peers", "cache_pool_write",
-           "cache_set_evict_policy", "cache_predictor_train", "cache_predict", "cache_predictor_get")
+           "cache_set_evict_policy", "cache_predictor_train", "cache_predict", "cache_predictor_get",
+           "cache_set_evict_granularity", "cache_live_entries")
 
 
 def load_library(path: str = LIB_PATH):
@@ -101,6 +104,10 @@ def load_library(path: str = LIB_PATH):
     L.cache_evict_apply.argtypes = [P, P, I64, P, P, P, P, P]
     L.cache_live_items.argtypes = [P]
     L.cache_live_items.restype = I64
+    L.cache_live_entries.argtypes = [P]
+    L.cache_live_entries.restype = I64
+    L.cache_set_evict_granularity.argtypes = [P, I32]
+    L.cache_set_evict_granularity.restype = ctypes.c_int
     L.cache_query_local.argtypes = [P, I64, P, I32, I32, P, P]
     L.cache_query_merge.argtypes = [P, I64, I64, I64, I32, P, P, P, P, P, P, P, P]
     L.cache_export_peer.argtypes = [P, ctypes.POINTER(PeerDesc)]
@@ -172,7 +179,8 @@ class NirvanaCache:
     def __init__(self, entry_capacity: int, latent_capacity: int | None = None, dim: int = 768,
                  latent_bytes: int = 32768, k_values=(5, 10, 15, 20, 25),
                  thresholds=(0.65, 0.75, 0.85, 0.90, 0.95), k_bias: int = 0, max_topk: int = MAX_TOPK,
-                 device: int | None = None, shard_rank: int = 0, shard_world: int = 1, latent_alias: bool = False):
+                 device: int | None = None, shard_rank: int = 0, shard_world: int = 1, latent_alias: bool = False,
+                 evict_granularity: int = EVICT_ITEM):
         if device is None:
             device = torch.cuda.current_device()
         self.device = device
@@ -181,7 +189,9 @@ class NirvanaCache:
         self.cfg = default_config(dim=dim, entry_capacity=entry_capacity, latent_capacity=latent_capacity,
                                   latent_bytes=latent_bytes, k_values=tuple(k_values),
                                   thresholds=tuple(thresholds), k_bias=k_bias, max_topk=max_topk,
-                                  shard_rank=shard_rank, shard_world=shard_world, latent_alias=int(latent_alias))
+                                  shard_rank=shard_rank, shard_world=shard_world, latent_alias=int(latent_alias),
+                                  evict_granularity=evict_granularity)
+        self.granularity = evict_granularity
         self.latent_capacity = latent_capacity
         self.shard_rank, self.shard_world = shard_rank, shard_world
         self.dim, self.latent_bytes, self.num_k = dim, latent_bytes, len(k_values)
@@ -357,6 +367,21 @@ class NirvanaCache:
     @property
     def live_items(self) -> int:
         return _lib.cache_live_items(self._h)
+
+    @property
+    def live_entries(self) -> int:
+        return _lib.cache_live_entries(self._h)
+
+    def set_evict_granularity(self, granularity: int):
+        """EVICT_ITEM (the paper's item granularity) or EVICT_ENTRY: evict(n) then removes n
+        whole entries by the aggregated policy score (include/nirvana_cache.h, R24)."""
+        _check(_lib.cache_set_evict_granularity(self._h, granularity))
+        self.granularity = granularity
+
+    @property
+    def evict_units(self) -> int:
+        """What evict(n) counts on this rank: live items, or live entries in entry mode."""
+        return self.live_entries if getattr(self, "granularity", EVICT_ITEM) == EVICT_ENTRY else self.live_items
 
     def set_profile_events(self, events):
         """events: 4 torch.cuda.Event(enable_timing=True) (recorded around ingest / score /

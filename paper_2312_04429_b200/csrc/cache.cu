@@ -221,6 +221,11 @@ cache_status cache_create(const cache_config* cfg, int device, cache_t** out) {
     c->km.num_k = c->num_k;
     c->km.k_bias = cfg->k_bias;
     c->km.policy = cfg->evict_policy;
+    c->km.gran = cfg->evict_granularity;
+    if (cfg->evict_granularity != CACHE_EVICT_ITEM && cfg->evict_granularity != CACHE_EVICT_ENTRY) {
+        delete c;
+        return fail(CACHE_E_INVALID_ARG, "cache_create: bad evict_granularity");
+    }
     if (cfg->evict_policy < CACHE_POLICY_LCBFU || cfg->evict_policy > CACHE_POLICY_FIFO) {
         delete c;
         return fail(CACHE_E_INVALID_ARG, "cache_create: bad evict_policy");
@@ -795,7 +800,8 @@ cache_status cache_evict(cache_t* c, int64_t n, uint64_t* out_evicted, uint64_t*
                          int64_t* out_n_dirty, void* stream) {
     if (!c) return fail(CACHE_E_INVALID_ARG, "cache_evict: null cache");
     if (n < 0) return fail(CACHE_E_INVALID_ARG, "cache_evict: n < 0");
-    if (n > c->live_items) return fail(CACHE_E_EVICT_RANGE, "cache_evict: n exceeds live items");
+    if (c->km.gran == CACHE_EVICT_ENTRY ? n > c->live_entries : n > c->live_items)
+        return fail(CACHE_E_EVICT_RANGE, "cache_evict: n exceeds live items (entries in entry mode)");
     if (out_n_dirty) *out_n_dirty = 0;
     if (n == 0) return CACHE_OK;
     DeviceGuard g(c->device);
@@ -817,12 +823,53 @@ cache_status cache_evict(cache_t* c, int64_t n, uint64_t* out_evicted, uint64_t*
     return CACHE_OK;
 }
 
+// Host bookkeeping of an entry-granularity eviction (k_evict_apply wrote one (key, slot) per
+// evicted entry): free every stored state's pool slot and the entry slot, in key order.
+static cache_status evict_entries_host(cache_t* c, int64_t n, uint64_t* out_evicted, uint64_t* out_dirty_ids,
+                                       int64_t* out_n_dirty) {
+    std::vector<unsigned long long> keys(n);
+    std::vector<int64_t> dslots(n);
+    if (n) {
+        CK(cudaMemcpy(keys.data(), c->ekey.p, n * 8, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(dslots.data(), c->edirty.p, n * 8, cudaMemcpyDeviceToHost));
+    }
+    std::vector<size_t> order(n);
+    for (int64_t i = 0; i < n; ++i) order[i] = i;
+    std::sort(order.begin(), order.end(), [&](size_t a, size_t b2) { return keys[a] < keys[b2]; });
+    std::vector<uint64_t> dids;
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t slot = dslots[order[i]];
+        const uint64_t id = c->h_ids[slot];
+        if (out_evicted) out_evicted[i] = id;
+        dids.push_back(id);
+        const uint32_t m = c->h_present[slot];
+        for (int j = 0; j < c->num_k; ++j) {
+            if (!((m >> j) & 1u)) continue;
+            if (!c->alias) c->free_l.push_back(c->h_lslot[slot * c->num_k + j]);
+            c->h_lslot[slot * c->num_k + j] = -1;
+            c->live_items--;
+        }
+        c->h_present[slot] = 0;
+        c->id2slot.erase(id);
+        c->free_e.push_back(slot);
+        c->live_entries--;
+    }
+    std::sort(dids.begin(), dids.end());
+    if (out_dirty_ids)
+        for (size_t i = 0; i < dids.size(); ++i) out_dirty_ids[i] = dids[i];
+    if (out_n_dirty) *out_n_dirty = (int64_t)dids.size();
+    std::sort(c->free_l.begin(), c->free_l.end(), std::greater<int64_t>());
+    std::sort(c->free_e.begin(), c->free_e.end(), std::greater<int64_t>());
+    while (c->hwm > 0 && c->h_present[c->hwm - 1] == 0) c->hwm--;
+    return CACHE_OK;
+}
+
 cache_status cache_evict_apply(cache_t* c, const cache_evict_state* st, int64_t cap, uint64_t* out_evicted,
                                int64_t* out_n, uint64_t* out_dirty_ids, int64_t* out_n_dirty, void* stream) {
     if (!c || !st || cap < 0) return fail(CACHE_E_INVALID_ARG, "cache_evict_apply: bad argument");
     DeviceGuard g(c->device);
     cudaStream_t s = (cudaStream_t)stream;
-    const int64_t bound = std::max<int64_t>(1, c->live_items);
+    const int64_t bound = std::max<int64_t>(1, std::max(c->live_items, c->live_entries));
     CK(c->ekey.ensure(bound));
     CK(c->elslot.ensure(bound));
     CK(c->ecnt.ensure(2));
@@ -838,6 +885,7 @@ cache_status cache_evict_apply(cache_t* c, const cache_evict_state* st, int64_t 
     if (out_n) *out_n = n;
     if (n > cap || (int64_t)cnt[1] > cap)
         return fail(CACHE_E_STATE, "cache_evict_apply: more evictions than the output capacity");
+    if (c->km.gran == CACHE_EVICT_ENTRY) return evict_entries_host(c, n, out_evicted, out_dirty_ids, out_n_dirty);
     std::vector<unsigned long long> keys(n);
     std::vector<int32_t> ls(n);
     std::vector<int64_t> dslots(cnt[1]);
@@ -919,6 +967,15 @@ cache_status cache_stats(cache_t* c, cache_stats_t* out) {
     out->queries = c->queries;
     out->free_entries = (int64_t)c->free_e.size();
     out->free_items = (int64_t)c->free_l.size();
+    return CACHE_OK;
+}
+
+int64_t cache_live_entries(const cache_t* c) { return c ? c->live_entries : 0; }
+
+cache_status cache_set_evict_granularity(cache_t* c, int32_t granularity) {
+    if (!c || (granularity != CACHE_EVICT_ITEM && granularity != CACHE_EVICT_ENTRY))
+        return fail(CACHE_E_INVALID_ARG, "cache_set_evict_granularity: bad argument");
+    c->km.gran = granularity;
     return CACHE_OK;
 }
 

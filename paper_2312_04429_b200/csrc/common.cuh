@@ -116,6 +116,7 @@ struct KMap {
     int32_t num_k;
     int32_t k_bias;
     int32_t policy;   // CACHE_POLICY_* (eviction kernels)
+    int32_t gran;     // CACHE_EVICT_ITEM / CACHE_EVICT_ENTRY
 };
 
 }  // namespace nv

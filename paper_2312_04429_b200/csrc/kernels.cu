@@ -477,6 +477,26 @@ __device__ __forceinline__ unsigned long long evict_key(const KMap& km, const ui
     return (sc << 35) | ((unsigned long long)id << 3) | (unsigned long long)j;
 }
 
+// Entry-granularity key (R24): the policy score aggregated over the entry's stored items
+// (LCBFU sum f*K, LFU sum f, LRU max last access, FIFO 0), saturated at 2^32-1, << 32 | id.
+__device__ __forceinline__ unsigned long long evict_key_entry(const KMap& km, const uint32_t* __restrict__ fcnt,
+                                                              const uint32_t* __restrict__ lastacc, int64_t e,
+                                                              uint32_t m, uint32_t id) {
+    unsigned long long sc = 0ull;
+    for (int j = 0; j < km.num_k; ++j) {
+        if (!((m >> j) & 1u)) continue;
+        const int64_t it = e * km.num_k + j;
+        switch (km.policy) {
+            case CACHE_POLICY_LRU: sc = max(sc, (unsigned long long)lastacc[it]); break;
+            case CACHE_POLICY_LFU: sc += fcnt[it]; break;
+            case CACHE_POLICY_FIFO: break;
+            default: sc += (unsigned long long)fcnt[it] * (unsigned long long)km.kv[j]; break;
+        }
+    }
+    if (sc > 0xFFFFFFFFull) sc = 0xFFFFFFFFull;
+    return (sc << 32) | (unsigned long long)id;
+}
+
 __global__ void __launch_bounds__(256)
 k_evict_hist(const uint32_t* __restrict__ present, const uint32_t* __restrict__ fcnt,
              const uint32_t* __restrict__ lastacc, const uint32_t* __restrict__ ids, int64_t n_slots, KMap km,
@@ -490,6 +510,11 @@ k_evict_hist(const uint32_t* __restrict__ present, const uint32_t* __restrict__ 
         const uint32_t m = present[e];
         if (!m) continue;
         const uint32_t id = ids[e];
+        if (km.gran == CACHE_EVICT_ENTRY) {
+            const unsigned long long key = evict_key_entry(km, fcnt, lastacc, e, m, id);
+            if ((key & mask) == prefix) atomicAdd(&sh[(key >> shift) & 255ull], 1u);
+            continue;
+        }
         for (int j = 0; j < km.num_k; ++j) {
             if (!((m >> j) & 1u)) continue;
             const unsigned long long key = evict_key(km, fcnt, lastacc, e, j, id);
@@ -531,6 +556,21 @@ k_evict_apply(uint32_t* __restrict__ present, uint32_t* __restrict__ fcnt, const
         const uint32_t m = present[e];
         if (!m) continue;
         const uint32_t id = ids[e];
+        if (km.gran == CACHE_EVICT_ENTRY) {
+            // whole entry: all stored states freed (the host frees their pool slots from its
+            // mirror), entry invalidated; one record per evicted entry in both lists
+            const unsigned long long key = evict_key_entry(km, fcnt, lastacc, e, m, id);
+            if (key <= T) {
+                for (int j = 0; j < km.num_k; ++j) fcnt[e * km.num_k + j] = 0u;
+                present[e] = 0u;
+                inv_e[e] = __int_as_float(0x7FC00000);
+                const unsigned long long at = atomicAdd(&counters[0], 1ull);
+                atomicAdd(&counters[1], 1ull);
+                ev_key[at] = key;
+                dirty_slot[at] = e;
+            }
+            continue;
+        }
         uint32_t keep = m;
         for (int j = 0; j < km.num_k; ++j) {
             if (!((m >> j) & 1u)) continue;

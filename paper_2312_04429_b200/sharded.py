@@ -114,6 +114,9 @@ class ShardedCache:
     def set_evict_policy(self, policy: int):
         self.cache.set_evict_policy(policy)
 
+    def set_evict_granularity(self, granularity: int):
+        self.cache.set_evict_granularity(granularity)
+
     def alloc_outputs(self, b_local: int, topk: int = 1, latents: bool = True):
         return self.cache.alloc_outputs(b_local, topk, latents)
 
@@ -129,11 +132,12 @@ class ShardedCache:
         return query_protocol(self.comm, q_local, topk, local_fn, merge_fn)
 
     def evict(self, n: int):
-        """Collective: evict the n globally lowest LCBFU items (every rank passes the same n)."""
-        live = self.comm.all_reduce_sum(torch.tensor([self.cache.live_items], dtype=torch.int64,
+        """Collective: evict the n globally lowest-keyed items (entries in entry mode; every
+        rank passes the same n)."""
+        live = self.comm.all_reduce_sum(torch.tensor([self.cache.evict_units], dtype=torch.int64,
                                                      device="cuda")).item()
         if n > live:
-            raise B.CacheError(B.E_EVICT_RANGE, "sharded evict: n exceeds live items")
+            raise B.CacheError(B.E_EVICT_RANGE, "sharded evict: n exceeds live items / entries")
         st = torch.tensor([0, 0, n], dtype=torch.int64, device="cuda")
         hist = torch.zeros(256, dtype=torch.int32, device="cuda")
         evict_protocol(self.comm, n, st, hist, self.cache.evict_hist, self.cache.evict_pick)
@@ -181,9 +185,9 @@ class VirtualShards:
         return cat
 
     def evict(self, n: int):
-        live = sum(c.live_items for c in self.caches)
+        live = sum(c.evict_units for c in self.caches)
         if n > live:
-            raise B.CacheError(B.E_EVICT_RANGE, "sharded evict: n exceeds live items")
+            raise B.CacheError(B.E_EVICT_RANGE, "sharded evict: n exceeds live items / entries")
         sts = [torch.tensor([0, 0, n], dtype=torch.int64, device="cuda") for _ in self.caches]
         hists = [torch.zeros(256, dtype=torch.int32, device="cuda") for _ in self.caches]
         for p in range(8):
@@ -203,6 +207,10 @@ class VirtualShards:
     def set_evict_policy(self, policy: int):
         for c in self.caches:
             c.set_evict_policy(policy)
+
+    def set_evict_granularity(self, granularity: int):
+        for c in self.caches:
+            c.set_evict_granularity(granularity)
 
     def stats(self):
         ss = [c.stats() for c in self.caches]
