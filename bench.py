@@ -190,8 +190,9 @@ def run_sharded(args, cfg):
     n, b = cfg["n"], cfg["b"]
     bl = b // world
     pool_slots = cfg.get("pool_slots", 262_144)
+    push = args.exchange == "push"
     sc = ShardedCache(comm, entry_capacity=(n + world - 1) // world + 1024, latent_capacity=pool_slots,
-                      dim=D, latent_bytes=L, latent_alias=True)
+                      dim=D, latent_bytes=L, latent_alias=True, push_max_nb=bl if push else 0, push_max_topk=1)
     for s in range(0, pool_slots, 8192):
         m = min(8192, pool_slots - s)
         sc.cache.pool_write(s, synth.latents_torch(s, m, 1, L, seed=7, device="cuda").view(m, L))
@@ -246,8 +247,12 @@ def run_sharded(args, cfg):
                     vs_baseline=None, dtype="bf16",
                     data="synthetic on-device (counter-hash clustered unit-norm 768-d entries, Zipf anchors)",
                     config=dict(workload=cfg["workload"], entries=n, batch=b, dim=D, latent_bytes=L, topk=1,
-                                scorer="tc", parallelism=f"entry-sharded x{world} (NCCL all-gather of queries "
-                                                         f"and 16-B records, P2P latent fetch)",
+                                scorer="tc",
+                                parallelism=(f"entry-sharded x{world} (fused push exchange: ingest kernel stores "
+                                             f"query rows and local-merge kernel stores 16-B records straight "
+                                             f"into peer arenas over NVLink, epoch flags; P2P latent fetch)")
+                                if push else (f"entry-sharded x{world} (NCCL all-gather of queries and 16-B "
+                                              f"records, P2P latent fetch)"),
                                 latent_pool=f"aliased, {pool_slots} slots per rank",
                                 l2="flushed between timed steps (512 MiB write)", hit_rate=float((k_np > 0).mean())),
                     kernel_ms=dict(score_local=sc_ms),
@@ -271,6 +276,8 @@ def main():
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--scorer", default="auto", choices=["auto", "tc", "tc1", "stream"],
                     help="tc1 = single-CTA tensor-core scan (auto/tc use CTA pairs for > 128 queries)")
+    ap.add_argument("--exchange", default="push", choices=["push", "nccl"],
+                    help="sharded configs (c4): fused P2P push exchange or NCCL all-gathers")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-maintenance", action="store_true")

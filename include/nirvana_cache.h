@@ -164,6 +164,11 @@ typedef struct {
     int64_t latent_bytes;
     void *lslot, *fcnt, *pool, *lastacc;           /* raw device pointers (same process)   */
     unsigned char ipc_lslot[64], ipc_fcnt[64], ipc_pool[64], ipc_lastacc[64]; /* IPC handles */
+    void *arena;                 /* push-exchange arena (cache_push_reserve) or NULL          */
+    int64_t arena_nb;            /* its geometry: max local batch, max topk                   */
+    int32_t arena_topk;
+    int32_t reserved2;
+    unsigned char ipc_arena[64];
 } cache_peer_desc;
 
 /* Fill *cfg with the paper's defaults: dim 768, K = {5,10,15,20,25}, Fig. 11
@@ -284,6 +289,37 @@ cache_status cache_query_merge(cache_t *c, int64_t b, int64_t row0, int64_t nb, 
                                int32_t *row_status, void *stream);
 cache_status cache_export_peer(cache_t *c, cache_peer_desc *out);
 cache_status cache_attach_peers(cache_t *c, int32_t world, const cache_peer_desc *descs);
+
+/* ---- sharded lookup with the exchanges fused into the kernels (SURVEY 8(e) "fusing the
+ * record push"; no collective library on the data path) ----
+ * Every rank owns an exchange ARENA in its HBM (flags, the global query batch as bf16 rows +
+ * inv-norms + statuses, and a record inbox); peers write into it over NVLink (P2P stores
+ * through CUDA IPC mappings).  Rank r's local batch is global rows [r*nb, r*nb + nb).
+ *  cache_push_reserve  allocate the arena for local batches <= max_nb and topk <= max_topk;
+ *                      call before cache_export_peer (the descriptor carries its IPC handle).
+ *  phase 1  cache_push_queries: ingest this rank's nb queries (the a1 rule) and store each
+ *           normalised row straight into EVERY rank's arena (the query all-gather fused
+ *           into the ingest kernel); the grid's last CTA publishes the batch epoch on every
+ *           rank's query flag for this sender (st.release.sys).
+ *  phase 2  cache_push_scan: wait for all ranks' query flags (ld.acquire.sys), tcgen05 scan
+ *           of this rank's shard for all world*nb rows, then the local merge stores each
+ *           row's top-k shard records straight into the OWNER's inbox (the record exchange
+ *           fused into the merge kernel) and publishes the epoch on the record flags.
+ *  phase 3  cache_push_merge: wait for all ranks' record flags, then merge this rank's own
+ *           rows exactly as cache_query_merge (P2P latent fetch, P2P counter atomics).
+ * Every rank calls the three phases in order, once per batch, with the same nb and topk
+ * (ranks in separate processes may call them back to back; virtual ranks in one process on
+ * one stream call phase 1 on all ranks, then phase 2, then phase 3).  Outputs as in
+ * cache_query_batch, nb rows.  Arena reuse across batches needs no extra barrier: a rank
+ * writes batch t+1 into a peer's arena only after the peer has published batch t+1's queries,
+ * i.e. after it finished merging batch t.  A wait that sees no progress for ~17 s traps
+ * (a dead peer fails the context instead of hanging it). */
+cache_status cache_push_reserve(cache_t *c, int64_t max_nb, int32_t max_topk);
+cache_status cache_push_queries(cache_t *c, int64_t nb, const void *queries, int32_t q_dtype, void *stream);
+cache_status cache_push_scan(cache_t *c, int64_t nb, int32_t topk, void *stream);
+cache_status cache_push_merge(cache_t *c, int64_t nb, int32_t topk, uint64_t *out_ids, float *out_scores,
+                              int32_t *out_k, void *latent_out, void **out_latent_ptr, int32_t *row_status,
+                              void *stream);
 
 /* ---- match predictor ----
  * A linear one-class SVM f(x) = <w, x> - rho over the cached embeddings (unit-scaled stored

@@ -63,7 +63,9 @@ class PeerDesc(ctypes.Structure):
                 ("reserved", ctypes.c_int32), ("latent_bytes", ctypes.c_int64), ("lslot", ctypes.c_void_p),
                 ("fcnt", ctypes.c_void_p), ("pool", ctypes.c_void_p), ("lastacc", ctypes.c_void_p),
                 ("ipc_lslot", ctypes.c_ubyte * 64), ("ipc_fcnt", ctypes.c_ubyte * 64),
-                ("ipc_pool", ctypes.c_ubyte * 64), ("ipc_lastacc", ctypes.c_ubyte * 64)]
+                ("ipc_pool", ctypes.c_ubyte * 64), ("ipc_lastacc", ctypes.c_ubyte * 64),
+                ("arena", ctypes.c_void_p), ("arena_nb", ctypes.c_int64), ("arena_topk", ctypes.c_int32),
+                ("reserved2", ctypes.c_int32), ("ipc_arena", ctypes.c_ubyte * 64)]
 
 
 SHARD_REC_BYTES = 16   # cache_shard_rec
@@ -76,7 +78,8 @@ EXPORTS = ("cache_default_config", "cache_create", "cache_destroy", "cache_inser
            "cache_evict_hist", "cache_evict_pick", "cache_evict_apply", "cache_live_items", "cache_query_local",
            "cache_query_merge", "cache_export_peer", "cache_attach_peers", "cache_pool_write",
            "cache_set_evict_policy", "cache_predictor_train", "cache_predict", "cache_predictor_get",
-           "cache_set_evict_granularity", "cache_live_entries")
+           "cache_set_evict_granularity", "cache_live_entries", "cache_push_reserve", "cache_push_queries",
+           "cache_push_scan", "cache_push_merge")
 
 
 def load_library(path: str = LIB_PATH):
@@ -106,6 +109,10 @@ def load_library(path: str = LIB_PATH):
     L.cache_live_items.restype = I64
     L.cache_live_entries.argtypes = [P]
     L.cache_live_entries.restype = I64
+    L.cache_push_reserve.argtypes = [P, I64, I32]
+    L.cache_push_queries.argtypes = [P, I64, P, I32, P]
+    L.cache_push_scan.argtypes = [P, I64, I32, P]
+    L.cache_push_merge.argtypes = [P, I64, I32, P, P, P, P, P, P, P]
     L.cache_set_evict_granularity.argtypes = [P, I32]
     L.cache_set_evict_granularity.restype = ctypes.c_int
     L.cache_query_local.argtypes = [P, I64, P, I32, I32, P, P]
@@ -338,6 +345,27 @@ class NirvanaCache:
         _check(_lib.cache_query_merge(self._h, b, row0, nb, topk, _ptr(recs_all), _ptr(out["ids"]),
                                       _ptr(out["scores"]), _ptr(out["k"]), _ptr(out.get("latents")),
                                       _ptr(out.get("ptrs")), _ptr(out.get("status")), _stream(stream)))
+        return out
+
+    # ---- push exchange (include/nirvana_cache.h, cache_push_*) ----
+    def push_reserve(self, max_nb: int, max_topk: int):
+        """Allocate this rank's exchange arena; before export_peer."""
+        _check(_lib.cache_push_reserve(self._h, max_nb, max_topk))
+
+    def push_queries(self, q_local: torch.Tensor, stream=None):
+        """Phase 1: ingest this rank's rows and store them into every rank's arena."""
+        dt = DTYPE_BF16 if q_local.dtype == torch.bfloat16 else DTYPE_F32
+        _check(_lib.cache_push_queries(self._h, q_local.shape[0], _ptr(q_local), dt, _stream(stream)))
+
+    def push_scan(self, nb: int, topk: int, stream=None):
+        """Phase 2: wait for every rank's rows, scan this shard, push records to their owners."""
+        _check(_lib.cache_push_scan(self._h, nb, topk, _stream(stream)))
+
+    def push_merge(self, nb: int, topk: int, out: dict, stream=None):
+        """Phase 3: wait for every rank's records, merge this rank's own nb rows into out."""
+        _check(_lib.cache_push_merge(self._h, nb, topk, _ptr(out["ids"]), _ptr(out["scores"]), _ptr(out["k"]),
+                                     _ptr(out.get("latents")), _ptr(out.get("ptrs")), _ptr(out.get("status")),
+                                     _stream(stream)))
         return out
 
     def export_peer(self) -> PeerDesc:

@@ -21,6 +21,29 @@ using namespace nv;
 namespace {
 thread_local std::string g_err = "no error";
 
+// Exchange arena of the push path (identical geometry on every rank, so peers derive the
+// offsets from the descriptor): flags | CTA counters | inv-norms | statuses | record inbox |
+// bf16 query rows (rows padded to a multiple of 128 for the scan's TMA boxes).
+struct ArenaLayout {
+    size_t qflag, rflag, done, invq, qstat, inbox, qg, total;
+    int64_t rows;   // padded global rows
+};
+ArenaLayout arena_layout(int world, int64_t max_nb, int topk, int dim) {
+    auto al = [](size_t x) { return (x + 1023) & ~size_t(1023); };
+    ArenaLayout L{};
+    L.rows = std::max<int64_t>(128, ((int64_t)world * max_nb + 127) / 128 * 128);
+    L.qflag = 0;                          // u32[kMaxWorld]: query flag per sender
+    L.rflag = 64;                         // u32[kMaxWorld]: record flag per sender
+    L.done = 128;                         // u32[2]: CTA counters of the two push kernels
+    size_t off = 1024;
+    L.invq = off;  off = al(off + (size_t)L.rows * 4);
+    L.qstat = off; off = al(off + (size_t)L.rows * 4);
+    L.inbox = off; off = al(off + (size_t)world * max_nb * topk * sizeof(cache_shard_rec));
+    L.qg = off;    off = al(off + (size_t)L.rows * dim * 2);
+    L.total = off;
+    return L;
+}
+
 // cache_query_batch_host: batches of >= kHostSplitMin queries are uploaded in kHostSplit
 // slices so the copy overlaps the scan (see cache_query_batch_host)
 constexpr int kHostSplit = 4;
@@ -164,6 +187,15 @@ struct cache_t {
     PeerPtrs peers{};
     bool peers_ok = false;
     std::vector<void*> ipc_opened;   // peer allocations opened through CUDA IPC
+    // push exchange (cache_push_*): this rank's arena and every rank's arena base
+    uint8_t* arena = nullptr;
+    int64_t arena_nb = 0;
+    int32_t arena_topk = 0;
+    uint8_t* peer_arena[kMaxWorld] = {};
+    bool push_ok = false;
+    uint32_t push_epoch = 0;
+    int64_t push_nb = -1;
+    int push_phase = 0;              // last phase run (1..3), for call-order checks
 };
 
 extern "C" {
@@ -286,6 +318,7 @@ cache_status cache_destroy(cache_t* c) {
     c->hq_out.release();
     cudaFree(c->emb); cudaFree(c->inv_e); cudaFree(c->ids); cudaFree(c->present);
     cudaFree(c->lslot); cudaFree(c->fcnt); cudaFree(c->lastacc); cudaFree(c->pool);
+    if (c->arena) cudaFree(c->arena);
     c->qbuf.release(); c->ystage.release(); c->invq.release(); c->invstage.release();
     c->qstat.release(); c->istat.release(); c->gk.release(); c->recs.release(); c->iplan.release(); c->cplan.release();
     c->hq_in.release(); c->hq_lat.release(); c->hq_ids.release(); c->hq_sc.release(); c->hq_k.release();
@@ -402,19 +435,12 @@ cache_status cache_insert(cache_t* c, int64_t n, const void* emb, int32_t emb_dt
     return n_accepted == n ? CACHE_OK : fail(CACHE_E_BAD_ROWS, "cache_insert: some rows rejected (row_status)");
 }
 
-// Query ingest + scan of this cache's entries: partial top-k record lists in c->recs
-// ([parts][b][kmax]); *parts_out = number of lists per query (0 for an empty cache).
-static cache_status scan_core(cache_t* c, int64_t b, const void* queries, int32_t q_dtype, int kmax,
-                              cudaStream_t s, int* parts_out) {
+// Scan of this cache's entries for b normalised query rows qrows (bf16, allocation padded to
+// a multiple of 128 rows; gk = the rows' k-th-best gate words, already zeroed): partial top-k
+// record lists in c->recs ([parts][b][kmax]); *parts_out = lists per query (0: empty cache).
+static cache_status scan_rows(cache_t* c, int64_t b, __nv_bfloat16* qrows, uint32_t* gk, int kmax, cudaStream_t s,
+                              int* parts_out) {
     const int64_t bpad = (b + 127) / 128 * 128;
-    CK(c->qbuf.ensure((size_t)bpad * c->dim));
-    CK(c->invq.ensure(bpad));
-    CK(c->qstat.ensure(bpad));
-    CK(c->gk.ensure(bpad));
-    CK(c->gsrc.ensure(bpad));
-    if (c->prof_on) CK(cudaEventRecord(c->prof[0], s));
-    launch_normalise(queries, q_dtype, b, c->dim, c->qbuf.p, c->invq.p, c->qstat.p, s, c->gk.p);
-    c->launches++;
     const int64_t n_slots = c->hwm;
     int parts = 0;
     bool prof1 = false;   // prof[1] is recorded right before the scoring launch (after host planning)
@@ -433,21 +459,21 @@ static cache_status scan_core(cache_t* c, int64_t b, const void* queries, int32_
             const bool pair = b > 128 && c->scorer != CACHE_SCORER_TC_SINGLE;
             tp = tc_plan(b, n_slots, c->sm_count, pair);
             parts = tp.parts;
-            if (bpad > b) CK(cudaMemsetAsync(c->qbuf.p + b * c->dim, 0, (bpad - b) * c->dim * 2, s));
+            if (bpad > b) CK(cudaMemsetAsync(qrows + b * c->dim, 0, (bpad - b) * c->dim * 2, s));
             CUtensorMap tm_q;
-            if (!encode_rows(&tm_q, c->qbuf.p, bpad, c->dim, 128))
+            if (!encode_rows(&tm_q, qrows, bpad, c->dim, 128))
                 return fail(CACHE_E_CUDA, "query: cuTensorMapEncodeTiled failed");
             CK(c->recs.ensure((size_t)parts * b * kmax));
             if (c->prof_on) { CK(cudaEventRecord(c->prof[1], s)); prof1 = true; }
             if (!launch_score_tc(kmax, tp, &tm_q, pair ? &c->tm_e128 : &c->tm_e, c->inv_e, c->ids, c->dim, b,
-                                 c->recs.p, c->gk.p, s))
+                                 c->recs.p, gk, s))
                 return fail(CACHE_E_UNSUPPORTED, "query: tensor-core scorer not built");
             c->launches++;
         } else {
             parts = stream_parts(n_slots, b);
             CK(c->recs.ensure((size_t)parts * b * kmax));
             if (c->prof_on) { CK(cudaEventRecord(c->prof[1], s)); prof1 = true; }
-            launch_score_stream(kmax, c->emb, c->inv_e, c->ids, n_slots, c->dim, c->qbuf.p, b, c->recs.p, parts, s);
+            launch_score_stream(kmax, c->emb, c->inv_e, c->ids, n_slots, c->dim, qrows, b, c->recs.p, parts, s);
             c->launches++;
         }
     }
@@ -455,6 +481,21 @@ static cache_status scan_core(cache_t* c, int64_t b, const void* queries, int32_
     if (c->prof_on) CK(cudaEventRecord(c->prof[2], s));   // end of the scan
     *parts_out = parts;
     return CACHE_OK;
+}
+
+// Query ingest + scan of this cache's entries (scan_rows on c->qbuf).
+static cache_status scan_core(cache_t* c, int64_t b, const void* queries, int32_t q_dtype, int kmax,
+                              cudaStream_t s, int* parts_out) {
+    const int64_t bpad = (b + 127) / 128 * 128;
+    CK(c->qbuf.ensure((size_t)bpad * c->dim));
+    CK(c->invq.ensure(bpad));
+    CK(c->qstat.ensure(bpad));
+    CK(c->gk.ensure(bpad));
+    CK(c->gsrc.ensure(bpad));
+    if (c->prof_on) CK(cudaEventRecord(c->prof[0], s));
+    launch_normalise(queries, q_dtype, b, c->dim, c->qbuf.p, c->invq.p, c->qstat.p, s, c->gk.p);
+    c->launches++;
+    return scan_rows(c, b, c->qbuf.p, c->gk.p, kmax, s, parts_out);
 }
 
 // tick = false: a later sub-batch of the same host batch (same LRU clock value).
@@ -526,9 +567,8 @@ cache_status cache_query_merge(cache_t* c, int64_t b, int64_t row0, int64_t nb, 
     DeviceGuard g(c->device);
     const int kmax = topk == 1 ? 1 : (topk <= 4 ? 4 : 16);
     c->clock++;   // every rank merges once per global batch -> the clocks agree across ranks
-    launch_merge_sharded(kmax, recs, c->world, b, row0, nb, topk, c->invq.p, c->qstat.p, c->peers, c->clock, c->L,
-                         c->km,
-                         out_ids, out_scores, out_k, (uint8_t*)latent_out, out_latent_ptr, row_status,
+    launch_merge_sharded(kmax, recs, b, row0, c->world, row0, nb, topk, c->invq.p, c->qstat.p, c->peers, c->clock,
+                         c->L, c->km, out_ids, out_scores, out_k, (uint8_t*)latent_out, out_latent_ptr, row_status,
                          (cudaStream_t)stream);
     c->launches++;
     CK(cudaGetLastError());
@@ -641,6 +681,13 @@ cache_status cache_export_peer(cache_t* c, cache_peer_desc* out) {
         CK(cudaIpcGetMemHandle(&h, c->pool));
         std::memcpy(out->ipc_pool, &h, 64);
     }
+    out->arena = c->arena;
+    out->arena_nb = c->arena_nb;
+    out->arena_topk = c->arena_topk;
+    if (c->arena) {
+        CK(cudaIpcGetMemHandle(&h, c->arena));
+        std::memcpy(out->ipc_arena, &h, 64);
+    }
     return CACHE_OK;
 }
 
@@ -649,16 +696,29 @@ cache_status cache_attach_peers(cache_t* c, int32_t world, const cache_peer_desc
     DeviceGuard g(c->device);
     const int32_t me = (int32_t)getpid();
     PeerPtrs p{};
+    bool push = c->arena != nullptr;
+    uint8_t* pa[kMaxWorld] = {};
     for (int r = 0; r < world; ++r) {
         const cache_peer_desc& d = descs[r];
         if (d.num_k != c->num_k || d.latent_bytes != c->L)
             return fail(CACHE_E_INVALID_ARG, "cache_attach_peers: peer configuration differs");
+        if (c->arena && (!d.arena || d.arena_nb != c->arena_nb || d.arena_topk != c->arena_topk))
+            push = false;   // some rank has no (or a differently sized) arena: no push exchange
         if (d.pid == me) {   // same process (own rank, or virtual ranks sharing one GPU)
             p.lslot[r] = (const int32_t*)d.lslot;
             p.fcnt[r] = (uint32_t*)d.fcnt;
             p.lastacc[r] = (uint32_t*)d.lastacc;
             p.pool[r] = (const uint8_t*)d.pool;
+            pa[r] = (uint8_t*)d.arena;
             continue;
+        }
+        if (d.arena && c->arena) {
+            void* ap = nullptr;
+            cudaIpcMemHandle_t ha;
+            std::memcpy(&ha, d.ipc_arena, 64);
+            CK(cudaIpcOpenMemHandle(&ap, ha, cudaIpcMemLazyEnablePeerAccess));
+            c->ipc_opened.push_back(ap);
+            pa[r] = (uint8_t*)ap;
         }
         void* ptr = nullptr;
         cudaIpcMemHandle_t h;
@@ -683,6 +743,120 @@ cache_status cache_attach_peers(cache_t* c, int32_t world, const cache_peer_desc
     }
     c->peers = p;
     c->peers_ok = true;
+    c->push_ok = push;
+    for (int r = 0; r < kMaxWorld; ++r) c->peer_arena[r] = r < world ? pa[r] : nullptr;
+    return CACHE_OK;
+}
+
+cache_status cache_push_reserve(cache_t* c, int64_t max_nb, int32_t max_topk) {
+    if (!c || max_nb < 1 || max_topk < 1 || max_topk > c->cfg.max_topk || (int64_t)c->world * max_nb > 0x7FFFFFFF)
+        return fail(CACHE_E_INVALID_ARG, "cache_push_reserve: bad argument");
+    if (c->world > kMaxWorld) return fail(CACHE_E_INVALID_ARG, "cache_push_reserve: world too large");
+    if (c->peers_ok) return fail(CACHE_E_STATE, "cache_push_reserve: call before cache_export_peer / attach");
+    DeviceGuard g(c->device);
+    if (c->arena) {
+        cudaFree(c->arena);
+        c->arena = nullptr;
+    }
+    const ArenaLayout L = arena_layout(c->world, max_nb, max_topk, c->dim);
+    CK(cudaMalloc(&c->arena, L.total));
+    CK(cudaMemset(c->arena, 0, L.total));
+    CK(cudaDeviceSynchronize());
+    c->arena_nb = max_nb;
+    c->arena_topk = max_topk;
+    c->push_epoch = 0;
+    c->push_phase = 0;
+    return CACHE_OK;
+}
+
+static PushSignal push_signal_of(cache_t* c, size_t flag_off, int counter) {
+    PushSignal sg{};
+    for (int r = 0; r < c->world; ++r) sg.flag[r] = (uint32_t*)(c->peer_arena[r] + flag_off) + c->rank;
+    sg.world = c->world;
+    sg.done = (uint32_t*)(c->arena + arena_layout(c->world, c->arena_nb, c->arena_topk, c->dim).done) + counter;
+    sg.epoch = c->push_epoch;
+    return sg;
+}
+
+cache_status cache_push_queries(cache_t* c, int64_t nb, const void* queries, int32_t q_dtype, void* stream) {
+    if (!c) return fail(CACHE_E_INVALID_ARG, "cache_push_queries: null cache");
+    if (!c->push_ok) return fail(CACHE_E_STATE, "cache_push_queries: no push arenas (cache_push_reserve on every rank, then export / attach)");
+    if (nb < 0 || nb > c->arena_nb || (nb > 0 && !queries) || (q_dtype != CACHE_DTYPE_F32 && q_dtype != CACHE_DTYPE_BF16))
+        return fail(CACHE_E_INVALID_ARG, "cache_push_queries: bad nb / queries / dtype");
+    if (c->push_phase != 0 && c->push_phase != 3) return fail(CACHE_E_STATE, "cache_push_queries: previous batch not merged");
+    DeviceGuard g(c->device);
+    const ArenaLayout L = arena_layout(c->world, c->arena_nb, c->arena_topk, c->dim);
+    c->push_epoch++;
+    c->push_nb = nb;
+    PushRows o{};
+    for (int r = 0; r < c->world; ++r) {
+        o.y[r] = (__nv_bfloat16*)(c->peer_arena[r] + L.qg);
+        o.inv[r] = (float*)(c->peer_arena[r] + L.invq);
+        o.status[r] = (int32_t*)(c->peer_arena[r] + L.qstat);
+    }
+    o.n = c->world;
+    launch_normalise_push(queries, q_dtype, nb, c->dim, o, (int64_t)c->rank * nb, push_signal_of(c, L.qflag, 0),
+                          (cudaStream_t)stream);
+    c->launches++;
+    c->push_phase = 1;
+    CK(cudaGetLastError());
+    return CACHE_OK;
+}
+
+cache_status cache_push_scan(cache_t* c, int64_t nb, int32_t topk, void* stream) {
+    if (!c) return fail(CACHE_E_INVALID_ARG, "cache_push_scan: null cache");
+    if (c->push_phase != 1 || nb != c->push_nb) return fail(CACHE_E_STATE, "cache_push_scan: call after cache_push_queries with the same nb");
+    if (topk < 1 || topk > c->arena_topk) return fail(CACHE_E_INVALID_ARG, "cache_push_scan: bad topk");
+    DeviceGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const ArenaLayout L = arena_layout(c->world, c->arena_nb, c->arena_topk, c->dim);
+    const int64_t bg = (int64_t)c->world * nb;
+    const int kmax = topk == 1 ? 1 : (topk <= 4 ? 4 : 16);
+    launch_wait_flags((const uint32_t*)(c->arena + L.qflag), c->world, c->push_epoch, s);
+    c->launches++;
+    int parts = 0;
+    if (bg > 0) {
+        CK(c->gk.ensure((bg + 127) / 128 * 128));
+        CK(cudaMemsetAsync(c->gk.p, 0, bg * 4, s));
+        cache_status r = scan_rows(c, bg, (__nv_bfloat16*)(c->arena + L.qg), c->gk.p, kmax, s, &parts);
+        if (r != CACHE_OK) return r;
+    }
+    PushRecs d{};
+    for (int r = 0; r < c->world; ++r) d.inbox[r] = (cache_shard_rec*)(c->peer_arena[r] + L.inbox);
+    d.nb = std::max<int64_t>(1, nb);
+    d.me = c->rank;
+    launch_local_merge_push(kmax, c->recs.p, parts, bg, topk, (const int32_t*)(c->arena + L.qstat), c->present,
+                            c->rank, d, push_signal_of(c, L.rflag, 1), s);
+    c->launches++;
+    c->push_phase = 2;
+    CK(cudaGetLastError());
+    return CACHE_OK;
+}
+
+cache_status cache_push_merge(cache_t* c, int64_t nb, int32_t topk, uint64_t* out_ids, float* out_scores,
+                              int32_t* out_k, void* latent_out, void** out_latent_ptr, int32_t* row_status,
+                              void* stream) {
+    if (!c) return fail(CACHE_E_INVALID_ARG, "cache_push_merge: null cache");
+    if (c->push_phase != 2 || nb != c->push_nb) return fail(CACHE_E_STATE, "cache_push_merge: call after cache_push_scan with the same nb");
+    if (topk < 1 || topk > c->arena_topk) return fail(CACHE_E_INVALID_ARG, "cache_push_merge: bad topk");
+    if (nb > 0 && (!out_ids || !out_scores || !out_k)) return fail(CACHE_E_INVALID_ARG, "cache_push_merge: null buffer");
+    DeviceGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const ArenaLayout L = arena_layout(c->world, c->arena_nb, c->arena_topk, c->dim);
+    const int kmax = topk == 1 ? 1 : (topk <= 4 ? 4 : 16);
+    launch_wait_flags((const uint32_t*)(c->arena + L.rflag), c->world, c->push_epoch, s);
+    c->launches++;
+    c->clock++;   // once per global batch on every rank, as cache_query_merge
+    if (nb > 0) {
+        launch_merge_sharded(kmax, (const cache_shard_rec*)(c->arena + L.inbox), nb, 0, c->world,
+                             (int64_t)c->rank * nb, nb, topk, (const float*)(c->arena + L.invq),
+                             (const int32_t*)(c->arena + L.qstat), c->peers, c->clock, c->L, c->km, out_ids,
+                             out_scores, out_k, (uint8_t*)latent_out, out_latent_ptr, row_status, s);
+        c->launches++;
+    }
+    c->queries += nb;
+    c->push_phase = 3;
+    CK(cudaGetLastError());
     return CACHE_OK;
 }
 

@@ -50,17 +50,35 @@ __device__ __forceinline__ float load_in<__nv_bfloat16>(const __nv_bfloat16* p) 
     return __bfloat162float(*p);
 }
 
-template <typename Tin, int NS>
-__global__ void __launch_bounds__(256) k_normalise(const Tin* __restrict__ x, int64_t n,
-                                                   __nv_bfloat16* __restrict__ y, float* __restrict__ inv,
-                                                   int32_t* __restrict__ status, uint32_t* __restrict__ gk) {
+// Stores of one normalised row: ND = 1 (k_normalise) or up to kMaxWorld destinations
+// (k_normalise_push: the same row into every rank's arena over NVLink).
+template <int ND>
+struct RowDst {
+    __nv_bfloat16* y[ND];
+    float* inv[ND];
+    int32_t* status[ND];
+    int n;
+};
+
+template <int ND>
+__device__ __forceinline__ void put_bf16(const RowDst<ND>& o, int64_t idx, __nv_bfloat16 v) {
+    if constexpr (ND == 1) o.y[0][idx] = v;
+    else
+        for (int d = 0; d < o.n; ++d) o.y[d][idx] = v;
+}
+template <int ND>
+__device__ __forceinline__ void put_meta(const RowDst<ND>& o, int64_t row, float inv, int32_t st) {
+    if constexpr (ND == 1) { o.inv[0][row] = inv; o.status[0][row] = st; }
+    else
+        for (int d = 0; d < o.n; ++d) { o.inv[d][row] = inv; o.status[d][row] = st; }
+}
+
+// One warp normalises input row xr into output row `orow` of every destination.
+template <typename Tin, int NS, int ND>
+__device__ __forceinline__ void normalise_row(const Tin* __restrict__ xr, int lane, const RowDst<ND>& o,
+                                              int64_t orow) {
     constexpr int dim = NS * 32;
-    const int lane = threadIdx.x & 31;
-    const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-    if (r >= n) return;   // warp-uniform
-    if (gk != nullptr && lane == 0) gk[r] = 0u;
-    const Tin* xr = x + r * (int64_t)dim;
-    __nv_bfloat16* yr = y + r * (int64_t)dim;
+    const int64_t ybase = orow * (int64_t)dim;
     float xf[NS];
     double v[NS];
     int bad = 0;
@@ -80,8 +98,8 @@ __global__ void __launch_bounds__(256) k_normalise(const Tin* __restrict__ x, in
         st = s == 0.0 ? CACHE_ROW_ZERO_NORM : (!isfinite(s) ? CACHE_ROW_NONFINITE : CACHE_ROW_OK);
     }
     if (st != CACHE_ROW_OK) {
-        for (int i = lane; i < dim; i += 32) yr[i] = __float2bfloat16_rn(0.0f);
-        if (lane == 0) { inv[r] = __int_as_float(0x7FC00000); status[r] = st; }
+        for (int i = lane; i < dim; i += 32) put_bf16(o, ybase + i, __float2bfloat16_rn(0.0f));
+        if (lane == 0) put_meta(o, orow, __int_as_float(0x7FC00000), st);
         return;
     }
     const double nu = __dsqrt_rn(s);
@@ -99,20 +117,100 @@ __global__ void __launch_bounds__(256) k_normalise(const Tin* __restrict__ x, in
         const long long dm = low - (1ll << 44);
         if ((dm <= 16 && dm >= -16) || fabs(y) < 0x1p-120) y = __ddiv_rn(x, nu);
         const __nv_bfloat16 b = __double2bfloat16(y);   // cvt.rn.bf16.f64
-        yr[lane + 32 * k] = b;
+        put_bf16(o, ybase + lane + 32 * k, b);
         const double yd = (double)__bfloat162float(b);
         v[k] = __dmul_rn(yd, yd);
     }
     const double s2 = warp_tree_sum<NS>(v);
     if (lane == 0) {
-        if (s2 == 0.0) {
-            inv[r] = __int_as_float(0x7FC00000);
-            status[r] = CACHE_ROW_ZERO_NORM;
-        } else {
-            inv[r] = __double2float_rn(__ddiv_rn(1.0, __dsqrt_rn(s2)));
-            status[r] = CACHE_ROW_OK;
+        if (s2 == 0.0) put_meta(o, orow, __int_as_float(0x7FC00000), CACHE_ROW_ZERO_NORM);
+        else put_meta(o, orow, __double2float_rn(__ddiv_rn(1.0, __dsqrt_rn(s2))), CACHE_ROW_OK);
+    }
+}
+
+template <typename Tin, int NS>
+__global__ void __launch_bounds__(256) k_normalise(const Tin* __restrict__ x, int64_t n,
+                                                   __nv_bfloat16* __restrict__ y, float* __restrict__ inv,
+                                                   int32_t* __restrict__ status, uint32_t* __restrict__ gk) {
+    const int lane = threadIdx.x & 31;
+    const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (r >= n) return;   // warp-uniform
+    if (gk != nullptr && lane == 0) gk[r] = 0u;
+    RowDst<1> o;
+    o.y[0] = y;
+    o.inv[0] = inv;
+    o.status[0] = status;
+    o.n = 1;
+    normalise_row<Tin, NS, 1>(x + r * (int64_t)(NS * 32), lane, o, r);
+}
+
+// Publish: every thread fences its stores at system scope, the CTA counts itself done, and
+// the last CTA of the grid stores the epoch into every consumer's flag word (release.sys).
+// A fence + relaxed RMW chain + fence orders every CTA's data before the flag.
+__device__ __forceinline__ void push_signal(const PushSignal& sg) {
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned prev = atomicAdd(sg.done, 1u);
+        if (prev == gridDim.x - 1) {
+            atomicExch(sg.done, 0u);   // ready for the next launch (stream-ordered)
+            __threadfence_system();
+            for (int d = 0; d < sg.world; ++d)
+                asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(sg.flag[d]), "r"(sg.epoch) : "memory");
         }
     }
+}
+
+// Query ingest fused with the all-gather: rank r normalises its own n rows and stores them
+// (bf16 row, inv-norm, status) into global rows [row0, row0 + n) of EVERY rank's arena.
+template <typename Tin, int NS>
+__global__ void __launch_bounds__(256) k_normalise_push(const Tin* __restrict__ x, int64_t n, PushRows out,
+                                                        int64_t row0, PushSignal sig) {
+    const int lane = threadIdx.x & 31;
+    const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (r < n) {
+        RowDst<kMaxWorld> o;
+        for (int d = 0; d < kMaxWorld; ++d) { o.y[d] = out.y[d]; o.inv[d] = out.inv[d]; o.status[d] = out.status[d]; }
+        o.n = out.n;
+        normalise_row<Tin, NS, kMaxWorld>(x + r * (int64_t)(NS * 32), lane, o, row0 + r);
+    }
+    push_signal(sig);
+}
+
+__global__ void k_wait_flags(const uint32_t* __restrict__ flags, int world, uint32_t epoch) {
+    const int t = threadIdx.x;
+    if (t >= world) return;
+    unsigned long long spins = 0;
+    for (;;) {
+        uint32_t v;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + t) : "memory");
+        if ((int32_t)(v - epoch) >= 0) break;
+        __nanosleep(256);
+        if (++spins > (1ull << 26)) __trap();   // a peer never published (> ~17 s): fail, don't hang
+    }
+}
+
+void launch_wait_flags(const uint32_t* flags, int world, uint32_t epoch, cudaStream_t s) {
+    k_wait_flags<<<1, 32, 0, s>>>(flags, world, epoch);
+}
+
+void launch_normalise_push(const void* x, int dtype, int64_t n, int dim, const PushRows& out, int64_t row0,
+                           const PushSignal& sig, cudaStream_t s) {
+    const unsigned grid = (unsigned)std::max<int64_t>(1, (n + 7) / 8);   // >= 1 CTA: always publish
+#define NV_NORMP_NS(NSV)                                                                              \
+    case NSV:                                                                                         \
+        if (dtype == CACHE_DTYPE_BF16)                                                                \
+            k_normalise_push<__nv_bfloat16, NSV><<<grid, 256, 0, s>>>((const __nv_bfloat16*)x, n, out, row0, sig); \
+        else                                                                                          \
+            k_normalise_push<float, NSV><<<grid, 256, 0, s>>>((const float*)x, n, out, row0, sig);   \
+        break;
+    switch (dim / 32) {
+        NV_NORMP_NS(2) NV_NORMP_NS(4) NV_NORMP_NS(6) NV_NORMP_NS(8) NV_NORMP_NS(10) NV_NORMP_NS(12)
+        NV_NORMP_NS(14) NV_NORMP_NS(16) NV_NORMP_NS(18) NV_NORMP_NS(20) NV_NORMP_NS(22) NV_NORMP_NS(24)
+        NV_NORMP_NS(26) NV_NORMP_NS(28) NV_NORMP_NS(30) NV_NORMP_NS(32)
+        default: break;
+    }
+#undef NV_NORMP_NS
 }
 
 void launch_normalise(const void* x, int dtype, int64_t n, int dim, __nv_bfloat16* y, float* inv,
@@ -615,56 +713,77 @@ void launch_evict_pick(unsigned int* hist, EvictState* st, int pass, cudaStream_
 // or local pointers for the own rank) and counts the access with an atomic on the owner's
 // counter -- the fetch is fused into the merge kernel, no second collective.
 // ---------------------------------------------------------------------------------------
-template <int KMAX>
+// kPush = false: records -> out[b][topk] (all-gathered by the caller).  kPush = true: the
+// records of global row b go straight into its owner's inbox (rank b / nb, row b % nb, sender
+// slot `owner`) over NVLink, then the grid publishes the epoch (record push fused with the
+// local merge: no collective).
+template <int KMAX, bool kPush>
 __global__ void __launch_bounds__(256)
 k_local_merge(const Rec* __restrict__ ws, int parts, int64_t B, int topk, const int32_t* __restrict__ qstatus,
-              const uint32_t* __restrict__ present, int owner, cache_shard_rec* __restrict__ out) {
+              const uint32_t* __restrict__ present, int owner, cache_shard_rec* __restrict__ out, PushRecs dst,
+              PushSignal sig) {
     const int lane = threadIdx.x & 31;
     const int64_t b = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-    if (b >= B) return;
-    TopK<KMAX> tk;
-    tk.init();
-    if (qstatus[b] == CACHE_ROW_OK) {
-        for (int p = lane; p < parts; p += 32) {
-            const Rec* r = ws + ((int64_t)p * B + b) * KMAX;
-            for (int i = 0; i < topk; ++i) {
-                const Rec rr = r[i];
-                if (rr.key == 0ull) break;
-                tk.offer_key(rr.key, rr.slot);
+    if (b < B) {
+        cache_shard_rec* o_row = kPush ? dst.inbox[b / dst.nb] + ((int64_t)dst.me * dst.nb + b % dst.nb) * topk
+                                       : out + b * topk;
+        TopK<KMAX> tk;
+        tk.init();
+        if (qstatus[b] == CACHE_ROW_OK) {
+            for (int p = lane; p < parts; p += 32) {
+                const Rec* r = ws + ((int64_t)p * B + b) * KMAX;
+                for (int i = 0; i < topk; ++i) {
+                    const Rec rr = r[i];
+                    if (rr.key == 0ull) break;
+                    tk.offer_key(rr.key, rr.slot);
+                }
+            }
+        }
+        for (int i = 0; i < topk; ++i) {
+            const unsigned long long m = warp_max_u64(tk.k[0]);
+            if (m != 0ull && tk.k[0] == m) {
+                cache_shard_rec o;
+                o.key = m;
+                o.slot = tk.s[0];
+                o.present_mask = (uint8_t)(present[tk.s[0]] & 0xFFu);
+                o.owner = (uint8_t)owner;
+                o.reserved = 0;
+                o_row[i] = o;
+                tk.pop();
+            }
+            if (m == 0ull && lane == 0) {
+                cache_shard_rec o{};
+                o_row[i] = o;
             }
         }
     }
-    for (int i = 0; i < topk; ++i) {
-        const unsigned long long m = warp_max_u64(tk.k[0]);
-        if (m != 0ull && tk.k[0] == m) {
-            cache_shard_rec o;
-            o.key = m;
-            o.slot = tk.s[0];
-            o.present_mask = (uint8_t)(present[tk.s[0]] & 0xFFu);
-            o.owner = (uint8_t)owner;
-            o.reserved = 0;
-            out[b * topk + i] = o;
-            tk.pop();
-        }
-        if (m == 0ull && lane == 0) {
-            cache_shard_rec o{};
-            out[b * topk + i] = o;
-        }
-    }
+    if (kPush) push_signal(sig);
 }
 
 void launch_local_merge(int kmax, const Rec* ws, int parts, int64_t B, int topk, const int32_t* qstatus,
                         const uint32_t* present, int owner, cache_shard_rec* out, cudaStream_t s) {
     if (B <= 0) return;
     const unsigned grid = (unsigned)((B + 7) / 8);
-    if (kmax == 1) k_local_merge<1><<<grid, 256, 0, s>>>(ws, parts, B, topk, qstatus, present, owner, out);
-    else if (kmax == 4) k_local_merge<4><<<grid, 256, 0, s>>>(ws, parts, B, topk, qstatus, present, owner, out);
-    else k_local_merge<16><<<grid, 256, 0, s>>>(ws, parts, B, topk, qstatus, present, owner, out);
+    const PushRecs d{};
+    const PushSignal g{};
+    if (kmax == 1) k_local_merge<1, false><<<grid, 256, 0, s>>>(ws, parts, B, topk, qstatus, present, owner, out, d, g);
+    else if (kmax == 4) k_local_merge<4, false><<<grid, 256, 0, s>>>(ws, parts, B, topk, qstatus, present, owner, out, d, g);
+    else k_local_merge<16, false><<<grid, 256, 0, s>>>(ws, parts, B, topk, qstatus, present, owner, out, d, g);
+}
+
+void launch_local_merge_push(int kmax, const Rec* ws, int parts, int64_t B, int topk, const int32_t* qstatus,
+                             const uint32_t* present, int owner, const PushRecs& dst, const PushSignal& sig,
+                             cudaStream_t s) {
+    const unsigned grid = (unsigned)std::max<int64_t>(1, (B + 7) / 8);   // >= 1 CTA: always publish
+    if (kmax == 1) k_local_merge<1, true><<<grid, 256, 0, s>>>(ws, parts, B, topk, qstatus, present, owner, nullptr, dst, sig);
+    else if (kmax == 4) k_local_merge<4, true><<<grid, 256, 0, s>>>(ws, parts, B, topk, qstatus, present, owner, nullptr, dst, sig);
+    else k_local_merge<16, true><<<grid, 256, 0, s>>>(ws, parts, B, topk, qstatus, present, owner, nullptr, dst, sig);
 }
 
 template <int KMAX>
 __global__ void __launch_bounds__(128)
-k_merge_sharded(const cache_shard_rec* __restrict__ recs, int world, int64_t B, int64_t row0, int topk,
+k_merge_sharded(const cache_shard_rec* __restrict__ recs, int64_t rec_stride, int64_t rec_row0, int world,
+                int64_t row0, int topk,
                 const float* __restrict__ inv_q, const int32_t* __restrict__ qstatus, PeerPtrs peers,
                 uint32_t clock, int64_t latent_bytes, KMap km, uint64_t* __restrict__ out_ids,
                 float* __restrict__ out_scores,
@@ -687,7 +806,7 @@ k_merge_sharded(const cache_shard_rec* __restrict__ recs, int world, int64_t B, 
         if (st == CACHE_ROW_OK) {
             for (int idx = lane; idx < world * topk; idx += 32) {
                 const int r = idx / topk, t = idx - r * topk;
-                const cache_shard_rec rec = recs[((int64_t)r * B + g) * topk + t];
+                const cache_shard_rec rec = recs[((int64_t)r * rec_stride + rec_row0 + i) * topk + t];
                 if (rec.key == 0ull || rec.key <= ck[KMAX - 1]) continue;
                 const uint32_t meta = ((uint32_t)rec.owner << 8) | rec.present_mask;
 #pragma unroll
@@ -765,16 +884,16 @@ k_merge_sharded(const cache_shard_rec* __restrict__ recs, int world, int64_t B, 
     }
 }
 
-void launch_merge_sharded(int kmax, const cache_shard_rec* recs, int world, int64_t B, int64_t row0, int64_t nb,
-                          int topk, const float* inv_q, const int32_t* qstatus, const PeerPtrs& peers,
-                          uint32_t clock, int64_t latent_bytes, const KMap& km, uint64_t* out_ids,
-                          float* out_scores, int32_t* out_k, uint8_t* latent_out, void** out_ptr,
+void launch_merge_sharded(int kmax, const cache_shard_rec* recs, int64_t rec_stride, int64_t rec_row0, int world,
+                          int64_t row0, int64_t nb, int topk, const float* inv_q, const int32_t* qstatus,
+                          const PeerPtrs& peers, uint32_t clock, int64_t latent_bytes, const KMap& km,
+                          uint64_t* out_ids, float* out_scores, int32_t* out_k, uint8_t* latent_out, void** out_ptr,
                           int32_t* out_status, cudaStream_t s) {
     if (nb <= 0) return;
-#define NV_MS(KM)                                                                                          \
-    k_merge_sharded<KM><<<(unsigned)nb, 128, 0, s>>>(recs, world, B, row0, topk, inv_q, qstatus, peers,     \
-                                                     clock, latent_bytes, km, out_ids, out_scores, out_k,   \
-                                                     latent_out, out_ptr, out_status)
+#define NV_MS(KM)                                                                                              \
+    k_merge_sharded<KM><<<(unsigned)nb, 128, 0, s>>>(recs, rec_stride, rec_row0, world, row0, topk, inv_q,     \
+                                                     qstatus, peers, clock, latent_bytes, km, out_ids,         \
+                                                     out_scores, out_k, latent_out, out_ptr, out_status)
     if (kmax == 1) NV_MS(1);
     else if (kmax == 4) NV_MS(4);
     else NV_MS(16);

@@ -99,10 +99,38 @@ struct PeerPtrs {                       // per-rank device pointers (own rank in
 };
 void launch_local_merge(int kmax, const Rec* ws, int parts, int64_t B, int topk, const int32_t* qstatus,
                         const uint32_t* present, int owner, cache_shard_rec* out, cudaStream_t s);
-void launch_merge_sharded(int kmax, const cache_shard_rec* recs, int world, int64_t B, int64_t row0, int64_t nb,
-                          int topk, const float* inv_q, const int32_t* qstatus, const PeerPtrs& peers,
-                          uint32_t clock, int64_t latent_bytes, const KMap& km, uint64_t* out_ids,
-                          float* out_scores, int32_t* out_k, uint8_t* latent_out, void** out_ptr,
+// recs[r][rec_row0 + i][topk] with row stride rec_stride (all-gathered lists: stride = B,
+// rec_row0 = row0; the push inbox: stride = nb, rec_row0 = 0); inv_q / qstatus by global row
+void launch_merge_sharded(int kmax, const cache_shard_rec* recs, int64_t rec_stride, int64_t rec_row0, int world,
+                          int64_t row0, int64_t nb, int topk, const float* inv_q, const int32_t* qstatus,
+                          const PeerPtrs& peers, uint32_t clock, int64_t latent_bytes, const KMap& km,
+                          uint64_t* out_ids, float* out_scores, int32_t* out_k, uint8_t* latent_out, void** out_ptr,
                           int32_t* out_status, cudaStream_t s);
+
+// ---- push exchange over peer memory (cache_push_*): producer kernels store their results
+// straight into the consumers' arenas and the last CTA to finish publishes an epoch flag ----
+struct PushSignal {
+    uint32_t* flag[kMaxWorld];   // this sender's flag word in every rank's arena
+    int world;
+    uint32_t* done;              // local CTA-completion counter (zero between launches)
+    uint32_t epoch;
+};
+struct PushRows {                // destinations of the pushed query rows, one per rank
+    __nv_bfloat16* y[kMaxWorld];
+    float* inv[kMaxWorld];
+    int32_t* status[kMaxWorld];
+    int n;
+};
+struct PushRecs {                // record inbox of every rank: [sender][nb][topk]
+    cache_shard_rec* inbox[kMaxWorld];
+    int64_t nb;                  // rows owned per rank: global row q belongs to rank q / nb
+    int me;
+};
+void launch_normalise_push(const void* x, int dtype, int64_t n, int dim, const PushRows& out, int64_t row0,
+                           const PushSignal& sig, cudaStream_t s);
+void launch_local_merge_push(int kmax, const Rec* ws, int parts, int64_t B, int topk, const int32_t* qstatus,
+                             const uint32_t* present, int owner, const PushRecs& dst, const PushSignal& sig,
+                             cudaStream_t s);
+void launch_wait_flags(const uint32_t* flags, int world, uint32_t epoch, cudaStream_t s);
 
 }  // namespace nv

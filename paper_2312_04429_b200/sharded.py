@@ -91,10 +91,16 @@ def _desc_from_bytes(b: bytes) -> B.PeerDesc:
 class ShardedCache:
     """One rank's handle of an entry-sharded cache (one process per GPU)."""
 
-    def __init__(self, comm: TorchComm, entry_capacity: int, latent_capacity: int | None = None, **kw):
+    def __init__(self, comm: TorchComm, entry_capacity: int, latent_capacity: int | None = None,
+                 push_max_nb: int = 0, push_max_topk: int = 1, **kw):
+        """push_max_nb > 0: reserve the exchange arena for the fused push path (query_into
+        then moves no data through the collective library); 0: all-gather path."""
         self.comm = comm
         self.cache = B.NirvanaCache(entry_capacity=entry_capacity, latent_capacity=latent_capacity,
                                     shard_rank=comm.rank, shard_world=comm.world, **kw)
+        self.push = push_max_nb > 0
+        if self.push:
+            self.cache.push_reserve(push_max_nb, push_max_topk)
         descs = comm.all_gather_object(_desc_bytes(self.cache.export_peer()))
         self.cache.attach_peers([_desc_from_bytes(d) for d in descs])
         self.latent_bytes = self.cache.latent_bytes
@@ -122,6 +128,12 @@ class ShardedCache:
 
     def query_into(self, q_local: torch.Tensor, out: dict, topk: int = 1, stream=None):
         """Collective: every rank passes its own b_local queries (same b_local everywhere)."""
+        if self.push:   # the three fused phases; the only cross-rank traffic is P2P stores
+            nb = q_local.shape[0]
+            self.cache.push_queries(q_local, stream)
+            self.cache.push_scan(nb, topk, stream)
+            return self.cache.push_merge(nb, topk, out, stream)
+
         def local_fn(qg):
             recs = torch.empty((qg.shape[0] * topk * B.SHARD_REC_BYTES,), dtype=torch.uint8, device=qg.device)
             return self.cache.query_local(qg, topk, recs, stream)
@@ -152,10 +164,15 @@ class VirtualShards:
     and the same merge/P2P code path as ShardedCache, with collectives replaced by copies.
     Used to test sharding invariance on a single B200."""
 
-    def __init__(self, world: int, entry_capacity: int, latent_capacity: int | None = None, **kw):
+    def __init__(self, world: int, entry_capacity: int, latent_capacity: int | None = None,
+                 push_max_nb: int = 0, push_max_topk: int = 1, **kw):
         self.world = world
         self.caches = [B.NirvanaCache(entry_capacity=entry_capacity, latent_capacity=latent_capacity,
                                       shard_rank=r, shard_world=world, **kw) for r in range(world)]
+        self.push = push_max_nb > 0
+        if self.push:
+            for c in self.caches:
+                c.push_reserve(push_max_nb, push_max_topk)
         descs = [c.export_peer() for c in self.caches]
         for c in self.caches:
             c.attach_peers(descs)
@@ -170,6 +187,13 @@ class VirtualShards:
         b = q_global.shape[0]
         assert b % self.world == 0
         bl = b // self.world
+        if self.push:   # one stream: every rank's phase 1, then phase 2, then phase 3
+            for r, c in enumerate(self.caches):
+                c.push_queries(q_global[r * bl:(r + 1) * bl])
+            for c in self.caches:
+                c.push_scan(bl, topk)
+            outs = [c.push_merge(bl, topk, c.alloc_outputs(bl, topk, latents)) for c in self.caches]
+            return {k: (torch.cat([o[k] for o in outs]) if outs[0][k] is not None else None) for k in outs[0]}
         recs = []
         for c in self.caches:
             r = torch.empty((b * topk * B.SHARD_REC_BYTES,), dtype=torch.uint8, device=q_global.device)
