@@ -36,11 +36,11 @@ def _make(B, oracle_mod, n, dim=768, L=L_SMALL, seed=1, present=None, cap=None, 
     return g, o, emb, cl, lat
 
 
-SCORERS = ["stream", "tc"]
+SCORERS = ["stream", "tc", "tc1"]   # CUDA-core scan; tcgen05 (CTA pairs above 128 queries); single-CTA tcgen05
 
 
 def _set(g, B, scorer):
-    g.set_scorer(B.SCORER_STREAM if scorer == "stream" else B.SCORER_TC)
+    g.set_scorer({"stream": B.SCORER_STREAM, "tc": B.SCORER_TC, "tc1": B.SCORER_TC_SINGLE}[scorer])
 
 
 def test_stored_rows_bit_identical(B, oracle_mod):
@@ -104,6 +104,21 @@ def test_ragged_sizes(B, oracle_mod, scorer, n, b):
     _set(g, B, scorer)
     q, _, _ = synth.queries(emb, cl, b, seed=b)
     out = gpu_to_numpy(g.query(torch.from_numpy(q).cuda(), topk=min(4, 16)))
+    check_batch(out, o, q, 4, expected_latent=lambda e, k: lat[e, synth.K_VALUES.index(k)])
+
+
+@pytest.mark.parametrize("scorer", SCORERS)
+@pytest.mark.parametrize("dim", [64, 128, 512, 1024])
+def test_other_dims(B, oracle_mod, scorer, dim):
+    """The whole path at other embedding widths (multiples of 64 up to the 1,024 maximum):
+    stored rows bit-identical, ids / K / bytes within the contract, several tiles + a tail."""
+    n, b = 700, 300
+    g, o, emb, cl, lat = _make(B, oracle_mod, n, dim=dim, seed=dim)
+    _set(g, B, scorer)
+    for i in (0, 123, n - 1):
+        assert np.array_equal(g.row_bf16(i), _bf16_bits(o.row(i)))
+    q, _, _ = synth.queries(emb, cl, b, seed=dim + 1)
+    out = gpu_to_numpy(g.query(torch.from_numpy(q).cuda(), topk=4))
     check_batch(out, o, q, 4, expected_latent=lambda e, k: lat[e, synth.K_VALUES.index(k)])
 
 
