@@ -23,6 +23,10 @@ cache_status cache_debug_tc_scores(cache_t *c, int64_t b, const void *queries, i
 /* Slot of entry `id` (host-synchronous), -1 if not live. */
 int64_t cache_debug_slot_of(cache_t *c, uint64_t id);
 
+/* The eviction path's GPU sort on its own: sorts n u64 keys (device pointer) ascending in
+ * place (LSD radix, 8 x 8-bit stable passes).  Synchronises `stream`. */
+cache_status cache_debug_sort_u64(uint64_t *keys, int64_t n, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -447,5 +447,15 @@ def debug_tc_scores(cache: NirvanaCache, q: torch.Tensor, stream=None) -> torch.
     return out
 
 
+_lib.cache_debug_sort_u64.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+_lib.cache_debug_sort_u64.restype = ctypes.c_int
+
+
+def debug_sort_u64(keys: torch.Tensor, stream=None) -> torch.Tensor:
+    """Sort a cuda int64 tensor (as u64 bit patterns) in place with the eviction path's sort."""
+    _check(_lib.cache_debug_sort_u64(_ptr(keys), keys.numel(), _stream(stream)))
+    return keys
+
+
 def debug_slot_of(cache: NirvanaCache, id_: int) -> int:
     return _lib.cache_debug_slot_of(cache._h, int(id_))

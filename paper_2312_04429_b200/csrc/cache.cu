@@ -144,7 +144,6 @@ struct cache_t {
     std::vector<uint32_t> h_present, h_ids;
     std::vector<int32_t> h_lslot;
     std::vector<int64_t> free_e, free_l;   // sorted descending: back() = lowest free slot
-    std::unordered_map<uint64_t, int64_t> id2slot;
     int64_t hwm = 0, live_entries = 0, live_items = 0, queries = 0;
     uint64_t next_id = 0;
     uint32_t clock = 0;             // query batches so far (the LRU logical clock)
@@ -162,6 +161,27 @@ struct cache_t {
     DevBuf<InsertPlan> iplan;
     DevBuf<CopyPlan> cplan;
     DevBuf<uint8_t> hq_in, hq_lat, hq_out;
+    // pinned host staging of an eviction's lists (keys, sorted keys, pool slots, entry slots,
+    // dirty slots): reused across calls, so no pageable copies or fresh-page faults
+    struct PinnedBuf {
+        void* p = nullptr;
+        size_t n = 0;
+        cudaError_t ensure(size_t bytes) {
+            if (bytes <= n) return cudaSuccess;
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            n = 0;
+            cudaError_t e = cudaHostAlloc(&p, std::max<size_t>(bytes, 64), cudaHostAllocDefault);
+            if (e == cudaSuccess) n = bytes;
+            return e;
+        }
+        void release() {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            n = 0;
+        }
+    } hev_keys, hev_sorted, hev_pool, hev_es, hev_ds, hev_did;
+    std::vector<int64_t> free_tmp;   // merge buffer of the free lists
     void* h_out = nullptr;   // pinned staging of the packed host-call results
     size_t h_out_n = 0;
     // host-call pipeline: query H2D copies on their own stream, one event per sub-batch
@@ -172,9 +192,11 @@ struct cache_t {
     DevBuf<int32_t> hq_k, hq_st;
     DevBuf<EvictState> est;
     DevBuf<unsigned int> ehist;
-    DevBuf<unsigned long long> ekey, ecnt;
-    DevBuf<int32_t> elslot;
-    DevBuf<int64_t> edirty;
+    DevBuf<unsigned long long> ekey, ekey2, ecnt;
+    DevBuf<int64_t> eslot;         // entry slot of each evicted item
+    DevBuf<uint32_t> escr;         // radix-sort scratch
+    DevBuf<unsigned long long> epool;    // pool slot of each evicted item (sorted for the free list)
+    DevBuf<unsigned long long> edirty, edid;   // dirty entries: slots, ids (each sorted on the GPU)
     // match predictor (NEXT-3)
     DevBuf<float> pw, prho, pgpart;
     DevBuf<uint32_t> pkeys;
@@ -323,7 +345,10 @@ cache_status cache_destroy(cache_t* c) {
     c->qstat.release(); c->istat.release(); c->gk.release(); c->recs.release(); c->iplan.release(); c->cplan.release();
     c->hq_in.release(); c->hq_lat.release(); c->hq_ids.release(); c->hq_sc.release(); c->hq_k.release();
     c->hq_st.release(); c->est.release(); c->ehist.release(); c->ekey.release(); c->ecnt.release();
-    c->elslot.release(); c->edirty.release();
+    c->ekey2.release(); c->eslot.release(); c->escr.release();
+    c->hev_keys.release(); c->hev_sorted.release(); c->hev_pool.release(); c->hev_es.release(); c->hev_ds.release();
+    c->hev_did.release();
+    c->epool.release(); c->edirty.release(); c->edid.release();
     delete c;
     return CACHE_OK;
 }
@@ -412,7 +437,6 @@ cache_status cache_insert(cache_t* c, int64_t n, const void* emb, int32_t emb_dt
             c->h_present[p.slot] = p.mask;
             c->h_ids[p.slot] = p.id;
             for (int j = 0; j < c->num_k; ++j) c->h_lslot[p.slot * c->num_k + j] = p.lslot[j];
-            c->id2slot[p.id] = p.slot;
             c->hwm = std::max(c->hwm, p.slot + 1);
             c->live_entries++;
             c->live_items += __builtin_popcount(p.mask);
@@ -997,45 +1021,17 @@ cache_status cache_evict(cache_t* c, int64_t n, uint64_t* out_evicted, uint64_t*
     return CACHE_OK;
 }
 
-// Host bookkeeping of an entry-granularity eviction (k_evict_apply wrote one (key, slot) per
-// evicted entry): free every stored state's pool slot and the entry slot, in key order.
-static cache_status evict_entries_host(cache_t* c, int64_t n, uint64_t* out_evicted, uint64_t* out_dirty_ids,
-                                       int64_t* out_n_dirty) {
-    std::vector<unsigned long long> keys(n);
-    std::vector<int64_t> dslots(n);
-    if (n) {
-        CK(cudaMemcpy(keys.data(), c->ekey.p, n * 8, cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(dslots.data(), c->edirty.p, n * 8, cudaMemcpyDeviceToHost));
-    }
-    std::vector<size_t> order(n);
-    for (int64_t i = 0; i < n; ++i) order[i] = i;
-    std::sort(order.begin(), order.end(), [&](size_t a, size_t b2) { return keys[a] < keys[b2]; });
-    std::vector<uint64_t> dids;
-    for (int64_t i = 0; i < n; ++i) {
-        const int64_t slot = dslots[order[i]];
-        const uint64_t id = c->h_ids[slot];
-        if (out_evicted) out_evicted[i] = id;
-        dids.push_back(id);
-        const uint32_t m = c->h_present[slot];
-        for (int j = 0; j < c->num_k; ++j) {
-            if (!((m >> j) & 1u)) continue;
-            if (!c->alias) c->free_l.push_back(c->h_lslot[slot * c->num_k + j]);
-            c->h_lslot[slot * c->num_k + j] = -1;
-            c->live_items--;
-        }
-        c->h_present[slot] = 0;
-        c->id2slot.erase(id);
-        c->free_e.push_back(slot);
-        c->live_entries--;
-    }
-    std::sort(dids.begin(), dids.end());
-    if (out_dirty_ids)
-        for (size_t i = 0; i < dids.size(); ++i) out_dirty_ids[i] = dids[i];
-    if (out_n_dirty) *out_n_dirty = (int64_t)dids.size();
-    std::sort(c->free_l.begin(), c->free_l.end(), std::greater<int64_t>());
-    std::sort(c->free_e.begin(), c->free_e.end(), std::greater<int64_t>());
-    while (c->hwm > 0 && c->h_present[c->hwm - 1] == 0) c->hwm--;
-    return CACHE_OK;
+// Merge k freed slots (ascending) into a free list kept sorted descending (back() = lowest
+// free slot, so allocation stays lowest-first and deterministic): one linear merge.
+static void merge_free(std::vector<int64_t>& fl, const unsigned long long* asc, int64_t k, std::vector<int64_t>& tmp) {
+    if (k <= 0) return;
+    tmp.resize(fl.size() + (size_t)k);
+    size_t i = 0, o = 0;
+    int64_t j = k - 1;   // asc read backwards = descending
+    while (i < fl.size() && j >= 0) tmp[o++] = fl[i] > (int64_t)asc[j] ? fl[i++] : (int64_t)asc[j--];
+    while (i < fl.size()) tmp[o++] = fl[i++];
+    while (j >= 0) tmp[o++] = (int64_t)asc[j--];
+    fl.swap(tmp);
 }
 
 cache_status cache_evict_apply(cache_t* c, const cache_evict_state* st, int64_t cap, uint64_t* out_evicted,
@@ -1043,76 +1039,130 @@ cache_status cache_evict_apply(cache_t* c, const cache_evict_state* st, int64_t 
     if (!c || !st || cap < 0) return fail(CACHE_E_INVALID_ARG, "cache_evict_apply: bad argument");
     DeviceGuard g(c->device);
     cudaStream_t s = (cudaStream_t)stream;
-    const int64_t bound = std::max<int64_t>(1, std::max(c->live_items, c->live_entries));
+    const bool entry_mode = c->km.gran == CACHE_EVICT_ENTRY;
+    // at most min(cap, live units) keys are <= the selected threshold on this rank
+    const int64_t bound = std::max<int64_t>(1, std::min<int64_t>(cap, entry_mode ? c->live_entries : c->live_items));
+    const int64_t dbound = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(cap, 1), c->live_entries));
     CK(c->ekey.ensure(bound));
-    CK(c->elslot.ensure(bound));
+    CK(c->ekey2.ensure(std::max(bound, dbound)));
+    CK(c->epool.ensure(bound));
+    CK(c->eslot.ensure(bound));
+    CK(c->escr.ensure(sort_scratch_words(std::max(bound, dbound))));
     CK(c->ecnt.ensure(2));
-    CK(c->edirty.ensure(std::max<int64_t>(1, c->live_entries)));
+    CK(c->edirty.ensure(dbound));
+    CK(c->edid.ensure(dbound));
     CK(cudaMemsetAsync(c->ecnt.p, 0, 16, s));
     launch_evict_apply(c->present, c->fcnt, c->lastacc, c->ids, c->lslot, c->inv_e, c->hwm, c->km,
-                       reinterpret_cast<const EvictState*>(st), c->ekey.p, c->elslot.p, c->ecnt.p, c->edirty.p, s);
+                       reinterpret_cast<const EvictState*>(st), c->ekey.p, c->epool.p, c->eslot.p, c->ecnt.p,
+                       c->edirty.p, c->edid.p, bound, dbound, s);
     c->launches++;
     unsigned long long cnt[2];
     CK(cudaMemcpyAsync(cnt, c->ecnt.p, 16, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    const int64_t n = (int64_t)cnt[0];
+    const int64_t n = (int64_t)cnt[0], nd = (int64_t)cnt[1];
     if (out_n) *out_n = n;
-    if (n > cap || (int64_t)cnt[1] > cap)
-        return fail(CACHE_E_STATE, "cache_evict_apply: more evictions than the output capacity");
-    if (c->km.gran == CACHE_EVICT_ENTRY) return evict_entries_host(c, n, out_evicted, out_dirty_ids, out_n_dirty);
-    std::vector<unsigned long long> keys(n);
-    std::vector<int32_t> ls(n);
-    std::vector<int64_t> dslots(cnt[1]);
-    CK(cudaMemcpy(keys.data(), c->ekey.p, n * 8, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(ls.data(), c->elslot.p, n * 4, cudaMemcpyDeviceToHost));
-    if (cnt[1]) CK(cudaMemcpy(dslots.data(), c->edirty.p, cnt[1] * 8, cudaMemcpyDeviceToHost));
-    // host mirrors + free lists (sorted so allocation stays deterministic)
-    std::vector<size_t> order(n);
-    for (int64_t i = 0; i < n; ++i) order[i] = i;
-    std::sort(order.begin(), order.end(), [&](size_t a, size_t b2) { return keys[a] < keys[b2]; });
-    for (int64_t i = 0; i < n; ++i) {
-        const unsigned long long k = keys[order[i]];
-        const uint64_t idj = k & ((1ull << 35) - 1);
-        if (out_evicted) out_evicted[i] = idj;
-        const uint64_t id = idj >> 3;
-        const int j = (int)(idj & 7);
-        auto it = c->id2slot.find(id);
-        if (it != c->id2slot.end()) {
-            c->h_present[it->second] &= ~(1u << j);
-            c->h_lslot[it->second * c->num_k + j] = -1;
+    if (n > cap || nd > cap || n > bound || nd > dbound)
+        return fail(CACHE_E_STATE, "cache_evict_apply: more evictions than the output capacity (n differs "
+                                   "between the selection and the apply?); handle state undefined");
+    // 1. the unsorted (key, entry slot) pairs for the per-item mirror updates
+    CK(c->hev_keys.ensure(n * 8));
+    CK(c->hev_es.ensure(n * 8));
+    if (n && !entry_mode) {
+        CK(cudaMemcpyAsync(c->hev_keys.p, c->ekey.p, n * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(c->hev_es.p, c->eslot.p, n * 8, cudaMemcpyDeviceToHost, s));
+    }
+    cudaEvent_t copied = nullptr;
+    CK(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
+    CK(cudaEventRecord(copied, s));
+    // 2. sorted lists, on the GPU while the host updates its mirrors: freed pool slots and dirty
+    //    slots (ascending, merged into the lowest-first free lists), dirty ids (the API order),
+    //    evicted keys (eviction order)
+    const bool pool_freed = !entry_mode && !c->alias;
+    CK(c->hev_pool.ensure((pool_freed ? n : 0) * 8));
+    CK(c->hev_ds.ensure(nd * 8));
+    CK(c->hev_did.ensure(nd * 8));
+    CK(c->hev_sorted.ensure(n * 8));
+    if (pool_freed && n) {
+        launch_sort_u64(c->epool.p, c->ekey2.p, n, c->escr.p, s, 32);
+        CK(cudaMemcpyAsync(c->hev_pool.p, c->epool.p, n * 8, cudaMemcpyDeviceToHost, s));
+    }
+    if (nd) {
+        launch_sort_u64(c->edirty.p, c->ekey2.p, nd, c->escr.p, s, 40);
+        CK(cudaMemcpyAsync(c->hev_ds.p, c->edirty.p, nd * 8, cudaMemcpyDeviceToHost, s));
+        launch_sort_u64(c->edid.p, c->ekey2.p, nd, c->escr.p, s, 32);
+        CK(cudaMemcpyAsync(c->hev_did.p, c->edid.p, nd * 8, cudaMemcpyDeviceToHost, s));
+    }
+    if (out_evicted && n) {
+        launch_sort_u64(c->ekey.p, c->ekey2.p, n, c->escr.p, s, 64);
+        CK(cudaMemcpyAsync(c->hev_sorted.p, c->ekey.p, n * 8, cudaMemcpyDeviceToHost, s));
+    }
+    c->launches += 12 * (pool_freed && n) + 24 * (nd > 0) + 24 * (out_evicted && n);
+    CK(cudaEventSynchronize(copied));
+    cudaEventDestroy(copied);
+    if (!entry_mode) {
+        const unsigned long long* keys = static_cast<const unsigned long long*>(c->hev_keys.p);
+        const int64_t* es = static_cast<const int64_t*>(c->hev_es.p);
+        for (int64_t i = 0; i < n; ++i) {
+            const int j = (int)(keys[i] & 7ull);
+            const int64_t slot = es[i];
+            c->h_present[slot] &= ~(1u << j);
+            c->h_lslot[slot * c->num_k + j] = -1;
         }
-        if (!c->alias) c->free_l.push_back(ls[order[i]]);   // aliased slots are shared, never freed
+        c->live_items -= n;
     }
-    c->live_items -= n;
-    std::vector<uint64_t> dids;
-    for (int64_t ds : dslots) {
-        dids.push_back(c->h_ids[ds]);
-        c->id2slot.erase(c->h_ids[ds]);
-        c->h_present[ds] = 0;
-        c->free_e.push_back(ds);
-        c->live_entries--;
+    CK(cudaStreamSynchronize(s));   // sorted lists landed
+    const unsigned long long* ds = static_cast<const unsigned long long*>(c->hev_ds.p);
+    if (entry_mode) {   // every stored state of an evicted entry is freed (pool slots from the mirror)
+        std::vector<unsigned long long> pool;
+        for (int64_t i = 0; i < nd; ++i) {
+            const int64_t slot = (int64_t)ds[i];
+            const uint32_t m = c->h_present[slot];
+            for (int j = 0; j < c->num_k; ++j) {
+                if (!((m >> j) & 1u)) continue;
+                if (!c->alias) pool.push_back((unsigned long long)c->h_lslot[slot * c->num_k + j]);
+                c->h_lslot[slot * c->num_k + j] = -1;
+                c->live_items--;
+            }
+        }
+        std::sort(pool.begin(), pool.end());
+        merge_free(c->free_l, pool.data(), (int64_t)pool.size(), c->free_tmp);
+    } else if (pool_freed) {
+        merge_free(c->free_l, static_cast<const unsigned long long*>(c->hev_pool.p), n, c->free_tmp);
     }
-    std::sort(dids.begin(), dids.end());
-    if (out_dirty_ids)
-        for (size_t i = 0; i < dids.size(); ++i) out_dirty_ids[i] = dids[i];
-    if (out_n_dirty) *out_n_dirty = (int64_t)dids.size();
-    std::sort(c->free_l.begin(), c->free_l.end(), std::greater<int64_t>());
-    std::sort(c->free_e.begin(), c->free_e.end(), std::greater<int64_t>());
+    for (int64_t i = 0; i < nd; ++i) c->h_present[(int64_t)ds[i]] = 0;
+    c->live_entries -= nd;
+    merge_free(c->free_e, ds, nd, c->free_tmp);
+    if (out_dirty_ids) std::memcpy(out_dirty_ids, c->hev_did.p, nd * 8);
+    if (out_n_dirty) *out_n_dirty = nd;
     // shrink the scan high-water mark past trailing empty slots
     while (c->hwm > 0 && c->h_present[c->hwm - 1] == 0) c->hwm--;
+    if (out_evicted && n) {
+        const unsigned long long* sorted = static_cast<const unsigned long long*>(c->hev_sorted.p);
+        // item key = score << 35 | id << 3 | j -> (id << 3 | j); entry key = score << 32 | id -> id
+        const unsigned long long m = entry_mode ? 0xFFFFFFFFull : ((1ull << 35) - 1);
+        for (int64_t i = 0; i < n; ++i) out_evicted[i] = sorted[i] & m;
+    }
     return CACHE_OK;
+}
+
+// Entry slot of id, or -1 (a scan of the host mirrors: only the inspection calls need it).
+static int64_t find_slot(const cache_t* c, uint64_t id) {
+    if (id > 0xFFFFFFFFull) return -1;
+    for (int64_t e = 0; e < c->hwm; ++e)
+        if (c->h_present[e] && c->h_ids[e] == (uint32_t)id) return e;
+    return -1;
 }
 
 cache_status cache_get_meta(cache_t* c, uint64_t id, uint64_t* f, uint32_t* present_mask) {
     if (!c) return fail(CACHE_E_INVALID_ARG, "cache_get_meta: null cache");
-    auto it = c->id2slot.find(id);
-    if (it == c->id2slot.end()) return fail(CACHE_E_INVALID_ARG, "cache_get_meta: unknown id");
+    const int64_t slot = find_slot(c, id);
+    if (slot < 0) return fail(CACHE_E_INVALID_ARG, "cache_get_meta: unknown id");
     DeviceGuard g(c->device);
     std::vector<uint32_t> fv(c->num_k);
     uint32_t m = 0;
     CK(cudaDeviceSynchronize());
-    CK(cudaMemcpy(fv.data(), c->fcnt + it->second * c->num_k, c->num_k * 4, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(&m, c->present + it->second, 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(fv.data(), c->fcnt + slot * c->num_k, c->num_k * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&m, c->present + slot, 4, cudaMemcpyDeviceToHost));
     if (f)
         for (int j = 0; j < c->num_k; ++j) f[j] = fv[j];
     if (present_mask) *present_mask = m;
@@ -1121,11 +1171,11 @@ cache_status cache_get_meta(cache_t* c, uint64_t id, uint64_t* f, uint32_t* pres
 
 cache_status cache_get_row(cache_t* c, uint64_t id, uint16_t* out_bf16) {
     if (!c || !out_bf16) return fail(CACHE_E_INVALID_ARG, "cache_get_row: null argument");
-    auto it = c->id2slot.find(id);
-    if (it == c->id2slot.end()) return fail(CACHE_E_INVALID_ARG, "cache_get_row: unknown id");
+    const int64_t slot = find_slot(c, id);
+    if (slot < 0) return fail(CACHE_E_INVALID_ARG, "cache_get_row: unknown id");
     DeviceGuard g(c->device);
     CK(cudaDeviceSynchronize());
-    CK(cudaMemcpy(out_bf16, c->emb + it->second * c->dim, c->dim * 2, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out_bf16, c->emb + slot * c->dim, c->dim * 2, cudaMemcpyDeviceToHost));
     return CACHE_OK;
 }
 
@@ -1215,8 +1265,23 @@ extern "C" cache_status cache_debug_tc_scores(cache_t* c, int64_t b, const void*
     return CACHE_OK;
 }
 
+extern "C" cache_status cache_debug_sort_u64(uint64_t* keys, int64_t n, void* stream) {
+    if (n < 0 || (n > 0 && !keys)) return fail(CACHE_E_INVALID_ARG, "cache_debug_sort_u64: bad argument");
+    if (n <= 1) return CACHE_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    DevBuf<unsigned long long> tmp;
+    DevBuf<uint32_t> scr;
+    CK(tmp.ensure(n));
+    CK(scr.ensure(sort_scratch_words(n)));
+    launch_sort_u64(reinterpret_cast<unsigned long long*>(keys), tmp.p, n, scr.p, s);
+    cudaError_t e = cudaStreamSynchronize(s);
+    tmp.release();
+    scr.release();
+    CK(e);
+    return CACHE_OK;
+}
+
 extern "C" int64_t cache_debug_slot_of(cache_t* c, uint64_t id) {
     if (!c) return -1;
-    auto it = c->id2slot.find(id);
-    return it == c->id2slot.end() ? -1 : it->second;
+    return find_slot(c, id);
 }

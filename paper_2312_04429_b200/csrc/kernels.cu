@@ -559,42 +559,58 @@ void launch_copy_latents(const uint8_t* src, const CopyPlan* plan, int64_t n, in
 // are invalidated (inv_norm = NaN) in the same kernel.
 // ---------------------------------------------------------------------------------------
 // Policy score of item (e, j) (CACHE_POLICY_*): LCBFU f*K, LRU last-access clock,
-// LFU f, FIFO 0 (the id decides).  Saturated at 2^29-1 to fit the 64-bit key.
-__device__ __forceinline__ unsigned long long evict_key(const KMap& km, const uint32_t* __restrict__ fcnt,
-                                                        const uint32_t* __restrict__ lastacc, int64_t e, int j,
-                                                        uint32_t id) {
-    const int64_t it = e * km.num_k + j;
-    unsigned long long sc;
-    switch (km.policy) {
-        case CACHE_POLICY_LRU: sc = lastacc[it]; break;
-        case CACHE_POLICY_LFU: sc = fcnt[it]; break;
-        case CACHE_POLICY_FIFO: sc = 0ull; break;
-        default: sc = (unsigned long long)fcnt[it] * (unsigned long long)km.kv[j]; break;
-    }
+// LFU f, FIFO 0 (the id decides).  Item key: min(score, 2^29-1) << 35 | id << 3 | j.
+// Entry key (R24): the policy score aggregated over the entry's stored items (LCBFU sum f*K,
+// LFU sum f, LRU max last access, FIFO 0), min(., 2^32-1) << 32 | id.
+// The kernels are instantiated per (policy, granularity) with the K values in registers: a
+// runtime switch and constant-bank loads per item made the sweep instruction-bound (ncu r1y:
+// ~120 SASS instructions per item, 68% issue-slot use at 1.1 TB/s).
+template <int POLICY>
+__device__ __forceinline__ unsigned long long item_score(const uint32_t* __restrict__ fcnt,
+                                                         const uint32_t* __restrict__ lastacc, int64_t it, int kvj) {
+    if constexpr (POLICY == CACHE_POLICY_LRU) return lastacc[it];
+    else if constexpr (POLICY == CACHE_POLICY_LFU) return fcnt[it];
+    else if constexpr (POLICY == CACHE_POLICY_FIFO) return 0ull;
+    else return (unsigned long long)fcnt[it] * (unsigned long long)(unsigned)kvj;
+}
+
+__device__ __forceinline__ unsigned long long item_key(unsigned long long sc, uint32_t id, int j) {
     if (sc > 0x1FFFFFFFull) sc = 0x1FFFFFFFull;
     return (sc << 35) | ((unsigned long long)id << 3) | (unsigned long long)j;
 }
 
-// Entry-granularity key (R24): the policy score aggregated over the entry's stored items
-// (LCBFU sum f*K, LFU sum f, LRU max last access, FIFO 0), saturated at 2^32-1, << 32 | id.
-__device__ __forceinline__ unsigned long long evict_key_entry(const KMap& km, const uint32_t* __restrict__ fcnt,
-                                                              const uint32_t* __restrict__ lastacc, int64_t e,
-                                                              uint32_t m, uint32_t id) {
+template <int POLICY>
+__device__ __forceinline__ unsigned long long entry_key(const uint32_t* __restrict__ fcnt,
+                                                        const uint32_t* __restrict__ lastacc, int64_t e, uint32_t m,
+                                                        uint32_t id, int nk, const int (&kv)[CACHE_MAX_K]) {
     unsigned long long sc = 0ull;
-    for (int j = 0; j < km.num_k; ++j) {
-        if (!((m >> j) & 1u)) continue;
-        const int64_t it = e * km.num_k + j;
-        switch (km.policy) {
-            case CACHE_POLICY_LRU: sc = max(sc, (unsigned long long)lastacc[it]); break;
-            case CACHE_POLICY_LFU: sc += fcnt[it]; break;
-            case CACHE_POLICY_FIFO: break;
-            default: sc += (unsigned long long)fcnt[it] * (unsigned long long)km.kv[j]; break;
-        }
+#pragma unroll
+    for (int j = 0; j < CACHE_MAX_K; ++j) {
+        if (j >= nk || !((m >> j) & 1u)) continue;
+        const unsigned long long v = item_score<POLICY>(fcnt, lastacc, e * nk + j, kv[j]);
+        if constexpr (POLICY == CACHE_POLICY_LRU) sc = v > sc ? v : sc;
+        else sc += v;
     }
     if (sc > 0xFFFFFFFFull) sc = 0xFFFFFFFFull;
     return (sc << 32) | (unsigned long long)id;
 }
 
+// Per-thread run-length aggregation of histogram increments: consecutive keys of a thread
+// mostly share a digit (early passes: almost all), so one shared atomic per run.
+struct DigitRun {
+    unsigned cur = 0xFFFFFFFFu, cnt = 0;
+    __device__ __forceinline__ void add(unsigned* sh, unsigned d) {
+        if (d == cur) { ++cnt; return; }
+        if (cnt) atomicAdd(&sh[cur], cnt);
+        cur = d;
+        cnt = 1;
+    }
+    __device__ __forceinline__ void flush(unsigned* sh) {
+        if (cnt) atomicAdd(&sh[cur], cnt);
+    }
+};
+
+template <int POLICY, int GRAN>
 __global__ void __launch_bounds__(256)
 k_evict_hist(const uint32_t* __restrict__ present, const uint32_t* __restrict__ fcnt,
              const uint32_t* __restrict__ lastacc, const uint32_t* __restrict__ ids, int64_t n_slots, KMap km,
@@ -602,23 +618,31 @@ k_evict_hist(const uint32_t* __restrict__ present, const uint32_t* __restrict__ 
     __shared__ unsigned int sh[256];
     sh[threadIdx.x] = 0;
     __syncthreads();
+    const int nk = km.num_k;
+    int kv[CACHE_MAX_K];
+#pragma unroll
+    for (int j = 0; j < CACHE_MAX_K; ++j) kv[j] = km.kv[j];
     const unsigned long long prefix = st->prefix, mask = st->mask;
+    DigitRun run;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_slots;
          e += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t m = present[e];
         if (!m) continue;
         const uint32_t id = ids[e];
-        if (km.gran == CACHE_EVICT_ENTRY) {
-            const unsigned long long key = evict_key_entry(km, fcnt, lastacc, e, m, id);
-            if ((key & mask) == prefix) atomicAdd(&sh[(key >> shift) & 255ull], 1u);
-            continue;
-        }
-        for (int j = 0; j < km.num_k; ++j) {
-            if (!((m >> j) & 1u)) continue;
-            const unsigned long long key = evict_key(km, fcnt, lastacc, e, j, id);
-            if ((key & mask) == prefix) atomicAdd(&sh[(key >> shift) & 255ull], 1u);
+        if constexpr (GRAN == CACHE_EVICT_ENTRY) {
+            const unsigned long long key = entry_key<POLICY>(fcnt, lastacc, e, m, id, nk, kv);
+            if ((key & mask) == prefix) run.add(sh, (unsigned)(key >> shift) & 255u);
+        } else {
+#pragma unroll
+            for (int j = 0; j < CACHE_MAX_K; ++j) {
+                if (j >= nk || !((m >> j) & 1u)) continue;
+                const unsigned long long key =
+                    item_key(item_score<POLICY>(fcnt, lastacc, e * nk + j, kv[j]), id, j);
+                if ((key & mask) == prefix) run.add(sh, (unsigned)(key >> shift) & 255u);
+            }
         }
     }
+    run.flush(sh);
     __syncthreads();
     if (sh[threadIdx.x]) atomicAdd(&hist[threadIdx.x], sh[threadIdx.x]);
 }
@@ -641,62 +665,128 @@ __global__ void k_evict_pick(unsigned int* __restrict__ hist, EvictState* __rest
     for (int d = threadIdx.x; d < 256; d += blockDim.x) hist[d] = 0;
 }
 
+// One output slot range per warp and key column: a ballot of the evicting lanes, one atomic by
+// the leader, each lane's index = its rank among them (per-lane atomics on one counter
+// serialised at L2).  Item mode also emits each item's entry slot so the host updates its
+// mirrors without an id lookup.  The sweep is warp-uniform (lane l takes slot base + l).
+__device__ __forceinline__ unsigned long long warp_claim(unsigned long long* counter, bool take, int lane) {
+    const unsigned bal = __ballot_sync(0xFFFFFFFFu, take);
+    unsigned long long base = 0;
+    if (bal) {
+        if (lane == __ffs(bal) - 1) base = atomicAdd(counter, (unsigned long long)__popc(bal));
+        base = __shfl_sync(0xFFFFFFFFu, base, __ffs(bal) - 1);
+    }
+    return base + (unsigned long long)__popc(bal & ((1u << lane) - 1u));
+}
+
+template <int POLICY, int GRAN>
 __global__ void __launch_bounds__(256)
 k_evict_apply(uint32_t* __restrict__ present, uint32_t* __restrict__ fcnt, const uint32_t* __restrict__ lastacc,
               const uint32_t* __restrict__ ids, const int32_t* __restrict__ lslot, float* __restrict__ inv_e,
               int64_t n_slots, KMap km,
               const EvictState* __restrict__ st, unsigned long long* __restrict__ ev_key,
-              int32_t* __restrict__ ev_lslot, unsigned long long* __restrict__ counters,
-              int64_t* __restrict__ dirty_slot) {
+              unsigned long long* __restrict__ ev_pool, int64_t* __restrict__ ev_eslot,
+              unsigned long long* __restrict__ counters, unsigned long long* __restrict__ dirty_slot,
+              unsigned long long* __restrict__ dirty_id, unsigned long long ev_cap, unsigned long long dirty_cap) {
     const unsigned long long T = st->prefix;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_slots;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t m = present[e];
-        if (!m) continue;
-        const uint32_t id = ids[e];
-        if (km.gran == CACHE_EVICT_ENTRY) {
+    const int lane = threadIdx.x & 31;
+    const int nk = km.num_k;
+    int kv[CACHE_MAX_K];
+#pragma unroll
+    for (int j = 0; j < CACHE_MAX_K; ++j) kv[j] = km.kv[j];
+    for (int64_t e0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); e0 < n_slots;
+         e0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = e0 + lane;
+        const uint32_t m = e < n_slots ? present[e] : 0u;
+        const uint32_t id = m ? ids[e] : 0u;
+        if constexpr (GRAN == CACHE_EVICT_ENTRY) {
             // whole entry: all stored states freed (the host frees their pool slots from its
             // mirror), entry invalidated; one record per evicted entry in both lists
-            const unsigned long long key = evict_key_entry(km, fcnt, lastacc, e, m, id);
-            if (key <= T) {
-                for (int j = 0; j < km.num_k; ++j) fcnt[e * km.num_k + j] = 0u;
+            const unsigned long long key = m ? entry_key<POLICY>(fcnt, lastacc, e, m, id, nk, kv) : 0ull;
+            const bool take = m && key <= T;
+            const unsigned long long at = warp_claim(&counters[0], take, lane);
+            if (take) {
+                for (int j = 0; j < nk; ++j) fcnt[e * nk + j] = 0u;
                 present[e] = 0u;
                 inv_e[e] = __int_as_float(0x7FC00000);
-                const unsigned long long at = atomicAdd(&counters[0], 1ull);
-                atomicAdd(&counters[1], 1ull);
-                ev_key[at] = key;
-                dirty_slot[at] = e;
+                if (at < ev_cap && at < dirty_cap) {   // overflow = caller error, reported by the host
+                    ev_key[at] = key;
+                    dirty_slot[at] = (unsigned long long)e;
+                    dirty_id[at] = id;
+                }
             }
-            continue;
-        }
-        uint32_t keep = m;
-        for (int j = 0; j < km.num_k; ++j) {
-            if (!((m >> j) & 1u)) continue;
-            const unsigned long long key = evict_key(km, fcnt, lastacc, e, j, id);
-            if (key <= T) {
-                keep &= ~(1u << j);
-                const unsigned long long at = atomicAdd(&counters[0], 1ull);
-                ev_key[at] = key;
-                ev_lslot[at] = lslot[e * km.num_k + j];
-                fcnt[e * km.num_k + j] = 0u;
+            (void)warp_claim(&counters[1], take, lane);   // dirty count = evicted count in entry mode
+        } else {
+            uint32_t keep = m;
+#pragma unroll
+            for (int j = 0; j < CACHE_MAX_K; ++j) {
+                if (j >= nk) break;   // warp-uniform
+                const bool has = (m >> j) & 1u;
+                const unsigned long long key =
+                    has ? item_key(item_score<POLICY>(fcnt, lastacc, e * nk + j, kv[j]), id, j) : 0ull;
+                const bool take = has && key <= T;
+                const unsigned long long at = warp_claim(&counters[0], take, lane);
+                if (take) {
+                    keep &= ~(1u << j);
+                    if (at < ev_cap) {
+                        ev_key[at] = key;
+                        ev_pool[at] = (unsigned long long)(uint32_t)lslot[e * nk + j];
+                        ev_eslot[at] = e;
+                    }
+                    fcnt[e * nk + j] = 0u;
+                }
             }
-        }
-        if (keep != m) {
-            present[e] = keep;
-            if (keep == 0u) {
-                inv_e[e] = __int_as_float(0x7FC00000);
-                const unsigned long long at = atomicAdd(&counters[1], 1ull);
-                dirty_slot[at] = e;
+            const bool dirty = m && keep == 0u;
+            if (keep != m) {
+                present[e] = keep;
+                if (dirty) inv_e[e] = __int_as_float(0x7FC00000);
+            }
+            const unsigned long long at = warp_claim(&counters[1], dirty, lane);
+            if (dirty && at < dirty_cap) {
+                dirty_slot[at] = (unsigned long long)e;
+                dirty_id[at] = id;
             }
         }
     }
 }
 
+// Grid = one wave of resident CTAs (the sweeps are grid-stride loops).
+template <typename K>
+static int one_wave(K kern) {
+    int bps = 0, dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 256, 0) != cudaSuccess || bps < 1) bps = 4;
+    return bps * sms;
+}
+
+#define NV_EVICT_DISPATCH(KERN, ...)                                                                   \
+    do {                                                                                               \
+        const int pol_ = km.policy, gr_ = km.gran;                                                     \
+        if (gr_ == CACHE_EVICT_ENTRY) {                                                                \
+            if (pol_ == CACHE_POLICY_LRU) KERN(CACHE_POLICY_LRU, CACHE_EVICT_ENTRY);                   \
+            else if (pol_ == CACHE_POLICY_LFU) KERN(CACHE_POLICY_LFU, CACHE_EVICT_ENTRY);              \
+            else if (pol_ == CACHE_POLICY_FIFO) KERN(CACHE_POLICY_FIFO, CACHE_EVICT_ENTRY);            \
+            else KERN(CACHE_POLICY_LCBFU, CACHE_EVICT_ENTRY);                                          \
+        } else {                                                                                       \
+            if (pol_ == CACHE_POLICY_LRU) KERN(CACHE_POLICY_LRU, CACHE_EVICT_ITEM);                    \
+            else if (pol_ == CACHE_POLICY_LFU) KERN(CACHE_POLICY_LFU, CACHE_EVICT_ITEM);               \
+            else if (pol_ == CACHE_POLICY_FIFO) KERN(CACHE_POLICY_FIFO, CACHE_EVICT_ITEM);             \
+            else KERN(CACHE_POLICY_LCBFU, CACHE_EVICT_ITEM);                                           \
+        }                                                                                              \
+    } while (0)
+
 void launch_evict_hist(const uint32_t* present, const uint32_t* fcnt, const uint32_t* lastacc, const uint32_t* ids,
                        int64_t n_slots, const KMap& km, const EvictState* st, int pass, unsigned int* hist,
                        cudaStream_t s) {
-    const int grid = (int)std::min<int64_t>(148 * 8, (n_slots + 255) / 256 + 1);
-    k_evict_hist<<<grid, 256, 0, s>>>(present, fcnt, lastacc, ids, n_slots, km, st, 56 - 8 * pass, hist);
+#define NV_HIST(P, G)                                                                                  \
+    do {                                                                                               \
+        static const int wave = one_wave(k_evict_hist<P, G>);                                          \
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(wave, (n_slots + 255) / 256));   \
+        k_evict_hist<P, G><<<grid, 256, 0, s>>>(present, fcnt, lastacc, ids, n_slots, km, st, 56 - 8 * pass, hist); \
+    } while (0)
+    NV_EVICT_DISPATCH(NV_HIST);
+#undef NV_HIST
 }
 
 void launch_evict_pick(unsigned int* hist, EvictState* st, int pass, cudaStream_t s) {
@@ -902,11 +992,19 @@ void launch_merge_sharded(int kmax, const cache_shard_rec* recs, int64_t rec_str
 
 void launch_evict_apply(uint32_t* present, uint32_t* fcnt, const uint32_t* lastacc, const uint32_t* ids,
                         const int32_t* lslot, float* inv_e, int64_t n_slots, const KMap& km, const EvictState* st,
-                        unsigned long long* ev_key, int32_t* ev_lslot, unsigned long long* counters,
-                        int64_t* dirty_slot, cudaStream_t s) {
-    const int grid = (int)std::min<int64_t>(148 * 8, (n_slots + 255) / 256 + 1);
-    k_evict_apply<<<grid, 256, 0, s>>>(present, fcnt, lastacc, ids, lslot, inv_e, n_slots, km, st, ev_key,
-                                       ev_lslot, counters, dirty_slot);
+                        unsigned long long* ev_key, unsigned long long* ev_pool, int64_t* ev_eslot,
+                        unsigned long long* counters, unsigned long long* dirty_slot, unsigned long long* dirty_id,
+                        int64_t ev_cap, int64_t dirty_cap, cudaStream_t s) {
+#define NV_APPLY(P, G)                                                                                 \
+    do {                                                                                               \
+        static const int wave = one_wave(k_evict_apply<P, G>);                                         \
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(wave, (n_slots + 255) / 256));   \
+        k_evict_apply<P, G><<<grid, 256, 0, s>>>(present, fcnt, lastacc, ids, lslot, inv_e, n_slots, km, st,  \
+                                                 ev_key, ev_pool, ev_eslot, counters, dirty_slot, dirty_id, \
+                                                 (unsigned long long)ev_cap, (unsigned long long)dirty_cap); \
+    } while (0)
+    NV_EVICT_DISPATCH(NV_APPLY);
+#undef NV_APPLY
 }
 
 }  // namespace nv

@@ -74,8 +74,14 @@ void launch_evict_hist(const uint32_t* present, const uint32_t* fcnt, const uint
 void launch_evict_pick(unsigned int* hist, EvictState* st, int pass, cudaStream_t s);
 void launch_evict_apply(uint32_t* present, uint32_t* fcnt, const uint32_t* lastacc, const uint32_t* ids,
                         const int32_t* lslot, float* inv_e, int64_t n_slots, const KMap& km, const EvictState* st,
-                        unsigned long long* ev_key, int32_t* ev_lslot, unsigned long long* counters,
-                        int64_t* dirty_slot, cudaStream_t s);
+                        unsigned long long* ev_key, unsigned long long* ev_pool, int64_t* ev_eslot,
+                        unsigned long long* counters, unsigned long long* dirty_slot, unsigned long long* dirty_id,
+                        int64_t ev_cap, int64_t dirty_cap, cudaStream_t s);
+// Ascending sort of n 64-bit keys whose values are < 2^bits (LSD radix, 8-bit digits, an even
+// number of stable passes); tmp: n keys, scratch: >= sort_scratch_words(n) u32.  Result in keys.
+int64_t sort_scratch_words(int64_t n);
+void launch_sort_u64(unsigned long long* keys, unsigned long long* tmp, int64_t n, uint32_t* scratch,
+                     cudaStream_t s, int bits = 64);
 
 // match predictor (predictor.cu)
 void pred_margins(const __nv_bfloat16* emb, const float* inv_e, int64_t n_slots, int dim, const float* w,

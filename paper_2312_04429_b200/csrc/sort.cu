@@ -1,0 +1,146 @@
+// sort.cu -- ascending LSD radix sort of 64-bit keys on the GPU.  Used for cache_evict's
+// out_evicted (the selected items in eviction = key order, R11 / R24): the selection kernels
+// emit keys in arbitrary order and sorting ~10^5-10^6 keys on the host cost tens of ms.
+//
+// 8 passes of 8-bit digits; every pass is stable:
+//   k_sort_count    per 2,048-key tile: digit counts (warp-aggregated shared atomics),
+//                   stored digit-major counts[d][tile], and the pass's digit totals
+//   k_sort_scan     one CTA per digit d: base = sum of the lower digits' totals, then a
+//                   block-parallel exclusive scan over the tiles -> the output position of
+//                   each tile's first key with digit d
+//   k_sort_scatter  the tile again in 8 rounds of 256 keys (index order): rank within the warp
+//                   from __match_any_sync, prefix over the warps per digit, running base per
+//                   digit across rounds -> every key lands after all earlier keys of its digit
+#include "kernels.h"
+
+namespace nv {
+
+constexpr int kSortThreads = 256, kSortRounds = 8, kSortTile = kSortThreads * kSortRounds;
+
+__global__ void __launch_bounds__(256)
+k_sort_count(const unsigned long long* __restrict__ keys, int64_t n, int shift, uint32_t* __restrict__ counts,
+             int64_t ntiles, uint32_t* __restrict__ dtot) {
+    __shared__ uint32_t sh[256];
+    sh[threadIdx.x] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t base = (int64_t)blockIdx.x * kSortTile;
+    for (int r = 0; r < kSortRounds; ++r) {
+        const int64_t i = base + r * kSortThreads + threadIdx.x;
+        const bool v = i < n;
+        const unsigned d = v ? (unsigned)((keys[i] >> shift) & 255ull) : 256u;
+        const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
+        if (v && lane == __ffs(peers) - 1) atomicAdd(&sh[d], (unsigned)__popc(peers));
+    }
+    __syncthreads();
+    const uint32_t c = sh[threadIdx.x];
+    counts[(int64_t)threadIdx.x * ntiles + blockIdx.x] = c;
+    if (c) atomicAdd(&dtot[threadIdx.x], c);
+}
+
+__device__ __forceinline__ uint32_t block_incl_scan_1024(uint32_t x, uint32_t* ws, uint32_t* total) {
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) ws[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t v = ws[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, v, o);
+            if (lane >= o) v += y;
+        }
+        ws[lane] = v;
+    }
+    __syncthreads();
+    const uint32_t r = x + (w ? ws[w - 1] : 0u);
+    *total = ws[31];
+    __syncthreads();
+    return r;
+}
+
+// CTA d: counts[d][0..ntiles) -> exclusive positions, offset by the keys of all digits < d.
+__global__ void __launch_bounds__(1024) k_sort_scan(uint32_t* __restrict__ counts, int64_t ntiles,
+                                                    const uint32_t* __restrict__ dtot) {
+    __shared__ uint32_t ws[32];
+    const int d = blockIdx.x, t = threadIdx.x;
+    uint32_t tot = 0;
+    uint32_t lower = (t < d) ? dtot[t] : 0u;   // 256 digits <= 1024 threads
+    uint32_t run = block_incl_scan_1024(lower, ws, &tot);
+    (void)run;
+    uint32_t carry = tot;                      // sum over digits < d
+    uint32_t* a = counts + (int64_t)d * ntiles;
+    for (int64_t i0 = 0; i0 < ntiles; i0 += 1024) {
+        const int64_t i = i0 + t;
+        const uint32_t c = i < ntiles ? a[i] : 0u;
+        uint32_t blk = 0;
+        const uint32_t incl = block_incl_scan_1024(c, ws, &blk);
+        if (i < ntiles) a[i] = carry + incl - c;
+        carry += blk;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+k_sort_scatter(const unsigned long long* __restrict__ in, unsigned long long* __restrict__ out, int64_t n, int shift,
+               const uint32_t* __restrict__ offs, int64_t ntiles) {
+    __shared__ uint32_t s_base[256];
+    __shared__ uint32_t s_tot[256];
+    __shared__ uint32_t s_w[8][256];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    s_base[threadIdx.x] = offs[(int64_t)threadIdx.x * ntiles + blockIdx.x];
+    const int64_t base = (int64_t)blockIdx.x * kSortTile;
+    for (int r = 0; r < kSortRounds; ++r) {
+#pragma unroll
+        for (int w = 0; w < 8; ++w) s_w[w][threadIdx.x] = 0u;
+        __syncthreads();
+        const int64_t i = base + r * kSortThreads + threadIdx.x;
+        const bool v = i < n;
+        const unsigned long long k = v ? in[i] : 0ull;
+        const unsigned d = v ? (unsigned)((k >> shift) & 255ull) : 256u;
+        const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
+        const unsigned rank = (unsigned)__popc(peers & ((1u << lane) - 1u));
+        if (v && lane == __ffs(peers) - 1) s_w[warp][d] = (unsigned)__popc(peers);
+        __syncthreads();
+        {   // thread = digit: exclusive prefix over the warps (warp order = index order)
+            uint32_t run = 0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) {
+                const uint32_t c = s_w[w][threadIdx.x];
+                s_w[w][threadIdx.x] = run;
+                run += c;
+            }
+            s_tot[threadIdx.x] = run;
+        }
+        __syncthreads();
+        if (v) out[(int64_t)s_base[d] + s_w[warp][d] + rank] = k;
+        __syncthreads();
+        s_base[threadIdx.x] += s_tot[threadIdx.x];
+    }
+}
+
+// scratch: counts[256][ntiles] | digit totals [8 passes][256]
+int64_t sort_scratch_words(int64_t n) { return 256 * std::max<int64_t>(1, (n + kSortTile - 1) / kSortTile) + 8 * 256; }
+
+void launch_sort_u64(unsigned long long* keys, unsigned long long* tmp, int64_t n, uint32_t* scratch,
+                     cudaStream_t s, int bits) {
+    if (n <= 1) return;
+    const int passes = ((std::min(64, std::max(8, bits)) + 15) / 16) * 2;   // even: result lands in keys
+    const int64_t ntiles = (n + kSortTile - 1) / kSortTile;
+    unsigned long long *src = keys, *dst = tmp;
+    uint32_t* dtot = scratch + 256 * ntiles;
+    cudaMemsetAsync(dtot, 0, 8 * 256 * sizeof(uint32_t), s);
+    for (int pass = 0; pass < passes; ++pass) {
+        const int shift = 8 * pass;
+        k_sort_count<<<(unsigned)ntiles, 256, 0, s>>>(src, n, shift, scratch, ntiles, dtot + 256 * pass);
+        k_sort_scan<<<256, 1024, 0, s>>>(scratch, ntiles, dtot + 256 * pass);
+        k_sort_scatter<<<(unsigned)ntiles, 256, 0, s>>>(src, dst, n, shift, scratch, ntiles);
+        std::swap(src, dst);
+    }
+    // an even number of passes: the result is back in `keys`
+}
+
+}  // namespace nv

@@ -1,0 +1,51 @@
+"""Eviction at C5's per-rank scale (100M entries over 8 GPUs -> 12.5M per rank):
+LCBFU cache_evict of 1% of the live items after a few query batches, timed end to end (the
+call is host-synchronous) plus the kernel split from a CUDA-event-free wall clock.
+usage: python scripts/evict_scale.py [n_entries] [policy] [granularity]"""
+import json
+import sys
+import time
+
+import numpy as np
+import torch
+
+import synth
+from paper_2312_04429_b200 import binding as B
+
+
+def main():
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 12_500_000
+    policy = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+    gran = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+    D = 768
+    g = B.NirvanaCache(entry_capacity=n + 1024, latent_capacity=1 << 16, dim=D, latent_bytes=256, latent_alias=True,
+                       evict_granularity=gran)
+    g.set_evict_policy(policy)
+    E = synth.TorchEntries(n, seed=5, device="cuda")
+    pres = synth.present_masks(n, seed=5)
+    t0 = time.perf_counter()
+    for s in range(0, n, 65536):
+        m = min(65536, n - s)
+        g.insert(E.rows(torch.arange(s, s + m, dtype=torch.int64, device="cuda")), None, present=pres[s:s + m])
+    torch.cuda.synchronize()
+    t_ins = time.perf_counter() - t0
+    for r in range(3):                       # give the counters some non-zero f
+        q, _, _ = E.queries(16384, qseed=11 + r)
+        g.query(q, topk=1, latents=False)
+    torch.cuda.synchronize()
+    res = dict(entries=n, policy=policy, granularity=gran, insert_s=t_ins, live_items=g.live_items)
+    units = g.live_entries if gran else g.live_items
+    for rep in range(3):
+        k = max(1, units // 100)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ev, dirty = g.evict(k)
+        t = time.perf_counter() - t0
+        res[f"evict{rep}"] = dict(n=k, ms=1e3 * t, dirty=len(dirty))
+    # HBM bytes per pass: present + ids (4 + 4) + the policy's per-item column (5 x 4) per slot
+    res["bytes_per_pass"] = (n + 1024) * (8 + 20)
+    print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()

@@ -9,12 +9,17 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HEADER = os.path.join(ROOT, "include", "nirvana_cache.h")
+HEADERS = sorted(os.path.join(ROOT, "include", f) for f in os.listdir(os.path.join(ROOT, "include"))
+                 if f.endswith(".h"))
 
 
 def _declared():
-    src = open(HEADER).read()
-    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(cache_\w+)\s*\(", src)))
+    names = set()
+    for h in HEADERS:
+        src = re.sub(r"/\*.*?\*/", "", open(h).read(), flags=re.S)
+        src = re.sub(r"#define[^\n]*", "", src)
+        names |= set(re.findall(r"\b(cache_\w+)\s*\(", src))
+    return sorted(names)
 
 
 @pytest.fixture(scope="module")
@@ -58,3 +63,32 @@ def test_create_rejects_bad_config_without_gpu(libpath):
     h = ctypes.c_void_p()
     rc = binding.lib().cache_create(ctypes.byref(cfg), 0, ctypes.byref(h))
     assert rc == binding.E_DIM and not h.value
+
+
+def test_struct_layouts_match_the_binding(tmp_path):
+    """sizeof / offsetof of every ABI struct, printed by a C program compiled against the
+    header, equal the ctypes mirrors in the binding."""
+    from paper_2312_04429_b200 import binding as B
+    structs = {"cache_config": B.CacheConfig, "cache_stats_t": B.CacheStats, "cache_peer_desc": B.PeerDesc}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "nirvana_cache.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f, _ in py._fields_:
+            lines.append(f'printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    lines += ['printf("cache_shard_rec size %zu\\n", sizeof(cache_shard_rec));',
+              'printf("cache_evict_state size %zu\\n", sizeof(cache_evict_state));', "return 0; }"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+                           str(src), "-o", str(exe)])
+    got = {}
+    for ln in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.splitlines():
+        *k, v = ln.split()
+        got[tuple(k)] = int(v)
+    for cname, py in structs.items():
+        assert got[(cname, "size")] == ctypes.sizeof(py), cname
+        for f, _ in py._fields_:
+            assert got[(cname, f)] == getattr(py, f).offset, (cname, f)
+    assert got[("cache_shard_rec", "size")] == B.SHARD_REC_BYTES == 16
+    assert got[("cache_evict_state", "size")] == B.EVICT_STATE_BYTES
