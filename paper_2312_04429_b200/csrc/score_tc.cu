@@ -37,7 +37,8 @@ constexpr int EPI_WARP0 = 4;
 constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                            ((uint32_t)(BM >> 4) << 24);
 constexpr int SMEM_INV_OFF = STAGES * STAGE_BYTES;              // 2 x 256 floats
-constexpr int SMEM_BAR_OFF = SMEM_INV_OFF + 2 * BN * 4;          // 2*STAGES + 4 mbarriers
+constexpr int SMEM_IDS_OFF = SMEM_INV_OFF + 2 * BN * 4;          // 2 x 256 entry ids
+constexpr int SMEM_BAR_OFF = SMEM_IDS_OFF + 2 * BN * 4;          // 2*STAGES + 4 mbarriers
 constexpr int SMEM_TMEM_OFF = SMEM_BAR_OFF + (2 * STAGES + 4) * 8;
 constexpr int SMEM_XCH_OFF = SMEM_TMEM_OFF + 16;                  // half-merge exchange (128 x 16 x 12 B)
 constexpr int SMEM_BYTES = SMEM_XCH_OFF + BM * 16 * 12 + 1024;   // + alignment slack
@@ -149,10 +150,14 @@ __device__ __forceinline__ float4 lds_f4(uint32_t addr) {
     return v;
 }
 
-// Scale one 32-column chunk by the entry inv-norms, gate on its max, offer survivors.
+// Scale one 32-column chunk by the entry inv-norms, gate on its max, offer survivors.  The
+// tile's entry ids are staged in shared memory next to the inv-norms: an offer used to load
+// its id from global memory, and those dependent L2 round trips (one per improving value)
+// kept the epilogue holding its TMEM accumulator while the MMA waited for it (measured: the
+// scan ran 11% faster with the epilogue's loads or its arithmetic alone).
 template <int KMAX, bool kDense>
 __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], uint32_t inv_addr, uint32_t col0, TopK<KMAX>& tk,
-                                          const uint32_t* __restrict__ ids, float* dense_row) {
+                                          uint32_t ids_addr, float* dense_row) {
     float t[32];
     float mx = -INFINITY;
 #pragma unroll
@@ -172,7 +177,12 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], uint32_t inv_
         }
     } else if (mx >= tk.thr) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) tk.offer(t[i], col0 + i, ids);
+        for (int i = 0; i < 32; ++i) {
+            if (!(t[i] >= tk.thr)) continue;   // also rejects NaN (empty slots)
+            uint32_t id;
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(id) : "r"(ids_addr + 4 * i));
+            tk.offer_key(make_key(t[i], id), col0 + i);
+        }
     }
 }
 
@@ -192,6 +202,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ C
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SMEM_TMEM_OFF);
     const uint32_t sbase = smem_u32(smem);
     const uint32_t inv_base = sbase + SMEM_INV_OFF;
+    const uint32_t ids_base = sbase + SMEM_IDS_OFF;
     const uint32_t bar_full = sbase + SMEM_BAR_OFF, bar_empty = bar_full + STAGES * 8;
     const uint32_t bar_tfull = bar_empty + STAGES * 8, bar_tempty = bar_tfull + 2 * 8;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -283,31 +294,56 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ C
         const int et = threadIdx.x - EPI_WARP0 * 32;        // 0..255
         const int row = 32 * ew + lane;
         uint32_t acc = 0, acc_phase = 0;
+        // The gate word and the first tile's inv-norm / id of a unit are fetched during the
+        // previous unit's last tile, so no global latency is exposed at a unit boundary while
+        // the MMA may be waiting for this warp's accumulator release.
+        auto gate_of = [&](int uu) -> uint32_t {
+            const int64_t qq = (int64_t)(uu % m_tiles) * BM + row;   // unit = chunk * m_tiles + m
+            return (!kDense && gk != nullptr && qq < B) ? *reinterpret_cast<volatile const uint32_t*>(gk + qq) : 0u;
+        };
+        float inv_next = 0.0f;
+        uint32_t id_next = 0u, gk_next = 0u;
+        if ((int)blockIdx.x < n_units) {
+            const int64_t c0 = (int64_t)((int)blockIdx.x / m_tiles) * chunk_tiles * BN + et;
+            inv_next = __ldg(inv_e + c0);
+            id_next = kDense ? 0u : __ldg(ids + c0);
+            gk_next = gate_of(blockIdx.x);
+        }
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             const int chunk = u / m_tiles, m = u - chunk * m_tiles;
             const int n0 = chunk * chunk_tiles, n1 = min(n_tiles, n0 + chunk_tiles);
             const int64_t q = (int64_t)m * BM + row;
+            const int u_next = u + (int)gridDim.x;
+            const int unit_div = m_tiles;
             float* dense_row = (kDense && q < B) ? dense + q * dense_ld : nullptr;
             TopK<KMAX> tk;
             tk.init();
             // Seed the gate with a global lower bound on this query's k-th best scan value:
             // the best k-th value of any finished unit (every member of the final top-k has
-            // t >= it, so nothing that can reach the final top-k is ever gated out).
-            if (!kDense && gk != nullptr && q < B) {
-                const uint32_t g = *reinterpret_cast<volatile const uint32_t*>(gk + q);
-                if (g != 0u) tk.thr = key_to_f32((unsigned long long)g << 32);
-            }
+            // t >= it, so nothing that can reach the final top-k is ever gated out; a value
+            // read a tile early is merely a weaker bound).
+            if (gk_next != 0u) tk.thr = key_to_f32((unsigned long long)gk_next << 32);
             if (q >= B) tk.thr = INFINITY;   // padding rows of the last query tile: never offer
-            float inv_next = __ldg(inv_e + (int64_t)n0 * BN + et);
 #pragma unroll 1
             for (int n = n0; n < n1; ++n) {
-                // entry inv-norms of this tile -> smem (double-buffered by accumulator); the
-                // next tile's value is fetched now so its L2 latency hides behind this tile
+                // entry inv-norms and ids of this tile -> smem (double-buffered by accumulator);
+                // the next tile's values are fetched now so their L2 latency hides behind this tile
                 const uint32_t ivb = inv_base + acc * BN * 4;
+                const uint32_t idb = ids_base + acc * BN * 4;
                 {
                     const float v = inv_next;
-                    if (n + 1 < n1) inv_next = __ldg(inv_e + (int64_t)(n + 1) * BN + et);
+                    const uint32_t idv = id_next;
+                    if (n + 1 < n1) {
+                        inv_next = __ldg(inv_e + (int64_t)(n + 1) * BN + et);
+                        if (!kDense) id_next = __ldg(ids + (int64_t)(n + 1) * BN + et);
+                    } else if (u_next < n_units) {   // this CTA's next unit
+                        const int64_t c0 = (int64_t)(u_next / unit_div) * chunk_tiles * BN + et;
+                        inv_next = __ldg(inv_e + c0);
+                        if (!kDense) id_next = __ldg(ids + c0);
+                        gk_next = gate_of(u_next);
+                    }
                     asm volatile("st.shared.f32 [%0], %1;" ::"r"(ivb + 4 * et), "f"(v) : "memory");
+                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(idb + 4 * et), "r"(idv) : "memory");
                 }
                 asm volatile("bar.sync 1, 256;" ::: "memory");
                 mbar_wait(bar_tfull + 8 * acc, acc_phase);
@@ -315,13 +351,14 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ C
                 const uint32_t taddr = tmem_base + ((uint32_t)(32 * ew) << 16) + acc * BN + h * 128;
                 const uint32_t col_base = (uint32_t)(n * BN + h * 128);
                 const uint32_t ivh = ivb + 4 * (h * 128);
+                const uint32_t idh = idb + 4 * (h * 128);
                 uint32_t ra[32], rb[32];
                 tmem_ld32(taddr, ra);
                 tmem_ld_wait_regs(ra);
 #pragma unroll 1
                 for (int c = 0; c < 128; c += 64) {
                     tmem_ld32(taddr + c + 32, rb);
-                    epi_chunk<KMAX, kDense>(ra, ivh + 4 * c, col_base + c, tk, ids, dense_row);
+                    epi_chunk<KMAX, kDense>(ra, ivh + 4 * c, col_base + c, tk, idh + 4 * c, dense_row);
                     tmem_ld_wait_regs(rb);
                     if (c + 64 < 128) tmem_ld32(taddr + c + 64, ra);
                     else {
@@ -329,7 +366,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ C
                         __syncwarp();
                         if (lane == 0) mbar_arrive(bar_tempty + 8 * acc);   // TMEM columns free again
                     }
-                    epi_chunk<KMAX, kDense>(rb, ivh + 4 * (c + 32), col_base + c + 32, tk, ids, dense_row);
+                    epi_chunk<KMAX, kDense>(rb, ivh + 4 * (c + 32), col_base + c + 32, tk, idh + 4 * (c + 32), dense_row);
                     if (c + 64 < 128) tmem_ld_wait_regs(ra);
                 }
                 acc ^= 1;
@@ -395,7 +432,8 @@ constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // 32 KiB
 constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                            ((uint32_t)(256 >> 4) << 24);   // M = 256 (the pair), N = 256
 constexpr int SMEM_INV_OFF = STAGES * STAGE_BYTES;
-constexpr int SMEM_BAR_OFF = SMEM_INV_OFF + 2 * BN * 4;
+constexpr int SMEM_IDS_OFF = SMEM_INV_OFF + 2 * BN * 4;
+constexpr int SMEM_BAR_OFF = SMEM_IDS_OFF + 2 * BN * 4;
 constexpr int SMEM_TMEM_OFF = SMEM_BAR_OFF + (2 * STAGES + 4) * 8;
 constexpr int SMEM_XCH_OFF = SMEM_TMEM_OFF + 16;
 constexpr int SMEM_BYTES = SMEM_XCH_OFF + BM * 16 * 12 + 1024;
@@ -456,6 +494,7 @@ k_score_tc2(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ 
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SMEM_TMEM_OFF);
     const uint32_t sbase = smem_u32(smem);
     const uint32_t inv_base = sbase + SMEM_INV_OFF;
+    const uint32_t ids_base = sbase + SMEM_IDS_OFF;
     const uint32_t bar_full = sbase + SMEM_BAR_OFF, bar_empty = bar_full + STAGES * 8;
     const uint32_t bar_tfull = bar_empty + STAGES * 8, bar_tempty = bar_tfull + 2 * 8;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -551,26 +590,48 @@ k_score_tc2(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ 
         const int row = 32 * ew + lane;
         const uint32_t tempty_leader = map_to_rank(bar_tempty, 0);
         uint32_t acc = 0, acc_phase = 0;
+        // next unit's gate word / first-tile inv-norm and id prefetched as in the 1-CTA kernel
+        auto gate_of = [&](int uu) -> uint32_t {
+            const int64_t qq = (int64_t)(2 * (uu % m_pairs) + (int)rank) * BM + row;
+            return (!kDense && gk != nullptr && qq < B) ? *reinterpret_cast<volatile const uint32_t*>(gk + qq) : 0u;
+        };
+        float inv_next = 0.0f;
+        uint32_t id_next = 0u, gk_next = 0u;
+        if (cid < n_units) {
+            const int64_t c0 = (int64_t)(cid / m_pairs) * chunk_tiles * BN + et;
+            inv_next = __ldg(inv_e + c0);
+            id_next = kDense ? 0u : __ldg(ids + c0);
+            gk_next = gate_of(cid);
+        }
         for (int u = cid; u < n_units; u += n_clusters) {
             const int chunk = u / m_pairs, mp = u - chunk * m_pairs;
             const int n0 = chunk * chunk_tiles, n1 = min(n_tiles, n0 + chunk_tiles);
             const int64_t q = (int64_t)(2 * mp + (int)rank) * BM + row;
+            const int u_next = u + n_clusters;
+            const int unit_div = m_pairs;
             float* dense_row = (kDense && q < B) ? dense + q * dense_ld : nullptr;
             TopK<KMAX> tk;
             tk.init();
-            if (!kDense && gk != nullptr && q < B) {
-                const uint32_t g = *reinterpret_cast<volatile const uint32_t*>(gk + q);
-                if (g != 0u) tk.thr = key_to_f32((unsigned long long)g << 32);
-            }
+            if (gk_next != 0u) tk.thr = key_to_f32((unsigned long long)gk_next << 32);
             if (q >= B) tk.thr = INFINITY;
-            float inv_next = __ldg(inv_e + (int64_t)n0 * BN + et);
 #pragma unroll 1
             for (int n = n0; n < n1; ++n) {
                 const uint32_t ivb = inv_base + acc * BN * 4;
+                const uint32_t idb = ids_base + acc * BN * 4;
                 {
                     const float v = inv_next;
-                    if (n + 1 < n1) inv_next = __ldg(inv_e + (int64_t)(n + 1) * BN + et);
+                    const uint32_t idv = id_next;
+                    if (n + 1 < n1) {
+                        inv_next = __ldg(inv_e + (int64_t)(n + 1) * BN + et);
+                        if (!kDense) id_next = __ldg(ids + (int64_t)(n + 1) * BN + et);
+                    } else if (u_next < n_units) {   // this CTA's next unit
+                        const int64_t c0 = (int64_t)(u_next / unit_div) * chunk_tiles * BN + et;
+                        inv_next = __ldg(inv_e + c0);
+                        if (!kDense) id_next = __ldg(ids + c0);
+                        gk_next = gate_of(u_next);
+                    }
                     asm volatile("st.shared.f32 [%0], %1;" ::"r"(ivb + 4 * et), "f"(v) : "memory");
+                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(idb + 4 * et), "r"(idv) : "memory");
                 }
                 asm volatile("bar.sync 1, 256;" ::: "memory");
                 mbar_wait(bar_tfull + 8 * acc, acc_phase);
@@ -578,13 +639,14 @@ k_score_tc2(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ 
                 const uint32_t taddr = tmem_base + ((uint32_t)(32 * ew) << 16) + acc * BN + h * 128;
                 const uint32_t col_base = (uint32_t)(n * BN + h * 128);
                 const uint32_t ivh = ivb + 4 * (h * 128);
+                const uint32_t idh = idb + 4 * (h * 128);
                 uint32_t ra[32], rb[32];
                 tmem_ld32(taddr, ra);
                 tmem_ld_wait_regs(ra);
 #pragma unroll 1
                 for (int c = 0; c < 128; c += 64) {
                     tmem_ld32(taddr + c + 32, rb);
-                    epi_chunk<KMAX, kDense>(ra, ivh + 4 * c, col_base + c, tk, ids, dense_row);
+                    epi_chunk<KMAX, kDense>(ra, ivh + 4 * c, col_base + c, tk, idh + 4 * c, dense_row);
                     tmem_ld_wait_regs(rb);
                     if (c + 64 < 128) tmem_ld32(taddr + c + 64, ra);
                     else {
@@ -595,7 +657,7 @@ k_score_tc2(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ 
                             else mbar_arrive_cluster(tempty_leader + 8 * acc);
                         }
                     }
-                    epi_chunk<KMAX, kDense>(rb, ivh + 4 * (c + 32), col_base + c + 32, tk, ids, dense_row);
+                    epi_chunk<KMAX, kDense>(rb, ivh + 4 * (c + 32), col_base + c + 32, tk, idh + 4 * (c + 32), dense_row);
                     if (c + 64 < 128) tmem_ld_wait_regs(ra);
                 }
                 acc ^= 1;
