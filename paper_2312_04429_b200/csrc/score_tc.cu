@@ -176,12 +176,28 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], uint32_t inv_
                 *reinterpret_cast<float4*>(dense_row + col0 + i) = make_float4(t[i], t[i + 1], t[i + 2], t[i + 3]);
         }
     } else if (mx >= tk.thr) {
+        if constexpr (KMAX == 1) {
+            // top-1: the chunk's best key is (mx, smallest id among the values equal to mx) --
+            // one offer instead of a dependent chain of up to 32 (early tiles, where the row's
+            // threshold is still low, used to hold the accumulator for 3-10 K cycles)
+            uint32_t best_id = 0xFFFFFFFFu, best_i = 0u;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-            if (!(t[i] >= tk.thr)) continue;   // also rejects NaN (empty slots)
-            uint32_t id;
-            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(id) : "r"(ids_addr + 4 * i));
-            tk.offer_key(make_key(t[i], id), col0 + i);
+            for (int i = 0; i < 32; ++i) {
+                if (t[i] == mx) {
+                    uint32_t id;
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(id) : "r"(ids_addr + 4 * i));
+                    if (id < best_id) { best_id = id; best_i = (uint32_t)i; }
+                }
+            }
+            tk.offer_key(make_key(mx, best_id), col0 + best_i);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                if (!(t[i] >= tk.thr)) continue;   // also rejects NaN (empty slots)
+                uint32_t id;
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(id) : "r"(ids_addr + 4 * i));
+                tk.offer_key(make_key(t[i], id), col0 + i);
+            }
         }
     }
 }
