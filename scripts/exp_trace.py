@@ -1,5 +1,9 @@
 """Experiment driver (not product): run the C2 lookup with a traced build of the scan and print
-per-tile epilogue hold times and MMA accumulator waits of cluster 0 (exp_get_trace)."""
+per-tile epilogue hold times and MMA accumulator waits of cluster 0 (exp_get_trace).
+
+The traced build: `git apply scripts/exp_trace_instrumentation.diff` (clock64 stamps in the
+CTA-pair kernel + an exp_get_trace export), `python -m paper_2312_04429_b200.build --force`,
+run this on the GPU, then `git apply -R` and rebuild.  Results: profiles/r01_epilogue_trace.txt."""
 import ctypes
 
 import numpy as np
