@@ -132,6 +132,7 @@ template <typename Tin, int NS>
 __global__ void __launch_bounds__(256) k_normalise(const Tin* __restrict__ x, int64_t n,
                                                    __nv_bfloat16* __restrict__ y, float* __restrict__ inv,
                                                    int32_t* __restrict__ status, uint32_t* __restrict__ gk) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // let the scan's prologue start
     const int lane = threadIdx.x & 31;
     const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     if (r >= n) return;   // warp-uniform
@@ -396,6 +397,8 @@ k_finalize(const Rec* __restrict__ ws, int parts, int64_t B, int topk, const flo
     __shared__ unsigned long long s_keys[kFinQ][KMAX];
     __shared__ uint32_t s_slots[kFinQ][KMAX];
     __shared__ long long s_src[kFinQ];
+    // launched with programmatic serialization behind the scan: wait for its records
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t b0 = (int64_t)blockIdx.x * kFinQ;
     const int64_t b = b0 + warp;
@@ -487,11 +490,19 @@ void launch_finalize(int kmax, const Rec* ws, int parts, int64_t B, int topk, co
                      uint8_t* latent_out, void** out_ptr, int32_t* out_status, cudaStream_t s) {
     if (B <= 0) return;
     const unsigned grid = (unsigned)((B + kFinQ - 1) / kFinQ);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
 #define NV_FIN(KM)                                                                                \
-    k_finalize<KM><<<grid, 256, 0, s>>>(ws, parts, B, topk, inv_q, qstatus, ids, present,         \
-                                        lslot, fcnt, lastacc, clock, pool, latent_bytes,          \
-                                        km, out_ids, out_scores, out_k, latent_out, out_ptr,      \
-                                        out_status)
+    cudaLaunchKernelEx(&cfg, k_finalize<KM>, ws, parts, B, topk, inv_q, qstatus, ids, present,    \
+                       lslot, fcnt, lastacc, clock, pool, latent_bytes, km, out_ids, out_scores,  \
+                       out_k, latent_out, out_ptr, out_status)
     if (kmax == 1) NV_FIN(1);
     else if (kmax == 4) NV_FIN(4);
     else NV_FIN(16);

@@ -78,6 +78,12 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
         : "memory");
 }
 
+// Programmatic dependent launch: the scan is launched while the ingest kernel is still running
+// (its prologue -- barrier init, TMEM allocation, tensor-map prefetch -- overlaps it) and waits
+// here for the ingest's results; it lets the finalize kernel launch early in turn.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // One lane of a converged warp (elect.sync): the rest of the warp stays in uniform control flow.
 __device__ __forceinline__ bool elect_one() {
     uint32_t e;
@@ -247,6 +253,8 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ C
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    pdl_wait();      // queries / inv-norms / gate words of the ingest kernel are visible from here
+    pdl_trigger();
 
     if (warp == 0) {
         // ------------------------------- TMA producer -------------------------------
@@ -542,6 +550,8 @@ k_score_tc2(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ 
     cluster_sync_all();   // peer barriers initialised, TMEM allocated in both CTAs
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    pdl_wait();      // queries / inv-norms / gate words of the ingest kernel are visible from here
+    pdl_trigger();
 
     if (warp == 0) {
         // ------------------------------- TMA producer (both CTAs) ---------------------
@@ -737,13 +747,15 @@ static bool launch_pair(const TcPlan& p, const CUtensorMap* tq, const CUtensorMa
     cfg.blockDim = dim3(NUM_THREADS_TC);
     cfg.dynamicSmemBytes = pair::SMEM_BYTES;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     const CUtensorMap q = *tq, e = *te;
     if (cudaLaunchKernelEx(&cfg, kern, q, e, inv_e, ids, dim, b, p.m_tiles, p.n_tiles, p.chunk_tiles, n_units,
                            ws, gk, dense, dense_ld) != cudaSuccess)
@@ -763,8 +775,20 @@ static bool launch(const TcPlan& p, const CUtensorMap* tq, const CUtensorMap* te
         attr_set = true;
     }
     const int n_units = p.n_chunks * p.m_tiles;
-    kern<<<p.grid, NUM_THREADS_TC, SMEM_BYTES, s>>>(*tq, *te, inv_e, ids, dim, b, p.m_tiles, p.n_tiles,
-                                                 p.chunk_tiles, n_units, ws, gk, dense, dense_ld);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)p.grid);
+    cfg.blockDim = dim3(NUM_THREADS_TC);
+    cfg.dynamicSmemBytes = SMEM_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const CUtensorMap q = *tq, e = *te;
+    if (cudaLaunchKernelEx(&cfg, kern, q, e, inv_e, ids, dim, b, p.m_tiles, p.n_tiles, p.chunk_tiles, n_units, ws,
+                           gk, dense, dense_ld) != cudaSuccess)
+        return false;
     return cudaPeekAtLastError() == cudaSuccess;
 }
 
