@@ -79,15 +79,16 @@ __device__ __forceinline__ void normalise_row(const Tin* __restrict__ xr, int la
                                               int64_t orow) {
     constexpr int dim = NS * 32;
     const int64_t ybase = orow * (int64_t)dim;
-    float xf[NS];
+    // the inputs are not kept across the two phases (re-read from L1 in phase 2): the 24 fp64
+    // squares + 24 fp32 inputs held 92 registers per thread and limited the kernel to 25%
+    // occupancy (latency-bound, ncu r1ai)
     double v[NS];
     int bad = 0;
 #pragma unroll
-    for (int k = 0; k < NS; ++k) xf[k] = load_in<Tin>(xr + lane + 32 * k);
-#pragma unroll
     for (int k = 0; k < NS; ++k) {
-        const double xv = (double)xf[k];
-        bad |= !isfinite(xf[k]);
+        const float xk = load_in<Tin>(xr + lane + 32 * k);
+        const double xv = (double)xk;
+        bad |= !isfinite(xk);
         v[k] = __dmul_rn(xv, xv);
     }
     bad = __any_sync(0xFFFFFFFFu, bad);
@@ -111,7 +112,7 @@ __device__ __forceinline__ void normalise_row(const Tin* __restrict__ xr, int la
     const double rnu = __drcp_rn(nu);
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
-        const double x = (double)xf[k];
+        const double x = (double)load_in<Tin>(xr + lane + 32 * k);
         double y = __dmul_rn(x, rnu);
         const long long low = (long long)((unsigned long long)__double_as_longlong(y) & ((1ull << 45) - 1));
         const long long dm = low - (1ll << 44);
@@ -129,7 +130,7 @@ __device__ __forceinline__ void normalise_row(const Tin* __restrict__ xr, int la
 }
 
 template <typename Tin, int NS>
-__global__ void __launch_bounds__(256) k_normalise(const Tin* __restrict__ x, int64_t n,
+__global__ void __launch_bounds__(256, 4) k_normalise(const Tin* __restrict__ x, int64_t n,
                                                    __nv_bfloat16* __restrict__ y, float* __restrict__ inv,
                                                    int32_t* __restrict__ status, uint32_t* __restrict__ gk) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // let the scan's prologue start
