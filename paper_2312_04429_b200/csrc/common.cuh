@@ -77,7 +77,7 @@ struct TopK {
             else if (key > k[i]) { k[i] = key; s[i] = slot; }
         }
         if (key > k[0]) { k[0] = key; s[0] = slot; }
-        if (k[KMAX - 1] != 0ull) thr = key_to_f32(k[KMAX - 1]);
+        if (k[KMAX - 1] != 0ull) thr = fmaxf(thr, key_to_f32(k[KMAX - 1]));   // thr may carry an outside bound
     }
     // Offer scan value t of entry slot `slot`; the id is loaded only when t can enter.
     __device__ __forceinline__ void offer(float t, uint32_t slot, const uint32_t* __restrict__ ids) {

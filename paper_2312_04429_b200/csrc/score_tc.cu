@@ -197,12 +197,24 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], uint32_t inv_
             }
             tk.offer_key(make_key(mx, best_id), col0 + best_i);
         } else {
+            // k > 1: a mask of the values passing the gate, then one compact loop over its set
+            // bits (the value picked from registers by a constant-index select chain).  Fully
+            // unrolling 32 inlined KMAX-slot insertions per chunk (x2 call sites x2 halves) blew
+            // the instruction cache: the C2 top-16 scan took 7 ms.
+            uint32_t mask = 0u;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                if (!(t[i] >= tk.thr)) continue;   // also rejects NaN (empty slots)
+            for (int i = 0; i < 32; ++i) mask |= (t[i] >= tk.thr ? 1u : 0u) << i;   // NaN fails
+#pragma unroll 1
+            while (mask) {
+                const int i = __ffs(mask) - 1;
+                mask &= mask - 1u;
+                float ti = t[0];
+#pragma unroll
+                for (int j = 1; j < 32; ++j) ti = (i == j) ? t[j] : ti;
+                if (!(ti >= tk.thr)) continue;   // the gate may have risen since the mask
                 uint32_t id;
                 asm volatile("ld.shared.u32 %0, [%1];" : "=r"(id) : "r"(ids_addr + 4 * i));
-                tk.offer_key(make_key(t[i], id), col0 + i);
+                tk.offer_key(make_key(ti, id), col0 + (uint32_t)i);
             }
         }
     }
@@ -347,6 +359,14 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ C
             // t >= it, so nothing that can reach the final top-k is ever gated out; a value
             // read a tile early is merely a weaker bound).
             if (gk_next != 0u) tk.thr = key_to_f32((unsigned long long)gk_next << 32);
+            // shared gate: every unit scanning query q publishes its running k-th best t into
+            // gk[q] after each tile and raises its own gate to gk[q] one tile later -- each is a
+            // lower bound on q's final k-th best, so nothing that can reach the final top-k is
+            // gated out.  Without it the concurrent first-wave units each started from -inf and,
+            // for k > 1, inserted most of their early values one by one while holding the TMEM
+            // accumulator (C2 top-16 scan 7.0 ms vs 0.37 ms for top-1).
+            const bool share = !kDense && gk != nullptr && q < B;
+            uint32_t g_known = gk_next;
             if (q >= B) tk.thr = INFINITY;   // padding rows of the last query tile: never offer
 #pragma unroll 1
             for (int n = n0; n < n1; ++n) {
@@ -354,6 +374,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ C
                 // the next tile's values are fetched now so their L2 latency hides behind this tile
                 const uint32_t ivb = inv_base + acc * BN * 4;
                 const uint32_t idb = ids_base + acc * BN * 4;
+                const uint32_t g_now = share ? *reinterpret_cast<volatile const uint32_t*>(gk + q) : 0u;  // used after this tile
                 {
                     const float v = inv_next;
                     const uint32_t idv = id_next;
@@ -393,6 +414,16 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ C
                     epi_chunk<KMAX, kDense>(rb, ivh + 4 * (c + 32), col_base + c + 32, tk, idh + 4 * (c + 32), dense_row);
                     if (c + 64 < 128) tmem_ld_wait_regs(ra);
                 }
+                if (share) {
+                    if (tk.k[KMAX - 1] != 0ull) {
+                        const uint32_t mine = (uint32_t)(tk.k[KMAX - 1] >> 32);
+                        if (mine > g_known) { atomicMax(gk + q, mine); g_known = mine; }
+                    }
+                    if (g_now > g_known) {
+                        g_known = g_now;
+                        tk.thr = fmaxf(tk.thr, key_to_f32((unsigned long long)g_now << 32));
+                    }
+                }
                 acc ^= 1;
                 if (acc == 0) acc_phase ^= 1;
             }
@@ -407,7 +438,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ C
                 }
                 asm volatile("bar.sync 2, 256;" ::: "memory");
                 if (h == 0) {
-#pragma unroll
+#pragma unroll 1
                     for (int i = 0; i < KMAX; ++i)
                         if (mk[row * KMAX + i]) tk.offer_key(mk[row * KMAX + i], ms[row * KMAX + i]);
                     if (q < B) {
@@ -639,11 +670,20 @@ k_score_tc2(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ 
             TopK<KMAX> tk;
             tk.init();
             if (gk_next != 0u) tk.thr = key_to_f32((unsigned long long)gk_next << 32);
+            // shared gate: every unit scanning query q publishes its running k-th best t into
+            // gk[q] after each tile and raises its own gate to gk[q] one tile later -- each is a
+            // lower bound on q's final k-th best, so nothing that can reach the final top-k is
+            // gated out.  Without it the concurrent first-wave units each started from -inf and,
+            // for k > 1, inserted most of their early values one by one while holding the TMEM
+            // accumulator (C2 top-16 scan 7.0 ms vs 0.37 ms for top-1).
+            const bool share = !kDense && gk != nullptr && q < B;
+            uint32_t g_known = gk_next;
             if (q >= B) tk.thr = INFINITY;
 #pragma unroll 1
             for (int n = n0; n < n1; ++n) {
                 const uint32_t ivb = inv_base + acc * BN * 4;
                 const uint32_t idb = ids_base + acc * BN * 4;
+                const uint32_t g_now = share ? *reinterpret_cast<volatile const uint32_t*>(gk + q) : 0u;  // used after this tile
                 {
                     const float v = inv_next;
                     const uint32_t idv = id_next;
@@ -686,6 +726,16 @@ k_score_tc2(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ 
                     epi_chunk<KMAX, kDense>(rb, ivh + 4 * (c + 32), col_base + c + 32, tk, idh + 4 * (c + 32), dense_row);
                     if (c + 64 < 128) tmem_ld_wait_regs(ra);
                 }
+                if (share) {
+                    if (tk.k[KMAX - 1] != 0ull) {
+                        const uint32_t mine = (uint32_t)(tk.k[KMAX - 1] >> 32);
+                        if (mine > g_known) { atomicMax(gk + q, mine); g_known = mine; }
+                    }
+                    if (g_now > g_known) {
+                        g_known = g_now;
+                        tk.thr = fmaxf(tk.thr, key_to_f32((unsigned long long)g_now << 32));
+                    }
+                }
                 acc ^= 1;
                 if (acc == 0) acc_phase ^= 1;
             }
@@ -698,7 +748,7 @@ k_score_tc2(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ 
                 }
                 asm volatile("bar.sync 2, 256;" ::: "memory");
                 if (h == 0) {
-#pragma unroll
+#pragma unroll 1
                     for (int i = 0; i < KMAX; ++i)
                         if (mk[row * KMAX + i]) tk.offer_key(mk[row * KMAX + i], ms[row * KMAX + i]);
                     if (q < B) {

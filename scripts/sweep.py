@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--batches", default="1,2,4,8,16,32,64,128,256,512,1024,4096")
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--scorers", default="stream,tc")
+    ap.add_argument("--topks", default="1", help="comma list of topk values (fused top-k width)")
     a = ap.parse_args()
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     n, L = a.n, 32768 if a.latents else 0
@@ -43,24 +44,24 @@ def main():
     qall, _, _ = synth.queries(emb, cl, bmax, seed=1001)
     for scorer in a.scorers.split(","):
         g.set_scorer(B.SCORER_STREAM if scorer == "stream" else B.SCORER_TC)
-        for b in [int(x) for x in a.batches.split(",")]:
+        for b, topk in [(int(x), int(k)) for x in a.batches.split(",") for k in a.topks.split(",")]:
             if scorer == "stream" and b > 64:
                 continue
             q = torch.from_numpy(qall[:b]).cuda()
-            out = g.alloc_outputs(b, 1, latents=bool(L))
+            out = g.alloc_outputs(b, topk, latents=bool(L))
             for _ in range(3):
-                g.query_into(q, out)
+                g.query_into(q, out, topk=topk)
             st, sc, fi = [], [], []
             for _ in range(a.steps):
                 flush.fill_(1.0)
-                g.query_into(q, out)
+                g.query_into(q, out, topk=topk)
                 ev[3].synchronize()
                 st.append(ev[0].elapsed_time(ev[3]))
                 sc.append(ev[1].elapsed_time(ev[2]))
                 fi.append(ev[2].elapsed_time(ev[3]))
             ms = statistics.median(st)
             scm = statistics.median(sc)
-            rec = dict(scorer=scorer, n=n, b=b, step_ms=ms, score_ms=scm, finalize_ms=statistics.median(fi),
+            rec = dict(scorer=scorer, n=n, b=b, topk=topk, step_ms=ms, score_ms=scm, finalize_ms=statistics.median(fi),
                        lookups_per_s=b / (ms / 1e3),
                        score_hbm_frac=n * 1540 / (scm / 1e3) / 1e9 / peaks["hbm_gbs"],
                        score_tensor_frac=2 * b * n * 768 / (scm / 1e3) / 1e12 / peaks["bf16_tflops"])
