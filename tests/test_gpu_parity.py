@@ -294,3 +294,41 @@ def test_aliased_latent_pool(B, oracle_mod):
     assert np.array_equal(ev, oev) and np.array_equal(d, od)
     with pytest.raises(B.CacheError):
         g.insert(torch.from_numpy(emb[:2]).cuda(), torch.zeros((2, 5, L2), dtype=torch.uint8, device="cuda"))
+
+
+def test_full_size_sampled_parity_c3(B, oracle_mod):
+    """C3's shape: 1M entries, B = 32 (the HBM-bound single-CTA scan, hundreds of partial lists
+    per query to merge), top-4; 8 sampled queries against the oracle's exact fp64 scan of all
+    1M entries, and the batch-wide properties for every query."""
+    n, b = 1_000_000, 32
+    emb, cl = synth.entries(n, seed=3001)
+    g = B.NirvanaCache(entry_capacity=n, dim=768, latent_bytes=0, latent_capacity=5 * n)
+    for s in range(0, n, 65536):
+        g.insert(torch.from_numpy(emb[s:s + 65536]).cuda())
+    q, _, _ = synth.queries(emb, cl, b, seed=3002)
+    out = gpu_to_numpy(g.query(torch.from_numpy(q).cuda(), topk=4, latents=False))
+    assert (np.diff(out["scores"], axis=1) <= 0).all()                 # best first
+    assert (out["ids"] < n).all() and (out["status"] == 0).all()
+    o = oracle_mod.OracleCache(dim=768, entry_capacity=n, latent_bytes=0)
+    o.insert(emb)
+    del emb
+    rows = list(np.random.default_rng(4).choice(b, 8, replace=False))
+    rep = check_batch(out, o, q, 4, rows=rows, adopt=False)
+    assert rep["max_dscore"] < 1e-4
+
+
+def test_large_batch_pair_kernel(B, oracle_mod):
+    """16,384 queries (the C4 global batch) on 100K entries: 64 CTA-pair query tiles; sampled
+    oracle parity plus the batch-wide properties."""
+    n, b = 100_000, 16384
+    emb, cl = synth.entries(n, seed=5001)
+    g = B.NirvanaCache(entry_capacity=n, dim=768, latent_bytes=0, latent_capacity=5 * n)
+    g.insert(torch.from_numpy(emb).cuda())
+    q, _, _ = synth.queries(emb, cl, b, seed=5002)
+    out = gpu_to_numpy(g.query(torch.from_numpy(q).cuda(), topk=1, latents=False))
+    assert (out["ids"][:, 0] < n).all()
+    o = oracle_mod.OracleCache(dim=768, entry_capacity=n, latent_bytes=0)
+    o.insert(emb)
+    rows = list(np.random.default_rng(5).choice(b, 32, replace=False)) + [0, b - 1]
+    rep = check_batch(out, o, q, 1, rows=rows, adopt=False)
+    assert rep["max_dscore"] < 1e-4
