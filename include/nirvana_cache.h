@@ -321,6 +321,20 @@ cache_status cache_push_merge(cache_t *c, int64_t nb, int32_t topk, uint64_t *ou
                               int32_t *out_k, void *latent_out, void **out_latent_ptr, int32_t *row_status,
                               void *stream);
 
+/* Fused distributed eviction (the radix-select histograms of cache_evict_hist / _pick without
+ * a collective): pass p's histogram kernel adds its counts straight into EVERY rank's arena
+ * accumulator (P2P atomics over NVLink) and publishes a per-pass epoch flag; the pick waits
+ * for all ranks' flags, reads the complete global histogram from its own arena and fixes the
+ * pass's digit (identically on every rank).  Collective: every rank calls, with the same n,
+ *   for p in 0..7: cache_push_evict_hist(c, n, p); cache_push_evict_pick(c, p);
+ *   then cache_push_evict_apply(c, n, ...)  (outputs as cache_evict_apply, capacity n)
+ * (virtual ranks in one process: hist(p) on all ranks, then pick(p) on all ranks).  The
+ * selection state lives in the cache.  Needs cache_push_reserve on every rank (the arena). */
+cache_status cache_push_evict_hist(cache_t *c, int64_t n, int32_t pass, void *stream);
+cache_status cache_push_evict_pick(cache_t *c, int32_t pass, void *stream);
+cache_status cache_push_evict_apply(cache_t *c, int64_t n, uint64_t *out_evicted, int64_t *out_n,
+                                    uint64_t *out_dirty_ids, int64_t *out_n_dirty, void *stream);
+
 /* ---- match predictor ----
  * A linear one-class SVM f(x) = <w, x> - rho over the cached embeddings (unit-scaled stored
  * values), "trained by utilizing all prompt embeddings stored in the VDB" with

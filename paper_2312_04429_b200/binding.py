@@ -79,7 +79,8 @@ EXPORTS = ("cache_default_config", "cache_create", "cache_destroy", "cache_inser
            "cache_query_merge", "cache_export_peer", "cache_attach_peers", "cache_pool_write",
            "cache_set_evict_policy", "cache_predictor_train", "cache_predict", "cache_predictor_get",
            "cache_set_evict_granularity", "cache_live_entries", "cache_push_reserve", "cache_push_queries",
-           "cache_push_scan", "cache_push_merge")
+           "cache_push_scan", "cache_push_merge", "cache_push_evict_hist", "cache_push_evict_pick",
+           "cache_push_evict_apply")
 
 
 def load_library(path: str = LIB_PATH):
@@ -113,6 +114,9 @@ def load_library(path: str = LIB_PATH):
     L.cache_push_queries.argtypes = [P, I64, P, I32, P]
     L.cache_push_scan.argtypes = [P, I64, I32, P]
     L.cache_push_merge.argtypes = [P, I64, I32, P, P, P, P, P, P, P]
+    L.cache_push_evict_hist.argtypes = [P, I64, I32, P]
+    L.cache_push_evict_pick.argtypes = [P, I32, P]
+    L.cache_push_evict_apply.argtypes = [P, I64, P, P, P, P, P]
     L.cache_set_evict_granularity.argtypes = [P, I32]
     L.cache_set_evict_granularity.restype = ctypes.c_int
     L.cache_query_local.argtypes = [P, I64, P, I32, I32, P, P]
@@ -367,6 +371,20 @@ class NirvanaCache:
                                      _ptr(out.get("latents")), _ptr(out.get("ptrs")), _ptr(out.get("status")),
                                      _stream(stream)))
         return out
+
+    def push_evict_hist(self, n: int, pass_: int, stream=None):
+        _check(_lib.cache_push_evict_hist(self._h, n, pass_, _stream(stream)))
+
+    def push_evict_pick(self, pass_: int, stream=None):
+        _check(_lib.cache_push_evict_pick(self._h, pass_, _stream(stream)))
+
+    def push_evict_apply(self, n: int, stream=None):
+        ev = np.empty(max(n, 1), dtype=np.uint64)
+        dirty = np.empty(max(n, 1), dtype=np.uint64)
+        cnt = np.zeros(1, dtype=np.int64)
+        nd = np.zeros(1, dtype=np.int64)
+        _check(_lib.cache_push_evict_apply(self._h, n, _ptr(ev), _ptr(cnt), _ptr(dirty), _ptr(nd), _stream(stream)))
+        return ev[: int(cnt[0])].copy(), dirty[: int(nd[0])].copy()
 
     def export_peer(self) -> PeerDesc:
         d = PeerDesc()

@@ -25,7 +25,7 @@ thread_local std::string g_err = "no error";
 // offsets from the descriptor): flags | CTA counters | inv-norms | statuses | record inbox |
 // bf16 query rows (rows padded to a multiple of 128 for the scan's TMA boxes).
 struct ArenaLayout {
-    size_t qflag, rflag, done, invq, qstat, inbox, qg, total;
+    size_t qflag, rflag, done, eflag, invq, qstat, inbox, qg, ehist, total;
     int64_t rows;   // padded global rows
 };
 ArenaLayout arena_layout(int world, int64_t max_nb, int topk, int dim) {
@@ -34,12 +34,14 @@ ArenaLayout arena_layout(int world, int64_t max_nb, int topk, int dim) {
     L.rows = std::max<int64_t>(128, ((int64_t)world * max_nb + 127) / 128 * 128);
     L.qflag = 0;                          // u32[kMaxWorld]: query flag per sender
     L.rflag = 64;                         // u32[kMaxWorld]: record flag per sender
-    L.done = 128;                         // u32[2]: CTA counters of the two push kernels
+    L.done = 128;                         // u32[4]: CTA counters of the push kernels
+    L.eflag = 256;                        // u32[8 passes][kMaxWorld]: eviction histogram flags
     size_t off = 1024;
     L.invq = off;  off = al(off + (size_t)L.rows * 4);
     L.qstat = off; off = al(off + (size_t)L.rows * 4);
     L.inbox = off; off = al(off + (size_t)world * max_nb * topk * sizeof(cache_shard_rec));
     L.qg = off;    off = al(off + (size_t)L.rows * dim * 2);
+    L.ehist = off; off = al(off + 8 * 256 * 4);   // global eviction histogram per radix pass
     L.total = off;
     return L;
 }
@@ -218,6 +220,8 @@ struct cache_t {
     uint32_t push_epoch = 0;
     int64_t push_nb = -1;
     int push_phase = 0;              // last phase run (1..3), for call-order checks
+    uint32_t evict_epoch = 0;        // fused distributed evictions so far
+    int evict_pass = -1;             // last pass whose pick ran (-1: none / done)
 };
 
 extern "C" {
@@ -790,6 +794,8 @@ cache_status cache_push_reserve(cache_t* c, int64_t max_nb, int32_t max_topk) {
     c->arena_topk = max_topk;
     c->push_epoch = 0;
     c->push_phase = 0;
+    c->evict_epoch = 0;
+    c->evict_pass = -1;
     return CACHE_OK;
 }
 
@@ -800,6 +806,57 @@ static PushSignal push_signal_of(cache_t* c, size_t flag_off, int counter) {
     sg.done = (uint32_t*)(c->arena + arena_layout(c->world, c->arena_nb, c->arena_topk, c->dim).done) + counter;
     sg.epoch = c->push_epoch;
     return sg;
+}
+
+// ---- fused distributed eviction selection (histograms over peer memory) ----
+cache_status cache_push_evict_hist(cache_t* c, int64_t n, int32_t pass, void* stream) {
+    if (!c) return fail(CACHE_E_INVALID_ARG, "cache_push_evict_hist: null cache");
+    if (!c->push_ok) return fail(CACHE_E_STATE, "cache_push_evict_hist: no push arenas");
+    if (pass < 0 || pass > 7 || (pass == 0 && n < 0)) return fail(CACHE_E_INVALID_ARG, "cache_push_evict_hist: bad pass / n");
+    if (pass != c->evict_pass + 1) return fail(CACHE_E_STATE, "cache_push_evict_hist: passes out of order");
+    DeviceGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const ArenaLayout L = arena_layout(c->world, c->arena_nb, c->arena_topk, c->dim);
+    if (pass == 0) {
+        CK(c->est.ensure(1));
+        EvictState st0{0ull, 0ull, (unsigned long long)n};
+        CK(cudaMemcpyAsync(c->est.p, &st0, sizeof(st0), cudaMemcpyHostToDevice, s));
+        c->evict_epoch++;
+    }
+    PushHist ph{};
+    for (int r = 0; r < c->world; ++r) ph.dst[r] = (unsigned int*)(c->peer_arena[r] + L.ehist) + 256 * pass;
+    ph.world = c->world;
+    PushSignal sig = push_signal_of(c, L.eflag + (size_t)pass * kMaxWorld * 4, 2);
+    sig.epoch = c->evict_epoch;
+    launch_evict_hist_push(c->present, c->fcnt, c->lastacc, c->ids, c->hwm, c->km, c->est.p, pass, ph, sig, s);
+    c->launches++;
+    CK(cudaGetLastError());
+    return CACHE_OK;
+}
+
+cache_status cache_push_evict_pick(cache_t* c, int32_t pass, void* stream) {
+    if (!c) return fail(CACHE_E_INVALID_ARG, "cache_push_evict_pick: null cache");
+    if (!c->push_ok || pass != c->evict_pass + 1 || pass > 7)
+        return fail(CACHE_E_STATE, "cache_push_evict_pick: call after cache_push_evict_hist of the same pass");
+    DeviceGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const ArenaLayout L = arena_layout(c->world, c->arena_nb, c->arena_topk, c->dim);
+    launch_wait_flags((const uint32_t*)(c->arena + L.eflag + (size_t)pass * kMaxWorld * 4), c->world, c->evict_epoch, s);
+    // the complete global histogram is in this rank's own arena; the pick zeroes it after use
+    launch_evict_pick((unsigned int*)(c->arena + L.ehist) + 256 * pass, c->est.p, pass, s);
+    c->launches += 2;
+    c->evict_pass = pass;
+    CK(cudaGetLastError());
+    return CACHE_OK;
+}
+
+cache_status cache_push_evict_apply(cache_t* c, int64_t n, uint64_t* out_evicted, int64_t* out_n,
+                                    uint64_t* out_dirty_ids, int64_t* out_n_dirty, void* stream) {
+    if (!c) return fail(CACHE_E_INVALID_ARG, "cache_push_evict_apply: null cache");
+    if (c->evict_pass != 7) return fail(CACHE_E_STATE, "cache_push_evict_apply: the 8 passes have not run");
+    c->evict_pass = -1;
+    return cache_evict_apply(c, reinterpret_cast<const cache_evict_state*>(c->est.p), n, out_evicted, out_n,
+                             out_dirty_ids, out_n_dirty, stream);
 }
 
 cache_status cache_push_queries(cache_t* c, int64_t nb, const void* queries, int32_t q_dtype, void* stream) {

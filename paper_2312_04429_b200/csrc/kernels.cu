@@ -626,7 +626,8 @@ template <int POLICY, int GRAN>
 __global__ void __launch_bounds__(256)
 k_evict_hist(const uint32_t* __restrict__ present, const uint32_t* __restrict__ fcnt,
              const uint32_t* __restrict__ lastacc, const uint32_t* __restrict__ ids, int64_t n_slots, KMap km,
-             const EvictState* __restrict__ st, int shift, unsigned int* __restrict__ hist) {
+             const EvictState* __restrict__ st, int shift, unsigned int* __restrict__ hist, PushHist ph,
+             PushSignal sig) {
     __shared__ unsigned int sh[256];
     sh[threadIdx.x] = 0;
     __syncthreads();
@@ -656,7 +657,13 @@ k_evict_hist(const uint32_t* __restrict__ present, const uint32_t* __restrict__ 
     }
     run.flush(sh);
     __syncthreads();
-    if (sh[threadIdx.x]) atomicAdd(&hist[threadIdx.x], sh[threadIdx.x]);
+    if (ph.world == 0) {
+        if (sh[threadIdx.x]) atomicAdd(&hist[threadIdx.x], sh[threadIdx.x]);
+    } else {   // fused all-reduce: add into every rank's accumulator, then publish the pass
+        if (sh[threadIdx.x])
+            for (int r = 0; r < ph.world; ++r) atomicAdd(ph.dst[r] + threadIdx.x, sh[threadIdx.x]);
+        push_signal(sig);
+    }
 }
 
 __global__ void k_evict_pick(unsigned int* __restrict__ hist, EvictState* __restrict__ st, int shift) {
@@ -795,10 +802,25 @@ void launch_evict_hist(const uint32_t* present, const uint32_t* fcnt, const uint
     do {                                                                                               \
         static const int wave = one_wave(k_evict_hist<P, G>);                                          \
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(wave, (n_slots + 255) / 256));   \
-        k_evict_hist<P, G><<<grid, 256, 0, s>>>(present, fcnt, lastacc, ids, n_slots, km, st, 56 - 8 * pass, hist); \
+        k_evict_hist<P, G><<<grid, 256, 0, s>>>(present, fcnt, lastacc, ids, n_slots, km, st, 56 - 8 * pass, hist, \
+                                                PushHist{}, PushSignal{});                             \
     } while (0)
     NV_EVICT_DISPATCH(NV_HIST);
 #undef NV_HIST
+}
+
+void launch_evict_hist_push(const uint32_t* present, const uint32_t* fcnt, const uint32_t* lastacc,
+                            const uint32_t* ids, int64_t n_slots, const KMap& km, const EvictState* st, int pass,
+                            const PushHist& ph, const PushSignal& sig, cudaStream_t s) {
+#define NV_HISTP(P, G)                                                                                 \
+    do {                                                                                               \
+        static const int wave = one_wave(k_evict_hist<P, G>);                                          \
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(wave, (n_slots + 255) / 256));   \
+        k_evict_hist<P, G><<<grid, 256, 0, s>>>(present, fcnt, lastacc, ids, n_slots, km, st, 56 - 8 * pass,  \
+                                                nullptr, ph, sig);                                     \
+    } while (0)
+    NV_EVICT_DISPATCH(NV_HISTP);
+#undef NV_HISTP
 }
 
 void launch_evict_pick(unsigned int* hist, EvictState* st, int pass, cudaStream_t s) {

@@ -138,5 +138,14 @@ void launch_local_merge_push(int kmax, const Rec* ws, int parts, int64_t B, int 
                              const uint32_t* present, int owner, const PushRecs& dst, const PushSignal& sig,
                              cudaStream_t s);
 void launch_wait_flags(const uint32_t* flags, int world, uint32_t epoch, cudaStream_t s);
+// Eviction histogram pass whose counts go straight into every rank's accumulator (P2P
+// atomics) instead of a local buffer for an all-reduce; the grid then publishes `sig`.
+struct PushHist {
+    unsigned int* dst[kMaxWorld];
+    int world;
+};
+void launch_evict_hist_push(const uint32_t* present, const uint32_t* fcnt, const uint32_t* lastacc,
+                            const uint32_t* ids, int64_t n_slots, const KMap& km, const EvictState* st, int pass,
+                            const PushHist& ph, const PushSignal& sig, cudaStream_t s);
 
 }  // namespace nv

@@ -150,10 +150,16 @@ class ShardedCache:
                                                      device="cuda")).item()
         if n > live:
             raise B.CacheError(B.E_EVICT_RANGE, "sharded evict: n exceeds live items / entries")
-        st = torch.tensor([0, 0, n], dtype=torch.int64, device="cuda")
-        hist = torch.zeros(256, dtype=torch.int32, device="cuda")
-        evict_protocol(self.comm, n, st, hist, self.cache.evict_hist, self.cache.evict_pick)
-        ev, dirty = self.cache.evict_apply(st, n)
+        if self.push:   # histograms reduced over peer memory by the kernels themselves
+            for p in range(8):
+                self.cache.push_evict_hist(n, p)
+                self.cache.push_evict_pick(p)
+            ev, dirty = self.cache.push_evict_apply(n)
+        else:
+            st = torch.tensor([0, 0, n], dtype=torch.int64, device="cuda")
+            hist = torch.zeros(256, dtype=torch.int32, device="cuda")
+            evict_protocol(self.comm, n, st, hist, self.cache.evict_hist, self.cache.evict_pick)
+            ev, dirty = self.cache.evict_apply(st, n)
         evs = self.comm.all_gather_object(ev.tolist())
         dts = self.comm.all_gather_object(dirty.tolist())
         return _merge_evicted(evs), np.array(sorted(x for d in dts for x in d), dtype=np.uint64)
@@ -212,6 +218,15 @@ class VirtualShards:
         live = sum(c.evict_units for c in self.caches)
         if n > live:
             raise B.CacheError(B.E_EVICT_RANGE, "sharded evict: n exceeds live items / entries")
+        if self.push:   # one stream: pass p's histogram on every rank, then every rank's pick
+            for p in range(8):
+                for c in self.caches:
+                    c.push_evict_hist(n, p)
+                for c in self.caches:
+                    c.push_evict_pick(p)
+            res = [c.push_evict_apply(n) for c in self.caches]
+            return (_merge_evicted([r[0].tolist() for r in res]),
+                    np.array(sorted(x for r in res for x in r[1].tolist()), dtype=np.uint64))
         sts = [torch.tensor([0, 0, n], dtype=torch.int64, device="cuda") for _ in self.caches]
         hists = [torch.zeros(256, dtype=torch.int32, device="cuda") for _ in self.caches]
         for p in range(8):

@@ -51,9 +51,11 @@ def test_push_virtual_shards_equal_single_cache(oracle_mod, world, topk):
         check_batch(s, o, q, topk, expected_latent=lambda e, k: lat[e, synth.K_VALUES.index(k)])
     for e in range(0, n, 11):
         assert np.array_equal(single.meta(e)[0], vs.meta(e)[0])
-    e1, d1 = single.evict(500)
-    e2, d2 = vs.evict(500)
-    assert np.array_equal(np.sort(e1), e2) and np.array_equal(d1, d2)
+    for nev in (500, 77, 1200):                              # fused eviction: successive epochs
+        e1, d1 = single.evict(nev)
+        e2, d2 = vs.evict(nev)
+        assert np.array_equal(np.sort(e1), e2) and np.array_equal(d1, d2)
+        assert vs.stats()["live_items"] == single.live_items
 
 
 def test_push_smaller_batch_and_bad_calls():
@@ -113,12 +115,19 @@ def _proc(rank, port, world, ret):
             out = sc.alloc_outputs(bl, 4, True)
             sc.query_into(mine, out, topk=4)
             torch.cuda.synchronize()
-            ref = single.query(mine, topk=4)
-            got, exp = gpu_to_numpy(out), gpu_to_numpy(ref)
+            full = gpu_to_numpy(single.query(torch.from_numpy(q).cuda(), topk=4))   # the whole global batch
+            got = gpu_to_numpy(out)
+            exp = {k: (v[rank * bl:(rank + 1) * bl] if v is not None else None) for k, v in full.items()}
             hit = exp["k"] > 0
             ok &= bool(np.array_equal(got["ids"], exp["ids"]) and np.array_equal(got["k"], exp["k"])
                        and np.array_equal(got["scores"].view(np.uint32), exp["scores"].view(np.uint32))
                        and np.array_equal(got["latents"][hit], exp["latents"][hit]))
+        # the fused eviction across the two processes equals the reference cache's eviction (it
+        # saw the same global batches, so its access counters are the sharded ones)
+        for nev in (150, 600):
+            ev, dirty = sc.evict(nev)
+            e1, d1 = single.evict(nev)
+            ok &= bool(np.array_equal(ev, np.sort(e1)) and np.array_equal(dirty, d1))
         ret[rank] = ok
     except Exception as e:                                   # noqa: BLE001
         ret[rank] = repr(e)
@@ -141,3 +150,28 @@ def test_push_two_processes_one_gpu():
         if p.is_alive():
             p.kill()
     assert dict(ret) == {0: True, 1: True}, dict(ret)
+
+
+@pytest.mark.parametrize("policy,gran", [(1, 0), (2, 1), (0, 1), (3, 0)])
+def test_push_eviction_policies(policy, gran):
+    """The fused (peer-memory) eviction selection under every policy and both granularities
+    equals one unsharded cache's eviction, over several rounds."""
+    from paper_2312_04429_b200 import binding as B, sharded as S
+    n = 900
+    emb, cl = synth.entries(n, seed=60 + policy)
+    single = B.NirvanaCache(entry_capacity=n, dim=768, latent_bytes=0, evict_granularity=gran)
+    vs = S.VirtualShards(3, entry_capacity=n, dim=768, latent_bytes=0, push_max_nb=64, push_max_topk=1,
+                         evict_granularity=gran)
+    for c in [single] + vs.caches:
+        c.set_evict_policy(policy)
+    single.insert(torch.from_numpy(emb).cuda())
+    vs.insert(torch.from_numpy(emb).cuda())
+    for r in range(3):
+        q, _, _ = synth.queries(emb, cl, 3 * 48, seed=90 + r)
+        qt = torch.from_numpy(q).cuda()
+        single.query(qt, latents=False)
+        vs.query(qt, latents=False)
+        nev = 50 + 40 * r
+        e1, d1 = single.evict(nev)
+        e2, d2 = vs.evict(nev)
+        assert np.array_equal(np.sort(e1), e2) and np.array_equal(d1, d2), (policy, gran, r)
