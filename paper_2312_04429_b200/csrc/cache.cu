@@ -158,7 +158,6 @@ struct cache_t {
     DevBuf<float> invq, invstage;
     DevBuf<int32_t> qstat, istat;
     DevBuf<uint32_t> gk;   // per-query global k-th-best gate of the tcgen05 scorer
-    DevBuf<long long> gsrc;   // per-query pool slot to gather (-1 = none)
     DevBuf<Rec> recs;
     DevBuf<InsertPlan> iplan;
     DevBuf<CopyPlan> cplan;
@@ -189,9 +188,6 @@ struct cache_t {
     // host-call pipeline: query H2D copies on their own stream, one event per sub-batch
     cudaStream_t hcopy = nullptr;
     cudaEvent_t hev[kHostSplit + 1] = {};
-    DevBuf<uint64_t> hq_ids;
-    DevBuf<float> hq_sc;
-    DevBuf<int32_t> hq_k, hq_st;
     DevBuf<EvictState> est;
     DevBuf<unsigned int> ehist;
     DevBuf<unsigned long long> ekey, ekey2, ecnt;
@@ -347,8 +343,8 @@ cache_status cache_destroy(cache_t* c) {
     if (c->arena) cudaFree(c->arena);
     c->qbuf.release(); c->ystage.release(); c->invq.release(); c->invstage.release();
     c->qstat.release(); c->istat.release(); c->gk.release(); c->recs.release(); c->iplan.release(); c->cplan.release();
-    c->hq_in.release(); c->hq_lat.release(); c->hq_ids.release(); c->hq_sc.release(); c->hq_k.release();
-    c->hq_st.release(); c->est.release(); c->ehist.release(); c->ekey.release(); c->ecnt.release();
+    c->hq_in.release(); c->hq_lat.release();
+    c->est.release(); c->ehist.release(); c->ekey.release(); c->ecnt.release();
     c->ekey2.release(); c->eslot.release(); c->escr.release();
     c->hev_keys.release(); c->hev_sorted.release(); c->hev_pool.release(); c->hev_es.release(); c->hev_ds.release();
     c->hev_did.release();
@@ -519,7 +515,6 @@ static cache_status scan_core(cache_t* c, int64_t b, const void* queries, int32_
     CK(c->invq.ensure(bpad));
     CK(c->qstat.ensure(bpad));
     CK(c->gk.ensure(bpad));
-    CK(c->gsrc.ensure(bpad));
     if (c->prof_on) CK(cudaEventRecord(c->prof[0], s));
     launch_normalise(queries, q_dtype, b, c->dim, c->qbuf.p, c->invq.p, c->qstat.p, s, c->gk.p);
     c->launches++;
