@@ -335,6 +335,25 @@ cache_status cache_push_evict_pick(cache_t *c, int32_t pass, void *stream);
 cache_status cache_push_evict_apply(cache_t *c, int64_t n, uint64_t *out_evicted, int64_t *out_n,
                                     uint64_t *out_dirty_ids, int64_t *out_n_dirty, void *stream);
 
+/* ---- cache-selector profiling (Alg. 2) ----
+ * "generates images at each value of K for a set of prompts with their nearest cache prompt.
+ * It then finds the minimum similarity score such that all generated images are above a
+ * quality threshold alpha".  The images and their quality come from the diffusion
+ * model (outside this library): the caller passes quality[j*b + i] = the quality reached by
+ * profiling prompt i when reconditioning its nearest cached prompt's state at K = k_values[j]
+ * (device pointer, num_k x b floats).  The library computes the prompt's similarity to its
+ * nearest cached entry with the exact top-1 scan (as cache_query_batch scores it; no access is
+ * counted) and, reading R25, returns per K the largest similarity at which some profiled
+ * image failed (quality <= alpha) -- so every profiled pair with s > threshold passed, matching
+ * the strict '>' of Fig. 11 -- or, if none failed, the smallest profiled similarity;
+ * thresholds are made non-decreasing in K.  out_thresholds: host, num_k doubles;
+ * out_failed: host, num_k int64 (1 if some pair failed at that K) or NULL.  Host-synchronous.
+ * cache_set_thresholds installs a table (non-decreasing) for later lookups. */
+cache_status cache_profile_thresholds(cache_t *c, int64_t b, const void *queries, int32_t q_dtype,
+                                      const float *quality, double alpha, double *out_thresholds,
+                                      int64_t *out_failed, void *stream);
+cache_status cache_set_thresholds(cache_t *c, const double *thresholds);
+
 /* ---- match predictor ----
  * A linear one-class SVM f(x) = <w, x> - rho over the cached embeddings (unit-scaled stored
  * values), "trained by utilizing all prompt embeddings stored in the VDB" with

@@ -80,7 +80,7 @@ EXPORTS = ("cache_default_config", "cache_create", "cache_destroy", "cache_inser
            "cache_set_evict_policy", "cache_predictor_train", "cache_predict", "cache_predictor_get",
            "cache_set_evict_granularity", "cache_live_entries", "cache_push_reserve", "cache_push_queries",
            "cache_push_scan", "cache_push_merge", "cache_push_evict_hist", "cache_push_evict_pick",
-           "cache_push_evict_apply")
+           "cache_push_evict_apply", "cache_profile_thresholds", "cache_set_thresholds")
 
 
 def load_library(path: str = LIB_PATH):
@@ -114,6 +114,8 @@ def load_library(path: str = LIB_PATH):
     L.cache_push_queries.argtypes = [P, I64, P, I32, P]
     L.cache_push_scan.argtypes = [P, I64, I32, P]
     L.cache_push_merge.argtypes = [P, I64, I32, P, P, P, P, P, P, P]
+    L.cache_profile_thresholds.argtypes = [P, I64, P, I32, P, ctypes.c_double, P, P, P]
+    L.cache_set_thresholds.argtypes = [P, P]
     L.cache_push_evict_hist.argtypes = [P, I64, I32, P]
     L.cache_push_evict_pick.argtypes = [P, I32, P]
     L.cache_push_evict_apply.argtypes = [P, I64, P, P, P, P, P]
@@ -371,6 +373,22 @@ class NirvanaCache:
                                      _ptr(out.get("latents")), _ptr(out.get("ptrs")), _ptr(out.get("status")),
                                      _stream(stream)))
         return out
+
+    # ---- cache-selector profiling (Alg. 2) ----
+    def profile_thresholds(self, q: torch.Tensor, quality: torch.Tensor, alpha: float = 0.9, stream=None):
+        """q: [b][dim] cuda profiling prompts; quality: [num_k][b] float32 cuda (the model's image
+        quality per prompt and K).  Returns (thresholds float64[num_k], failed bool[num_k])."""
+        dt = DTYPE_BF16 if q.dtype == torch.bfloat16 else DTYPE_F32
+        quality = quality.contiguous().to(torch.float32)
+        thr = np.empty(self.num_k, dtype=np.float64)
+        failed = np.zeros(self.num_k, dtype=np.int64)
+        _check(_lib.cache_profile_thresholds(self._h, q.shape[0], _ptr(q), dt, _ptr(quality), float(alpha),
+                                             _ptr(thr), _ptr(failed), _stream(stream)))
+        return thr, failed.astype(bool)
+
+    def set_thresholds(self, thresholds):
+        t = np.ascontiguousarray(thresholds, dtype=np.float64)
+        _check(_lib.cache_set_thresholds(self._h, _ptr(t)))
 
     def push_evict_hist(self, n: int, pass_: int, stream=None):
         _check(_lib.cache_push_evict_hist(self._h, n, pass_, _stream(stream)))

@@ -599,6 +599,62 @@ cache_status cache_query_merge(cache_t* c, int64_t b, int64_t row0, int64_t nb, 
     return CACHE_OK;
 }
 
+// ---- cache-selector profiling (Alg. 2) ----
+cache_status cache_profile_thresholds(cache_t* c, int64_t b, const void* queries, int32_t q_dtype, const float* quality,
+                                      double alpha, double* out_thresholds, int64_t* out_failed, void* stream) {
+    if (!c) return fail(CACHE_E_INVALID_ARG, "cache_profile_thresholds: null cache");
+    if (b <= 0 || b > 0x7FFFFFFF || !queries || !quality || !out_thresholds ||
+        (q_dtype != CACHE_DTYPE_F32 && q_dtype != CACHE_DTYPE_BF16) || !(alpha == alpha))
+        return fail(CACHE_E_INVALID_ARG, "cache_profile_thresholds: bad argument");
+    if (c->live_entries == 0) return fail(CACHE_E_STATE, "cache_profile_thresholds: empty cache");
+    DeviceGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    int parts = 0;
+    cache_status r = scan_core(c, b, queries, q_dtype, 1, s, &parts);   // exact top-1, no access counted
+    if (r != CACHE_OK) return r;
+    DevBuf<cache_shard_rec> recs;
+    DevBuf<uint32_t> red;   // fail[num_k] | smin
+    CK(recs.ensure(b));
+    CK(red.ensure(c->num_k + 1));
+    CK(cudaMemsetAsync(red.p, 0, c->num_k * 4, s));
+    CK(cudaMemsetAsync(red.p + c->num_k, 0xFF, 4, s));
+    launch_local_merge(1, c->recs.p, parts, b, 1, c->qstat.p, c->present, c->rank, recs.p, s);
+    launch_profile_reduce(recs.p, c->invq.p, c->qstat.p, b, quality, c->num_k, (float)alpha, red.p, red.p + c->num_k, s);
+    c->launches += 2;
+    std::vector<uint32_t> h(c->num_k + 1);
+    CK(cudaMemcpyAsync(h.data(), red.p, (c->num_k + 1) * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    recs.release();
+    red.release();
+    auto from_orderable = [](uint32_t o) {
+        const uint32_t u = (o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o;
+        float f;
+        std::memcpy(&f, &u, 4);
+        return (double)f;
+    };
+    if (h[c->num_k] == 0xFFFFFFFFu) return fail(CACHE_E_STATE, "cache_profile_thresholds: no profiling query had a valid match");
+    const double smin = from_orderable(h[c->num_k]);
+    double prev = -INFINITY;
+    for (int j = 0; j < c->num_k; ++j) {
+        // R25: no failing pair -> the smallest profiled similarity (the evidence's lower edge);
+        // thresholds made non-decreasing in K (a larger K never applies below a smaller one's)
+        double t = h[j] ? from_orderable(h[j]) : smin;
+        if (out_failed) out_failed[j] = h[j] ? 1 : 0;
+        t = std::max(t, prev);
+        out_thresholds[j] = prev = t;
+    }
+    return CACHE_OK;
+}
+
+cache_status cache_set_thresholds(cache_t* c, const double* thresholds) {
+    if (!c || !thresholds) return fail(CACHE_E_INVALID_ARG, "cache_set_thresholds: null argument");
+    for (int j = 0; j < c->num_k; ++j)
+        if (!(thresholds[j] == thresholds[j]) || (j > 0 && thresholds[j] < thresholds[j - 1]))
+            return fail(CACHE_E_INVALID_ARG, "cache_set_thresholds: thresholds must be non-decreasing numbers");
+    for (int j = 0; j < c->num_k; ++j) c->km.thr[j] = c->cfg.thresholds[j] = thresholds[j];
+    return CACHE_OK;
+}
+
 cache_status cache_predictor_train(cache_t* c, double nu, int32_t epochs, double lr0, void* stream) {
     if (!c || !(nu > 0.0 && nu < 1.0) || epochs < 0 || !(lr0 > 0.0))
         return fail(CACHE_E_INVALID_ARG, "cache_predictor_train: bad nu / epochs / lr0");

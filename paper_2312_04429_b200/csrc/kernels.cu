@@ -511,6 +511,36 @@ void launch_finalize(int kmax, const Rec* ws, int parts, int64_t B, int topk, co
 }
 
 // ---------------------------------------------------------------------------------------
+// Cache-selector profiling (Alg. 2): the similarity of each profiling prompt to its
+// nearest cached prompt (the top-1 record of the scan, scored exactly as cache_query_batch
+// reports it) against the quality the model reached at each K.  Reading R25: the threshold of
+// K is the largest similarity at which some profiled image failed (quality <= alpha), so every
+// profiled pair with s > threshold passed -- the runtime rule of Fig. 11 is strict '>'.
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+k_profile_reduce(const cache_shard_rec* __restrict__ recs, const float* __restrict__ inv_q,
+                 const int32_t* __restrict__ qstatus, int64_t b, const float* __restrict__ quality, int num_k,
+                 float alpha, uint32_t* __restrict__ fail, uint32_t* __restrict__ smin) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < b; i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long key = recs[i].key;
+        if (key == 0ull || qstatus[i] != CACHE_ROW_OK) continue;
+        const float sc = fminf(fmaxf(key_to_f32(key) * inv_q[i], -1.0f), 1.0f);
+        const uint32_t o = orderable_f32(sc);
+        atomicMin(smin, o);
+        for (int j = 0; j < num_k; ++j)
+            if (quality[(int64_t)j * b + i] <= alpha) atomicMax(&fail[j], o);
+    }
+}
+
+void launch_profile_reduce(const cache_shard_rec* recs, const float* inv_q, const int32_t* qstatus, int64_t b,
+                           const float* quality, int num_k, float alpha, uint32_t* fail, uint32_t* smin,
+                           cudaStream_t s) {
+    if (b <= 0) return;
+    const unsigned grid = (unsigned)std::min<int64_t>(148 * 4, (b + 255) / 256);
+    k_profile_reduce<<<grid, 256, 0, s>>>(recs, inv_q, qstatus, b, quality, num_k, alpha, fail, smin);
+}
+
+// ---------------------------------------------------------------------------------------
 // Insert: commit normalised rows into their slots and copy latent payloads.
 // ---------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(128)

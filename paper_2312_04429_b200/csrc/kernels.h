@@ -83,6 +83,13 @@ int64_t sort_scratch_words(int64_t n);
 void launch_sort_u64(unsigned long long* keys, unsigned long long* tmp, int64_t n, uint32_t* scratch,
                      cudaStream_t s, int bits = 64);
 
+// Cache-selector profiling (Alg. 2): per profiling query i with a live nearest entry
+// (rec[i].key != 0), s_i = clamp(t_i * inv_q[i]); for every K_j with quality[j*b + i] <= alpha,
+// fail[j] = max(fail[j], orderable(s_i)); smin = min over all valid i of orderable(s_i).
+void launch_profile_reduce(const cache_shard_rec* recs, const float* inv_q, const int32_t* qstatus, int64_t b,
+                           const float* quality, int num_k, float alpha, uint32_t* fail, uint32_t* smin,
+                           cudaStream_t s);
+
 // match predictor (predictor.cu)
 void pred_margins(const __nv_bfloat16* emb, const float* inv_e, int64_t n_slots, int dim, const float* w,
                   uint32_t* keys, cudaStream_t s);
