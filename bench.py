@@ -1,6 +1,6 @@
 """Benchmark of the batched NIRVANA cache lookup (BASELINE.json metric) on B200.
 
-python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c1] [--batch B]
+python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c1|c4|c5] [--batch B]
 python bench.py --impl reference ...     (the fp64 CPU oracle, timed on the host cores)
 
 One step = one full lookup batch through the C ABI: query ingest (normalise + bf16), exact
@@ -44,6 +44,14 @@ CONFIGS = {
     "c4": dict(n=10_000_000, b=16384, sharded=True,
                workload="C4: 10M cached entries x 768-d bf16 sharded across N B200, 16,384-query global batches, "
                         "NCCL all-gather top-k merge, P2P latent fetch"),
+    # configs[4]: 100M entries sharded across the N GPUs (the whole cache on one B200 at N = 1:
+    # 154 GB of bf16 rows + 7 GB of metadata), Zipf-popular queries over entries, and every
+    # round = one 16K-query lookup batch + LCBFU eviction of 1% of the live items + re-insertion
+    # of as many fresh prompts as the eviction removed (strong scaling)
+    "c5": dict(n=100_000_000, b=16384, sharded=True, maintenance=0.01, pool_slots=131_072,
+               workload="C5: 100M cached entries x 768-d bf16 sharded across N B200, 16,384-query global "
+                        "batches of Zipf-popular queries, LCBFU eviction of 1% of the live items + "
+                        "re-insertion per round"),
 }
 
 
@@ -191,7 +199,12 @@ def run_sharded(args, cfg):
     bl = b // world
     pool_slots = cfg.get("pool_slots", 262_144)
     push = args.exchange == "push"
-    sc = ShardedCache(comm, entry_capacity=(n + world - 1) // world + 1024, latent_capacity=pool_slots,
+    maint = cfg.get("maintenance", 0.0)
+    per_rank = (n + world - 1) // world
+    # C5 re-inserts as many entries as each round's eviction removed: 0.5% entry headroom
+    # absorbs the uneven per-rank split of dirty entries vs placement of the fresh ones
+    sc = ShardedCache(comm, entry_capacity=per_rank + (per_rank // 200 if maint else 0) + 1024,
+                      latent_capacity=pool_slots,
                       dim=D, latent_bytes=L, latent_alias=True, push_max_nb=bl if push else 0, push_max_topk=1)
     for s in range(0, pool_slots, 8192):
         m = min(8192, pool_slots - s)
@@ -216,6 +229,40 @@ def run_sharded(args, cfg):
     dist.barrier()
     step_ms, score_ms = [], []
     launches0 = sc.cache.kernel_launches
+    next_row = n                 # fresh prompts of later rounds: rows n, n+1, ... of the same recipe
+    m_ev, m_ins, m_items, m_dirty = [], [], [], []
+
+    def maintenance_round():
+        # a9 + a10 at C5: evict 1% of the live items (collective, exact global LCBFU selection
+        # with the histograms reduced over peer memory), then insert as many fresh prompts as
+        # the eviction removed whole (their states come from the aliased pool)
+        nonlocal next_row
+        live = comm.all_reduce_sum(torch.tensor([sc.cache.evict_units], dtype=torch.int64,
+                                                device="cuda")).item()
+        nev = max(1, int(live * maint))
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        _, nd = sc.evict(nev, lists=False)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        nd = comm.all_reduce_sum(torch.tensor([nd], dtype=torch.int64, device="cuda")).item()
+        for s0 in range(0, nd, 65536):
+            m = min(65536, nd - s0)
+            sc.insert(E.rows(torch.arange(next_row + s0, next_row + s0 + m, dtype=torch.int64, device="cuda")),
+                      None)
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        next_row += nd
+        tt = torch.tensor([t1 - t0, t2 - t1], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        m_ev.append(1e3 * float(tt[0]))
+        m_ins.append(1e3 * float(tt[1]))
+        m_items.append(nev)
+        m_dirty.append(nd)
+
+    if maint:
+        maintenance_round()      # warm-up round (lazy workspace allocations)
     with Clocks(torch.cuda.current_device()) as clk:
         for _ in range(args.steps):
             flush.fill_(1.0)
@@ -226,6 +273,8 @@ def run_sharded(args, cfg):
             e1.synchronize()
             step_ms.append(e0.elapsed_time(e1))
             score_ms.append(ev[1].elapsed_time(ev[2]))
+            if maint:
+                maintenance_round()
     launches = sc.cache.kernel_launches - launches0
     sc.cache.set_profile_events(None)
     t = torch.tensor([sum(step_ms)], device="cuda", dtype=torch.float64)
@@ -262,6 +311,16 @@ def run_sharded(args, cfg):
                                                          "power cap)", traffic=None,
                                   algorithmic_per_launch=flops),
                     cpu_baseline=None, e2e=None, gpu_launches=launches, clocks=clk.summary())
+        if maint:
+            lk = tot / args.steps
+            line["maintenance"] = dict(
+                evict_items=m_items[1:], evict_ms=m_ev[1:], dirty_removed=m_dirty[1:], insert_entries=m_dirty[1:],
+                insert_ms=m_ins[1:], round_ms=[lk + a + c for a, c in zip(m_ev[1:], m_ins[1:])],
+                lookups_per_s_incl_maintenance=b * args.steps / ((tot + sum(m_ev[1:]) + sum(m_ins[1:])) / 1e3),
+                note="per timed round, after the lookup: LCBFU eviction of 1% of the live items (8 radix-select "
+                     "passes, histograms summed over peer memory, apply + dirty-entry removal; host wall clock "
+                     "max over ranks) and the insertion of as many fresh prompts as it removed (normalise + "
+                     "slot allocation + metadata; aliased latent pool); value counts the lookups only")
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
 

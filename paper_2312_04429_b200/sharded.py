@@ -143,9 +143,10 @@ class ShardedCache:
 
         return query_protocol(self.comm, q_local, topk, local_fn, merge_fn)
 
-    def evict(self, n: int):
+    def evict(self, n: int, lists: bool = True):
         """Collective: evict the n globally lowest-keyed items (entries in entry mode; every
-        rank passes the same n)."""
+        rank passes the same n).  lists=False skips gathering the evicted / dirty id lists to
+        every rank and returns this rank's (evicted count, dirty count) instead."""
         live = self.comm.all_reduce_sum(torch.tensor([self.cache.evict_units], dtype=torch.int64,
                                                      device="cuda")).item()
         if n > live:
@@ -160,6 +161,8 @@ class ShardedCache:
             hist = torch.zeros(256, dtype=torch.int32, device="cuda")
             evict_protocol(self.comm, n, st, hist, self.cache.evict_hist, self.cache.evict_pick)
             ev, dirty = self.cache.evict_apply(st, n)
+        if not lists:
+            return len(ev), len(dirty)
         evs = self.comm.all_gather_object(ev.tolist())
         dts = self.comm.all_gather_object(dirty.tolist())
         return _merge_evicted(evs), np.array(sorted(x for d in dts for x in d), dtype=np.uint64)
