@@ -337,6 +337,8 @@ def main():
                     help="tc1 = single-CTA tensor-core scan (auto/tc use CTA pairs for > 128 queries)")
     ap.add_argument("--exchange", default="push", choices=["push", "nccl"],
                     help="sharded configs (c4): fused P2P push exchange or NCCL all-gathers")
+    ap.add_argument("--slices", type=int, default=0,
+                    help="query slices of cache_query_batch (0 = library auto, 1 = one scan launch)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-maintenance", action="store_true")
@@ -364,6 +366,7 @@ def main():
     g, emb, cl, pres = build_cache(B, torch, cfg, seed=1000, dev=dev)
     g.set_scorer({"auto": B.SCORER_AUTO, "tc": B.SCORER_TC, "tc1": B.SCORER_TC_SINGLE,
                   "stream": B.SCORER_STREAM}[args.scorer])
+    g.set_query_slices(args.slices)
     b = cfg["b"]
     q_np, _, _ = synth.queries(emb, cl, b, seed=1001 + 7919 * rank)
     q = torch.from_numpy(q_np).cuda()
@@ -433,8 +436,17 @@ def main():
     # the gather (finalize) kernel is HBM-bound: 2 x 32 KiB per hit (pool read + denoiser-buffer
     # write) + the partial records it merges; reported beside the dominant kernel
     fin_ms = statistics.mean(fin_ms)
-    hits = int((out["k"] > 0).sum().item())
-    g_bytes = 2 * L * hits + b * 16 * 64
+    # with query slices the events time the LAST slice's finalize (the earlier ones run on the
+    # library's side stream under the next slice's scan): count that slice's rows and hits
+    # (slice rule of cache_set_query_slices: auto = 2 slices for b >= 2,048 on the tensor-core
+    # scorer; slices of ceil(b / n) rounded up to 256 rows)
+    ns = args.slices if args.slices > 0 else (2 if b >= 2048 and scorer_used == "tc" else 1)
+    if args.scorer == "tc1":
+        ns = 1
+    sub = -(-(-(-b // ns)) // 256) * 256 if ns > 1 else b
+    last0 = ((b - 1) // sub) * sub if ns > 1 else 0
+    hits = int((out["k"][last0:] > 0).sum().item())
+    g_bytes = 2 * L * hits + (b - last0) * 16 * 64
     gather_roof = dict(bound="hbm", achieved=g_bytes / (fin_ms / 1e3) / 1e9, peak=hbm, unit="GB/s",
                        frac=g_bytes / (fin_ms / 1e3) / 1e9 / hbm, kernel="finalize_gather",
                        algorithmic_per_launch=g_bytes)
@@ -503,7 +515,7 @@ def main():
                     config=dict(workload=cfg["workload"], entries=n, batch=b, dim=D, latent_bytes=L, topk=1,
                                 scorer=scorer_used, l2="flushed between timed steps (512 MiB write)",
                                 parallelism=f"replicas x{world}" if world > 1 else "single GPU",
-                                hit_rate=float((k_np > 0).mean())),
+                                hit_rate=float((k_np > 0).mean()), query_slices=ns),
                     kernel_ms=dict(ingest=statistics.mean(prep_ms), score=sc_ms, finalize_gather=fin_ms),
                     roofline=roof, roofline_gather=gather_roof, cpu_baseline=cpu, e2e=e2e, gpu_launches=launches,
                     clocks=clk.summary(),

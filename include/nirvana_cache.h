@@ -391,10 +391,23 @@ cache_status cache_set_evict_granularity(cache_t *c, int32_t granularity);
 /* Force a scoring kernel (CACHE_SCORER_*); AUTO by default. */
 cache_status cache_set_scorer(cache_t *c, int32_t scorer);
 
+/* Query slicing of cache_query_batch (a scheduling choice; results are identical for every
+ * value -- each query's answer depends only on its own row and the pre-batch state, R9).
+ * With n > 1 slices the tensor-core scan runs as n launches over consecutive query slices of
+ * a multiple of 256 rows, and slice i's finalize + latent gather (a1-a8's HBM-bound tail,
+ * P:434-435) runs on a library-owned side stream concurrently with slice i+1's scan; the call's
+ * stream waits for all of them before later work.  0 = auto (2 slices for batches of >= 2,048
+ * queries on the tensor-core scorer, else 1), 1 = never, 2..8 = that many slices (batches of
+ * more than 256 queries).  CACHE_E_INVALID_ARG outside [0, 8]. */
+cache_status cache_set_query_slices(cache_t *c, int32_t slices);
+
 /* Profiling hook: `events` points to 4 cudaEvent_t handles (host array, or NULL to disable).
  * When set, every cache_query_batch records events[0] before query ingest, events[1] before
  * the scoring kernel, events[2] before the finalize/gather kernel and events[3] after it, on
- * the call's stream, so a caller can time each kernel with cudaEventElapsedTime. */
+ * the call's stream, so a caller can time each kernel with cudaEventElapsedTime.  With query
+ * slices (cache_set_query_slices) events[1]..events[2] span every slice's scan (the side-stream
+ * finalizes of the earlier slices run inside that span) and events[2]..events[3] the last
+ * slice's finalize. */
 cache_status cache_set_profile_events(cache_t *c, void *const *events);
 
 /* Number of kernels the library launched on this handle so far (for launch accounting). */

@@ -74,7 +74,8 @@ EVICT_STATE_BYTES = 24  # cache_evict_state
 
 EXPORTS = ("cache_default_config", "cache_create", "cache_destroy", "cache_insert", "cache_query_batch",
            "cache_query_batch_host", "cache_evict", "cache_get_meta", "cache_get_row", "cache_stats",
-           "cache_set_scorer", "cache_set_profile_events", "cache_kernel_launches", "cache_last_error",
+           "cache_set_scorer", "cache_set_query_slices", "cache_set_profile_events", "cache_kernel_launches",
+           "cache_last_error",
            "cache_evict_hist", "cache_evict_pick", "cache_evict_apply", "cache_live_items", "cache_query_local",
            "cache_query_merge", "cache_export_peer", "cache_attach_peers", "cache_pool_write",
            "cache_set_evict_policy", "cache_predictor_train", "cache_predict", "cache_predictor_get",
@@ -100,6 +101,7 @@ def load_library(path: str = LIB_PATH):
     L.cache_get_row.argtypes = [P, U64, P]
     L.cache_stats.argtypes = [P, ctypes.POINTER(CacheStats)]
     L.cache_set_scorer.argtypes = [P, I32]
+    L.cache_set_query_slices.argtypes = [P, I32]
     L.cache_set_evict_policy.argtypes = [P, I32]
     L.cache_set_evict_policy.restype = ctypes.c_int
     L.cache_set_profile_events.argtypes = [P, P]
@@ -140,7 +142,7 @@ def load_library(path: str = LIB_PATH):
     L.cache_last_error.restype = ctypes.c_char_p
     for fn in ("cache_create", "cache_destroy", "cache_insert", "cache_query_batch", "cache_query_batch_host",
                "cache_evict", "cache_get_meta", "cache_get_row", "cache_stats", "cache_set_scorer",
-               "cache_set_profile_events"):
+               "cache_set_query_slices", "cache_set_profile_events"):
         getattr(L, fn).restype = ctypes.c_int
     return L
 
@@ -313,6 +315,10 @@ class NirvanaCache:
 
     def set_scorer(self, scorer: int):
         _check(_lib.cache_set_scorer(self._h, scorer))
+
+    def set_query_slices(self, slices: int):
+        """0 = auto, 1 = one scan launch, n = n query slices (finalize overlapped with the next scan)."""
+        _check(_lib.cache_set_query_slices(self._h, slices))
 
     # ------------------------- match predictor (NEXT-3) --------------------------------
     def train_predictor(self, nu: float = 0.001, epochs: int = 50, lr0: float = 0.5, stream=None):

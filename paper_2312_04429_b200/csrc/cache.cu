@@ -50,6 +50,11 @@ ArenaLayout arena_layout(int world, int64_t max_nb, int topk, int dim) {
 // slices so the copy overlaps the scan (see cache_query_batch_host)
 constexpr int kHostSplit = 4;
 constexpr int64_t kHostSplitMin = 2048;
+// cache_query_batch: tensor-core batches of >= kDevSplitMin queries are scanned in query
+// slices so each slice's finalize + gather overlaps the next slice's scan (query_sliced)
+constexpr int kDevSplitMax = 8;
+constexpr int kDevSplitAuto = 2;
+constexpr int64_t kDevSplitMin = 2048;
 
 cache_status fail(cache_status st, const std::string& msg) {
     g_err = msg;
@@ -188,6 +193,10 @@ struct cache_t {
     // host-call pipeline: query H2D copies on their own stream, one event per sub-batch
     cudaStream_t hcopy = nullptr;
     cudaEvent_t hev[kHostSplit + 1] = {};
+    // device query slices (query_sliced): finalize stream, one event per scanned slice + join
+    int qslices = 0;   // 0 = auto (kDevSplitAuto for b >= kDevSplitMin), 1 = never, n = n slices
+    cudaStream_t qside = nullptr;
+    cudaEvent_t qev[kDevSplitMax + 1] = {};
     DevBuf<EvictState> est;
     DevBuf<unsigned int> ehist;
     DevBuf<unsigned long long> ekey, ekey2, ecnt;
@@ -337,6 +346,9 @@ cache_status cache_destroy(cache_t* c) {
     for (cudaEvent_t e : c->hev)
         if (e) cudaEventDestroy(e);
     if (c->hcopy) cudaStreamDestroy(c->hcopy);
+    for (cudaEvent_t e : c->qev)
+        if (e) cudaEventDestroy(e);
+    if (c->qside) cudaStreamDestroy(c->qside);
     c->hq_out.release();
     cudaFree(c->emb); cudaFree(c->inv_e); cudaFree(c->ids); cudaFree(c->present);
     cudaFree(c->lslot); cudaFree(c->fcnt); cudaFree(c->lastacc); cudaFree(c->pool);
@@ -462,11 +474,14 @@ cache_status cache_insert(cache_t* c, int64_t n, const void* emb, int32_t emb_dt
 // Scan of this cache's entries for b normalised query rows qrows (bf16, allocation padded to
 // a multiple of 128 rows; gk = the rows' k-th-best gate words, already zeroed): partial top-k
 // record lists in c->recs ([parts][b][kmax]); *parts_out = lists per query (0: empty cache).
+// recs_at != nullptr: write the lists there (the caller sized it, see query_sliced) and
+// record no profiling events.
 static cache_status scan_rows(cache_t* c, int64_t b, __nv_bfloat16* qrows, uint32_t* gk, int kmax, cudaStream_t s,
-                              int* parts_out) {
+                              int* parts_out, Rec* recs_at = nullptr) {
     const int64_t bpad = (b + 127) / 128 * 128;
     const int64_t n_slots = c->hwm;
     int parts = 0;
+    const bool prof_on = c->prof_on && recs_at == nullptr;
     bool prof1 = false;   // prof[1] is recorded right before the scoring launch (after host planning)
     if (n_slots > 0) {
         bool use_tc = false;
@@ -487,22 +502,23 @@ static cache_status scan_rows(cache_t* c, int64_t b, __nv_bfloat16* qrows, uint3
             CUtensorMap tm_q;
             if (!encode_rows(&tm_q, qrows, bpad, c->dim, 128))
                 return fail(CACHE_E_CUDA, "query: cuTensorMapEncodeTiled failed");
-            CK(c->recs.ensure((size_t)parts * b * kmax));
-            if (c->prof_on) { CK(cudaEventRecord(c->prof[1], s)); prof1 = true; }
+            if (!recs_at) CK(c->recs.ensure((size_t)parts * b * kmax));
+            if (prof_on) { CK(cudaEventRecord(c->prof[1], s)); prof1 = true; }
             if (!launch_score_tc(kmax, tp, &tm_q, pair ? &c->tm_e128 : &c->tm_e, c->inv_e, c->ids, c->dim, b,
-                                 c->recs.p, gk, s))
+                                 recs_at ? recs_at : c->recs.p, gk, s))
                 return fail(CACHE_E_UNSUPPORTED, "query: tensor-core scorer not built");
             c->launches++;
         } else {
             parts = stream_parts(n_slots, b);
-            CK(c->recs.ensure((size_t)parts * b * kmax));
-            if (c->prof_on) { CK(cudaEventRecord(c->prof[1], s)); prof1 = true; }
-            launch_score_stream(kmax, c->emb, c->inv_e, c->ids, n_slots, c->dim, qrows, b, c->recs.p, parts, s);
+            if (!recs_at) CK(c->recs.ensure((size_t)parts * b * kmax));
+            if (prof_on) { CK(cudaEventRecord(c->prof[1], s)); prof1 = true; }
+            launch_score_stream(kmax, c->emb, c->inv_e, c->ids, n_slots, c->dim, qrows, b,
+                                recs_at ? recs_at : c->recs.p, parts, s);
             c->launches++;
         }
     }
-    if (c->prof_on && !prof1) CK(cudaEventRecord(c->prof[1], s));
-    if (c->prof_on) CK(cudaEventRecord(c->prof[2], s));   // end of the scan
+    if (prof_on && !prof1) CK(cudaEventRecord(c->prof[1], s));
+    if (prof_on) CK(cudaEventRecord(c->prof[2], s));   // end of the scan
     *parts_out = parts;
     return CACHE_OK;
 }
@@ -521,11 +537,97 @@ static cache_status scan_core(cache_t* c, int64_t b, const void* queries, int32_
     return scan_rows(c, b, c->qbuf.p, c->gk.p, kmax, s, parts_out);
 }
 
+// Number of device query slices for a batch of b (1 = one scan launch).
+static int query_slices(const cache_t* c, int64_t b) {
+    if (c->hwm <= 0 || c->scorer == CACHE_SCORER_STREAM || c->scorer == CACHE_SCORER_TC_SINGLE ||
+        !c->tm_e_ok || !tc_supported(c->dim))
+        return 1;
+    if (c->qslices == 1) return 1;
+    if (c->qslices == 0 && b < kDevSplitMin) return 1;
+    const int ns = c->qslices > 0 ? c->qslices : kDevSplitAuto;
+    const int64_t sub = ((b + ns - 1) / ns + 255) / 256 * 256;
+    return (int)((b + sub - 1) / sub);
+}
+
+// Large tensor-core batches: one ingest launch, then the scan as ns launches over query
+// slices of `sub` rows (multiples of 256), and slice i's finalize + gather -- HBM-bound --
+// on a side stream while slice i+1's scan -- tensor-bound -- runs.  One finalize CTA (40
+// registers x 256 threads, 160 B of shared memory) fits beside the scan CTA on every SM
+// (134 x 384 registers, 221 KiB), so the gather of slice i is hidden behind the next scan;
+// only the last slice's finalize is exposed.  Results are identical to one launch: each
+// query's answer depends only on its own row and the pre-batch state (R9), the counter
+// increments are atomics, and the whole batch is one LRU clock tick.
+static cache_status query_sliced(cache_t* c, int64_t b, int ns, const void* queries, int32_t q_dtype,
+                                 int32_t topk, int kmax, uint64_t* out_ids, float* out_scores, int32_t* out_k,
+                                 void* latent_out, void** out_ptr, int32_t* row_status, cudaStream_t s,
+                                 bool tick) {
+    const int64_t sub = ((b + ns - 1) / ns + 255) / 256 * 256;
+    const int64_t bpad = (b + 127) / 128 * 128;
+    CK(c->qbuf.ensure((size_t)bpad * c->dim));
+    CK(c->invq.ensure(bpad));
+    CK(c->qstat.ensure(bpad));
+    CK(c->gk.ensure(bpad));
+    int64_t off[kDevSplitMax + 1], roff[kDevSplitMax];
+    int parts[kDevSplitMax];
+    size_t tot = 0;
+    int n = 0;
+    for (int64_t o = 0; o < b; o += sub, ++n) {
+        const int64_t nb = std::min(sub, b - o);
+        off[n] = o;
+        parts[n] = tc_plan(nb, c->hwm, c->sm_count, nb > 128).parts;
+        roff[n] = (int64_t)tot;
+        tot += (size_t)parts[n] * nb * kmax;
+    }
+    off[n] = b;
+    if (n != ns) return fail(CACHE_E_STATE, "query: slice plan mismatch");
+    CK(c->recs.ensure(tot));   // before any launch: the buffer is not reallocated under a slice
+    if (!c->qside) CK(cudaStreamCreateWithFlags(&c->qside, cudaStreamNonBlocking));
+    for (cudaEvent_t& e : c->qev)
+        if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    if (c->prof_on) CK(cudaEventRecord(c->prof[0], s));
+    launch_normalise(queries, q_dtype, b, c->dim, c->qbuf.p, c->invq.p, c->qstat.p, s, c->gk.p);
+    c->launches++;
+    if (c->prof_on) CK(cudaEventRecord(c->prof[1], s));
+    for (int i = 0; i < n; ++i) {
+        const int64_t nb = off[i + 1] - off[i];
+        int p = 0;
+        cache_status r = scan_rows(c, nb, c->qbuf.p + off[i] * c->dim, c->gk.p + off[i], kmax, s, &p,
+                                   c->recs.p + roff[i]);
+        if (r != CACHE_OK) return r;
+        if (p != parts[i]) return fail(CACHE_E_STATE, "query: slice parts mismatch");
+        if (i + 1 < n) CK(cudaEventRecord(c->qev[i], s));
+    }
+    if (c->prof_on) CK(cudaEventRecord(c->prof[2], s));
+    if (tick) c->clock++;   // one query batch = one tick of the LRU clock
+    uint8_t* lat = (uint8_t*)latent_out;
+    for (int i = 0; i < n; ++i) {
+        const int64_t o = off[i], nb = off[i + 1] - off[i];
+        const bool last = i + 1 == n;
+        cudaStream_t fs = last ? s : c->qside;
+        if (!last) CK(cudaStreamWaitEvent(c->qside, c->qev[i], 0));
+        launch_finalize(kmax, c->recs.p + roff[i], parts[i], nb, topk, c->invq.p + o, c->qstat.p + o, c->ids,
+                        c->present, c->lslot, c->fcnt, c->lastacc, c->clock, c->pool, c->L, c->km,
+                        out_ids + o * topk, out_scores + o * topk, out_k + o, lat ? lat + o * c->L : nullptr,
+                        out_ptr ? out_ptr + o : nullptr, row_status ? row_status + o : nullptr, fs, last);
+        c->launches++;
+    }
+    if (c->prof_on) CK(cudaEventRecord(c->prof[3], s));
+    CK(cudaEventRecord(c->qev[kDevSplitMax], c->qside));   // join: s continues after every slice
+    CK(cudaStreamWaitEvent(s, c->qev[kDevSplitMax], 0));
+    CK(cudaGetLastError());
+    c->queries += b;
+    return CACHE_OK;
+}
+
 // tick = false: a later sub-batch of the same host batch (same LRU clock value).
 static cache_status query_core(cache_t* c, int64_t b, const void* queries, int32_t q_dtype, int32_t topk,
                                uint64_t* out_ids, float* out_scores, int32_t* out_k, void* latent_out,
                                void** out_ptr, int32_t* row_status, cudaStream_t s, bool tick = true) {
     const int kmax = topk == 1 ? 1 : (topk <= 4 ? 4 : 16);
+    const int ns = query_slices(c, b);
+    if (ns > 1)
+        return query_sliced(c, b, ns, queries, q_dtype, topk, kmax, out_ids, out_scores, out_k, latent_out, out_ptr,
+                            row_status, s, tick);
     int parts = 0;
     cache_status r = scan_core(c, b, queries, q_dtype, kmax, s, &parts);
     if (r != CACHE_OK) return r;
@@ -1322,6 +1424,12 @@ cache_status cache_set_scorer(cache_t* c, int32_t scorer) {
     if (!c || scorer < CACHE_SCORER_AUTO || scorer > CACHE_SCORER_TC_SINGLE)
         return fail(CACHE_E_INVALID_ARG, "cache_set_scorer: bad argument");
     c->scorer = scorer;
+    return CACHE_OK;
+}
+
+cache_status cache_set_query_slices(cache_t* c, int32_t slices) {
+    if (!c || slices < 0 || slices > kDevSplitMax) return fail(CACHE_E_INVALID_ARG, "cache_set_query_slices: bad argument");
+    c->qslices = slices;
     return CACHE_OK;
 }
 

@@ -73,6 +73,30 @@ __device__ __forceinline__ void put_meta(const RowDst<ND>& o, int64_t row, float
         for (int d = 0; d < o.n; ++d) { o.inv[d][row] = inv; o.status[d][row] = st; }
 }
 
+// Phase 2 by correctly rounded division, for a row where some y = x * rcp(nu) landed near a
+// bf16 rounding midpoint (rare).  Kept out of line so the compiler cannot if-convert the
+// 24 divisions into the fast path (it did: 26 MUFU.RCP64H + 188 DFMA per row, ncu s3).
+template <typename Tin, int NS, int ND>
+__device__ __noinline__ void normalise_row_exact(const Tin* __restrict__ xr, int lane, const RowDst<ND>& o,
+                                                 int64_t orow, double nu) {
+    constexpr int dim = NS * 32;
+    const int64_t ybase = orow * (int64_t)dim;
+    double v[NS];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+        const double x = (double)load_in<Tin>(xr + lane + 32 * k);
+        const __nv_bfloat16 b = __double2bfloat16(__ddiv_rn(x, nu));
+        put_bf16(o, ybase + lane + 32 * k, b);
+        const double yd = (double)__bfloat162float(b);
+        v[k] = __dmul_rn(yd, yd);
+    }
+    const double s2 = warp_tree_sum<NS>(v);
+    if (lane == 0) {
+        if (s2 == 0.0) put_meta(o, orow, __int_as_float(0x7FC00000), CACHE_ROW_ZERO_NORM);
+        else put_meta(o, orow, __double2float_rn(__ddiv_rn(1.0, __dsqrt_rn(s2))), CACHE_ROW_OK);
+    }
+}
+
 // One warp normalises input row xr into output row `orow` of every destination.
 template <typename Tin, int NS, int ND>
 __device__ __forceinline__ void normalise_row(const Tin* __restrict__ xr, int lane, const RowDst<ND>& o,
@@ -107,20 +131,27 @@ __device__ __forceinline__ void normalise_row(const Tin* __restrict__ xr, int la
     // bf16_RNE(x / nu) without a division per element: y = x * rcp(nu) is within ~2 fp64 ulps
     // of x / nu, so both round to the same bf16 unless y lies within a few ulps of a bf16
     // rounding midpoint (the 45 fp64 mantissa bits below the bf16 LSB == 2^44) or in the bf16
-    // subnormal range -- then the exact correctly rounded division is used.  Bit-identical
+    // subnormal range -- then the whole row is redone with the exact correctly rounded
+    // division (normalise_row_exact, which overwrites every stored value).  Bit-identical
     // to bf16_RNE(__ddiv_rn(x, nu)) by construction.
     const double rnu = __drcp_rn(nu);
+    int near = 0;
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
         const double x = (double)load_in<Tin>(xr + lane + 32 * k);
-        double y = __dmul_rn(x, rnu);
+        const double y = __dmul_rn(x, rnu);
         const long long low = (long long)((unsigned long long)__double_as_longlong(y) & ((1ull << 45) - 1));
         const long long dm = low - (1ll << 44);
-        if ((dm <= 16 && dm >= -16) || fabs(y) < 0x1p-120) y = __ddiv_rn(x, nu);
+        near |= (dm <= 16 && dm >= -16) || fabs(y) < 0x1p-120;
         const __nv_bfloat16 b = __double2bfloat16(y);   // cvt.rn.bf16.f64
         put_bf16(o, ybase + lane + 32 * k, b);
         const double yd = (double)__bfloat162float(b);
         v[k] = __dmul_rn(yd, yd);
+    }
+    if (__any_sync(0xFFFFFFFFu, near)) {   // warp-uniform, rare
+        __syncwarp();
+        normalise_row_exact<Tin, NS, ND>(xr, lane, o, orow, nu);
+        return;
     }
     const double s2 = warp_tree_sum<NS>(v);
     if (lane == 0) {
@@ -488,7 +519,7 @@ void launch_finalize(int kmax, const Rec* ws, int parts, int64_t B, int topk, co
                      const int32_t* lslot, uint32_t* fcnt, uint32_t* lastacc, uint32_t clock,
                      const uint8_t* pool, int64_t latent_bytes,
                      const KMap& km, uint64_t* out_ids, float* out_scores, int32_t* out_k,
-                     uint8_t* latent_out, void** out_ptr, int32_t* out_status, cudaStream_t s) {
+                     uint8_t* latent_out, void** out_ptr, int32_t* out_status, cudaStream_t s, bool pdl) {
     if (B <= 0) return;
     const unsigned grid = (unsigned)((B + kFinQ - 1) / kFinQ);
     cudaLaunchConfig_t cfg{};
@@ -499,7 +530,7 @@ void launch_finalize(int kmax, const Rec* ws, int parts, int64_t B, int topk, co
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl ? 1 : 0;   // no PDL edge when the launch follows an event wait on a side stream
 #define NV_FIN(KM)                                                                                \
     cudaLaunchKernelEx(&cfg, k_finalize<KM>, ws, parts, B, topk, inv_q, qstatus, ids, present,    \
                        lslot, fcnt, lastacc, clock, pool, latent_bytes, km, out_ids, out_scores,  \

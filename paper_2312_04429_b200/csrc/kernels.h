@@ -59,7 +59,8 @@ void launch_finalize(int kmax, const Rec* ws, int parts, int64_t B, int topk, co
                      const int32_t* lslot, uint32_t* fcnt, uint32_t* lastacc, uint32_t clock,
                      const uint8_t* pool, int64_t latent_bytes,
                      const KMap& km, uint64_t* out_ids, float* out_scores, int32_t* out_k,
-                     uint8_t* latent_out, void** out_ptr, int32_t* out_status, cudaStream_t s);
+                     uint8_t* latent_out, void** out_ptr, int32_t* out_status, cudaStream_t s,
+                     bool pdl = true);
 
 void launch_insert_commit(const __nv_bfloat16* ystage, const float* invstage, const InsertPlan* plan,
                           int64_t n_valid, int dim, int num_k, __nv_bfloat16* emb, float* inv_e,
