@@ -438,9 +438,8 @@ def main():
     fin_ms = statistics.mean(fin_ms)
     # with query slices the events time the LAST slice's finalize (the earlier ones run on the
     # library's side stream under the next slice's scan): count that slice's rows and hits
-    # (slice rule of cache_set_query_slices: auto = 2 slices for b >= 2,048 on the tensor-core
-    # scorer; slices of ceil(b / n) rounded up to 256 rows)
-    ns = args.slices if args.slices > 0 else (2 if b >= 2048 and scorer_used == "tc" else 1)
+    # (slice rule of cache_set_query_slices: slices of ceil(b / n) rounded up to 256 rows)
+    ns = args.slices if args.slices > 0 else 1   # library auto = one launch
     if args.scorer == "tc1":
         ns = 1
     sub = -(-(-(-b // ns)) // 256) * 256 if ns > 1 else b

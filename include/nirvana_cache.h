@@ -396,9 +396,10 @@ cache_status cache_set_scorer(cache_t *c, int32_t scorer);
  * With n > 1 slices the tensor-core scan runs as n launches over consecutive query slices of
  * a multiple of 256 rows, and slice i's finalize + latent gather (a1-a8's HBM-bound tail,
  * P:434-435) runs on a library-owned side stream concurrently with slice i+1's scan; the call's
- * stream waits for all of them before later work.  0 = auto (2 slices for batches of >= 2,048
- * queries on the tensor-core scorer, else 1), 1 = never, 2..8 = that many slices (batches of
- * more than 256 queries).  CACHE_E_INVALID_ARG outside [0, 8]. */
+ * stream waits for all of them before later work.  0 = auto (currently one launch: at C2 the
+ * concurrent finalize slows the scan by more than the gather it hides),
+ * 1 = never, 2..8 = that many slices (batches of more than 256 queries).
+ * CACHE_E_INVALID_ARG outside [0, 8]. */
 cache_status cache_set_query_slices(cache_t *c, int32_t slices);
 
 /* Profiling hook: `events` points to 4 cudaEvent_t handles (host array, or NULL to disable).

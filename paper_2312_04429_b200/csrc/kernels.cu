@@ -134,18 +134,29 @@ __device__ __forceinline__ void normalise_row(const Tin* __restrict__ xr, int la
     // subnormal range -- then the whole row is redone with the exact correctly rounded
     // division (normalise_row_exact, which overwrites every stored value).  Bit-identical
     // to bf16_RNE(__ddiv_rn(x, nu)) by construction.
+    //
+    // Off those cases y is a normal bf16-range value (|y| <= ~1) that is not a rounding tie,
+    // so RNE to 8 significant bits is "add half an LSB, truncate" on the bit pattern (a carry
+    // into the exponent is the correct rounding up), and the bf16 is read off the rounded
+    // double -- integer ops instead of cvt.rn.bf16.f64 plus two conversions back to fp64
+    // (the XU conversion pipe was the busiest unit, ncu s3).  Exact zeros (x = +-0) round to
+    // themselves.
     const double rnu = __drcp_rn(nu);
     int near = 0;
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
         const double x = (double)load_in<Tin>(xr + lane + 32 * k);
         const double y = __dmul_rn(x, rnu);
-        const long long low = (long long)((unsigned long long)__double_as_longlong(y) & ((1ull << 45) - 1));
-        const long long dm = low - (1ll << 44);
-        near |= (dm <= 16 && dm >= -16) || fabs(y) < 0x1p-120;
-        const __nv_bfloat16 b = __double2bfloat16(y);   // cvt.rn.bf16.f64
-        put_bf16(o, ybase + lane + 32 * k, b);
-        const double yd = (double)__bfloat162float(b);
+        const unsigned long long u = (unsigned long long)__double_as_longlong(y);
+        const long long dm = (long long)(u & ((1ull << 45) - 1)) - (1ll << 44);
+        // 0 < |y| < 2^-120 as one unsigned compare of the sign-stripped pattern (u << 1)
+        near |= (dm <= 16 && dm >= -16) || ((u << 1) - 1ull < (0x3870000000000000ull << 1) - 1ull);
+        const unsigned long long r = (u + (1ull << 44)) & ~((1ull << 45) - 1);   // RNE to bf16 precision
+        const uint32_t hi = (uint32_t)(r >> 32);
+        const uint32_t e11 = (hi >> 20) & 0x7FFu;
+        const uint32_t bits = ((hi >> 16) & 0x8000u) | (e11 ? ((e11 - 896u) << 7) : 0u) | ((hi >> 13) & 0x7Fu);
+        put_bf16(o, ybase + lane + 32 * k, __ushort_as_bfloat16((unsigned short)bits));
+        const double yd = __longlong_as_double((long long)r);   // == the stored bf16, exactly
         v[k] = __dmul_rn(yd, yd);
     }
     if (__any_sync(0xFFFFFFFFu, near)) {   // warp-uniform, rare

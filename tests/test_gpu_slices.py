@@ -52,9 +52,9 @@ def test_slices_bit_identical_to_one_launch(B, oracle_mod, b, topk):
         return [(tuple(int(x) for x in f), m) for f, m in (g.meta(int(i)) for i in hit_ids)]
     ref_meta = metas(ref_g)
     ref_ev = ref_g.evict(300)
-    # 0 = auto (2 slices at b = 4,096, one launch at 1,100); b = 1,100 with 3 / 8 requested
+    # 0 = auto (one launch); b = 1,100 with 3 / 8 requested
     # gives slices of 512 + 512 + 76 (the last on the single-CTA kernel) / 4 x 256 + 76
-    for slices in (0, 2, 3, 8):
+    for slices in (0, 2, 3, 4, 8):
         g = _cache(B, emb, lat, pres, slices)
         outs = _run(g, qs, topk)
         for o, r in zip(outs, ref):
