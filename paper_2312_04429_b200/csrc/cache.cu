@@ -152,8 +152,10 @@ struct cache_t {
     CUtensorMap tm_e128;            // TMA map of emb (box 64 x 128): CTA-pair scan (half a tile per CTA)
     bool tm_e_ok = false;
     // host mirrors / allocators
-    std::vector<uint32_t> h_present, h_ids;
-    std::vector<int32_t> h_lslot;
+    // host mirror of the entry slots: live flag + id (allocation, high-water mark, inspection);
+    // presence masks, latent slots and counters live on the device only
+    std::vector<uint8_t> h_live;
+    std::vector<uint32_t> h_ids;
     std::vector<int64_t> free_e, free_l;   // sorted descending: back() = lowest free slot
     int64_t hwm = 0, live_entries = 0, live_items = 0, queries = 0;
     uint64_t next_id = 0;
@@ -190,7 +192,7 @@ struct cache_t {
             p = nullptr;
             n = 0;
         }
-    } hev_keys, hev_sorted, hev_pool, hev_es, hev_ds, hev_did;
+    } hev_sorted, hev_pool, hev_ds, hev_did;
     std::vector<int64_t> free_tmp;   // merge buffer of the free lists
     void* h_out = nullptr;   // pinned staging of the packed host-call results
     size_t h_out_n = 0;
@@ -330,9 +332,8 @@ cache_status cache_create(const cache_config* cfg, int device, cache_t** out) {
     if ((e = cudaDeviceSynchronize()) != cudaSuccess) return bail(e, "init");
     c->tm_e_ok = encode_rows(&c->tm_e, c->emb, c->cap_pad, c->dim, 256) &&
                  encode_rows(&c->tm_e128, c->emb, c->cap_pad, c->dim, 128);
-    c->h_present.assign(c->cap_pad, 0);
+    c->h_live.assign(c->cap_pad, 0);
     c->h_ids.assign(c->cap_pad, 0);
-    c->h_lslot.assign((size_t)c->cap_pad * c->num_k, -1);
     c->free_e.resize(c->cap);
     for (int64_t i = 0; i < c->cap; ++i) c->free_e[i] = c->cap - 1 - i;
     c->free_l.resize(c->lcap);
@@ -362,7 +363,7 @@ cache_status cache_destroy(cache_t* c) {
     c->hq_in.release(); c->hq_lat.release();
     c->est.release(); c->ehist.release(); c->ekey.release(); c->ecnt.release();
     c->ekey2.release(); c->eslot.release(); c->escr.release();
-    c->hev_keys.release(); c->hev_sorted.release(); c->hev_pool.release(); c->hev_es.release(); c->hev_ds.release();
+    c->hev_sorted.release(); c->hev_pool.release(); c->hev_ds.release();
     c->hev_did.release();
     c->epool.release(); c->edirty.release(); c->edid.release();
     delete c;
@@ -450,9 +451,8 @@ cache_status cache_insert(cache_t* c, int64_t n, const void* emb, int32_t emb_dt
                 if (latents) cp.push_back(CopyPlan{gr * c->num_k + j, p.lslot[j]});
             }
             plan.push_back(p);
-            c->h_present[p.slot] = p.mask;
+            c->h_live[p.slot] = 1;
             c->h_ids[p.slot] = p.id;
-            for (int j = 0; j < c->num_k; ++j) c->h_lslot[p.slot * c->num_k + j] = p.lslot[j];
             c->hwm = std::max(c->hwm, p.slot + 1);
             c->live_entries++;
             c->live_items += __builtin_popcount(p.mask);
@@ -1257,48 +1257,42 @@ cache_status cache_evict_apply(cache_t* c, const cache_evict_state* st, int64_t 
     // at most min(cap, live units) keys are <= the selected threshold on this rank
     const int64_t bound = std::max<int64_t>(1, std::min<int64_t>(cap, entry_mode ? c->live_entries : c->live_items));
     const int64_t dbound = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(cap, 1), c->live_entries));
+    // freed pool slots: one per evicted item, or up to num_k per evicted entry in entry mode
+    const int64_t pbound = entry_mode ? bound * c->num_k : bound;
     CK(c->ekey.ensure(bound));
-    CK(c->ekey2.ensure(std::max(bound, dbound)));
-    CK(c->epool.ensure(bound));
+    CK(c->ekey2.ensure(std::max(pbound, dbound)));
+    CK(c->epool.ensure(pbound));
     CK(c->eslot.ensure(bound));
-    CK(c->escr.ensure(sort_scratch_words(std::max(bound, dbound))));
-    CK(c->ecnt.ensure(2));
+    CK(c->escr.ensure(sort_scratch_words(std::max(pbound, dbound))));
+    CK(c->ecnt.ensure(3));
     CK(c->edirty.ensure(dbound));
     CK(c->edid.ensure(dbound));
-    CK(cudaMemsetAsync(c->ecnt.p, 0, 16, s));
+    CK(cudaMemsetAsync(c->ecnt.p, 0, 24, s));
     launch_evict_apply(c->present, c->fcnt, c->lastacc, c->ids, c->lslot, c->inv_e, c->hwm, c->km,
                        reinterpret_cast<const EvictState*>(st), c->ekey.p, c->epool.p, c->eslot.p, c->ecnt.p,
                        c->edirty.p, c->edid.p, bound, dbound, s);
     c->launches++;
-    unsigned long long cnt[2];
-    CK(cudaMemcpyAsync(cnt, c->ecnt.p, 16, cudaMemcpyDeviceToHost, s));
+    unsigned long long cnt[3];
+    CK(cudaMemcpyAsync(cnt, c->ecnt.p, 24, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     const int64_t n = (int64_t)cnt[0], nd = (int64_t)cnt[1];
+    const int64_t nfreed = entry_mode ? (int64_t)cnt[2] : n;   // stored states removed
     if (out_n) *out_n = n;
-    if (n > cap || nd > cap || n > bound || nd > dbound)
+    if (n > cap || nd > cap || n > bound || nd > dbound || nfreed > pbound)
         return fail(CACHE_E_STATE, "cache_evict_apply: more evictions than the output capacity (n differs "
                                    "between the selection and the apply?); handle state undefined");
-    // 1. the unsorted (key, entry slot) pairs for the per-item mirror updates
-    CK(c->hev_keys.ensure(n * 8));
-    CK(c->hev_es.ensure(n * 8));
-    if (n && !entry_mode) {
-        CK(cudaMemcpyAsync(c->hev_keys.p, c->ekey.p, n * 8, cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(c->hev_es.p, c->eslot.p, n * 8, cudaMemcpyDeviceToHost, s));
-    }
-    cudaEvent_t copied = nullptr;
-    CK(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
-    CK(cudaEventRecord(copied, s));
-    // 2. sorted lists, on the GPU while the host updates its mirrors: freed pool slots and dirty
-    //    slots (ascending, merged into the lowest-first free lists), dirty ids (the API order),
-    //    evicted keys (eviction order)
-    const bool pool_freed = !entry_mode && !c->alias;
-    CK(c->hev_pool.ensure((pool_freed ? n : 0) * 8));
+    // Sorted lists, on the GPU: freed pool slots and dirty slots (ascending, merged into the
+    // lowest-first free lists), dirty ids (the API order), evicted keys (eviction order).  The
+    // host keeps no per-item mirror: the apply kernel lists the pool slots it freed (entry mode
+    // included), and the host's entry mirror only records which slots are live.
+    const bool pool_freed = !c->alias && nfreed > 0;
+    CK(c->hev_pool.ensure((pool_freed ? nfreed : 0) * 8));
     CK(c->hev_ds.ensure(nd * 8));
     CK(c->hev_did.ensure(nd * 8));
     CK(c->hev_sorted.ensure(n * 8));
-    if (pool_freed && n) {
-        launch_sort_u64(c->epool.p, c->ekey2.p, n, c->escr.p, s, 32);
-        CK(cudaMemcpyAsync(c->hev_pool.p, c->epool.p, n * 8, cudaMemcpyDeviceToHost, s));
+    if (pool_freed) {
+        launch_sort_u64(c->epool.p, c->ekey2.p, nfreed, c->escr.p, s, 32);
+        CK(cudaMemcpyAsync(c->hev_pool.p, c->epool.p, nfreed * 8, cudaMemcpyDeviceToHost, s));
     }
     if (nd) {
         launch_sort_u64(c->edirty.p, c->ekey2.p, nd, c->escr.p, s, 40);
@@ -1310,46 +1304,18 @@ cache_status cache_evict_apply(cache_t* c, const cache_evict_state* st, int64_t 
         launch_sort_u64(c->ekey.p, c->ekey2.p, n, c->escr.p, s, 64);
         CK(cudaMemcpyAsync(c->hev_sorted.p, c->ekey.p, n * 8, cudaMemcpyDeviceToHost, s));
     }
-    c->launches += 12 * (pool_freed && n) + 24 * (nd > 0) + 24 * (out_evicted && n);
-    CK(cudaEventSynchronize(copied));
-    cudaEventDestroy(copied);
-    if (!entry_mode) {
-        const unsigned long long* keys = static_cast<const unsigned long long*>(c->hev_keys.p);
-        const int64_t* es = static_cast<const int64_t*>(c->hev_es.p);
-        for (int64_t i = 0; i < n; ++i) {
-            const int j = (int)(keys[i] & 7ull);
-            const int64_t slot = es[i];
-            c->h_present[slot] &= ~(1u << j);
-            c->h_lslot[slot * c->num_k + j] = -1;
-        }
-        c->live_items -= n;
-    }
+    c->launches += 12 * pool_freed + 24 * (nd > 0) + 24 * (out_evicted && n);
+    c->live_items -= nfreed;
     CK(cudaStreamSynchronize(s));   // sorted lists landed
     const unsigned long long* ds = static_cast<const unsigned long long*>(c->hev_ds.p);
-    if (entry_mode) {   // every stored state of an evicted entry is freed (pool slots from the mirror)
-        std::vector<unsigned long long> pool;
-        for (int64_t i = 0; i < nd; ++i) {
-            const int64_t slot = (int64_t)ds[i];
-            const uint32_t m = c->h_present[slot];
-            for (int j = 0; j < c->num_k; ++j) {
-                if (!((m >> j) & 1u)) continue;
-                if (!c->alias) pool.push_back((unsigned long long)c->h_lslot[slot * c->num_k + j]);
-                c->h_lslot[slot * c->num_k + j] = -1;
-                c->live_items--;
-            }
-        }
-        std::sort(pool.begin(), pool.end());
-        merge_free(c->free_l, pool.data(), (int64_t)pool.size(), c->free_tmp);
-    } else if (pool_freed) {
-        merge_free(c->free_l, static_cast<const unsigned long long*>(c->hev_pool.p), n, c->free_tmp);
-    }
-    for (int64_t i = 0; i < nd; ++i) c->h_present[(int64_t)ds[i]] = 0;
+    if (pool_freed) merge_free(c->free_l, static_cast<const unsigned long long*>(c->hev_pool.p), nfreed, c->free_tmp);
+    for (int64_t i = 0; i < nd; ++i) c->h_live[(int64_t)ds[i]] = 0;
     c->live_entries -= nd;
     merge_free(c->free_e, ds, nd, c->free_tmp);
     if (out_dirty_ids) std::memcpy(out_dirty_ids, c->hev_did.p, nd * 8);
     if (out_n_dirty) *out_n_dirty = nd;
     // shrink the scan high-water mark past trailing empty slots
-    while (c->hwm > 0 && c->h_present[c->hwm - 1] == 0) c->hwm--;
+    while (c->hwm > 0 && c->h_live[c->hwm - 1] == 0) c->hwm--;
     if (out_evicted && n) {
         const unsigned long long* sorted = static_cast<const unsigned long long*>(c->hev_sorted.p);
         // item key = score << 35 | id << 3 | j -> (id << 3 | j); entry key = score << 32 | id -> id
@@ -1363,7 +1329,7 @@ cache_status cache_evict_apply(cache_t* c, const cache_evict_state* st, int64_t 
 static int64_t find_slot(const cache_t* c, uint64_t id) {
     if (id > 0xFFFFFFFFull) return -1;
     for (int64_t e = 0; e < c->hwm; ++e)
-        if (c->h_present[e] && c->h_ids[e] == (uint32_t)id) return e;
+        if (c->h_live[e] && c->h_ids[e] == (uint32_t)id) return e;
     return -1;
 }
 

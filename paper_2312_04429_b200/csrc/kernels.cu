@@ -791,11 +791,19 @@ k_evict_apply(uint32_t* __restrict__ present, uint32_t* __restrict__ fcnt, const
         const uint32_t m = e < n_slots ? present[e] : 0u;
         const uint32_t id = m ? ids[e] : 0u;
         if constexpr (GRAN == CACHE_EVICT_ENTRY) {
-            // whole entry: all stored states freed (the host frees their pool slots from its
-            // mirror), entry invalidated; one record per evicted entry in both lists
+            // whole entry: all stored states freed (their pool slots listed in ev_pool, counted
+            // in counters[2]), entry invalidated; one record per evicted entry in both lists
             const unsigned long long key = m ? entry_key<POLICY>(fcnt, lastacc, e, m, id, nk, kv) : 0ull;
             const bool take = m && key <= T;
             const unsigned long long at = warp_claim(&counters[0], take, lane);
+#pragma unroll
+            for (int j = 0; j < CACHE_MAX_K; ++j) {
+                if (j >= nk) break;   // warp-uniform
+                const bool freed = take && ((m >> j) & 1u);
+                const unsigned long long pat = warp_claim(&counters[2], freed, lane);
+                if (freed && pat < ev_cap * (unsigned long long)nk)
+                    ev_pool[pat] = (unsigned long long)(uint32_t)lslot[e * nk + j];
+            }
             if (take) {
                 for (int j = 0; j < nk; ++j) fcnt[e * nk + j] = 0u;
                 present[e] = 0u;

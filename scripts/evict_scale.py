@@ -41,7 +41,17 @@ def main():
         t0 = time.perf_counter()
         ev, dirty = g.evict(k)
         t = time.perf_counter() - t0
-        res[f"evict{rep}"] = dict(n=k, ms=1e3 * t, dirty=len(dirty))
+        # re-insert as many fresh prompts as entries were removed (the C5 round's second half)
+        nn = len(dirty)
+        rows = E.rows(torch.arange(n + 10_000_000 * (rep + 1), n + 10_000_000 * (rep + 1) + nn,
+                                   dtype=torch.int64, device="cuda")) if nn else None
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        if nn:
+            g.insert(rows, None)
+        torch.cuda.synchronize()
+        ti = time.perf_counter() - t1
+        res[f"evict{rep}"] = dict(n=k, ms=1e3 * t, dirty=nn, insert_ms=1e3 * ti)
     # HBM bytes per pass: present + ids (4 + 4) + the policy's per-item column (5 x 4) per slot
     res["bytes_per_pass"] = (n + 1024) * (8 + 20)
     print(json.dumps(res))
