@@ -247,14 +247,18 @@ def run_sharded(args, cfg):
         torch.cuda.synchronize()
         t1 = time.perf_counter()
         nd = comm.all_reduce_sum(torch.tensor([nd], dtype=torch.int64, device="cuda")).item()
+        t_ins = 0.0
         for s0 in range(0, nd, 65536):
             m = min(65536, nd - s0)
-            sc.insert(E.rows(torch.arange(next_row + s0, next_row + s0 + m, dtype=torch.int64, device="cuda")),
-                      None)
-        torch.cuda.synchronize()
-        t2 = time.perf_counter()
+            # the fresh prompts' embeddings are generated outside the timed insert call
+            rows = E.rows(torch.arange(next_row + s0, next_row + s0 + m, dtype=torch.int64, device="cuda"))
+            torch.cuda.synchronize()
+            ta = time.perf_counter()
+            sc.insert(rows, None)
+            torch.cuda.synchronize()
+            t_ins += time.perf_counter() - ta
         next_row += nd
-        tt = torch.tensor([t1 - t0, t2 - t1], device="cuda", dtype=torch.float64)
+        tt = torch.tensor([t1 - t0, t_ins], device="cuda", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         m_ev.append(1e3 * float(tt[0]))
         m_ins.append(1e3 * float(tt[1]))
@@ -472,8 +476,24 @@ def main():
             t = torch.tensor([et], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             et = float(t.item())
+        # the host link's own rate for the same bytes (a plain pinned copy of the query batch):
+        # the end-to-end call cannot beat max(device step, this copy)
+        qd_raw = torch.empty_like(qh, device="cuda")
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        qd_raw.copy_(qh, non_blocking=True)
+        torch.cuda.synchronize()
+        h0.record()
+        for _ in range(args.steps):
+            qd_raw.copy_(qh, non_blocking=True)
+        h1.record()
+        torch.cuda.synchronize()
+        h2d_ms = h0.elapsed_time(h1) / args.steps
+        bound_ms = max(h2d_ms, tot / args.steps)
         e2e = dict(value=b * world * args.steps / (et / 1e3), unit=UNIT, h2d_bytes_per_step=b * D * 4,
                    d2h_bytes_per_step=b * (8 + 4 + 4 + 4),
+                   h2d_gbs=b * D * 4 / (h2d_ms / 1e3) / 1e9,
+                   bound=dict(ms=bound_ms, by="host-to-device copy" if h2d_ms > tot / args.steps else "device step",
+                              frac=bound_ms / (et / args.steps)),
                    note="cache_query_batch_host: fp32 queries from pinned host memory in, ids/scores/K/status "
                         "back to pinned host memory, latent states gathered into the denoiser's device input "
                         "buffer; wall clock around the synchronous call")
