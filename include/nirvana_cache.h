@@ -258,7 +258,8 @@ cache_status cache_evict(cache_t *c, int64_t n, uint64_t *out_evicted, uint64_t 
  * cache_evict_apply evicts this rank's items with key <= st->prefix (the n-th smallest key)
  * and removes its dirty entries.  Outputs are host arrays of capacity `cap`: evicted items
  * (id << 3 | j) in key order, removed entry ids ascending; counts in *out_n / *out_n_dirty.
- * Synchronises `stream`. */
+ * out_evicted and/or out_dirty_ids may be NULL: that list is then neither sorted nor copied
+ * (the counts are still reported).  Synchronises `stream`. */
 cache_status cache_evict_hist(cache_t *c, const cache_evict_state *st, int32_t pass,
                               uint32_t *hist, void *stream);
 cache_status cache_evict_pick(cache_t *c, uint32_t *hist, cache_evict_state *st, int32_t pass,

@@ -402,12 +402,15 @@ class NirvanaCache:
     def push_evict_pick(self, pass_: int, stream=None):
         _check(_lib.cache_push_evict_pick(self._h, pass_, _stream(stream)))
 
-    def push_evict_apply(self, n: int, stream=None):
-        ev = np.empty(max(n, 1), dtype=np.uint64)
-        dirty = np.empty(max(n, 1), dtype=np.uint64)
+    def push_evict_apply(self, n: int, stream=None, lists: bool = True):
+        """lists=False: only the counts come back (returns (n_evicted, n_dirty))."""
+        ev = np.empty(max(n, 1), dtype=np.uint64) if lists else None
+        dirty = np.empty(max(n, 1), dtype=np.uint64) if lists else None
         cnt = np.zeros(1, dtype=np.int64)
         nd = np.zeros(1, dtype=np.int64)
         _check(_lib.cache_push_evict_apply(self._h, n, _ptr(ev), _ptr(cnt), _ptr(dirty), _ptr(nd), _stream(stream)))
+        if not lists:
+            return int(cnt[0]), int(nd[0])
         return ev[: int(cnt[0])].copy(), dirty[: int(nd[0])].copy()
 
     def export_peer(self) -> PeerDesc:
@@ -425,13 +428,16 @@ class NirvanaCache:
     def evict_pick(self, hist: torch.Tensor, state: torch.Tensor, pass_: int, stream=None):
         _check(_lib.cache_evict_pick(self._h, _ptr(hist), _ptr(state), pass_, _stream(stream)))
 
-    def evict_apply(self, state: torch.Tensor, cap: int, stream=None):
-        ev = np.empty(max(cap, 1), dtype=np.uint64)
-        dirty = np.empty(max(cap, 1), dtype=np.uint64)
+    def evict_apply(self, state: torch.Tensor, cap: int, stream=None, lists: bool = True):
+        """lists=False: only the counts come back (returns (n_evicted, n_dirty))."""
+        ev = np.empty(max(cap, 1), dtype=np.uint64) if lists else None
+        dirty = np.empty(max(cap, 1), dtype=np.uint64) if lists else None
         n = np.zeros(1, dtype=np.int64)
         nd = np.zeros(1, dtype=np.int64)
         _check(_lib.cache_evict_apply(self._h, _ptr(state), cap, _ptr(ev), _ptr(n), _ptr(dirty), _ptr(nd),
                                       _stream(stream)))
+        if not lists:
+            return int(n[0]), int(nd[0])
         return ev[: int(n[0])].copy(), dirty[: int(nd[0])].copy()
 
     @property

@@ -86,6 +86,9 @@ struct DevBuf {
         if (e == cudaSuccess) n = need;
         return e;
     }
+    // workspaces whose size creeps up call after call (eviction lists): grow by >= 1.25x so
+    // the next call does not free + reallocate (cudaFree synchronises the device)
+    cudaError_t ensure_grow(size_t need) { return need <= n ? cudaSuccess : ensure(std::max(need, n + n / 4)); }
     void release() {
         if (p) cudaFree(p);
         p = nullptr;
@@ -180,6 +183,9 @@ struct cache_t {
         size_t n = 0;
         cudaError_t ensure(size_t bytes) {
             if (bytes <= n) return cudaSuccess;
+            // >= 1.25x growth: pinning is slow (tens of ms for tens of MB), and eviction sizes
+            // creep up round after round
+            bytes = std::max(bytes, n + n / 4);
             if (p) cudaFreeHost(p);
             p = nullptr;
             n = 0;
@@ -1259,14 +1265,14 @@ cache_status cache_evict_apply(cache_t* c, const cache_evict_state* st, int64_t 
     const int64_t dbound = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(cap, 1), c->live_entries));
     // freed pool slots: one per evicted item, or up to num_k per evicted entry in entry mode
     const int64_t pbound = entry_mode ? bound * c->num_k : bound;
-    CK(c->ekey.ensure(bound));
-    CK(c->ekey2.ensure(std::max(pbound, dbound)));
-    CK(c->epool.ensure(pbound));
-    CK(c->eslot.ensure(bound));
-    CK(c->escr.ensure(sort_scratch_words(std::max(pbound, dbound))));
+    CK(c->ekey.ensure_grow(bound));
+    CK(c->ekey2.ensure_grow(std::max(pbound, dbound)));
+    CK(c->epool.ensure_grow(pbound));
+    CK(c->eslot.ensure_grow(bound));
+    CK(c->escr.ensure_grow(sort_scratch_words(std::max(pbound, dbound))));
     CK(c->ecnt.ensure(3));
-    CK(c->edirty.ensure(dbound));
-    CK(c->edid.ensure(dbound));
+    CK(c->edirty.ensure_grow(dbound));
+    CK(c->edid.ensure_grow(dbound));
     CK(cudaMemsetAsync(c->ecnt.p, 0, 24, s));
     launch_evict_apply(c->present, c->fcnt, c->lastacc, c->ids, c->lslot, c->inv_e, c->hwm, c->km,
                        reinterpret_cast<const EvictState*>(st), c->ekey.p, c->epool.p, c->eslot.p, c->ecnt.p,
@@ -1288,8 +1294,8 @@ cache_status cache_evict_apply(cache_t* c, const cache_evict_state* st, int64_t 
     const bool pool_freed = !c->alias && nfreed > 0;
     CK(c->hev_pool.ensure((pool_freed ? nfreed : 0) * 8));
     CK(c->hev_ds.ensure(nd * 8));
-    CK(c->hev_did.ensure(nd * 8));
-    CK(c->hev_sorted.ensure(n * 8));
+    if (out_dirty_ids) CK(c->hev_did.ensure(nd * 8));
+    if (out_evicted) CK(c->hev_sorted.ensure(n * 8));
     if (pool_freed) {
         launch_sort_u64(c->epool.p, c->ekey2.p, nfreed, c->escr.p, s, 32);
         CK(cudaMemcpyAsync(c->hev_pool.p, c->epool.p, nfreed * 8, cudaMemcpyDeviceToHost, s));
@@ -1297,14 +1303,16 @@ cache_status cache_evict_apply(cache_t* c, const cache_evict_state* st, int64_t 
     if (nd) {
         launch_sort_u64(c->edirty.p, c->ekey2.p, nd, c->escr.p, s, 40);
         CK(cudaMemcpyAsync(c->hev_ds.p, c->edirty.p, nd * 8, cudaMemcpyDeviceToHost, s));
-        launch_sort_u64(c->edid.p, c->ekey2.p, nd, c->escr.p, s, 32);
-        CK(cudaMemcpyAsync(c->hev_did.p, c->edid.p, nd * 8, cudaMemcpyDeviceToHost, s));
+        if (out_dirty_ids) {
+            launch_sort_u64(c->edid.p, c->ekey2.p, nd, c->escr.p, s, 32);
+            CK(cudaMemcpyAsync(c->hev_did.p, c->edid.p, nd * 8, cudaMemcpyDeviceToHost, s));
+        }
     }
     if (out_evicted && n) {
         launch_sort_u64(c->ekey.p, c->ekey2.p, n, c->escr.p, s, 64);
         CK(cudaMemcpyAsync(c->hev_sorted.p, c->ekey.p, n * 8, cudaMemcpyDeviceToHost, s));
     }
-    c->launches += 12 * pool_freed + 24 * (nd > 0) + 24 * (out_evicted && n);
+    c->launches += 12 * pool_freed + 12 * (nd > 0) + 12 * (nd > 0 && out_dirty_ids) + 24 * (out_evicted && n);
     c->live_items -= nfreed;
     CK(cudaStreamSynchronize(s));   // sorted lists landed
     const unsigned long long* ds = static_cast<const unsigned long long*>(c->hev_ds.p);

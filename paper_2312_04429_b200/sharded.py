@@ -155,14 +155,15 @@ class ShardedCache:
             for p in range(8):
                 self.cache.push_evict_hist(n, p)
                 self.cache.push_evict_pick(p)
-            ev, dirty = self.cache.push_evict_apply(n)
+            res = self.cache.push_evict_apply(n, lists=lists)
         else:
             st = torch.tensor([0, 0, n], dtype=torch.int64, device="cuda")
             hist = torch.zeros(256, dtype=torch.int32, device="cuda")
             evict_protocol(self.comm, n, st, hist, self.cache.evict_hist, self.cache.evict_pick)
-            ev, dirty = self.cache.evict_apply(st, n)
+            res = self.cache.evict_apply(st, n, lists=lists)
         if not lists:
-            return len(ev), len(dirty)
+            return res   # this rank's (evicted count, dirty count)
+        ev, dirty = res
         evs = self.comm.all_gather_object(ev.tolist())
         dts = self.comm.all_gather_object(dirty.tolist())
         return _merge_evicted(evs), np.array(sorted(x for d in dts for x in d), dtype=np.uint64)

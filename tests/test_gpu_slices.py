@@ -84,3 +84,33 @@ def test_slices_argument_checks(B):
             g.set_query_slices(bad)
     g.set_query_slices(8)
     g.set_query_slices(0)
+
+
+def test_evict_without_lists_matches(B):
+    """cache_evict with NULL output lists (counts only) leaves exactly the state the listed call
+    does: same live counts, same later lookups, same next eviction (entry and item mode)."""
+    from paper_2312_04429_b200.binding import _lib, _ptr
+    n = 6000
+    emb, cl = synth.entries(n, seed=631)
+    pres = synth.present_masks(n, seed=631)
+    lat = synth.latents_np(np.arange(n), 5, L, seed=631)
+    q = synth.queries(emb, cl, 700, seed=632)[0]
+    for gran in (0, 1):
+        a, b = _cache(B, emb, lat, pres, 0), _cache(B, emb, lat, pres, 0)
+        for g in (a, b):
+            g.set_evict_granularity(gran)
+            g.query(torch.from_numpy(q).cuda())
+        k = 500 if gran else 4000
+        a.evict(k)
+        nd = np.zeros(1, dtype=np.int64)
+        assert _lib.cache_evict(b._h, k, None, None, _ptr(nd), None) == 0
+        assert a.stats() == b.stats()
+        ra, rb = (gpu_to_numpy(g.query(torch.from_numpy(q).cuda())) for g in (a, b))
+        for key in ("ids", "scores", "k"):
+            assert np.array_equal(ra[key], rb[key]), (gran, key)
+        hit = ra["k"] > 0
+        assert np.array_equal(ra["latents"][hit], rb["latents"][hit])
+        ea, eb = a.evict(k // 2), b.evict(k // 2)
+        assert np.array_equal(ea[0], eb[0]) and np.array_equal(ea[1], eb[1])
+        a.close()
+        b.close()
