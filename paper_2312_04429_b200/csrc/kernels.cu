@@ -426,9 +426,17 @@ void launch_score_stream(int kmax, const __nv_bfloat16* emb, const float* inv_e,
 // 32 KiB states into latent_out with 8 16-byte loads in flight per thread, so the
 // merges of one CTA overlap the copies of the others.
 // ---------------------------------------------------------------------------------------
-constexpr int kFinQ = 8;
+// Queries per CTA: the gather is latency-bound on the bytes each SM has in flight (8 x 16 B
+// loads per thread), so top-1 uses 4 queries per CTA capped at 32 registers (8 CTAs = 2,048
+// threads per SM, all 1,024 CTAs of a 4,096-query batch resident at once); top-k > 1 keeps 8
+// (its register top-k needs more registers).
 template <int KMAX>
-__global__ void __launch_bounds__(256)
+struct FinCfg {
+    static constexpr int Q = KMAX == 1 ? 4 : 8;
+    static constexpr int MINB = KMAX == 1 ? 8 : 1;
+};
+template <int KMAX>
+__global__ void __launch_bounds__(256, FinCfg<KMAX>::MINB)
 k_finalize(const Rec* __restrict__ ws, int parts, int64_t B, int topk, const float* __restrict__ inv_q,
            const int32_t* __restrict__ qstatus, const uint32_t* __restrict__ ids,
            const uint32_t* __restrict__ present, const int32_t* __restrict__ lslot,
@@ -437,6 +445,7 @@ k_finalize(const Rec* __restrict__ ws, int parts, int64_t B, int topk, const flo
            KMap km, uint64_t* __restrict__ out_ids, float* __restrict__ out_scores,
            int32_t* __restrict__ out_k, uint8_t* __restrict__ latent_out, void** __restrict__ out_ptr,
            int32_t* __restrict__ out_status) {
+    constexpr int kFinQ = FinCfg<KMAX>::Q;
     __shared__ unsigned long long s_keys[kFinQ][KMAX];
     __shared__ uint32_t s_slots[kFinQ][KMAX];
     __shared__ long long s_src[kFinQ];
@@ -445,11 +454,12 @@ k_finalize(const Rec* __restrict__ ws, int parts, int64_t B, int topk, const flo
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t b0 = (int64_t)blockIdx.x * kFinQ;
     const int64_t b = b0 + warp;
-    if (lane == 0) s_src[warp] = -1;
-    unsigned long long* s_key = s_keys[warp];
-    uint32_t* s_slot = s_slots[warp];
-    const int st = b < B ? qstatus[b] : CACHE_ROW_ZERO_NORM;
-    if (b < B) {
+    const bool mine = warp < kFinQ && b < B;   // warp w merges query b0 + w (warps >= kFinQ only copy)
+    if (lane == 0 && warp < kFinQ) s_src[warp] = -1;
+    unsigned long long* s_key = s_keys[warp < kFinQ ? warp : 0];
+    uint32_t* s_slot = s_slots[warp < kFinQ ? warp : 0];
+    const int st = mine ? qstatus[b] : CACHE_ROW_ZERO_NORM;
+    if (mine) {
         TopK<KMAX> tk;
         tk.init();
         if (st == CACHE_ROW_OK) {
@@ -532,7 +542,8 @@ void launch_finalize(int kmax, const Rec* ws, int parts, int64_t B, int topk, co
                      const KMap& km, uint64_t* out_ids, float* out_scores, int32_t* out_k,
                      uint8_t* latent_out, void** out_ptr, int32_t* out_status, cudaStream_t s, bool pdl) {
     if (B <= 0) return;
-    const unsigned grid = (unsigned)((B + kFinQ - 1) / kFinQ);
+    const int q = kmax == 1 ? FinCfg<1>::Q : FinCfg<16>::Q;
+    const unsigned grid = (unsigned)((B + q - 1) / q);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(256);
