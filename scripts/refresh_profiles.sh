@@ -26,3 +26,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_fi
 for gr in 0 1; do
   timeout 300 python scripts/evict_scale.py 12500000 0 $gr >> ${o}_evict_12p5m.jsonl 2>> ${o}_evict_err.log; echo "evict$gr=$?"
 done
+# memcheck of the newest paths (query slices with the side-stream finalizes; eviction without
+# output lists; entry-mode pool-slot listing)
+timeout 1200 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_slices.py -q -x \
+  -k "argument or without_lists or (1100 and 1-)" > ${o}_sanitizer_memcheck_slices.log 2>&1; echo "memcheck=$?"
