@@ -65,12 +65,48 @@ def _peaks():
 
 
 class Clocks:
-    """nvidia-smi sampler during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock + clock-event-reason sampler during the timed region (B200_PROFILING.md clocks
+    line): NVML polled every ~2 ms on a thread (a C2 timed region lasts only ~15 ms, shorter
+    than nvidia-smi's start-up); nvidia-smi -lms 100 if NVML is unavailable."""
+
+    _BITS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
 
     def __init__(self, index: int):
-        self.index, self.rows, self.proc = index, [], None
+        self.index, self.rows, self.proc, self.nv = index, [], None, None
+        self.stop = threading.Event()
+
+    def _nvml_handle(self):
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        p = torch.cuda.get_device_properties(self.index)
+        try:
+            return pynvml.nvmlDeviceGetHandleByPciBusId(
+                f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0".encode())
+        except Exception:
+            return pynvml.nvmlDeviceGetHandleByIndex(self.index)
 
     def __enter__(self):
+        try:
+            import pynvml
+            h = self._nvml_handle()
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            get_r = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+            first = threading.Event()
+
+            def poll():
+                while not self.stop.is_set():
+                    self.rows.append((pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM), mx, get_r(h)))
+                    first.set()
+                    time.sleep(0.002)
+
+            self.nv = threading.Thread(target=poll, daemon=True)
+            self.nv.start()
+            first.wait(timeout=1.0)   # the first sample precedes the timed region
+            return self
+        except Exception:
+            self.nv = None
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
@@ -89,6 +125,9 @@ class Clocks:
             self.rows.append([x.strip() for x in line.split(",")])
 
     def __exit__(self, *a):
+        if self.nv:
+            self.stop.set()
+            self.nv.join(timeout=1.0)
         if self.proc:
             time.sleep(0.15)
             self.proc.terminate()
@@ -100,13 +139,18 @@ class Clocks:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        if self.nv is not None:
+            sm = [float(r[0]) for r in self.rows]
+            reasons = sorted({name for r in self.rows for bit, name in self._BITS.items() if r[2] & bit})
+            return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(self.rows[0][1]), "reasons": reasons,
+                    "samples": len(self.rows), "source": "nvml"}
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4)
                           if len(r) > 3 + i and r[3 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows), "source": "nvidia-smi"}
 
 
 def build_cache(B, torch, cfg, seed, dev):
