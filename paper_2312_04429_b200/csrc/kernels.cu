@@ -430,12 +430,15 @@ void launch_score_stream(int kmax, const __nv_bfloat16* emb, const float* inv_e,
 // loads per thread), so top-1 uses 4 queries per CTA capped at 32 registers (8 CTAs = 2,048
 // threads per SM, all 1,024 CTAs of a 4,096-query batch resident at once); top-k > 1 keeps 8
 // (its register top-k needs more registers).
+// Small batches (b <= 512, e.g. C3's 1-32 queries) take one query per CTA: the whole CTA copies
+// that query's state in one round of loads instead of four back-to-back rounds.
 template <int KMAX>
 struct FinCfg {
     static constexpr int Q = KMAX == 1 ? 4 : 8;
     static constexpr int MINB = KMAX == 1 ? 8 : 1;
 };
-template <int KMAX>
+constexpr int64_t kFinSmallB = 512;
+template <int KMAX, int QPB = FinCfg<KMAX>::Q>
 __global__ void __launch_bounds__(256, FinCfg<KMAX>::MINB)
 k_finalize(const Rec* __restrict__ ws, int parts, int64_t B, int topk, const float* __restrict__ inv_q,
            const int32_t* __restrict__ qstatus, const uint32_t* __restrict__ ids,
@@ -445,7 +448,7 @@ k_finalize(const Rec* __restrict__ ws, int parts, int64_t B, int topk, const flo
            KMap km, uint64_t* __restrict__ out_ids, float* __restrict__ out_scores,
            int32_t* __restrict__ out_k, uint8_t* __restrict__ latent_out, void** __restrict__ out_ptr,
            int32_t* __restrict__ out_status) {
-    constexpr int kFinQ = FinCfg<KMAX>::Q;
+    constexpr int kFinQ = QPB;
     __shared__ unsigned long long s_keys[kFinQ][KMAX];
     __shared__ uint32_t s_slots[kFinQ][KMAX];
     __shared__ long long s_src[kFinQ];
@@ -542,7 +545,8 @@ void launch_finalize(int kmax, const Rec* ws, int parts, int64_t B, int topk, co
                      const KMap& km, uint64_t* out_ids, float* out_scores, int32_t* out_k,
                      uint8_t* latent_out, void** out_ptr, int32_t* out_status, cudaStream_t s, bool pdl) {
     if (B <= 0) return;
-    const int q = kmax == 1 ? FinCfg<1>::Q : FinCfg<16>::Q;
+    const bool small = B <= kFinSmallB;
+    const int q = small ? 1 : (kmax == 1 ? FinCfg<1>::Q : FinCfg<16>::Q);
     const unsigned grid = (unsigned)((B + q - 1) / q);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
@@ -553,10 +557,10 @@ void launch_finalize(int kmax, const Rec* ws, int parts, int64_t B, int topk, co
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;   // no PDL edge when the launch follows an event wait on a side stream
-#define NV_FIN(KM)                                                                                \
-    cudaLaunchKernelEx(&cfg, k_finalize<KM>, ws, parts, B, topk, inv_q, qstatus, ids, present,    \
-                       lslot, fcnt, lastacc, clock, pool, latent_bytes, km, out_ids, out_scores,  \
-                       out_k, latent_out, out_ptr, out_status)
+#define NV_FIN(KM)                                                                                      \
+    cudaLaunchKernelEx(&cfg, small ? k_finalize<KM, 1> : k_finalize<KM>, ws, parts, B, topk, inv_q, qstatus, \
+                       ids, present, lslot, fcnt, lastacc, clock, pool, latent_bytes, km, out_ids,          \
+                       out_scores, out_k, latent_out, out_ptr, out_status)
     if (kmax == 1) NV_FIN(1);
     else if (kmax == 4) NV_FIN(4);
     else NV_FIN(16);
