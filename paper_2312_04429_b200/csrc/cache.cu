@@ -487,7 +487,7 @@ cache_status cache_insert(cache_t* c, int64_t n, const void* emb, int32_t emb_dt
 // recs_at != nullptr: write the lists there (the caller sized it, see query_sliced) and
 // record no profiling events.
 static cache_status scan_rows(cache_t* c, int64_t b, __nv_bfloat16* qrows, uint32_t* gk, int kmax, cudaStream_t s,
-                              int* parts_out, Rec* recs_at = nullptr) {
+                              int* parts_out, Rec* recs_at = nullptr, bool pad_zeroed = false) {
     const int64_t bpad = (b + 127) / 128 * 128;
     const int64_t n_slots = c->hwm;
     int parts = 0;
@@ -508,7 +508,9 @@ static cache_status scan_rows(cache_t* c, int64_t b, __nv_bfloat16* qrows, uint3
             const bool pair = b > 128 && c->scorer != CACHE_SCORER_TC_SINGLE;
             tp = tc_plan(b, n_slots, c->sm_count, pair);
             parts = tp.parts;
-            if (bpad > b) CK(cudaMemsetAsync(qrows + b * c->dim, 0, (bpad - b) * c->dim * 2, s));
+            // (scan_core zeroes the pad rows before the ingest launch instead: a memset between the
+            // ingest and the scan would break their programmatic-dependent-launch overlap)
+            if (bpad > b && !pad_zeroed) CK(cudaMemsetAsync(qrows + b * c->dim, 0, (bpad - b) * c->dim * 2, s));
             CUtensorMap tm_q;
             if (!encode_rows(&tm_q, qrows, bpad, c->dim, 128))
                 return fail(CACHE_E_CUDA, "query: cuTensorMapEncodeTiled failed");
@@ -541,10 +543,11 @@ static cache_status scan_core(cache_t* c, int64_t b, const void* queries, int32_
     CK(c->invq.ensure(bpad));
     CK(c->qstat.ensure(bpad));
     CK(c->gk.ensure(bpad));
+    if (bpad > b) CK(cudaMemsetAsync(c->qbuf.p + b * c->dim, 0, (bpad - b) * c->dim * 2, s));   // tile padding
     if (c->prof_on) CK(cudaEventRecord(c->prof[0], s));
     launch_normalise(queries, q_dtype, b, c->dim, c->qbuf.p, c->invq.p, c->qstat.p, s, c->gk.p);
     c->launches++;
-    return scan_rows(c, b, c->qbuf.p, c->gk.p, kmax, s, parts_out);
+    return scan_rows(c, b, c->qbuf.p, c->gk.p, kmax, s, parts_out, nullptr, true);
 }
 
 // Number of device query slices for a batch of b (1 = one scan launch).

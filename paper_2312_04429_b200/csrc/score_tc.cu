@@ -265,6 +265,20 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ C
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // The entry tiles do not depend on the ingest kernel: the producer issues the first STAGES
+    // stages' entry loads (into the empty ring) before waiting for it, their query loads after.
+    int pre = 0;
+    if (warp == 0 && lane == 0) {
+        for (int u = blockIdx.x; u < n_units && pre < STAGES; u += gridDim.x) {
+            const int chunk = u / m_tiles;
+            const int n0 = chunk * chunk_tiles, n1 = min(n_tiles, n0 + chunk_tiles);
+            for (int n = n0; n < n1 && pre < STAGES; ++n)
+                for (int kc = 0; kc < kch && pre < STAGES; ++kc, ++pre) {
+                    mbar_expect_tx(bar_full + 8 * pre, STAGE_BYTES);
+                    tma_load_2d(sbase + pre * STAGE_BYTES + A_BYTES, &tmap_e, bar_full + 8 * pre, kc * BK, n * BN);
+                }
+        }
+    }
     pdl_wait();      // queries / inv-norms / gate words of the ingest kernel are visible from here
     pdl_trigger();
 
@@ -272,16 +286,21 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ C
         // ------------------------------- TMA producer -------------------------------
         if (lane == 0) {
             uint32_t stage = 0, phase = 0;
+            int it = 0;
             for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
                 const int chunk = u / m_tiles, m = u - chunk * m_tiles;
                 const int n0 = chunk * chunk_tiles, n1 = min(n_tiles, n0 + chunk_tiles);
                 for (int n = n0; n < n1; ++n) {
-                    for (int kc = 0; kc < kch; ++kc) {
-                        mbar_wait(bar_empty + 8 * stage, phase ^ 1);
+                    for (int kc = 0; kc < kch; ++kc, ++it) {
                         const uint32_t sa = sbase + stage * STAGE_BYTES;
-                        mbar_expect_tx(bar_full + 8 * stage, STAGE_BYTES);
-                        tma_load_2d(sa, &tmap_q, bar_full + 8 * stage, kc * BK, m * BM);
-                        tma_load_2d(sa + A_BYTES, &tmap_e, bar_full + 8 * stage, kc * BK, n * BN);
+                        if (it < pre) {   // entry half already in flight, stage's tx already expected
+                            tma_load_2d(sa, &tmap_q, bar_full + 8 * stage, kc * BK, m * BM);
+                        } else {
+                            mbar_wait(bar_empty + 8 * stage, phase ^ 1);
+                            mbar_expect_tx(bar_full + 8 * stage, STAGE_BYTES);
+                            tma_load_2d(sa, &tmap_q, bar_full + 8 * stage, kc * BK, m * BM);
+                            tma_load_2d(sa + A_BYTES, &tmap_e, bar_full + 8 * stage, kc * BK, n * BN);
+                        }
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
                 }
@@ -581,6 +600,22 @@ k_score_tc2(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ 
     cluster_sync_all();   // peer barriers initialised, TMEM allocated in both CTAs
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // Entry tiles first (independent of the ingest kernel), as in the single-CTA kernel: both
+    // CTAs issue their halves of the first STAGES stages' entry tiles before the PDL wait; the
+    // leader's barrier expects all four loads of a stage once.
+    int pre = 0;
+    if (warp == 0 && lane == 0) {
+        for (int u = cid; u < n_units && pre < STAGES; u += n_clusters) {
+            const int chunk = u / m_pairs;
+            const int n0 = chunk * chunk_tiles, n1 = min(n_tiles, n0 + chunk_tiles);
+            for (int n = n0; n < n1 && pre < STAGES; ++n)
+                for (int kc = 0; kc < kch && pre < STAGES; ++kc, ++pre) {
+                    if (rank == 0) mbar_expect_tx(bar_full + 8 * pre, 2 * STAGE_BYTES);
+                    tma_load_2d_pair(sbase + pre * STAGE_BYTES + A_BYTES, &tmap_e, bar_full + 8 * pre, kc * BK,
+                                     n * BN + (int)rank * (BN / 2));
+                }
+        }
+    }
     pdl_wait();      // queries / inv-norms / gate words of the ingest kernel are visible from here
     pdl_trigger();
 
@@ -588,18 +623,23 @@ k_score_tc2(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ 
         // ------------------------------- TMA producer (both CTAs) ---------------------
         if (lane == 0) {
             uint32_t stage = 0, phase = 0;
+            int it = 0;
             for (int u = cid; u < n_units; u += n_clusters) {
                 const int chunk = u / m_pairs, mp = u - chunk * m_pairs;
                 const int n0 = chunk * chunk_tiles, n1 = min(n_tiles, n0 + chunk_tiles);
                 const int qrow = (2 * mp + (int)rank) * BM;
                 for (int n = n0; n < n1; ++n) {
-                    for (int kc = 0; kc < kch; ++kc) {
-                        mbar_wait(bar_empty + 8 * stage, phase ^ 1);
+                    for (int kc = 0; kc < kch; ++kc, ++it) {
                         const uint32_t sa = sbase + stage * STAGE_BYTES;
-                        if (rank == 0) mbar_expect_tx(bar_full + 8 * stage, 2 * STAGE_BYTES);
-                        tma_load_2d_pair(sa, &tmap_q, bar_full + 8 * stage, kc * BK, qrow);
-                        tma_load_2d_pair(sa + A_BYTES, &tmap_e, bar_full + 8 * stage, kc * BK,
-                                         n * BN + (int)rank * (BN / 2));
+                        if (it < pre) {   // entry half already in flight, stage's tx already expected
+                            tma_load_2d_pair(sa, &tmap_q, bar_full + 8 * stage, kc * BK, qrow);
+                        } else {
+                            mbar_wait(bar_empty + 8 * stage, phase ^ 1);
+                            if (rank == 0) mbar_expect_tx(bar_full + 8 * stage, 2 * STAGE_BYTES);
+                            tma_load_2d_pair(sa, &tmap_q, bar_full + 8 * stage, kc * BK, qrow);
+                            tma_load_2d_pair(sa + A_BYTES, &tmap_e, bar_full + 8 * stage, kc * BK,
+                                             n * BN + (int)rank * (BN / 2));
+                        }
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
                 }
