@@ -26,6 +26,10 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--scorers", default="stream,tc")
     ap.add_argument("--topks", default="1", help="comma list of topk values (fused top-k width)")
+    ap.add_argument("--flush", default="write", choices=["write", "write+read", "none"],
+                    help="L2 treatment between steps: write 512 MiB (bench.py's rule; the dirty lines are "
+                         "written back during the next step), write then read a second 512 MiB buffer "
+                         "(cold and clean), or nothing")
     a = ap.parse_args()
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     n, L = a.n, 32768 if a.latents else 0
@@ -38,6 +42,7 @@ def main():
         g.insert(torch.from_numpy(emb[s:s + m]).cuda(), lat, present=pres[s:s + m])
         del lat
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    flush2 = torch.ones(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda") if a.flush == "write+read" else None
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     g.set_profile_events(ev)
     bmax = max(int(x) for x in a.batches.split(","))
@@ -53,7 +58,10 @@ def main():
                 g.query_into(q, out, topk=topk)
             st, sc, fi = [], [], []
             for _ in range(a.steps):
-                flush.fill_(1.0)
+                if a.flush != "none":
+                    flush.fill_(1.0)
+                if flush2 is not None:
+                    flush2.sum()
                 g.query_into(q, out, topk=topk)
                 ev[3].synchronize()
                 st.append(ev[0].elapsed_time(ev[3]))
@@ -61,7 +69,7 @@ def main():
                 fi.append(ev[2].elapsed_time(ev[3]))
             ms = statistics.median(st)
             scm = statistics.median(sc)
-            rec = dict(scorer=scorer, n=n, b=b, topk=topk, step_ms=ms, score_ms=scm, finalize_ms=statistics.median(fi),
+            rec = dict(scorer=scorer, n=n, b=b, topk=topk, flush=a.flush, step_ms=ms, score_ms=scm, finalize_ms=statistics.median(fi),
                        lookups_per_s=b / (ms / 1e3),
                        score_hbm_frac=n * 1540 / (scm / 1e3) / 1e9 / peaks["hbm_gbs"],
                        score_tensor_frac=2 * b * n * 768 / (scm / 1e3) / 1e12 / peaks["bf16_tflops"])
