@@ -418,11 +418,11 @@ void launch_score_stream(int kmax, const __nv_bfloat16* emb, const float* inv_e,
 }
 
 // ---------------------------------------------------------------------------------------
-// Finalize + gather: 8 queries per 256-thread CTA.  Warp w merges query b0+w's `parts`
+// Finalize + gather: Q queries per 256-thread CTA (see FinCfg).  Warp w < Q merges query b0+w's `parts`
 // partial lists under the total order (R3) -> top-k; its lane 0 applies the Fig. 11 map
 // (largest j with s > thr[j], strict, compared in fp64 on the clamped fp32
 // score), the knob (R20) and the hole rule (m = present & ((2 << j*) - 1),
-// j = 31 - clz(m)) and counts the access.  Then the whole CTA streams the (up to 8) selected
+// j = 31 - clz(m)) and counts the access.  Then the whole CTA streams the (up to Q) selected
 // 32 KiB states into latent_out with 8 16-byte loads in flight per thread, so the
 // merges of one CTA overlap the copies of the others.
 // ---------------------------------------------------------------------------------------
