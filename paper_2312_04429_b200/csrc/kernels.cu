@@ -147,16 +147,20 @@ __device__ __forceinline__ void normalise_row(const Tin* __restrict__ xr, int la
     for (int k = 0; k < NS; ++k) {
         const double x = (double)load_in<Tin>(xr + lane + 32 * k);
         const double y = __dmul_rn(x, rnu);
-        const unsigned long long u = (unsigned long long)__double_as_longlong(y);
-        const long long dm = (long long)(u & ((1ull << 45) - 1)) - (1ll << 44);
-        // 0 < |y| < 2^-120 as one unsigned compare of the sign-stripped pattern (u << 1)
-        near |= (dm <= 16 && dm >= -16) || ((u << 1) - 1ull < (0x3870000000000000ull << 1) - 1ull);
-        const unsigned long long r = (u + (1ull << 44)) & ~((1ull << 45) - 1);   // RNE to bf16 precision
-        const uint32_t hi = (uint32_t)(r >> 32);
-        const uint32_t e11 = (hi >> 20) & 0x7FFu;
-        const uint32_t bits = ((hi >> 16) & 0x8000u) | (e11 ? ((e11 - 896u) << 7) : 0u) | ((hi >> 13) & 0x7Fu);
+        // all on 32-bit halves (the 64-bit forms cost ~2x the integer instructions, and the
+        // kernel is issue-bound: ncu s24, 55% issue slots busy)
+        const uint32_t lo = (uint32_t)__double2loint(y), hi = (uint32_t)__double2hiint(y);
+        // near a midpoint: |(u mod 2^45) - 2^44| <= 16  <=>  (u + 2^44 + 16) mod 2^45 <= 32
+        uint32_t tlo, thi;
+        asm("add.cc.u32 %0, %2, 16;\n\taddc.u32 %1, %3, 4096;" : "=r"(tlo), "=r"(thi) : "r"(lo), "r"(hi));
+        const uint32_t ahi = hi & 0x7FFFFFFFu;
+        near |= (((thi & 0x1FFFu) == 0u) & (tlo <= 32u)) | ((ahi < 0x38700000u) & ((ahi | lo) != 0u));
+        // RNE to bf16 precision: + 2^44 (bit 12 of the high word), clear bits 0..44 (the low
+        // word entirely); the bf16 is sign | (e11 - 896) << 7 | top 7 mantissa bits
+        const uint32_t rhi = (hi + 0x1000u) & ~0x1FFFu;
+        const uint32_t bits = ((rhi >> 16) & 0x8000u) | ((rhi & 0x7FF00000u) ? ((rhi >> 13) & 0x3FFFFu) - 0x1C000u : 0u);
         put_bf16(o, ybase + lane + 32 * k, __ushort_as_bfloat16((unsigned short)bits));
-        const double yd = __longlong_as_double((long long)r);   // == the stored bf16, exactly
+        const double yd = __hiloint2double((int)rhi, 0);   // == the stored bf16, exactly
         v[k] = __dmul_rn(yd, yd);
     }
     if (__any_sync(0xFFFFFFFFu, near)) {   // warp-uniform, rare
