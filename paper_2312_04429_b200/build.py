@@ -39,17 +39,22 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    objs = []
-    logs = []
-    for src in SOURCES:
+    extra = os.environ.get("NV_BUILD_EXTRA_FLAGS", "").split()   # experiments only (e.g. -DNV_EXP_...)
+
+    def compile_one(src):
         obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        extra = os.environ.get("NV_BUILD_EXTRA_FLAGS", "").split()   # experiments only (e.g. -DNV_EXP_...)
         cmd = [_nvcc(), *ARCH, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
-        logs.append(r.stdout + r.stderr)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{r.stdout}\n{r.stderr}")
-        objs.append(obj)
+        return obj, r.stdout + r.stderr
+
+    # the translation units are independent: compile them concurrently
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
+        res = list(ex.map(compile_one, SOURCES))
+    objs = [o for o, _ in res]
+    logs = [l for _, l in res]
     tmp = LIB + f".{os.getpid()}.tmp"
     cmd = [_nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
     r = subprocess.run(cmd, capture_output=True, text=True)
