@@ -1,7 +1,8 @@
 """Eviction at C5's per-rank scale (100M entries over 8 GPUs -> 12.5M per rank):
 LCBFU cache_evict of 1% of the live items after a few query batches, timed end to end (the
-call is host-synchronous) plus the kernel split from a CUDA-event-free wall clock.
-usage: python scripts/evict_scale.py [n_entries] [policy] [granularity]"""
+call is host-synchronous), then the re-insertion of as many fresh prompts as entries were
+removed; EVICT_REPS rounds (default 3).
+usage: [EVICT_REPS=n] python scripts/evict_scale.py [n_entries] [policy] [granularity]"""
 import json
 import sys
 import time
