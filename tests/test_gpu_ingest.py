@@ -1,11 +1,15 @@
-"""Ingest normalisation at volume: every stored bf16 row is bit-identical to the oracle's
-bf16_RNE(x / ||x||) (R2) -- 20,000 rows of mixed magnitudes, fp32 and bf16 inputs, plus rows
-whose quotients land exactly on bf16 rounding midpoints (the exact-division fallback path)."""
+"""Ingest normalisation at volume: stored bf16 rows equal the oracle's plain bf16_RNE(x / ||x||)
+with the index-order fp64 norm (R2) bit for bit, up to the proved summation-order accept set
+(tests/parity.py check_stored_row: a component may differ only where the exact quotient lies
+within the fp64 error bound of a bf16 midpoint; the count is reported and expected 0) --
+2,000 of 20,000 rows of mixed magnitudes, fp32 and bf16 inputs, plus rows whose quotients lie
+close to bf16 rounding midpoints (the kernel's exact-division fallback path)."""
 import numpy as np
 import pytest
 import torch
 
 import synth
+from tests.parity import check_stored_row
 
 pytestmark = pytest.mark.gpu
 
@@ -32,9 +36,12 @@ def test_stored_rows_bit_identical_at_volume(oracle_mod):
         emb[i] = row
     g = B.NirvanaCache(entry_capacity=n, latent_capacity=5 * n, dim=768, latent_bytes=0)
     g.insert(torch.from_numpy(emb).cuda())
-    for i in list(range(60)) + list(rng.choice(n, 500, replace=False)):
+    accepted = 0
+    for i in list(range(60)) + list(rng.choice(n, 2000, replace=False)):
         _, y = oracle_mod.normalise(emb[i].astype(np.float64))
-        assert np.array_equal(g.row_bf16(int(i)), _bits(y)), i
+        accepted += check_stored_row(g.row_bf16(int(i)), emb[i], y)
+    print(f"stored-row accept-set components (fp32 inputs): {accepted}")
+    assert accepted == 0
     # bf16 inputs go through the same rule
     eb = torch.from_numpy(emb[:300]).to(torch.bfloat16)
     g2 = B.NirvanaCache(entry_capacity=300, latent_capacity=1500, dim=768, latent_bytes=0)
@@ -42,5 +49,5 @@ def test_stored_rows_bit_identical_at_volume(oracle_mod):
     ebits = eb.view(torch.int16).numpy().view(np.uint16)
     o = oracle_mod.OracleCache(dim=768, entry_capacity=300)
     o.insert(ebits, emb_is_bf16=True)
-    for i in range(300):
-        assert np.array_equal(g2.row_bf16(i), _bits(o.row(i))), i
+    xb = eb.float().numpy()
+    assert sum(check_stored_row(g2.row_bf16(i), xb[i], o.row(i)) for i in range(300)) == 0

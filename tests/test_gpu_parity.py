@@ -4,7 +4,7 @@ import pytest
 import torch
 
 import synth
-from tests.parity import check_batch, gpu_to_numpy
+from tests.parity import check_batch, check_stored_row, gpu_to_numpy
 
 pytestmark = pytest.mark.gpu
 
@@ -44,9 +44,12 @@ def _set(g, B, scorer):
 
 
 def test_stored_rows_bit_identical(B, oracle_mod):
+    """Stored rows equal the oracle's plain index-order normalisation bit for bit, up to the
+    proved summation-order accept set (tests/parity.py check_stored_row; expected count 0)."""
     g, o, emb, _, _ = _make(B, oracle_mod, 300, L=0, seed=3)
-    for i in range(300):
-        assert np.array_equal(g.row_bf16(i), _bf16_bits(o.row(i))), i
+    accepted = sum(check_stored_row(g.row_bf16(i), emb[i], o.row(i)) for i in range(300))
+    print(f"stored-row accept-set components: {accepted}")
+    assert accepted == 0
 
 
 @pytest.mark.parametrize("scorer", SCORERS)
@@ -116,7 +119,7 @@ def test_other_dims(B, oracle_mod, scorer, dim):
     g, o, emb, cl, lat = _make(B, oracle_mod, n, dim=dim, seed=dim)
     _set(g, B, scorer)
     for i in (0, 123, n - 1):
-        assert np.array_equal(g.row_bf16(i), _bf16_bits(o.row(i)))
+        assert check_stored_row(g.row_bf16(i), emb[i], o.row(i)) == 0
     q, _, _ = synth.queries(emb, cl, b, seed=dim + 1)
     out = gpu_to_numpy(g.query(torch.from_numpy(q).cuda(), topk=4))
     check_batch(out, o, q, 4, expected_latent=lambda e, k: lat[e, synth.K_VALUES.index(k)])
@@ -247,8 +250,8 @@ def test_scorers_agree_bitwise_on_ids(B, oracle_mod):
 
 def test_full_size_sampled_parity_c2(B, oracle_mod):
     """C2 at full size in the bench's launch configuration (100K entries, B = 4,096, TC path):
-    every query's (entry, K, score) checked against the oracle on a sample of 24 queries, plus
-    properties that hold at any size for all queries."""
+    (entry, K, every score) of 512 sampled queries checked against the oracle's exact scan of all
+    100K entries (16 host threads), plus properties that hold at any size for all queries."""
     n, b, L = 100_000, 4096, 32768
     emb, cl = synth.entries(n, seed=1001)
     pres = synth.present_masks(n, seed=1001)
@@ -268,8 +271,9 @@ def test_full_size_sampled_parity_c2(B, oracle_mod):
         e, k = int(out["ids"][i, 0]), int(out["k"][i])
         exp = synth.latent_np([e], synth.K_VALUES.index(k), L, seed=1001)[0]
         assert np.array_equal(out["latents"][i], exp)
-    rows = list(np.random.default_rng(3).choice(b, 24, replace=False))
+    rows = list(np.random.default_rng(3).choice(b, 510, replace=False)) + [0, b - 1]
     rep = check_batch(out, o, q, 1, rows=rows, adopt=False)
+    print(rep)
     assert rep["max_dscore"] < 1e-4
 
 
@@ -298,8 +302,8 @@ def test_aliased_latent_pool(B, oracle_mod):
 
 def test_full_size_sampled_parity_c3(B, oracle_mod):
     """C3's shape: 1M entries, B = 32 (the HBM-bound single-CTA scan, hundreds of partial lists
-    per query to merge), top-4; 8 sampled queries against the oracle's exact fp64 scan of all
-    1M entries, and the batch-wide properties for every query."""
+    per query to merge), top-4; all 32 queries, every rank, against the oracle's exact fp64 scan of
+    all 1M entries, and the batch-wide properties for every query."""
     n, b = 1_000_000, 32
     emb, cl = synth.entries(n, seed=3001)
     g = B.NirvanaCache(entry_capacity=n, dim=768, latent_bytes=0, latent_capacity=5 * n)
@@ -312,8 +316,8 @@ def test_full_size_sampled_parity_c3(B, oracle_mod):
     o = oracle_mod.OracleCache(dim=768, entry_capacity=n, latent_bytes=0)
     o.insert(emb)
     del emb
-    rows = list(np.random.default_rng(4).choice(b, 8, replace=False))
-    rep = check_batch(out, o, q, 4, rows=rows, adopt=False)
+    rep = check_batch(out, o, q, 4, adopt=False)
+    print(rep)
     assert rep["max_dscore"] < 1e-4
 
 
@@ -329,6 +333,7 @@ def test_large_batch_pair_kernel(B, oracle_mod):
     assert (out["ids"][:, 0] < n).all()
     o = oracle_mod.OracleCache(dim=768, entry_capacity=n, latent_bytes=0)
     o.insert(emb)
-    rows = list(np.random.default_rng(5).choice(b, 32, replace=False)) + [0, b - 1]
+    rows = list(np.random.default_rng(5).choice(b, 254, replace=False)) + [0, b - 1]
     rep = check_batch(out, o, q, 1, rows=rows, adopt=False)
+    print(rep)
     assert rep["max_dscore"] < 1e-4
