@@ -1,15 +1,20 @@
 """Benchmark of the batched NIRVANA cache lookup (BASELINE.json metric) on B200.
 
-python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c1|c4|c5] [--batch B]
+python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4|c2|c3|c5|c1] [--batch B]
 python bench.py --impl reference ...     (the fp64 CPU oracle, timed on the host cores)
 
-One step = one full lookup batch through the C ABI: query ingest (normalise + bf16), exact
-cosine scan of every cached entry with fused top-k, cross-split merge + Fig. 11 K map + hole
-rule, latent gather of the hit states and LCBFU access counters.  Inputs are seeded,
-synthetic, resident in HBM; L2 is flushed (a 512 MiB write) between timed steps and the
-step time is taken with CUDA events on the launching stream.  For N > 1 every rank holds
-its own replica of the cache and serves its own batches (weak scaling, no data-path
-collective); the max over ranks is reported.  Rank 0 prints one JSON line.
+One step = one full lookup batch: query ingest (normalise + bf16), exact cosine scan of every
+cached entry with fused top-k, merge across scan splits (and across shards), Fig. 11 K map +
+hole rule, latent gather of the hit states and LCBFU access counters.  Inputs are seeded,
+synthetic, resident in HBM; L2 is flushed (a 512 MiB write) between timed steps and the step
+time is taken with CUDA events on the launching stream, max over ranks.
+
+Default workload: C4 (BASELINE.json configs[3]) -- one 10M-entry cache sharded over the N
+GPUs, a 16,384-query global batch (16,384/N queries brought by each rank), strong scaling, so
+that N = 1, 2, 4, 8 form one curve.  `--gpus N` without a torchrun environment re-launches
+this script under torch.distributed.run with N ranks (one per GPU, rendezvous on 127.0.0.1).
+`--config c2` is the 100K-entry single-GPU tensor-core workload (N > 1: independent replicas).
+Rank 0 prints one JSON line.
 """
 from __future__ import annotations
 
@@ -43,7 +48,7 @@ CONFIGS = {
     # configs[3]: 10M entries sharded across the N GPUs, 16K-query global batches (strong scaling)
     "c4": dict(n=10_000_000, b=16384, sharded=True,
                workload="C4: 10M cached entries x 768-d bf16 sharded across N B200, 16,384-query global batches, "
-                        "NCCL all-gather top-k merge, P2P latent fetch"),
+                        "top-1 merge across shards, K map, P2P latent fetch"),
     # configs[4]: 100M entries sharded across the N GPUs (the whole cache on one B200 at N = 1:
     # 154 GB of bf16 rows + 7 GB of metadata), Zipf-popular queries over entries, and every
     # round = one 16K-query lookup batch + LCBFU eviction of 1% of the live items + re-insertion
@@ -185,10 +190,14 @@ def _oracle_queries_parallel(o, rows, nthreads):
         list(ex.map(lambda r: o.query(r[None, :], topk=1, want_latents=False, apply_counters=False), rows))
 
 
-def cpu_baseline(emb, pres, q, budget_s=12.0):
+def cpu_baseline(emb, pres, q, budget_s=12.0, n_total=None):
     """Time the fp64 oracle (as it stands) on a bounded sample of the same workload: on one
-    host thread, then on every host core (one query per thread at a time)."""
+    host thread, then on every host core (one query per thread at a time).  When emb is a
+    slice of a larger cache (n_total rows; C4/C5), the scan cost is linear in the number of
+    entries, so the rate over the slice is scaled by len(emb) / n_total to the full cache."""
     import oracle
+    n_total = n_total or emb.shape[0]
+    scale = emb.shape[0] / n_total
     o = oracle.OracleCache(dim=D, entry_capacity=emb.shape[0], latent_bytes=0)
     o.insert(emb, present=pres)
     done, t0 = 0, time.perf_counter()
@@ -204,45 +213,68 @@ def cpu_baseline(emb, pres, q, budget_s=12.0):
     _oracle_queries_parallel(o, q[:m], nt)
     dtn = time.perf_counter() - t0
     o.close()
-    return dict(value=m / dtn, unit=UNIT, cores=nt, kind="oracle",
-                sample=f"{m} queries of the same batch against the full {emb.shape[0]}-entry cache "
+    what = (f"the full {emb.shape[0]}-entry cache" if scale == 1 else
+            f"the first {emb.shape[0]} entries of the {n_total}-entry cache, rate x {scale:.4g} "
+            f"(the exhaustive scan is linear in the entry count)")
+    return dict(value=m / dtn * scale, unit=UNIT, cores=nt, kind="oracle",
+                sample=f"{m} queries of the same batch against {what} "
                        f"(fp64 scan + full sort + K map + holes; stored without latent payload bytes), "
                        f"{nt} host threads, {dtn:.1f} s",
-                single_thread=dict(value=v1, cores=1, sample=f"{done} queries, {dt1:.1f} s"))
+                single_thread=dict(value=v1 * scale, cores=1, sample=f"{done} queries, {dt1:.1f} s"))
+
+
+REF_SLICE = int(os.environ.get("REF_SLICE", "200000"))   # entries of a C4/C5 cache the oracle scans per sampled query (rate scaled)
 
 
 def run_reference(args, cfg):
+    """The reference arm: the fp64 oracle, unchanged, on the host cores (rank 0 only; other
+    ranks exit without work).  Each step = one query per host thread of the workload's batch
+    against the full cache (C1-C3) or against a REF_SLICE-entry slice of it with the rate
+    scaled to the full cache (C4/C5: 10M-100M entries x 768 fp64 do not fit a bounded sample)."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if rank != 0:
         return
     import synth
     n = cfg["n"]
-    emb, cl = synth.entries(n, seed=1000)
-    pres = synth.present_masks(n, seed=1000)
-    q, _, _ = synth.queries(emb, cl, cfg["b"], seed=1001)
+    if cfg.get("sharded"):
+        import torch
+        ns = min(n, REF_SLICE)
+        E = synth.TorchEntries(ns, seed=1000, device="cpu")
+        emb = E.rows(torch.arange(ns, dtype=torch.int64)).numpy()
+        pres = synth.present_masks(ns, seed=1000)
+        q = E.queries(min(cfg["b"], 4096), qseed=1001)[0].numpy()
+        scale = ns / n
+        sample = (f"{{per_step}} queries per step against a {ns}-entry slice of the {n}-entry cache (same "
+                  f"recipe), rate x {scale:.4g} (the exhaustive scan is linear in the entry count)")
+    else:
+        emb, cl = synth.entries(n, seed=1000)
+        pres = synth.present_masks(n, seed=1000)
+        q, _, _ = synth.queries(emb, cl, cfg["b"], seed=1001)
+        scale = 1.0
+        sample = f"{{per_step}} queries per step of the {cfg['b']}-query batch, full {n}-entry scan"
     import oracle
-    o = oracle.OracleCache(dim=D, entry_capacity=n, latent_bytes=0)
+    o = oracle.OracleCache(dim=D, entry_capacity=emb.shape[0], latent_bytes=0)
     o.insert(emb, present=pres)
     nt = _host_threads()
     # one query per host thread per step (the oracle unchanged; see _oracle_queries_parallel)
-    per_step = max(1, min(cfg["b"], int(os.environ.get("REF_QUERIES_PER_STEP", str(nt)))))
+    per_step = max(1, min(q.shape[0], int(os.environ.get("REF_QUERIES_PER_STEP", str(nt)))))
     for w in range(args.warmup):
         _oracle_queries_parallel(o, q[:per_step], nt)
-    times = []
+    times, done = [], 0
     for s in range(args.steps):
-        sel = q[(s * per_step) % cfg["b"]:][:per_step]
+        sel = q[(s * per_step) % q.shape[0]:][:per_step]
         t0 = time.perf_counter()
         _oracle_queries_parallel(o, sel, nt)
         times.append(time.perf_counter() - t0)
-    v = sum(len(q[(s * per_step) % cfg["b"]:][:per_step]) for s in range(args.steps)) / sum(times)
-    line = dict(impl="reference", metric=METRIC, value=v, unit=UNIT, n_gpus=args.gpus, steps=args.steps,
+        done += len(sel)
+    v = done / sum(times) * scale
+    line = dict(impl="reference", metric=METRIC, value=v, unit=UNIT, n_gpus=world, steps=args.steps,
                 warmup=args.warmup, ms_per_step=1e3 * statistics.mean(times), higher_is_better=True,
-                scaling="weak", vs_baseline=None, dtype="f64", data="synthetic",
+                scaling="strong" if cfg.get("sharded") else "weak", vs_baseline=None, dtype="f64", data="synthetic",
                 config=dict(workload=cfg["workload"], entries=n, batch=cfg["b"], dim=D, latent_bytes=L, topk=1,
                             parallelism=f"{nt} host threads (fp64 oracle, one query per thread)"),
-                cpu_baseline=dict(value=v, unit=UNIT, cores=nt, kind="oracle",
-                                  sample=f"{per_step} queries per step of the {cfg['b']}-query batch, "
-                                         f"full {n}-entry scan, {nt} host threads"),
+                cpu_baseline=dict(value=v, unit=UNIT, cores=nt, kind="oracle", sample=sample.format(per_step=per_step)),
                 e2e=dict(value=v, unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0))
     print(json.dumps(line), flush=True)
 
@@ -258,9 +290,14 @@ def run_sharded(args, cfg):
     import synth
 
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
+    os.environ.setdefault("MASTER_PORT", str(_free_port()))
     os.environ.setdefault("RANK", "0")
     os.environ.setdefault("WORLD_SIZE", "1")
+    if int(os.environ["WORLD_SIZE"]) > 1:
+        # NCCL's communicator set-up lines (ranks, transports) go to the log (stderr), not stdout
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -355,6 +392,56 @@ def run_sharded(args, cfg):
     t = torch.tensor([sum(step_ms)], device="cuda", dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     tot = float(t.item())
+    k_np = out["k"].cpu().numpy()
+    # end to end through the public sharded API (ShardedCache.query_host): every step copies
+    # this rank's fp32 query rows from pinned host memory, runs the collective lookup and reads
+    # ids / scores / K / status back into pinned host memory; max over ranks of the wall time
+    e2e = None
+    if not args.no_e2e:
+        qh = q.cpu().pin_memory()
+        ho = dict(ids=torch.empty((bl, 1), dtype=torch.int64).pin_memory(),
+                  scores=torch.empty((bl, 1), dtype=torch.float32).pin_memory(),
+                  k=torch.empty(bl, dtype=torch.int32).pin_memory(),
+                  status=torch.empty(bl, dtype=torch.int32).pin_memory())
+        for _ in range(2):
+            sc.query_host(qh, ho, out)
+        e_ms = []
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            sc.query_host(qh, ho, out)
+            e_ms.append(1e3 * (time.perf_counter() - t0))
+        et = torch.tensor([sum(e_ms)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        et = float(et.item())
+        qd_raw = torch.empty_like(qh, device="cuda")
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        qd_raw.copy_(qh, non_blocking=True)
+        torch.cuda.synchronize()
+        h0.record()
+        for _ in range(args.steps):
+            qd_raw.copy_(qh, non_blocking=True)
+        h1.record()
+        torch.cuda.synchronize()
+        h2d_ms = h0.elapsed_time(h1) / args.steps
+        bound_ms = max(h2d_ms, tot / args.steps)
+        if not maint:   # (C5's eviction rounds change the cache between the two measurements)
+            assert np.array_equal(ho["k"].numpy(), k_np), "host-API lookup disagrees with the device-buffer lookup"
+        e2e = dict(value=b * args.steps / (et / 1e3), unit=UNIT, h2d_bytes_per_step=b * D * 4,
+                   d2h_bytes_per_step=b * (8 + 4 + 4 + 4), h2d_gbs=bl * D * 4 / (h2d_ms / 1e3) / 1e9,
+                   bound=dict(ms=bound_ms, by="host-to-device copy" if h2d_ms > tot / args.steps else "device step",
+                              frac=bound_ms / (et / args.steps)),
+                   note="ShardedCache.query_host on every rank: fp32 queries from pinned host memory in, "
+                        "ids/scores/K/status back to pinned host memory, latent states fetched into the "
+                        "denoiser's device input buffer; wall clock, max over ranks")
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ns = min(n, REF_SLICE)
+        emb_s = E.rows(torch.arange(ns, dtype=torch.int64, device="cuda")).cpu().numpy()
+        cpu = cpu_baseline(emb_s, pres[:ns], q.cpu().numpy(), n_total=n)
+        del emb_s
     hbm, tflops, peak_src = _peaks()
     try:
         tf_sus = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops_sustained"]
@@ -364,7 +451,6 @@ def run_sharded(args, cfg):
     sc_ms = statistics.mean(score_ms)
     flops = 2.0 * b * n_local * D
     ach = flops / (sc_ms / 1e3) / 1e12
-    k_np = out["k"].cpu().numpy()
     if rank == 0:
         line = dict(metric=METRIC, value=b * args.steps / (tot / 1e3), unit=UNIT, n_gpus=world, steps=args.steps,
                     warmup=args.warmup, ms_per_step=tot / args.steps, higher_is_better=True, scaling="strong",
@@ -383,9 +469,10 @@ def run_sharded(args, cfg):
                     roofline=dict(bound="tensor", achieved=ach, peak=tf_sus, unit="TFLOP/s", frac=ach / tf_sus,
                                   kernel="score_tc (rank 0 shard)",
                                   peak_source=peak_src + ", sustained bf16 (a ~0.2 s kernel runs under the "
-                                                         "power cap)", traffic=None,
+                                                         "power cap)",
+                                  traffic=_ncu_traffic("tc", f"{args.config}_n{world}") or _ncu_traffic("tc", args.config),
                                   algorithmic_per_launch=flops),
-                    cpu_baseline=None, e2e=None, gpu_launches=launches, clocks=clk.summary())
+                    cpu_baseline=cpu, e2e=e2e, gpu_launches=launches, clocks=clk.summary())
         if maint:
             lk = tot / args.steps
             line["maintenance"] = dict(
@@ -400,32 +487,90 @@ def run_sharded(args, cfg):
     dist.destroy_process_group()
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def _spawn(args) -> int:
+    """`--gpus N` without a torch.distributed environment: re-launch this script with N ranks
+    (one process per GPU) under torch.distributed.run on 127.0.0.1; rank 0 prints the line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def run_dry(args):
+    """Launcher / rendezvous / max-over-ranks check without a GPU (gloo): the same rank plumbing
+    as the GPU runs, a barrier + tiny all-reduce as the "step"; rank 0 prints a line flagged
+    dry_run with no throughput.  Used by the CPU tests of the spawner."""
+    import torch
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", str(_free_port()))
+    os.environ.setdefault("RANK", "0")
+    os.environ.setdefault("WORLD_SIZE", "1")
+    dist.init_process_group("gloo")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    for _ in range(args.warmup):
+        dist.barrier()
+    times = []
+    for _ in range(args.steps):
+        dist.barrier()
+        t0 = time.perf_counter()
+        x = torch.full((1,), float(rank))
+        dist.all_reduce(x)
+        times.append(time.perf_counter() - t0)
+        assert x.item() == world * (world - 1) / 2
+    t = torch.tensor([sum(times)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps(dict(dry_run=True, metric=METRIC, value=None, unit=UNIT, n_gpus=world, steps=args.steps,
+                              warmup=args.warmup, ms_per_step=1e3 * float(t.item()) / max(1, args.steps),
+                              note="launcher check only (gloo barrier + all-reduce per step, no GPU work)")),
+              flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=list(CONFIGS))
+    ap.add_argument("--config", default="c4", choices=list(CONFIGS))
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--scorer", default="auto", choices=["auto", "tc", "tc1", "stream"],
                     help="tc1 = single-CTA tensor-core scan (auto/tc use CTA pairs for > 128 queries)")
     ap.add_argument("--exchange", default="push", choices=["push", "nccl"],
-                    help="sharded configs (c4): fused P2P push exchange or NCCL all-gathers")
+                    help="sharded configs (c4, c5): fused P2P push exchange or NCCL all-gathers")
     ap.add_argument("--slices", type=int, default=0,
                     help="query slices of cache_query_batch (0 = library auto, 1 = one scan launch)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-maintenance", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help="launcher check on CPU (gloo), no GPU work")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(_spawn(args))
+    if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        print(f"bench.py: WORLD_SIZE={os.environ['WORLD_SIZE']} overrides --gpus {args.gpus}", file=sys.stderr)
     cfg = dict(CONFIGS[args.config])
     if args.batch:
         cfg["b"] = args.batch
+    if args.dry_run:
+        return run_dry(args)
     if args.impl == "reference":
         return run_reference(args, cfg)
     if cfg.get("sharded"):
         return run_sharded(args, cfg)
+    return run_single(args, cfg)
 
+
+def run_single(args, cfg):
+    """C1-C3 (and C2 replicas at N > 1): one cache per GPU."""
     import torch
     import torch.distributed as dist
     from paper_2312_04429_b200 import binding as B

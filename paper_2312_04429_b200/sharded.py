@@ -143,6 +143,23 @@ class ShardedCache:
 
         return query_protocol(self.comm, q_local, topk, local_fn, merge_fn)
 
+    def query_host(self, q_host: torch.Tensor, out_host: dict, out_dev: dict, topk: int = 1, stream=None):
+        """End-to-end collective lookup from host memory: this rank's b_local fp32 (or bf16)
+        query rows are copied from (pinned) host memory, looked up with query_into, and the
+        ids / scores / K / status come back to out_host (pinned tensors); the latent states stay
+        in out_dev["latents"], the denoiser's device input buffer.  Synchronises the stream."""
+        s = stream if stream is not None else torch.cuda.current_stream()
+        qd = getattr(self, "_q_stage", None)
+        if qd is None or qd.shape != q_host.shape or qd.dtype != q_host.dtype:
+            qd = self._q_stage = torch.empty(q_host.shape, dtype=q_host.dtype, device="cuda")
+        with torch.cuda.stream(s):
+            qd.copy_(q_host, non_blocking=True)
+            self.query_into(qd, out_dev, topk, s)
+            for k in ("ids", "scores", "k", "status"):
+                out_host[k].copy_(out_dev[k], non_blocking=True)
+        s.synchronize()
+        return out_host
+
     def evict(self, n: int, lists: bool = True):
         """Collective: evict the n globally lowest-keyed items (entries in entry mode; every
         rank passes the same n).  lists=False skips gathering the evicted / dirty id lists to
