@@ -41,7 +41,9 @@ typedef enum {
     CACHE_E_EVICT_RANGE = 4, /* evict n > live items                          */
     CACHE_E_BAD_ROWS = 5,    /* some input rows rejected; per-row codes were written       */
     CACHE_E_CUDA = 6,        /* CUDA runtime/driver error                                  */
-    CACHE_E_NCCL = 7,        /* reserved (multi-rank plumbing lives above the ABI)         */
+    CACHE_E_NCCL = 7,        /* a peer rank failed: a push-exchange wait timed out (dead or
+                                stalled rank, cache_set_peer_timeout), or (binding) an NCCL
+                                collective of the sharded protocol failed                   */
     CACHE_E_OOM = 8,         /* device allocation failed                                   */
     CACHE_E_STATE = 9,       /* call not valid in the handle's state (e.g. id space spent) */
     CACHE_E_UNSUPPORTED = 10 /* requested variant not built for this configuration         */
@@ -169,6 +171,8 @@ typedef struct {
     int32_t arena_topk;
     int32_t reserved2;
     unsigned char ipc_arena[64];
+    uint64_t process_token;      /* random per-process identity: raw pointers are used only when
+                                    pid AND token match (PID namespaces can repeat pids)      */
 } cache_peer_desc;
 
 /* Fill *cfg with the paper's defaults: dim 768, K = {5,10,15,20,25}, Fig. 11
@@ -191,8 +195,10 @@ cache_status cache_destroy(cache_t *c);
  *   present    device or host pointer, n bitmasks (bit j set = K_j is stored), or NULL = all
  *   out_ids    host pointer, n ids (CACHE_NO_ID for a rejected row); may be NULL
  *   row_status host pointer, n CACHE_ROW_* codes; may be NULL
- * Each accepted row is normalised in fp64 (fixed tree-order sum of squares, correctly
- * rounded sqrt and division) and rounded to bf16 (RNE) -- reading R2.  Rows with
+ * Each accepted row is normalised in fp64 (sum of squares in a fixed halving-tree order,
+ * correctly rounded sqrt and division) and rounded to bf16 (RNE) -- reading R2: a stored
+ * component can differ from the plain index-order definition only where the exact quotient
+ * lies within the two summation orders' fp64 error bound of a bf16 rounding midpoint.  Rows with
  * non-finite components or zero norm are rejected (CACHE_E_BAD_ROWS after the valid rows
  * are stored).  If the accepted rows exceed the free entry or latent capacity the call
  * returns CACHE_E_FULL and stores nothing (no automatic eviction, R14).
@@ -224,6 +230,16 @@ cache_status cache_query_batch(cache_t *c, int64_t b, const void *queries, int32
                                int32_t *out_k, void *latent_out, void **out_latent_ptr,
                                int32_t *row_status, void *stream);
 
+/* Read-only batched lookup: the ids, scores and K that cache_query_batch would report for the
+ * same cache state, but NO access is counted (no LCBFU counter, no LRU clock tick) and no
+ * state is gathered.  For measurements that must not disturb the eviction state: the match
+ * predictor's would-hit statistics of requests it sends to scratch generation (Alg. 1 line 2,
+ * a predicted miss performs no search), and profiling.  Buffers as cache_query_batch
+ * (device pointers); asynchronous on `stream`. */
+cache_status cache_query_peek(cache_t *c, int64_t b, const void *queries, int32_t q_dtype, int32_t topk,
+                              uint64_t *out_ids, float *out_scores, int32_t *out_k, int32_t *row_status,
+                              void *stream);
+
 /* Same lookup called from the host (the end-to-end call a serving process makes): queries,
  * out_ids, out_scores, out_k and row_status are host pointers (pinned memory recommended);
  * the library copies the queries in, runs the lookup, copies ids/scores/K/status back in one
@@ -248,6 +264,12 @@ cache_status cache_query_batch_host(cache_t *c, int64_t b, const void *queries, 
  * entry score, then id) and out_dirty_ids the same ids ascending (*out_n_dirty = n). */
 cache_status cache_evict(cache_t *c, int64_t n, uint64_t *out_evicted, uint64_t *out_dirty_ids,
                          int64_t *out_n_dirty, void *stream);
+
+/* The full 64-bit unit keys (R11 / R24: score << 35 | id << 3 | j, or score << 32 | id) of the
+ * last cache_evict / cache_evict_apply / cache_push_evict_apply that returned its evicted list,
+ * in eviction order (ascending).  Lets a sharded caller merge the ranks' lists into the global
+ * eviction order.  out: host array of capacity cap; *out_n = the number of keys available. */
+cache_status cache_last_evicted_keys(cache_t *c, uint64_t *out, int64_t cap, int64_t *out_n);
 
 /* ---- distributed eviction building blocks (cache_evict = these three with no exchange) ----
  * The n lowest LCBFU keys across all shards are found by an 8-pass MSB-first radix select
@@ -313,9 +335,18 @@ cache_status cache_attach_peers(cache_t *c, int32_t world, const cache_peer_desc
  * one stream call phase 1 on all ranks, then phase 2, then phase 3).  Outputs as in
  * cache_query_batch, nb rows.  Arena reuse across batches needs no extra barrier: a rank
  * writes batch t+1 into a peer's arena only after the peer has published batch t+1's queries,
- * i.e. after it finished merging batch t.  A wait that sees no progress for ~17 s traps
- * (a dead peer fails the context instead of hanging it). */
+ * i.e. after it finished merging batch t.
+ * Failure (failure detection): a wait that sees no progress from some rank within
+ * the peer timeout (default 10 s; cache_set_peer_timeout, or NIRVANA_PEER_TIMEOUT_MS at
+ * create) marks the handle failed instead of hanging or trapping: the kernels behind it skip
+ * every peer load / store, the CUDA context stays usable, and every later cache_push_* call
+ * (and cache_push_status, which synchronises `stream` first) returns CACHE_E_NCCL.  The
+ * outputs of the failed batch are undefined; local (unsharded) calls keep working. */
 cache_status cache_push_reserve(cache_t *c, int64_t max_nb, int32_t max_topk);
+/* Synchronise `stream`, then CACHE_E_NCCL if a peer wait of this handle timed out, else OK. */
+cache_status cache_push_status(cache_t *c, void *stream);
+/* Peer timeout of the push-exchange waits (ms > 0). */
+cache_status cache_set_peer_timeout(cache_t *c, int64_t timeout_ms);
 cache_status cache_push_queries(cache_t *c, int64_t nb, const void *queries, int32_t q_dtype, void *stream);
 cache_status cache_push_scan(cache_t *c, int64_t nb, int32_t topk, void *stream);
 cache_status cache_push_merge(cache_t *c, int64_t nb, int32_t topk, uint64_t *out_ids, float *out_scores,

@@ -65,7 +65,8 @@ class PeerDesc(ctypes.Structure):
                 ("ipc_lslot", ctypes.c_ubyte * 64), ("ipc_fcnt", ctypes.c_ubyte * 64),
                 ("ipc_pool", ctypes.c_ubyte * 64), ("ipc_lastacc", ctypes.c_ubyte * 64),
                 ("arena", ctypes.c_void_p), ("arena_nb", ctypes.c_int64), ("arena_topk", ctypes.c_int32),
-                ("reserved2", ctypes.c_int32), ("ipc_arena", ctypes.c_ubyte * 64)]
+                ("reserved2", ctypes.c_int32), ("ipc_arena", ctypes.c_ubyte * 64),
+                ("process_token", ctypes.c_uint64)]
 
 
 SHARD_REC_BYTES = 16   # cache_shard_rec
@@ -81,7 +82,8 @@ EXPORTS = ("cache_default_config", "cache_create", "cache_destroy", "cache_inser
            "cache_set_evict_policy", "cache_predictor_train", "cache_predict", "cache_predictor_get",
            "cache_set_evict_granularity", "cache_live_entries", "cache_push_reserve", "cache_push_queries",
            "cache_push_scan", "cache_push_merge", "cache_push_evict_hist", "cache_push_evict_pick",
-           "cache_push_evict_apply", "cache_profile_thresholds", "cache_set_thresholds")
+           "cache_push_evict_apply", "cache_profile_thresholds", "cache_set_thresholds", "cache_query_peek",
+           "cache_push_status", "cache_set_peer_timeout", "cache_last_evicted_keys")
 
 
 def load_library(path: str = LIB_PATH):
@@ -96,6 +98,14 @@ def load_library(path: str = LIB_PATH):
     L.cache_insert.argtypes = [P, I64, P, I32, P, P, P, P, P]
     L.cache_query_batch.argtypes = [P, I64, P, I32, I32, P, P, P, P, P, P, P]
     L.cache_query_batch_host.argtypes = [P, I64, P, I32, I32, P, P, P, P, P, P]
+    L.cache_query_peek.argtypes = [P, I64, P, I32, I32, P, P, P, P, P]
+    L.cache_query_peek.restype = ctypes.c_int
+    L.cache_last_evicted_keys.argtypes = [P, P, I64, P]
+    L.cache_last_evicted_keys.restype = ctypes.c_int
+    L.cache_push_status.argtypes = [P, P]
+    L.cache_push_status.restype = ctypes.c_int
+    L.cache_set_peer_timeout.argtypes = [P, I64]
+    L.cache_set_peer_timeout.restype = ctypes.c_int
     L.cache_evict.argtypes = [P, I64, P, P, P, P]
     L.cache_get_meta.argtypes = [P, U64, P, P]
     L.cache_get_row.argtypes = [P, U64, P]
@@ -273,6 +283,16 @@ class NirvanaCache:
         out = self.alloc_outputs(q.shape[0], topk, latents)
         return self.query_into(q, out, topk, stream)
 
+    def peek(self, q: torch.Tensor, topk: int = 1, stream=None):
+        """Read-only lookup (cache_query_peek): ids / scores / K as query() would report them,
+        with no access counted, no LRU clock tick and no latent gather."""
+        assert q.is_cuda and q.is_contiguous() and q.dim() == 2 and q.shape[1] == self.dim
+        out = self.alloc_outputs(q.shape[0], topk, latents=False)
+        dt = DTYPE_BF16 if q.dtype == torch.bfloat16 else DTYPE_F32
+        _check(_lib.cache_query_peek(self._h, q.shape[0], _ptr(q), dt, topk, _ptr(out["ids"]), _ptr(out["scores"]),
+                                     _ptr(out["k"]), _ptr(out["status"]), _stream(stream)))
+        return out
+
     def query_host(self, q: np.ndarray, topk: int = 1, latents: bool = True, out: dict | None = None, stream=None):
         """End-to-end lookup with host buffers (pinned numpy-compatible tensors recommended)."""
         b = q.shape[0]
@@ -379,6 +399,21 @@ class NirvanaCache:
                                      _ptr(out.get("latents")), _ptr(out.get("ptrs")), _ptr(out.get("status")),
                                      _stream(stream)))
         return out
+
+    def last_evicted_keys(self) -> np.ndarray:
+        """64-bit unit keys of the last eviction that returned its list, in eviction order."""
+        n = np.zeros(1, dtype=np.int64)
+        _check(_lib.cache_last_evicted_keys(self._h, None, 0, _ptr(n)))
+        out = np.empty(max(int(n[0]), 1), dtype=np.uint64)
+        _check(_lib.cache_last_evicted_keys(self._h, _ptr(out), int(n[0]), _ptr(n)))
+        return out[: int(n[0])]
+
+    def push_status(self, stream=None):
+        """Synchronise the stream; CacheError(E_NCCL) if a peer wait of this handle timed out."""
+        _check(_lib.cache_push_status(self._h, _stream(stream)))
+
+    def set_peer_timeout(self, ms: int):
+        _check(_lib.cache_set_peer_timeout(self._h, int(ms)))
 
     # ---- cache-selector profiling (Alg. 2) ----
     def profile_thresholds(self, q: torch.Tensor, quality: torch.Tensor, alpha: float = 0.9, stream=None):
@@ -507,3 +542,29 @@ def debug_sort_u64(keys: torch.Tensor, stream=None) -> torch.Tensor:
 
 def debug_slot_of(cache: NirvanaCache, id_: int) -> int:
     return _lib.cache_debug_slot_of(cache._h, int(id_))
+
+
+_lib.cache_debug_sort_u64_ex.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64,
+                                         ctypes.c_int32, ctypes.c_void_p]
+_lib.cache_debug_sort_u64_ex.restype = ctypes.c_int
+_lib.cache_debug_evict_stats.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+_lib.cache_debug_evict_stats.restype = ctypes.c_int
+_lib.cache_debug_set_evict_cand_cap.argtypes = [ctypes.c_void_p, ctypes.c_int64]
+_lib.cache_debug_set_evict_cand_cap.restype = ctypes.c_int
+
+
+def debug_sort_u64_ex(keys: torch.Tensor, bits: int = 64, base: int = 0, small: bool = False, stream=None):
+    """The eviction sorts with their options: keys in [base, base + 2^bits), or the one-CTA sort."""
+    _check(_lib.cache_debug_sort_u64_ex(_ptr(keys), keys.numel(), bits, base, int(small), _stream(stream)))
+    return keys
+
+
+def debug_evict_stats(cache: NirvanaCache) -> dict:
+    """Last cache_evict: levels, full sweeps, compaction level (0 = none), candidates."""
+    a = (ctypes.c_int64 * 4)()
+    _check(_lib.cache_debug_evict_stats(cache._h, a))
+    return dict(levels=a[0], full_sweeps=a[1], compact_level=a[2], candidates=a[3])
+
+
+def debug_set_evict_cand_cap(cache: NirvanaCache, cap: int):
+    _check(_lib.cache_debug_set_evict_cand_cap(cache._h, int(cap)))

@@ -12,7 +12,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libnirvana_cache.so")
-SOURCES = ["cache.cu", "kernels.cu", "score_tc.cu", "predictor.cu", "sort.cu"]
+SOURCES = ["cache.cu", "kernels.cu", "score_tc.cu", "predictor.cu", "sort.cu", "evict.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "--expt-relaxed-constexpr", "-DNDEBUG"]

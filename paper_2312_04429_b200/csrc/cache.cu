@@ -5,6 +5,8 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -216,6 +218,12 @@ struct cache_t {
     DevBuf<uint32_t> escr;         // radix-sort scratch
     DevBuf<unsigned long long> epool;    // pool slot of each evicted item (sorted for the free list)
     DevBuf<unsigned long long> edirty, edid;   // dirty entries: slots, ids (each sorted on the GPU)
+    DevBuf<unsigned long long> ckey;     // fused eviction (evict.cu): candidate keys / slots
+    DevBuf<uint32_t> cslot;
+    DevBuf<uint8_t> selws;               // per-level histograms + SelOut
+    int64_t last_sel[4] = {0, 0, 0, 0};  // levels, full sweeps, compaction level, candidates
+    int64_t cand_cap_override = -1;      // test hook (cache_debug_set_evict_cand_cap); -1 = auto
+    int64_t last_ev_n = 0;               // unit keys of the last eviction (in hev_sorted), in order
     // match predictor (NEXT-3)
     DevBuf<float> pw, prho, pgpart;
     DevBuf<uint32_t> pkeys;
@@ -238,8 +246,22 @@ struct cache_t {
     int64_t push_nb = -1;
     int push_phase = 0;              // last phase run (1..3), for call-order checks
     uint32_t evict_epoch = 0;        // fused distributed evictions so far
+    // failure detection of the push exchange: a peer wait that times out sets the device abort
+    // word (consumers skip their peer accesses) and the mapped host word (the host reports
+    // CACHE_E_NCCL from then on instead of hanging or trapping)
+    DevBuf<uint32_t> abortw;
+    uint32_t* errw_h = nullptr;      // pinned, mapped
+    uint32_t* errw_d = nullptr;      // its device alias
+    unsigned long long peer_timeout_ns = 10ull * 1000 * 1000 * 1000;
     int evict_pass = -1;             // last pass whose pick ran (-1: none / done)
 };
+
+static bool peer_failed(const cache_t* c) { return c->errw_h && *(volatile const uint32_t*)c->errw_h != 0u; }
+
+static cache_status peer_fail(const char* where) {
+    return fail(CACHE_E_NCCL, std::string(where) + ": a peer rank did not publish within the peer timeout (dead or "
+                              "stalled rank); the sharded exchange of this handle is stopped -- rebuild it");
+}
 
 extern "C" {
 
@@ -278,6 +300,11 @@ static cudaError_t reserve_evict(cache_t* c, int64_t items, int64_t entries) {
     if ((e = c->hev_sorted.ensure(items * 8)) != cudaSuccess) return e;
     if (!c->alias && (e = c->hev_pool.ensure(items * 8)) != cudaSuccess) return e;
     if ((e = c->hev_ds.ensure(entries * 8)) != cudaSuccess) return e;
+    // fused eviction: candidate buffers (1/16 of the units) and the per-level histograms
+    const int64_t ccap = std::max<int64_t>(65536, c->cap * c->num_k / 16);
+    if ((e = c->ckey.ensure_grow(ccap)) != cudaSuccess) return e;
+    if ((e = c->cslot.ensure_grow(ccap)) != cudaSuccess) return e;
+    if ((e = c->selws.ensure((size_t)kSelMaxLevels * kSelBins * 4 + sizeof(SelOut))) != cudaSuccess) return e;
     return c->hev_did.ensure(entries * 8);
 }
 
@@ -356,6 +383,12 @@ cache_status cache_create(const cache_config* cfg, int device, cache_t** out) {
     cudaMemset(c->lslot, 0xFF, (size_t)c->cap_pad * c->num_k * 4);
     cudaMemset(c->fcnt, 0, (size_t)c->cap_pad * c->num_k * 4);
     cudaMemset(c->lastacc, 0, (size_t)c->cap_pad * c->num_k * 4);
+    if ((e = c->abortw.ensure(1)) != cudaSuccess) return bail(e, "abort word");
+    cudaMemset(c->abortw.p, 0, 4);
+    if ((e = cudaHostAlloc((void**)&c->errw_h, 64, cudaHostAllocMapped)) != cudaSuccess) return bail(e, "error word");
+    *(volatile uint32_t*)c->errw_h = 0u;
+    if ((e = cudaHostGetDevicePointer((void**)&c->errw_d, c->errw_h, 0)) != cudaSuccess) return bail(e, "error word");
+    if (const char* t = std::getenv("NIRVANA_PEER_TIMEOUT_MS")) c->peer_timeout_ns = std::strtoull(t, nullptr, 10) * 1000000ull;
     if ((e = cudaDeviceSynchronize()) != cudaSuccess) return bail(e, "init");
     c->tm_e_ok = encode_rows(&c->tm_e, c->emb, c->cap_pad, c->dim, 256) &&
                  encode_rows(&c->tm_e128, c->emb, c->cap_pad, c->dim, 128);
@@ -397,6 +430,9 @@ cache_status cache_destroy(cache_t* c) {
     c->hev_sorted.release(); c->hev_pool.release(); c->hev_ds.release();
     c->hev_did.release();
     c->epool.release(); c->edirty.release(); c->edid.release();
+    c->ckey.release(); c->cslot.release(); c->selws.release();
+    c->abortw.release();
+    if (c->errw_h) cudaFreeHost(c->errw_h);
     delete c;
     return CACHE_OK;
 }
@@ -660,10 +696,11 @@ static cache_status query_sliced(cache_t* c, int64_t b, int ns, const void* quer
 // tick = false: a later sub-batch of the same host batch (same LRU clock value).
 static cache_status query_core(cache_t* c, int64_t b, const void* queries, int32_t q_dtype, int32_t topk,
                                uint64_t* out_ids, float* out_scores, int32_t* out_k, void* latent_out,
-                               void** out_ptr, int32_t* row_status, cudaStream_t s, bool tick = true) {
+                               void** out_ptr, int32_t* row_status, cudaStream_t s, bool tick = true,
+                               bool count = true) {
     const int kmax = topk == 1 ? 1 : (topk <= 4 ? 4 : 16);
     const int ns = query_slices(c, b);
-    if (ns > 1)
+    if (ns > 1 && count)
         return query_sliced(c, b, ns, queries, q_dtype, topk, kmax, out_ids, out_scores, out_k, latent_out, out_ptr,
                             row_status, s, tick);
     int parts = 0;
@@ -672,12 +709,12 @@ static cache_status query_core(cache_t* c, int64_t b, const void* queries, int32
     if (c->prof_on) CK(cudaEventRecord(c->prof[2], s));
     if (tick) c->clock++;   // one query batch = one tick of the LRU clock
     launch_finalize(kmax, c->recs.p, parts, b, topk, c->invq.p, c->qstat.p, c->ids, c->present, c->lslot,
-                    c->fcnt, c->lastacc, c->clock, c->pool, c->L, c->km, out_ids, out_scores, out_k,
+                    count ? c->fcnt : nullptr, count ? c->lastacc : nullptr, c->clock, c->pool, c->L, c->km, out_ids, out_scores, out_k,
                     (uint8_t*)latent_out, out_ptr, row_status, s);
     c->launches++;
     if (c->prof_on) CK(cudaEventRecord(c->prof[3], s));
     CK(cudaGetLastError());
-    c->queries += b;
+    if (count) c->queries += b;
     return CACHE_OK;
 }
 
@@ -695,6 +732,20 @@ cache_status cache_query_batch(cache_t* c, int64_t b, const void* queries, int32
     DeviceGuard g(c->device);
     return query_core(c, b, queries, q_dtype, topk, out_ids, out_scores, out_k, latent_out, out_latent_ptr,
                       row_status, (cudaStream_t)stream);
+}
+
+cache_status cache_query_peek(cache_t* c, int64_t b, const void* queries, int32_t q_dtype, int32_t topk,
+                              uint64_t* out_ids, float* out_scores, int32_t* out_k, int32_t* row_status,
+                              void* stream) {
+    if (!c) return fail(CACHE_E_INVALID_ARG, "cache_query_peek: null cache");
+    if (b < 0 || b > 0x7FFFFFFF || topk < 1 || topk > c->cfg.max_topk ||
+        (q_dtype != CACHE_DTYPE_F32 && q_dtype != CACHE_DTYPE_BF16))
+        return fail(CACHE_E_INVALID_ARG, "cache_query_peek: bad b / topk / dtype");
+    if (b == 0) return CACHE_OK;
+    if (!queries || !out_ids || !out_scores || !out_k) return fail(CACHE_E_INVALID_ARG, "cache_query_peek: null buffer");
+    DeviceGuard g(c->device);
+    return query_core(c, b, queries, q_dtype, topk, out_ids, out_scores, out_k, nullptr, nullptr, row_status,
+                      (cudaStream_t)stream, /*tick=*/false, /*count=*/false);
 }
 
 cache_status cache_query_local(cache_t* c, int64_t b, const void* queries, int32_t q_dtype, int32_t topk,
@@ -876,12 +927,30 @@ cache_status cache_pool_write(cache_t* c, int64_t slot0, int64_t n, const void* 
     return CACHE_OK;
 }
 
+// Identity of this process for cache_attach_peers: raw device pointers are usable only inside
+// the exporting process.  A pid alone is not enough (ranks in separate PID namespaces, e.g. one
+// container per GPU, can share one), so every process draws a random 64-bit token once.
+static uint64_t process_token() {
+    static const uint64_t tok = [] {
+        uint64_t t = 0;
+        if (FILE* f = std::fopen("/dev/urandom", "rb")) {
+            if (std::fread(&t, sizeof(t), 1, f) != 1) t = 0;
+            std::fclose(f);
+        }
+        t ^= (uint64_t)getpid() * 0x9E3779B97F4A7C15ull;
+        t ^= (uint64_t)std::chrono::high_resolution_clock::now().time_since_epoch().count();
+        return t ? t : 1ull;
+    }();
+    return tok;
+}
+
 cache_status cache_export_peer(cache_t* c, cache_peer_desc* out) {
     if (!c || !out) return fail(CACHE_E_INVALID_ARG, "cache_export_peer: null argument");
     DeviceGuard g(c->device);
     std::memset(out, 0, sizeof(*out));
     out->device = c->device;
     out->pid = (int32_t)getpid();
+    out->process_token = process_token();
     out->num_k = c->num_k;
     out->latent_bytes = c->L;
     out->lslot = c->lslot;
@@ -914,6 +983,7 @@ cache_status cache_attach_peers(cache_t* c, int32_t world, const cache_peer_desc
     if (!c || !descs || world != c->world) return fail(CACHE_E_INVALID_ARG, "cache_attach_peers: bad argument");
     DeviceGuard g(c->device);
     const int32_t me = (int32_t)getpid();
+    const uint64_t tok = process_token();
     PeerPtrs p{};
     bool push = c->arena != nullptr;
     uint8_t* pa[kMaxWorld] = {};
@@ -923,7 +993,7 @@ cache_status cache_attach_peers(cache_t* c, int32_t world, const cache_peer_desc
             return fail(CACHE_E_INVALID_ARG, "cache_attach_peers: peer configuration differs");
         if (c->arena && (!d.arena || d.arena_nb != c->arena_nb || d.arena_topk != c->arena_topk))
             push = false;   // some rank has no (or a differently sized) arena: no push exchange
-        if (d.pid == me) {   // same process (own rank, or virtual ranks sharing one GPU)
+        if (d.pid == me && d.process_token == tok) {   // same process (own rank, or virtual ranks on one GPU)
             p.lslot[r] = (const int32_t*)d.lslot;
             p.fcnt[r] = (uint32_t*)d.fcnt;
             p.lastacc[r] = (uint32_t*)d.lastacc;
@@ -960,10 +1030,33 @@ cache_status cache_attach_peers(cache_t* c, int32_t world, const cache_peer_desc
             p.pool[r] = (const uint8_t*)ptr;
         }
     }
+    p.abort = c->abortw.p;
     c->peers = p;
     c->peers_ok = true;
     c->push_ok = push;
     for (int r = 0; r < kMaxWorld; ++r) c->peer_arena[r] = r < world ? pa[r] : nullptr;
+    return CACHE_OK;
+}
+
+cache_status cache_last_evicted_keys(cache_t* c, uint64_t* out, int64_t cap, int64_t* out_n) {
+    if (!c || cap < 0 || (cap > 0 && !out)) return fail(CACHE_E_INVALID_ARG, "cache_last_evicted_keys: bad argument");
+    const int64_t n = std::min<int64_t>(cap, c->last_ev_n);
+    if (n > 0) std::memcpy(out, c->hev_sorted.p, (size_t)n * 8);
+    if (out_n) *out_n = c->last_ev_n;
+    return CACHE_OK;
+}
+
+cache_status cache_push_status(cache_t* c, void* stream) {
+    if (!c) return fail(CACHE_E_INVALID_ARG, "cache_push_status: null cache");
+    DeviceGuard g(c->device);
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    if (peer_failed(c)) return peer_fail("cache_push_status");
+    return CACHE_OK;
+}
+
+cache_status cache_set_peer_timeout(cache_t* c, int64_t timeout_ms) {
+    if (!c || timeout_ms <= 0) return fail(CACHE_E_INVALID_ARG, "cache_set_peer_timeout: bad argument");
+    c->peer_timeout_ns = (unsigned long long)timeout_ms * 1000000ull;
     return CACHE_OK;
 }
 
@@ -996,12 +1089,19 @@ static PushSignal push_signal_of(cache_t* c, size_t flag_off, int counter) {
     sg.world = c->world;
     sg.done = (uint32_t*)(c->arena + arena_layout(c->world, c->arena_nb, c->arena_topk, c->dim).done) + counter;
     sg.epoch = c->push_epoch;
+    sg.abort = c->abortw.p;
     return sg;
+}
+
+
+static void wait_flags(cache_t* c, const uint32_t* flags, uint32_t epoch, cudaStream_t s) {
+    launch_wait_flags(flags, c->world, epoch, c->peer_timeout_ns, c->abortw.p, c->errw_d, s);
 }
 
 // ---- fused distributed eviction selection (histograms over peer memory) ----
 cache_status cache_push_evict_hist(cache_t* c, int64_t n, int32_t pass, void* stream) {
     if (!c) return fail(CACHE_E_INVALID_ARG, "cache_push_evict_hist: null cache");
+    if (peer_failed(c)) return peer_fail("cache_push_evict_hist");
     if (!c->push_ok) return fail(CACHE_E_STATE, "cache_push_evict_hist: no push arenas");
     if (pass < 0 || pass > 7 || (pass == 0 && n < 0)) return fail(CACHE_E_INVALID_ARG, "cache_push_evict_hist: bad pass / n");
     if (pass != c->evict_pass + 1) return fail(CACHE_E_STATE, "cache_push_evict_hist: passes out of order");
@@ -1027,12 +1127,13 @@ cache_status cache_push_evict_hist(cache_t* c, int64_t n, int32_t pass, void* st
 
 cache_status cache_push_evict_pick(cache_t* c, int32_t pass, void* stream) {
     if (!c) return fail(CACHE_E_INVALID_ARG, "cache_push_evict_pick: null cache");
+    if (peer_failed(c)) return peer_fail("cache_push_evict_pick");
     if (!c->push_ok || pass != c->evict_pass + 1 || pass > 7)
         return fail(CACHE_E_STATE, "cache_push_evict_pick: call after cache_push_evict_hist of the same pass");
     DeviceGuard g(c->device);
     cudaStream_t s = (cudaStream_t)stream;
     const ArenaLayout L = arena_layout(c->world, c->arena_nb, c->arena_topk, c->dim);
-    launch_wait_flags((const uint32_t*)(c->arena + L.eflag + (size_t)pass * kMaxWorld * 4), c->world, c->evict_epoch, s);
+    wait_flags(c, (const uint32_t*)(c->arena + L.eflag + (size_t)pass * kMaxWorld * 4), c->evict_epoch, s);
     // the complete global histogram is in this rank's own arena; the pick zeroes it after use
     launch_evict_pick((unsigned int*)(c->arena + L.ehist) + 256 * pass, c->est.p, pass, s);
     c->launches += 2;
@@ -1044,6 +1145,7 @@ cache_status cache_push_evict_pick(cache_t* c, int32_t pass, void* stream) {
 cache_status cache_push_evict_apply(cache_t* c, int64_t n, uint64_t* out_evicted, int64_t* out_n,
                                     uint64_t* out_dirty_ids, int64_t* out_n_dirty, void* stream) {
     if (!c) return fail(CACHE_E_INVALID_ARG, "cache_push_evict_apply: null cache");
+    if (peer_failed(c)) return peer_fail("cache_push_evict_apply");
     if (c->evict_pass != 7) return fail(CACHE_E_STATE, "cache_push_evict_apply: the 8 passes have not run");
     c->evict_pass = -1;
     return cache_evict_apply(c, reinterpret_cast<const cache_evict_state*>(c->est.p), n, out_evicted, out_n,
@@ -1052,6 +1154,7 @@ cache_status cache_push_evict_apply(cache_t* c, int64_t n, uint64_t* out_evicted
 
 cache_status cache_push_queries(cache_t* c, int64_t nb, const void* queries, int32_t q_dtype, void* stream) {
     if (!c) return fail(CACHE_E_INVALID_ARG, "cache_push_queries: null cache");
+    if (peer_failed(c)) return peer_fail("cache_push_queries");
     if (!c->push_ok) return fail(CACHE_E_STATE, "cache_push_queries: no push arenas (cache_push_reserve on every rank, then export / attach)");
     if (nb < 0 || nb > c->arena_nb || (nb > 0 && !queries) || (q_dtype != CACHE_DTYPE_F32 && q_dtype != CACHE_DTYPE_BF16))
         return fail(CACHE_E_INVALID_ARG, "cache_push_queries: bad nb / queries / dtype");
@@ -1077,6 +1180,7 @@ cache_status cache_push_queries(cache_t* c, int64_t nb, const void* queries, int
 
 cache_status cache_push_scan(cache_t* c, int64_t nb, int32_t topk, void* stream) {
     if (!c) return fail(CACHE_E_INVALID_ARG, "cache_push_scan: null cache");
+    if (peer_failed(c)) return peer_fail("cache_push_scan");
     if (c->push_phase != 1 || nb != c->push_nb) return fail(CACHE_E_STATE, "cache_push_scan: call after cache_push_queries with the same nb");
     if (topk < 1 || topk > c->arena_topk) return fail(CACHE_E_INVALID_ARG, "cache_push_scan: bad topk");
     DeviceGuard g(c->device);
@@ -1084,7 +1188,7 @@ cache_status cache_push_scan(cache_t* c, int64_t nb, int32_t topk, void* stream)
     const ArenaLayout L = arena_layout(c->world, c->arena_nb, c->arena_topk, c->dim);
     const int64_t bg = (int64_t)c->world * nb;
     const int kmax = topk == 1 ? 1 : (topk <= 4 ? 4 : 16);
-    launch_wait_flags((const uint32_t*)(c->arena + L.qflag), c->world, c->push_epoch, s);
+    wait_flags(c, (const uint32_t*)(c->arena + L.qflag), c->push_epoch, s);
     c->launches++;
     int parts = 0;
     if (bg > 0) {
@@ -1109,6 +1213,7 @@ cache_status cache_push_merge(cache_t* c, int64_t nb, int32_t topk, uint64_t* ou
                               int32_t* out_k, void* latent_out, void** out_latent_ptr, int32_t* row_status,
                               void* stream) {
     if (!c) return fail(CACHE_E_INVALID_ARG, "cache_push_merge: null cache");
+    if (peer_failed(c)) return peer_fail("cache_push_merge");
     if (c->push_phase != 2 || nb != c->push_nb) return fail(CACHE_E_STATE, "cache_push_merge: call after cache_push_scan with the same nb");
     if (topk < 1 || topk > c->arena_topk) return fail(CACHE_E_INVALID_ARG, "cache_push_merge: bad topk");
     if (nb > 0 && (!out_ids || !out_scores || !out_k)) return fail(CACHE_E_INVALID_ARG, "cache_push_merge: null buffer");
@@ -1116,7 +1221,7 @@ cache_status cache_push_merge(cache_t* c, int64_t nb, int32_t topk, uint64_t* ou
     cudaStream_t s = (cudaStream_t)stream;
     const ArenaLayout L = arena_layout(c->world, c->arena_nb, c->arena_topk, c->dim);
     const int kmax = topk == 1 ? 1 : (topk <= 4 ? 4 : 16);
-    launch_wait_flags((const uint32_t*)(c->arena + L.rflag), c->world, c->push_epoch, s);
+    wait_flags(c, (const uint32_t*)(c->arena + L.rflag), c->push_epoch, s);
     c->launches++;
     c->clock++;   // once per global batch on every rank, as cache_query_merge
     if (nb > 0) {
@@ -1242,32 +1347,7 @@ cache_status cache_evict_pick(cache_t* c, uint32_t* hist, cache_evict_state* st,
 
 int64_t cache_live_items(const cache_t* c) { return c ? c->live_items : 0; }
 
-cache_status cache_evict(cache_t* c, int64_t n, uint64_t* out_evicted, uint64_t* out_dirty_ids,
-                         int64_t* out_n_dirty, void* stream) {
-    if (!c) return fail(CACHE_E_INVALID_ARG, "cache_evict: null cache");
-    if (n < 0) return fail(CACHE_E_INVALID_ARG, "cache_evict: n < 0");
-    if (c->km.gran == CACHE_EVICT_ENTRY ? n > c->live_entries : n > c->live_items)
-        return fail(CACHE_E_EVICT_RANGE, "cache_evict: n exceeds live items (entries in entry mode)");
-    if (out_n_dirty) *out_n_dirty = 0;
-    if (n == 0) return CACHE_OK;
-    DeviceGuard g(c->device);
-    cudaStream_t s = (cudaStream_t)stream;
-    CK(c->est.ensure(1));
-    CK(c->ehist.ensure(256));
-    EvictState st0{0ull, 0ull, (unsigned long long)n};
-    CK(cudaMemcpyAsync(c->est.p, &st0, sizeof(st0), cudaMemcpyHostToDevice, s));
-    cache_evict_state* st = reinterpret_cast<cache_evict_state*>(c->est.p);
-    for (int pass = 0; pass < 8; ++pass) {
-        cache_status r = cache_evict_hist(c, st, pass, c->ehist.p, stream);
-        if (r != CACHE_OK) return r;
-        if ((r = cache_evict_pick(c, c->ehist.p, st, pass, stream)) != CACHE_OK) return r;
-    }
-    int64_t got = 0;
-    cache_status r = cache_evict_apply(c, st, n, out_evicted, &got, out_dirty_ids, out_n_dirty, stream);
-    if (r != CACHE_OK) return r;
-    if (got != n) return fail(CACHE_E_STATE, "cache_evict: selection count mismatch (internal error)");
-    return CACHE_OK;
-}
+static int bitlen(unsigned long long v) { return v ? 64 - __builtin_clzll(v) : 0; }
 
 // Merge k freed slots (ascending) into a free list kept sorted descending (back() = lowest
 // free slot, so allocation stays lowest-first and deterministic): one linear merge.
@@ -1282,65 +1362,59 @@ static void merge_free(std::vector<int64_t>& fl, const unsigned long long* asc, 
     fl.swap(tmp);
 }
 
-cache_status cache_evict_apply(cache_t* c, const cache_evict_state* st, int64_t cap, uint64_t* out_evicted,
-                               int64_t* out_n, uint64_t* out_dirty_ids, int64_t* out_n_dirty, void* stream) {
-    if (!c || !st || cap < 0) return fail(CACHE_E_INVALID_ARG, "cache_evict_apply: bad argument");
-    DeviceGuard g(c->device);
-    cudaStream_t s = (cudaStream_t)stream;
+// Second half of every eviction (fused cache_evict and the protocol's cache_evict_apply): the
+// device lists (evicted keys in c->ekey, freed pool slots in c->epool, dirty slots / ids in
+// c->edirty / c->edid) are sorted on the GPU -- lists of <= kSmallSort keys by one CTA each in
+// a single launch, longer ones by LSD radix over only the bits their range spans (evicted keys:
+// [kbase, kbase + 2^kbits)) -- copied to pinned host memory, and the host's entry mirror and
+// free lists are updated.  n / nd / nfreed: evicted units, dirty entries, freed pool slots.
+static cache_status evict_finish(cache_t* c, int64_t n, int64_t nd, int64_t nfreed, unsigned long long kbase, int kbits,
+                                 uint64_t* out_evicted, uint64_t* out_dirty_ids, int64_t* out_n_dirty,
+                                 cudaStream_t s) {
     const bool entry_mode = c->km.gran == CACHE_EVICT_ENTRY;
-    // at most min(cap, live units) keys are <= the selected threshold on this rank
-    const int64_t bound = std::max<int64_t>(1, std::min<int64_t>(cap, entry_mode ? c->live_entries : c->live_items));
-    const int64_t dbound = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(cap, 1), c->live_entries));
-    // freed pool slots: one per evicted item, or up to num_k per evicted entry in entry mode
-    const int64_t pbound = entry_mode ? bound * c->num_k : bound;
-    CK(c->ekey.ensure_grow(bound));
-    CK(c->ekey2.ensure_grow(std::max(pbound, dbound)));
-    CK(c->epool.ensure_grow(pbound));
-    CK(c->eslot.ensure_grow(bound));
-    CK(c->escr.ensure_grow(sort_scratch_words(std::max(pbound, dbound))));
-    CK(c->ecnt.ensure(3));
-    CK(c->edirty.ensure_grow(dbound));
-    CK(c->edid.ensure_grow(dbound));
-    CK(cudaMemsetAsync(c->ecnt.p, 0, 24, s));
-    launch_evict_apply(c->present, c->fcnt, c->lastacc, c->ids, c->lslot, c->inv_e, c->hwm, c->km,
-                       reinterpret_cast<const EvictState*>(st), c->ekey.p, c->epool.p, c->eslot.p, c->ecnt.p,
-                       c->edirty.p, c->edid.p, bound, dbound, s);
-    c->launches++;
-    unsigned long long cnt[3];
-    CK(cudaMemcpyAsync(cnt, c->ecnt.p, 24, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    const int64_t n = (int64_t)cnt[0], nd = (int64_t)cnt[1];
-    const int64_t nfreed = entry_mode ? (int64_t)cnt[2] : n;   // stored states removed
-    if (out_n) *out_n = n;
-    if (n > cap || nd > cap || n > bound || nd > dbound || nfreed > pbound)
-        return fail(CACHE_E_STATE, "cache_evict_apply: more evictions than the output capacity (n differs "
-                                   "between the selection and the apply?); handle state undefined");
-    // Sorted lists, on the GPU: freed pool slots and dirty slots (ascending, merged into the
-    // lowest-first free lists), dirty ids (the API order), evicted keys (eviction order).  The
-    // host keeps no per-item mirror: the apply kernel lists the pool slots it freed (entry mode
-    // included), and the host's entry mirror only records which slots are live.
     const bool pool_freed = !c->alias && nfreed > 0;
     CK(c->hev_pool.ensure((pool_freed ? nfreed : 0) * 8));
     CK(c->hev_ds.ensure(nd * 8));
     if (out_dirty_ids) CK(c->hev_did.ensure(nd * 8));
     if (out_evicted) CK(c->hev_sorted.ensure(n * 8));
-    if (pool_freed) {
-        launch_sort_u64(c->epool.p, c->ekey2.p, nfreed, c->escr.p, s, 32);
-        CK(cudaMemcpyAsync(c->hev_pool.p, c->epool.p, nfreed * 8, cudaMemcpyDeviceToHost, s));
-    }
+    struct Job {
+        unsigned long long* keys;
+        int64_t n;
+        int bits;
+        unsigned long long base;
+        void* host;
+        unsigned long long* res;
+    };
+    Job jobs[4];
+    int nj = 0;
+    if (pool_freed) jobs[nj++] = Job{c->epool.p, nfreed, std::max(1, bitlen((unsigned long long)std::max<int64_t>(1, c->lcap) - 1)), 0ull, c->hev_pool.p, nullptr};
     if (nd) {
-        launch_sort_u64(c->edirty.p, c->ekey2.p, nd, c->escr.p, s, 40);
-        CK(cudaMemcpyAsync(c->hev_ds.p, c->edirty.p, nd * 8, cudaMemcpyDeviceToHost, s));
-        if (out_dirty_ids) {
-            launch_sort_u64(c->edid.p, c->ekey2.p, nd, c->escr.p, s, 32);
-            CK(cudaMemcpyAsync(c->hev_did.p, c->edid.p, nd * 8, cudaMemcpyDeviceToHost, s));
+        jobs[nj++] = Job{c->edirty.p, nd, std::max(1, bitlen((unsigned long long)std::max<int64_t>(1, c->hwm) - 1)), 0ull, c->hev_ds.p, nullptr};
+        if (out_dirty_ids)
+            jobs[nj++] = Job{c->edid.p, nd, std::max(1, bitlen(c->next_id ? c->next_id - 1 : 0)), 0ull, c->hev_did.p, nullptr};
+    }
+    if (out_evicted && n) jobs[nj++] = Job{c->ekey.p, n, std::max(1, kbits), kbase, c->hev_sorted.p, nullptr};
+    SortSegs small{};
+    for (int i = 0; i < nj; ++i) {
+        Job& jb = jobs[i];
+        if (jb.n <= kSmallSort) {
+            small.s[small.k++] = SortSeg{jb.keys, jb.n};
+            jb.res = jb.keys;
+        } else {
+            jb.res = launch_sort_u64(jb.keys, c->ekey2.p, jb.n, c->escr.p, s, jb.bits, jb.base);
+            c->launches += sort_launches(jb.n, jb.bits);
+            if (jb.res == c->ekey2.p) {   // tmp is shared by the lists: land this one in its own buffer
+                CK(cudaMemcpyAsync(jb.keys, jb.res, jb.n * 8, cudaMemcpyDeviceToDevice, s));
+                jb.res = jb.keys;
+            }
         }
     }
-    if (out_evicted && n) {
-        launch_sort_u64(c->ekey.p, c->ekey2.p, n, c->escr.p, s, 64);
-        CK(cudaMemcpyAsync(c->hev_sorted.p, c->ekey.p, n * 8, cudaMemcpyDeviceToHost, s));
+    if (small.k) {
+        launch_sort_small(small, s);
+        c->launches++;
     }
-    c->launches += 12 * pool_freed + 12 * (nd > 0) + 12 * (nd > 0 && out_dirty_ids) + 24 * (out_evicted && n);
+    CK(cudaGetLastError());
+    for (int i = 0; i < nj; ++i) CK(cudaMemcpyAsync(jobs[i].host, jobs[i].res, jobs[i].n * 8, cudaMemcpyDeviceToHost, s));
     c->live_items -= nfreed;
     CK(cudaStreamSynchronize(s));   // sorted lists landed
     const unsigned long long* ds = static_cast<const unsigned long long*>(c->hev_ds.p);
@@ -1352,6 +1426,7 @@ cache_status cache_evict_apply(cache_t* c, const cache_evict_state* st, int64_t 
     if (out_n_dirty) *out_n_dirty = nd;
     // shrink the scan high-water mark past trailing empty slots
     while (c->hwm > 0 && c->h_live[c->hwm - 1] == 0) c->hwm--;
+    c->last_ev_n = out_evicted ? n : 0;
     if (out_evicted && n) {
         const unsigned long long* sorted = static_cast<const unsigned long long*>(c->hev_sorted.p);
         // item key = score << 35 | id << 3 | j -> (id << 3 | j); entry key = score << 32 | id -> id
@@ -1359,6 +1434,117 @@ cache_status cache_evict_apply(cache_t* c, const cache_evict_state* st, int64_t 
         for (int64_t i = 0; i < n; ++i) out_evicted[i] = sorted[i] & m;
     }
     return CACHE_OK;
+}
+
+// Eviction list workspaces for up to `bound` evicted units / `dbound` dirty entries.
+static cudaError_t evict_lists(cache_t* c, int64_t bound, int64_t dbound, int64_t pbound) {
+    cudaError_t e;
+    if ((e = c->ekey.ensure_grow(bound)) != cudaSuccess) return e;
+    if ((e = c->ekey2.ensure_grow(std::max(std::max(pbound, dbound), bound))) != cudaSuccess) return e;
+    if ((e = c->epool.ensure_grow(pbound)) != cudaSuccess) return e;
+    if ((e = c->escr.ensure_grow(sort_scratch_words(std::max(std::max(pbound, dbound), bound)))) != cudaSuccess) return e;
+    if ((e = c->edirty.ensure_grow(dbound)) != cudaSuccess) return e;
+    return c->edid.ensure_grow(dbound);
+}
+
+// cache_evict: the fused select + apply of evict.cu (one cooperative launch), then
+// evict_finish.  The protocol's building blocks (cache_evict_hist / _pick / _apply) remain for
+// the distributed eviction, whose histograms are summed over ranks between passes.
+cache_status cache_evict(cache_t* c, int64_t n, uint64_t* out_evicted, uint64_t* out_dirty_ids,
+                         int64_t* out_n_dirty, void* stream) {
+    if (!c) return fail(CACHE_E_INVALID_ARG, "cache_evict: null cache");
+    if (n < 0) return fail(CACHE_E_INVALID_ARG, "cache_evict: n < 0");
+    const bool entry_mode = c->km.gran == CACHE_EVICT_ENTRY;
+    if (entry_mode ? n > c->live_entries : n > c->live_items)
+        return fail(CACHE_E_EVICT_RANGE, "cache_evict: n exceeds live items (entries in entry mode)");
+    if (out_n_dirty) *out_n_dirty = 0;
+    if (n == 0) return CACHE_OK;
+    DeviceGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    // exactly n units go; dirty entries: n in entry mode, <= min(n, live entries) in item mode
+    const int64_t dbound = std::max<int64_t>(1, std::min<int64_t>(n, c->live_entries));
+    const int64_t pbound = entry_mode ? n * c->num_k : n;
+    CK(evict_lists(c, n, dbound, pbound));
+    const int64_t units = entry_mode ? c->live_entries : c->live_items;
+    const int64_t ccap = std::max<int64_t>(65536, units / 16);
+    CK(c->ckey.ensure_grow(ccap));
+    CK(c->cslot.ensure_grow(ccap));
+    const size_t ws = (size_t)kSelMaxLevels * kSelBins * 4 + sizeof(SelOut);
+    CK(c->selws.ensure(ws));
+    CK(cudaMemsetAsync(c->selws.p, 0, ws, s));
+    SelOut* so = reinterpret_cast<SelOut*>(c->selws.p + (size_t)kSelMaxLevels * kSelBins * 4);
+    SelArgs a{};
+    a.present = c->present;
+    a.fcnt = c->fcnt;
+    a.lastacc = c->lastacc;
+    a.ids = c->ids;
+    a.lslot = c->lslot;
+    a.inv_e = c->inv_e;
+    a.n_slots = c->hwm;
+    a.n = (unsigned long long)n;
+    a.hist = reinterpret_cast<uint32_t*>(c->selws.p);
+    a.cand_key = c->ckey.p;
+    a.cand_slot = c->cslot.p;
+    a.cand_cap = (unsigned long long)(c->cand_cap_override >= 0 ? std::min<int64_t>(c->cand_cap_override, c->ckey.n)
+                                                                 : (int64_t)c->ckey.n);
+    a.ev_key = c->ekey.p;
+    a.ev_pool = c->epool.p;
+    a.dirty_slot = c->edirty.p;
+    a.dirty_id = c->edid.p;
+    a.ev_cap = (unsigned long long)n;
+    a.pool_cap = (unsigned long long)pbound;
+    a.dirty_cap = (unsigned long long)dbound;
+    a.out = so;
+    CK(launch_evict_select(a, c->km, s));
+    c->launches++;
+    SelOut h{};
+    CK(cudaMemcpyAsync(&h, so, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    c->last_sel[0] = h.levels;
+    c->last_sel[1] = h.full_sweeps;
+    c->last_sel[2] = h.compact_level;
+    c->last_sel[3] = (int64_t)h.cnt[3];
+    const int64_t got = (int64_t)h.cnt[0], nd = (int64_t)h.cnt[1];
+    const int64_t nfreed = entry_mode ? (int64_t)h.cnt[2] : got;
+    if (h.err || got != n || nd > dbound || nfreed > pbound)
+        return fail(CACHE_E_STATE, "cache_evict: selection count mismatch (internal error); handle state undefined");
+    const unsigned long long kmin = ~h.kmin_inv;
+    return evict_finish(c, n, nd, nfreed, kmin, bitlen(h.T - kmin), out_evicted, out_dirty_ids, out_n_dirty, s);
+}
+
+cache_status cache_evict_apply(cache_t* c, const cache_evict_state* st, int64_t cap, uint64_t* out_evicted,
+                               int64_t* out_n, uint64_t* out_dirty_ids, int64_t* out_n_dirty, void* stream) {
+    if (!c || !st || cap < 0) return fail(CACHE_E_INVALID_ARG, "cache_evict_apply: bad argument");
+    DeviceGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool entry_mode = c->km.gran == CACHE_EVICT_ENTRY;
+    // at most min(cap, live units) keys are <= the selected threshold on this rank
+    const int64_t bound = std::max<int64_t>(1, std::min<int64_t>(cap, entry_mode ? c->live_entries : c->live_items));
+    const int64_t dbound = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(cap, 1), c->live_entries));
+    // freed pool slots: one per evicted item, or up to num_k per evicted entry in entry mode
+    const int64_t pbound = entry_mode ? bound * c->num_k : bound;
+    CK(evict_lists(c, bound, dbound, pbound));
+    CK(c->eslot.ensure_grow(bound));
+    CK(c->ecnt.ensure(3));
+    CK(cudaMemsetAsync(c->ecnt.p, 0, 24, s));
+    launch_evict_apply(c->present, c->fcnt, c->lastacc, c->ids, c->lslot, c->inv_e, c->hwm, c->km,
+                       reinterpret_cast<const EvictState*>(st), c->ekey.p, c->epool.p, c->eslot.p, c->ecnt.p,
+                       c->edirty.p, c->edid.p, bound, dbound, s, c->abortw.p);
+    c->launches++;
+    unsigned long long cnt[3];
+    CK(cudaMemcpyAsync(cnt, c->ecnt.p, 24, cudaMemcpyDeviceToHost, s));
+    EvictState hst{};
+    CK(cudaMemcpyAsync(&hst, st, sizeof(hst), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (peer_failed(c)) return peer_fail("cache_evict_apply");   // the selection's exchange failed: nothing applied
+    const int64_t n = (int64_t)cnt[0], nd = (int64_t)cnt[1];
+    const int64_t nfreed = entry_mode ? (int64_t)cnt[2] : n;   // stored states removed
+    if (out_n) *out_n = n;
+    if (n > cap || nd > cap || n > bound || nd > dbound || nfreed > pbound)
+        return fail(CACHE_E_STATE, "cache_evict_apply: more evictions than the output capacity (n differs "
+                                   "between the selection and the apply?); handle state undefined");
+    // evicted keys are <= the selected key (st->prefix)
+    return evict_finish(c, n, nd, nfreed, 0ull, bitlen(hst.prefix), out_evicted, out_dirty_ids, out_n_dirty, s);
 }
 
 // Entry slot of id, or -1 (a scan of the host mirrors: only the inspection calls need it).
@@ -1488,18 +1674,48 @@ extern "C" cache_status cache_debug_tc_scores(cache_t* c, int64_t b, const void*
 }
 
 extern "C" cache_status cache_debug_sort_u64(uint64_t* keys, int64_t n, void* stream) {
-    if (n < 0 || (n > 0 && !keys)) return fail(CACHE_E_INVALID_ARG, "cache_debug_sort_u64: bad argument");
+    return cache_debug_sort_u64_ex(keys, n, 64, 0ull, 0, stream);
+}
+
+extern "C" cache_status cache_debug_sort_u64_ex(uint64_t* keys, int64_t n, int32_t bits, uint64_t base, int32_t small,
+                                                void* stream) {
+    if (n < 0 || (n > 0 && !keys) || bits < 1 || bits > 64 || (small && n > kSmallSort))
+        return fail(CACHE_E_INVALID_ARG, "cache_debug_sort_u64_ex: bad argument");
     if (n <= 1) return CACHE_OK;
     cudaStream_t s = (cudaStream_t)stream;
+    auto* k = reinterpret_cast<unsigned long long*>(keys);
+    if (small) {
+        SortSegs sg{};
+        sg.s[0] = SortSeg{k, n};
+        sg.k = 1;
+        launch_sort_small(sg, s);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(s));
+        return CACHE_OK;
+    }
     DevBuf<unsigned long long> tmp;
     DevBuf<uint32_t> scr;
     CK(tmp.ensure(n));
     CK(scr.ensure(sort_scratch_words(n)));
-    launch_sort_u64(reinterpret_cast<unsigned long long*>(keys), tmp.p, n, scr.p, s);
+    unsigned long long* r = launch_sort_u64(k, tmp.p, n, scr.p, s, bits, base);
+    if (r != k) cudaMemcpyAsync(k, r, n * 8, cudaMemcpyDeviceToDevice, s);
     cudaError_t e = cudaStreamSynchronize(s);
     tmp.release();
     scr.release();
     CK(e);
+    return CACHE_OK;
+}
+
+// Statistics of the last fused cache_evict: levels, full sweeps, compaction level, candidates.
+extern "C" cache_status cache_debug_evict_stats(cache_t* c, int64_t* out4) {
+    if (!c || !out4) return fail(CACHE_E_INVALID_ARG, "cache_debug_evict_stats: bad argument");
+    for (int i = 0; i < 4; ++i) out4[i] = c->last_sel[i];
+    return CACHE_OK;
+}
+
+extern "C" cache_status cache_debug_set_evict_cand_cap(cache_t* c, int64_t cap) {
+    if (!c) return fail(CACHE_E_INVALID_ARG, "cache_debug_set_evict_cand_cap: null cache");
+    c->cand_cap_override = cap < 0 ? -1 : cap;
     return CACHE_OK;
 }
 

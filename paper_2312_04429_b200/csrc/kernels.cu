@@ -8,6 +8,7 @@
 //                    clearing, dirty-entry removal (a9)
 #include "common.cuh"
 #include "kernels.h"
+#include "evict.cuh"
 
 namespace nv {
 
@@ -195,6 +196,10 @@ __global__ void __launch_bounds__(256, 4) k_normalise(const Tin* __restrict__ x,
 // Publish: every thread fences its stores at system scope, the CTA counts itself done, and
 // the last CTA of the grid stores the epoch into every consumer's flag word (release.sys).
 // A fence + relaxed RMW chain + fence orders every CTA's data before the flag.
+__device__ __forceinline__ bool push_aborted(const PushSignal& sg) {
+    return sg.abort && *(volatile const uint32_t*)sg.abort;
+}
+
 __device__ __forceinline__ void push_signal(const PushSignal& sg) {
     __threadfence_system();
     __syncthreads();
@@ -214,6 +219,7 @@ __device__ __forceinline__ void push_signal(const PushSignal& sg) {
 template <typename Tin, int NS>
 __global__ void __launch_bounds__(256) k_normalise_push(const Tin* __restrict__ x, int64_t n, PushRows out,
                                                         int64_t row0, PushSignal sig) {
+    if (push_aborted(sig)) return;   // a peer failed: no more stores into peer memory
     const int lane = threadIdx.x & 31;
     const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     if (r < n) {
@@ -225,21 +231,32 @@ __global__ void __launch_bounds__(256) k_normalise_push(const Tin* __restrict__ 
     push_signal(sig);
 }
 
-__global__ void k_wait_flags(const uint32_t* __restrict__ flags, int world, uint32_t epoch) {
+__global__ void k_wait_flags(const uint32_t* __restrict__ flags, int world, uint32_t epoch,
+                             unsigned long long timeout_ns, uint32_t* abort, uint32_t* err_host) {
     const int t = threadIdx.x;
     if (t >= world) return;
-    unsigned long long spins = 0;
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     for (;;) {
         uint32_t v;
         asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + t) : "memory");
         if ((int32_t)(v - epoch) >= 0) break;
-        __nanosleep(256);
-        if (++spins > (1ull << 26)) __trap();   // a peer never published (> ~17 s): fail, don't hang
+        if (*(volatile uint32_t*)abort) break;   // an earlier wait already failed
+        unsigned long long now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        if (now - t0 > timeout_ns) {   // rank t never published: flag it, do not hang or trap
+            atomicOr(abort, 1u << t);
+            *(volatile uint32_t*)err_host = 1u;
+            __threadfence_system();
+            break;
+        }
+        __nanosleep(1000);
     }
 }
 
-void launch_wait_flags(const uint32_t* flags, int world, uint32_t epoch, cudaStream_t s) {
-    k_wait_flags<<<1, 32, 0, s>>>(flags, world, epoch);
+void launch_wait_flags(const uint32_t* flags, int world, uint32_t epoch, unsigned long long timeout_ns,
+                       uint32_t* abort, uint32_t* err_host, cudaStream_t s) {
+    k_wait_flags<<<1, 32, 0, s>>>(flags, world, epoch, timeout_ns, abort, err_host);
 }
 
 void launch_normalise_push(const void* x, int dtype, int64_t n, int dim, const PushRows& out, int64_t row0,
@@ -511,8 +528,10 @@ k_finalize(const Rec* __restrict__ ws, int parts, int64_t B, int topk, const flo
                         const int j = 31 - __clz(m);
                         K = km.kv[j];
                         src = lslot[(int64_t)slot * km.num_k + j];
-                        atomicAdd(fcnt + (int64_t)slot * km.num_k + j, 1u);
-                        lastacc[(int64_t)slot * km.num_k + j] = clock;   // LRU clock (same value for all hits)
+                        if (fcnt) {   // null: a read-only lookup (cache_query_peek) counts no access
+                            atomicAdd(fcnt + (int64_t)slot * km.num_k + j, 1u);
+                            lastacc[(int64_t)slot * km.num_k + j] = clock;   // LRU clock (same value for all hits)
+                        }
                     }
                 }
             }
@@ -661,57 +680,7 @@ void launch_copy_latents(const uint8_t* src, const CopyPlan* plan, int64_t n, in
 // evicted: presence bit cleared, latent slot freed; entries left with no K are dirty and
 // are invalidated (inv_norm = NaN) in the same kernel.
 // ---------------------------------------------------------------------------------------
-// Policy score of item (e, j) (CACHE_POLICY_*): LCBFU f*K, LRU last-access clock,
-// LFU f, FIFO 0 (the id decides).  Item key: min(score, 2^29-1) << 35 | id << 3 | j.
-// Entry key (R24): the policy score aggregated over the entry's stored items (LCBFU sum f*K,
-// LFU sum f, LRU max last access, FIFO 0), min(., 2^32-1) << 32 | id.
-// The kernels are instantiated per (policy, granularity) with the K values in registers: a
-// runtime switch and constant-bank loads per item made the sweep instruction-bound (ncu r1y:
-// ~120 SASS instructions per item, 68% issue-slot use at 1.1 TB/s).
-template <int POLICY>
-__device__ __forceinline__ unsigned long long item_score(const uint32_t* __restrict__ fcnt,
-                                                         const uint32_t* __restrict__ lastacc, int64_t it, int kvj) {
-    if constexpr (POLICY == CACHE_POLICY_LRU) return lastacc[it];
-    else if constexpr (POLICY == CACHE_POLICY_LFU) return fcnt[it];
-    else if constexpr (POLICY == CACHE_POLICY_FIFO) return 0ull;
-    else return (unsigned long long)fcnt[it] * (unsigned long long)(unsigned)kvj;
-}
-
-__device__ __forceinline__ unsigned long long item_key(unsigned long long sc, uint32_t id, int j) {
-    if (sc > 0x1FFFFFFFull) sc = 0x1FFFFFFFull;
-    return (sc << 35) | ((unsigned long long)id << 3) | (unsigned long long)j;
-}
-
-template <int POLICY>
-__device__ __forceinline__ unsigned long long entry_key(const uint32_t* __restrict__ fcnt,
-                                                        const uint32_t* __restrict__ lastacc, int64_t e, uint32_t m,
-                                                        uint32_t id, int nk, const int (&kv)[CACHE_MAX_K]) {
-    unsigned long long sc = 0ull;
-#pragma unroll
-    for (int j = 0; j < CACHE_MAX_K; ++j) {
-        if (j >= nk || !((m >> j) & 1u)) continue;
-        const unsigned long long v = item_score<POLICY>(fcnt, lastacc, e * nk + j, kv[j]);
-        if constexpr (POLICY == CACHE_POLICY_LRU) sc = v > sc ? v : sc;
-        else sc += v;
-    }
-    if (sc > 0xFFFFFFFFull) sc = 0xFFFFFFFFull;
-    return (sc << 32) | (unsigned long long)id;
-}
-
-// Per-thread run-length aggregation of histogram increments: consecutive keys of a thread
-// mostly share a digit (early passes: almost all), so one shared atomic per run.
-struct DigitRun {
-    unsigned cur = 0xFFFFFFFFu, cnt = 0;
-    __device__ __forceinline__ void add(unsigned* sh, unsigned d) {
-        if (d == cur) { ++cnt; return; }
-        if (cnt) atomicAdd(&sh[cur], cnt);
-        cur = d;
-        cnt = 1;
-    }
-    __device__ __forceinline__ void flush(unsigned* sh) {
-        if (cnt) atomicAdd(&sh[cur], cnt);
-    }
-};
+// item_score / item_key / entry_key / DigitRun: evict.cuh (shared with evict.cu).
 
 template <int POLICY, int GRAN>
 __global__ void __launch_bounds__(256)
@@ -719,6 +688,7 @@ k_evict_hist(const uint32_t* __restrict__ present, const uint32_t* __restrict__ 
              const uint32_t* __restrict__ lastacc, const uint32_t* __restrict__ ids, int64_t n_slots, KMap km,
              const EvictState* __restrict__ st, int shift, unsigned int* __restrict__ hist, PushHist ph,
              PushSignal sig) {
+    if (ph.world && push_aborted(sig)) return;
     __shared__ unsigned int sh[256];
     sh[threadIdx.x] = 0;
     __syncthreads();
@@ -775,19 +745,7 @@ __global__ void k_evict_pick(unsigned int* __restrict__ hist, EvictState* __rest
     for (int d = threadIdx.x; d < 256; d += blockDim.x) hist[d] = 0;
 }
 
-// One output slot range per warp and key column: a ballot of the evicting lanes, one atomic by
-// the leader, each lane's index = its rank among them (per-lane atomics on one counter
-// serialised at L2).  Item mode also emits each item's entry slot so the host updates its
-// mirrors without an id lookup.  The sweep is warp-uniform (lane l takes slot base + l).
-__device__ __forceinline__ unsigned long long warp_claim(unsigned long long* counter, bool take, int lane) {
-    const unsigned bal = __ballot_sync(0xFFFFFFFFu, take);
-    unsigned long long base = 0;
-    if (bal) {
-        if (lane == __ffs(bal) - 1) base = atomicAdd(counter, (unsigned long long)__popc(bal));
-        base = __shfl_sync(0xFFFFFFFFu, base, __ffs(bal) - 1);
-    }
-    return base + (unsigned long long)__popc(bal & ((1u << lane) - 1u));
-}
+// warp_claim: evict.cuh.
 
 template <int POLICY, int GRAN>
 __global__ void __launch_bounds__(256)
@@ -797,7 +755,9 @@ k_evict_apply(uint32_t* __restrict__ present, uint32_t* __restrict__ fcnt, const
               const EvictState* __restrict__ st, unsigned long long* __restrict__ ev_key,
               unsigned long long* __restrict__ ev_pool, int64_t* __restrict__ ev_eslot,
               unsigned long long* __restrict__ counters, unsigned long long* __restrict__ dirty_slot,
-              unsigned long long* __restrict__ dirty_id, unsigned long long ev_cap, unsigned long long dirty_cap) {
+              unsigned long long* __restrict__ dirty_id, unsigned long long ev_cap, unsigned long long dirty_cap,
+              const uint32_t* __restrict__ abort) {
+    if (abort && *(volatile const uint32_t*)abort) return;   // the distributed selection did not finish
     const unsigned long long T = st->prefix;
     const int lane = threadIdx.x & 31;
     const int nk = km.num_k;
@@ -878,21 +838,7 @@ static int one_wave(K kern) {
     return bps * sms;
 }
 
-#define NV_EVICT_DISPATCH(KERN, ...)                                                                   \
-    do {                                                                                               \
-        const int pol_ = km.policy, gr_ = km.gran;                                                     \
-        if (gr_ == CACHE_EVICT_ENTRY) {                                                                \
-            if (pol_ == CACHE_POLICY_LRU) KERN(CACHE_POLICY_LRU, CACHE_EVICT_ENTRY);                   \
-            else if (pol_ == CACHE_POLICY_LFU) KERN(CACHE_POLICY_LFU, CACHE_EVICT_ENTRY);              \
-            else if (pol_ == CACHE_POLICY_FIFO) KERN(CACHE_POLICY_FIFO, CACHE_EVICT_ENTRY);            \
-            else KERN(CACHE_POLICY_LCBFU, CACHE_EVICT_ENTRY);                                          \
-        } else {                                                                                       \
-            if (pol_ == CACHE_POLICY_LRU) KERN(CACHE_POLICY_LRU, CACHE_EVICT_ITEM);                    \
-            else if (pol_ == CACHE_POLICY_LFU) KERN(CACHE_POLICY_LFU, CACHE_EVICT_ITEM);               \
-            else if (pol_ == CACHE_POLICY_FIFO) KERN(CACHE_POLICY_FIFO, CACHE_EVICT_ITEM);             \
-            else KERN(CACHE_POLICY_LCBFU, CACHE_EVICT_ITEM);                                           \
-        }                                                                                              \
-    } while (0)
+// NV_EVICT_DISPATCH: evict.cuh.
 
 void launch_evict_hist(const uint32_t* present, const uint32_t* fcnt, const uint32_t* lastacc, const uint32_t* ids,
                        int64_t n_slots, const KMap& km, const EvictState* st, int pass, unsigned int* hist,
@@ -945,6 +891,7 @@ __global__ void __launch_bounds__(256)
 k_local_merge(const Rec* __restrict__ ws, int parts, int64_t B, int topk, const int32_t* __restrict__ qstatus,
               const uint32_t* __restrict__ present, int owner, cache_shard_rec* __restrict__ out, PushRecs dst,
               PushSignal sig) {
+    if (kPush && push_aborted(sig)) return;
     const int lane = threadIdx.x & 31;
     const int64_t b = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     if (b < B) {
@@ -1012,6 +959,7 @@ k_merge_sharded(const cache_shard_rec* __restrict__ recs, int64_t rec_stride, in
                 float* __restrict__ out_scores,
                 int32_t* __restrict__ out_k, uint8_t* __restrict__ latent_out, void** __restrict__ out_ptr,
                 int32_t* __restrict__ out_status) {
+    if (peers.abort && *(volatile const uint32_t*)peers.abort) return;   // a peer failed: no P2P reads
     __shared__ unsigned long long s_key[KMAX];
     __shared__ uint32_t s_slot[KMAX];
     __shared__ long long s_src;
@@ -1127,14 +1075,14 @@ void launch_evict_apply(uint32_t* present, uint32_t* fcnt, const uint32_t* lasta
                         const int32_t* lslot, float* inv_e, int64_t n_slots, const KMap& km, const EvictState* st,
                         unsigned long long* ev_key, unsigned long long* ev_pool, int64_t* ev_eslot,
                         unsigned long long* counters, unsigned long long* dirty_slot, unsigned long long* dirty_id,
-                        int64_t ev_cap, int64_t dirty_cap, cudaStream_t s) {
+                        int64_t ev_cap, int64_t dirty_cap, cudaStream_t s, const uint32_t* abort) {
 #define NV_APPLY(P, G)                                                                                 \
     do {                                                                                               \
         static const int wave = one_wave(k_evict_apply<P, G>);                                         \
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(wave, (n_slots + 255) / 256));   \
         k_evict_apply<P, G><<<grid, 256, 0, s>>>(present, fcnt, lastacc, ids, lslot, inv_e, n_slots, km, st,  \
                                                  ev_key, ev_pool, ev_eslot, counters, dirty_slot, dirty_id, \
-                                                 (unsigned long long)ev_cap, (unsigned long long)dirty_cap); \
+                                                 (unsigned long long)ev_cap, (unsigned long long)dirty_cap, abort); \
     } while (0)
     NV_EVICT_DISPATCH(NV_APPLY);
 #undef NV_APPLY

@@ -77,12 +77,56 @@ void launch_evict_apply(uint32_t* present, uint32_t* fcnt, const uint32_t* lasta
                         const int32_t* lslot, float* inv_e, int64_t n_slots, const KMap& km, const EvictState* st,
                         unsigned long long* ev_key, unsigned long long* ev_pool, int64_t* ev_eslot,
                         unsigned long long* counters, unsigned long long* dirty_slot, unsigned long long* dirty_id,
-                        int64_t ev_cap, int64_t dirty_cap, cudaStream_t s);
-// Ascending sort of n 64-bit keys whose values are < 2^bits (LSD radix, 8-bit digits, an even
-// number of stable passes); tmp: n keys, scratch: >= sort_scratch_words(n) u32.  Result in keys.
+                        int64_t ev_cap, int64_t dirty_cap, cudaStream_t s, const uint32_t* abort = nullptr);
+// Ascending sort of n 64-bit keys with base <= key < base + 2^bits (LSD radix over key - base,
+// ceil(bits/8) stable 8-bit passes); tmp: n keys, scratch: >= sort_scratch_words(n) u32.
+// Returns the buffer that holds the result (keys or tmp).
 int64_t sort_scratch_words(int64_t n);
-void launch_sort_u64(unsigned long long* keys, unsigned long long* tmp, int64_t n, uint32_t* scratch,
-                     cudaStream_t s, int bits = 64);
+unsigned long long* launch_sort_u64(unsigned long long* keys, unsigned long long* tmp, int64_t n, uint32_t* scratch,
+                                    cudaStream_t s, int bits = 64, unsigned long long base = 0ull);
+int sort_launches(int64_t n, int bits);
+// Up to 4 lists of <= kSmallSort keys, each sorted in place by one CTA (one launch).
+constexpr int kSmallSort = 16384;
+struct SortSeg {
+    unsigned long long* keys;
+    int64_t n;
+};
+struct SortSegs {
+    SortSeg s[4];
+    int k;
+};
+void launch_sort_small(const SortSegs& segs, cudaStream_t s);
+
+// Fused single-cache eviction (evict.cu): the exact n smallest unit keys selected and applied
+// in ONE cooperative launch (see evict.cu for the algorithm).  `out` is zeroed by the caller.
+struct SelOut {
+    unsigned long long cnt[4];    // evicted units, dirty entries, freed pool slots (entry mode), candidates
+    unsigned long long kmin_inv;  // ~(smallest live key)
+    unsigned long long T;         // threshold: every unit with key <= T was evicted
+    uint32_t levels, full_sweeps, compact_level, err;
+};
+constexpr int kSelBins = 4096, kSelMaxLevels = 8;
+struct SelArgs {
+    uint32_t* present;
+    uint32_t* fcnt;
+    const uint32_t* lastacc;
+    const uint32_t* ids;
+    const int32_t* lslot;
+    float* inv_e;
+    int64_t n_slots;
+    unsigned long long n;              // units to evict (<= live units)
+    uint32_t* hist;                    // [kSelMaxLevels][kSelBins], zeroed by the caller
+    unsigned long long* cand_key;      // candidate compaction buffers
+    uint32_t* cand_slot;
+    unsigned long long cand_cap;
+    unsigned long long* ev_key;        // evicted unit keys (unsorted), capacity ev_cap
+    unsigned long long* ev_pool;       // freed pool slots, capacity pool_cap
+    unsigned long long* dirty_slot;    // dirty entries, capacity dirty_cap
+    unsigned long long* dirty_id;
+    unsigned long long ev_cap, pool_cap, dirty_cap;
+    SelOut* out;
+};
+cudaError_t launch_evict_select(const SelArgs& a, const KMap& km, cudaStream_t s);
 
 // Cache-selector profiling (Alg. 2): per profiling query i with a live nearest entry
 // (rec[i].key != 0), s_i = clamp(t_i * inv_q[i]); for every K_j with quality[j*b + i] <= alpha,
@@ -110,6 +154,7 @@ struct PeerPtrs {                       // per-rank device pointers (own rank in
     uint32_t* fcnt[kMaxWorld];
     uint32_t* lastacc[kMaxWorld];
     const uint8_t* pool[kMaxWorld];
+    const uint32_t* abort;                  // this rank's abort word (k_wait_flags timeout) or null
 };
 void launch_local_merge(int kmax, const Rec* ws, int parts, int64_t B, int topk, const int32_t* qstatus,
                         const uint32_t* present, int owner, cache_shard_rec* out, cudaStream_t s);
@@ -128,6 +173,8 @@ struct PushSignal {
     int world;
     uint32_t* done;              // local CTA-completion counter (zero between launches)
     uint32_t epoch;
+    const uint32_t* abort;       // this rank's abort word: set once a peer wait timed out -> no more
+                                 // stores into peer memory, no more publication
 };
 struct PushRows {                // destinations of the pushed query rows, one per rank
     __nv_bfloat16* y[kMaxWorld];
@@ -145,7 +192,12 @@ void launch_normalise_push(const void* x, int dtype, int64_t n, int dim, const P
 void launch_local_merge_push(int kmax, const Rec* ws, int parts, int64_t B, int topk, const int32_t* qstatus,
                              const uint32_t* present, int owner, const PushRecs& dst, const PushSignal& sig,
                              cudaStream_t s);
-void launch_wait_flags(const uint32_t* flags, int world, uint32_t epoch, cudaStream_t s);
+// Wait until every rank's flag reached `epoch`; a rank that has not published within
+// timeout_ns (globaltimer) sets bit r of *abort (device) and *err_host (mapped host memory) and
+// the wait returns, so the consumers behind it skip their peer accesses and the host reports
+// CACHE_E_NCCL instead of the context dying (round 1: __trap) or the stream hanging.
+void launch_wait_flags(const uint32_t* flags, int world, uint32_t epoch, unsigned long long timeout_ns,
+                       uint32_t* abort, uint32_t* err_host, cudaStream_t s);
 // Eviction histogram pass whose counts go straight into every rank's accumulator (P2P
 // atomics) instead of a local buffer for an all-reduce; the grid then publishes `sig`.
 struct PushHist {

@@ -2,7 +2,9 @@
 // out_evicted (the selected items in eviction = key order, R11 / R24): the selection kernels
 // emit keys in arbitrary order and sorting ~10^5-10^6 keys on the host cost tens of ms.
 //
-// 8 passes of 8-bit digits; every pass is stable:
+// ceil(bits / 8) passes of 8-bit digits over (key - base), so a list whose keys span a narrow
+// range (evicted keys: [min key, threshold]; slots: [0, hwm)) needs only the passes that range
+// has; every pass is stable:
 //   k_sort_count    per 2,048-key tile: digit counts (warp-aggregated shared atomics),
 //                   stored digit-major counts[d][tile], and the pass's digit totals
 //   k_sort_scan     one CTA per digit d: base = sum of the lower digits' totals, then a
@@ -18,8 +20,8 @@ namespace nv {
 constexpr int kSortThreads = 256, kSortRounds = 8, kSortTile = kSortThreads * kSortRounds;
 
 __global__ void __launch_bounds__(256)
-k_sort_count(const unsigned long long* __restrict__ keys, int64_t n, int shift, uint32_t* __restrict__ counts,
-             int64_t ntiles, uint32_t* __restrict__ dtot) {
+k_sort_count(const unsigned long long* __restrict__ keys, int64_t n, int shift, unsigned long long kbase,
+             uint32_t* __restrict__ counts, int64_t ntiles, uint32_t* __restrict__ dtot) {
     __shared__ uint32_t sh[256];
     sh[threadIdx.x] = 0;
     __syncthreads();
@@ -28,7 +30,7 @@ k_sort_count(const unsigned long long* __restrict__ keys, int64_t n, int shift, 
     for (int r = 0; r < kSortRounds; ++r) {
         const int64_t i = base + r * kSortThreads + threadIdx.x;
         const bool v = i < n;
-        const unsigned d = v ? (unsigned)((keys[i] >> shift) & 255ull) : 256u;
+        const unsigned d = v ? (unsigned)(((keys[i] - kbase) >> shift) & 255ull) : 256u;
         const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
         if (v && lane == __ffs(peers) - 1) atomicAdd(&sh[d], (unsigned)__popc(peers));
     }
@@ -86,7 +88,7 @@ __global__ void __launch_bounds__(1024) k_sort_scan(uint32_t* __restrict__ count
 
 __global__ void __launch_bounds__(256)
 k_sort_scatter(const unsigned long long* __restrict__ in, unsigned long long* __restrict__ out, int64_t n, int shift,
-               const uint32_t* __restrict__ offs, int64_t ntiles) {
+               unsigned long long kbase, const uint32_t* __restrict__ offs, int64_t ntiles) {
     __shared__ uint32_t s_base[256];
     __shared__ uint32_t s_tot[256];
     __shared__ uint32_t s_w[8][256];
@@ -100,7 +102,7 @@ k_sort_scatter(const unsigned long long* __restrict__ in, unsigned long long* __
         const int64_t i = base + r * kSortThreads + threadIdx.x;
         const bool v = i < n;
         const unsigned long long k = v ? in[i] : 0ull;
-        const unsigned d = v ? (unsigned)((k >> shift) & 255ull) : 256u;
+        const unsigned d = v ? (unsigned)(((k - kbase) >> shift) & 255ull) : 256u;
         const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
         const unsigned rank = (unsigned)__popc(peers & ((1u << lane) - 1u));
         if (v && lane == __ffs(peers) - 1) s_w[warp][d] = (unsigned)__popc(peers);
@@ -125,22 +127,60 @@ k_sort_scatter(const unsigned long long* __restrict__ in, unsigned long long* __
 // scratch: counts[256][ntiles] | digit totals [8 passes][256]
 int64_t sort_scratch_words(int64_t n) { return 256 * std::max<int64_t>(1, (n + kSortTile - 1) / kSortTile) + 8 * 256; }
 
-void launch_sort_u64(unsigned long long* keys, unsigned long long* tmp, int64_t n, uint32_t* scratch,
-                     cudaStream_t s, int bits) {
-    if (n <= 1) return;
-    const int passes = ((std::min(64, std::max(8, bits)) + 15) / 16) * 2;   // even: result lands in keys
+// Small lists: one CTA per list sorts up to kSmallSort keys in shared memory (bitonic network
+// over the next power of two, padding = all-ones keys) -- one launch for several lists instead
+// of 3 launches per radix pass each.
+__global__ void __launch_bounds__(1024) k_sort_small(SortSegs segs) {
+    extern __shared__ unsigned long long sk[];
+    const SortSeg sg = segs.s[blockIdx.x];
+    const int n = (int)sg.n;
+    int N = 2;
+    while (N < n) N <<= 1;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) sk[i] = i < n ? sg.keys[i] : ~0ull;
+    __syncthreads();
+    for (int k = 2; k <= N; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int p = threadIdx.x; p < N / 2; p += blockDim.x) {
+                const int i = 2 * j * (p / j) + (p % j), ixj = i + j;
+                const unsigned long long a = sk[i], b = sk[ixj];
+                if ((a > b) == ((i & k) == 0)) { sk[i] = b; sk[ixj] = a; }
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) sg.keys[i] = sk[i];
+}
+
+void launch_sort_small(const SortSegs& segs, cudaStream_t s) {
+    if (segs.k <= 0) return;
+    static bool attr = (cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kSmallSort * 8), true);
+    (void)attr;
+    int64_t mx = 2;
+    for (int i = 0; i < segs.k; ++i) mx = std::max<int64_t>(mx, segs.s[i].n);
+    int N = 2;
+    while (N < mx) N <<= 1;
+    k_sort_small<<<segs.k, 1024, (size_t)N * 8, s>>>(segs);
+}
+
+unsigned long long* launch_sort_u64(unsigned long long* keys, unsigned long long* tmp, int64_t n, uint32_t* scratch,
+                                    cudaStream_t s, int bits, unsigned long long base) {
+    if (n <= 1) return keys;
+    const int passes = (std::min(64, std::max(1, bits)) + 7) / 8;
     const int64_t ntiles = (n + kSortTile - 1) / kSortTile;
     unsigned long long *src = keys, *dst = tmp;
     uint32_t* dtot = scratch + 256 * ntiles;
     cudaMemsetAsync(dtot, 0, 8 * 256 * sizeof(uint32_t), s);
     for (int pass = 0; pass < passes; ++pass) {
         const int shift = 8 * pass;
-        k_sort_count<<<(unsigned)ntiles, 256, 0, s>>>(src, n, shift, scratch, ntiles, dtot + 256 * pass);
+        k_sort_count<<<(unsigned)ntiles, 256, 0, s>>>(src, n, shift, base, scratch, ntiles, dtot + 256 * pass);
         k_sort_scan<<<256, 1024, 0, s>>>(scratch, ntiles, dtot + 256 * pass);
-        k_sort_scatter<<<(unsigned)ntiles, 256, 0, s>>>(src, dst, n, shift, scratch, ntiles);
+        k_sort_scatter<<<(unsigned)ntiles, 256, 0, s>>>(src, dst, n, shift, base, scratch, ntiles);
         std::swap(src, dst);
     }
-    // an even number of passes: the result is back in `keys`
+    return src;   // the buffer holding the sorted keys (keys for an even number of passes)
 }
+
+int sort_launches(int64_t n, int bits) { return n <= 1 ? 0 : 1 + 3 * ((std::min(64, std::max(1, bits)) + 7) / 8); }
 
 }  // namespace nv

@@ -81,16 +81,22 @@ def request_latency(k_used: int, lat: LatencyParams) -> float:
 
 class ServingLoop:
     """cache: an object with lookup(q) -> (ids, K), admit(emb, latents), evict(n) -> (evicted,
-    dirty), free() -> (free entries, free items) and, with use_predictor, train_predictor()
-    and predict(q) -> bool flags; see GpuCache for the library adapter.
+    dirty), free() -> (free entries, free items), capacity_items and, with use_predictor,
+    train_predictor(), predict(q) -> bool flags and (optional) peek(q) -> K without counting
+    an access; see GpuCache for the library adapter.
 
     With the match predictor (Alg. 1 line 2) a predicted miss goes straight
-    to scratch generation without the search (latency C, arrow 1 of the overview); it
-    is retrained when more than 5% of the cached entries changed since the last training
-    (P:485-486)."""
+    to scratch generation WITHOUT the search (latency C, arrow 1 of the overview): only
+    the rows the predictor accepts are looked up, so rejected requests count no access.  It is
+    retrained when more than 5% of the cached entries changed since the last training
+    (P:485-486).  Whether a rejected request would have hit (recall) is measured
+    with the cache's read-only peek, which leaves the eviction state untouched.
+
+    keep_log: record every step (per-request K and latency, evicted / dirty ids, admitted
+    prompts) in self.log -- the per-request parity tests compare it with the oracle's loop."""
 
     def __init__(self, cache, k_values, lat: LatencyParams = LatencyParams(), make_latents=None,
-                 use_predictor: bool = False, retrain_threshold: float = 0.05):
+                 use_predictor: bool = False, retrain_threshold: float = 0.05, keep_log: bool = False):
         self.cache, self.k_values, self.lat = cache, tuple(k_values), lat
         self.make_latents = make_latents
         self.report = RunReport(k_values=self.k_values)
@@ -100,6 +106,7 @@ class ServingLoop:
         self._trained_on = 0
         self.pred_stats = dict(predicted_true=0, predicted_true_hit=0, predicted_false=0,
                                predicted_false_would_hit=0, searched_missed=0, retrains=0)
+        self.keep_log, self.log = keep_log, []
 
     def _maybe_retrain(self):
         fe, _ = self.cache.free()
@@ -113,33 +120,45 @@ class ServingLoop:
         return True
 
     def step(self, q: np.ndarray):
-        ids, ks = self.cache.lookup(q)
+        b = len(q)
         gate = None
         if self.use_predictor and self._maybe_retrain():
-            gate = self.cache.predict(q)
+            gate = np.asarray(self.cache.predict(q), dtype=bool)
+        ids = np.full(b, np.iinfo(np.uint64).max, dtype=np.uint64)
+        ks = np.zeros(b, dtype=np.int32)
+        searched = np.arange(b) if gate is None else np.nonzero(gate)[0]
+        if len(searched):   # Alg. 1 lines 4-5: search_VDB + heuristics_K for the accepted rows only
+            ids_s, ks_s = self.cache.lookup(q[searched] if gate is not None else q)
+            ids[searched], ks[searched] = ids_s, ks_s
         r = self.report
-        for i, k in enumerate(ks.tolist()):
+        lat_step = []
+        if gate is not None:
+            ps = self.pred_stats
+            rej = np.nonzero(~gate)[0]
+            ps["predicted_true"] += len(searched)
+            ps["predicted_true_hit"] += int(np.count_nonzero(ks[searched] > 0))
+            ps["searched_missed"] += int(np.count_nonzero(ks[searched] == 0))
+            ps["predicted_false"] += len(rej)
+            if len(rej) and hasattr(self.cache, "peek"):   # would-hit, without counting an access
+                ps["predicted_false_would_hit"] += int(np.count_nonzero(self.cache.peek(q[rej]) > 0))
+        for i in range(b):
+            k = int(ks[i])
             r.requests += 1
-            if gate is not None:
-                ps = self.pred_stats
-                if gate[i]:
-                    ps["predicted_true"] += 1
-                    ps["predicted_true_hit"] += int(k > 0)
-                    ps["searched_missed"] += int(k == 0)
-                else:                       # arrow 1: scratch without searching
-                    ps["predicted_false"] += 1
-                    ps["predicted_false_would_hit"] += int(k > 0)
-                    r.steps += self.lat.N
-                    r.latencies.append(self.lat.C)
-                    ks[i] = 0
-                    continue
             if k > 0:
                 r.hits_at[k] = r.hits_at.get(k, 0) + 1
             r.steps += self.lat.N - k
-            r.latencies.append(request_latency(k, self.lat))
+            # a predicted miss skips the search: scratch generation alone, latency C (arrow 1)
+            lt = request_latency(k, self.lat) if gate is None or gate[i] else self.lat.C
+            r.latencies.append(lt)
+            lat_step.append(lt)
         miss = np.nonzero(ks == 0)[0]
+        ev = dirty = np.zeros(0, np.uint64)
+        m = 0
         if len(miss):
-            self._admit(q[miss])
+            ev, dirty, m = self._admit(q[miss])
+        if self.keep_log:
+            self.log.append(dict(k=ks.copy(), latency=lat_step, evicted=np.asarray(ev, np.uint64),
+                                 dirty=np.asarray(dirty, np.uint64), admitted=m))
         return ids, ks
 
     def predictor_summary(self):
@@ -151,13 +170,18 @@ class ServingLoop:
         return ps
 
     def _admit(self, emb: np.ndarray):
+        """LCBFU admission of a batch's misses (reading R26): one eviction of the
+        shortfall (items, or |K| items per missing entry slot; never more than the live items)
+        before inserting; the misses that still do not fit are not admitted."""
         nk = len(self.k_values)
         need_e, need_i = len(emb), len(emb) * nk
         fe, fi = self.cache.free()
         short = max(0, need_i - fi)
         if fe < need_e:          # entries only come back when all of an entry's K are evicted
             short = max(short, (need_e - fe) * nk)
-        if short:
+        short = min(short, self.cache.capacity_items - fi)   # the live items
+        ev = dirty = np.zeros(0, np.uint64)
+        if short > 0:
             ev, dirty = self.cache.evict(short)
             self.report.evicted_items += len(ev)
             self.report.dirty_removed += len(dirty)
@@ -165,12 +189,13 @@ class ServingLoop:
             fe, fi = self.cache.free()
         m = min(len(emb), fe, fi // nk)
         if m <= 0:
-            return
+            return ev, dirty, 0
         lat = self.make_latents(self._admitted, m) if self.make_latents else None
         self.cache.admit(emb[:m], lat)
         self._admitted += m
         self._changed += m
         self.report.admitted_prompts += m
+        return ev, dirty, m
 
 
 class GpuCache:
@@ -180,6 +205,8 @@ class GpuCache:
         import torch
         self.c, self.torch, self.device, self.nu = cache, torch, device, nu
         self.capacity_entries = cache.cfg.entry_capacity
+        self.capacity_items = cache.cfg.latent_capacity
+        self.last_out = None   # the last lookup's device outputs (ids, scores, k, ...)
 
     def train_predictor(self):
         self.c.train_predictor(nu=self.nu)
@@ -190,7 +217,12 @@ class GpuCache:
 
     def lookup(self, q):
         out = self.c.query(self.torch.from_numpy(np.ascontiguousarray(q)).to(self.device), topk=1)
+        self.last_out = out
         return out["ids"][:, 0].cpu().numpy().view(np.uint64), out["k"].cpu().numpy()
+
+    def peek(self, q):
+        out = self.c.peek(self.torch.from_numpy(np.ascontiguousarray(q)).to(self.device), topk=1)
+        return out["k"].cpu().numpy()
 
     def admit(self, emb, latents):
         self.c.insert(self.torch.from_numpy(np.ascontiguousarray(emb)).to(self.device), latents)

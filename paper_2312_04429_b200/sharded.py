@@ -28,8 +28,27 @@ import torch
 from . import binding as B
 
 
+def _comm_errors(fn):
+    """A failed collective (NCCL error, or the process group's timeout / watchdog when a rank
+    died or stalled) surfaces as CacheError(E_NCCL), the status the C ABI reports when a
+    push-exchange wait times out (failure detection)."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrap(*a, **kw):
+        try:
+            return fn(*a, **kw)
+        except B.CacheError:
+            raise
+        except (RuntimeError, ValueError) as e:   # torch.distributed raises DistBackendError etc.
+            raise B.CacheError(B.E_NCCL, f"collective {fn.__name__} failed: {e}") from e
+    return wrap
+
+
 class TorchComm:
-    """Collectives of one process group (one rank per GPU)."""
+    """Collectives of one process group (one rank per GPU).  Create the group with a timeout
+    (init_process_group(timeout=...)) so that a dead rank fails the collectives instead of
+    hanging them; the failure is reported as CacheError(E_NCCL)."""
 
     def __init__(self, group=None, device: str = "cuda"):
         import torch.distributed as dist
@@ -37,20 +56,24 @@ class TorchComm:
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
 
+    @_comm_errors
     def all_gather(self, t: torch.Tensor) -> torch.Tensor:
         out = torch.empty((self.world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
         self.dist.all_gather_into_tensor(out.view(-1), t.contiguous().view(-1), group=self.group)
         return out
 
+    @_comm_errors
     def all_reduce_sum(self, t: torch.Tensor) -> torch.Tensor:
         self.dist.all_reduce(t, group=self.group)
         return t
 
+    @_comm_errors
     def all_reduce_min_int(self, v: int) -> int:
         t = torch.tensor([v], dtype=torch.int64, device=self.device)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
         return int(t.item())
 
+    @_comm_errors
     def all_gather_object(self, obj):
         out = [None] * self.world
         self.dist.all_gather_object(out, obj, group=self.group)
@@ -158,7 +181,16 @@ class ShardedCache:
             for k in ("ids", "scores", "k", "status"):
                 out_host[k].copy_(out_dev[k], non_blocking=True)
         s.synchronize()
+        if self.push:
+            self.cache.push_status(s)   # E_NCCL if a peer wait of this batch timed out
         return out_host
+
+    def status(self, stream=None):
+        """Synchronise; CacheError(E_NCCL) if this rank's push exchange saw a peer time out."""
+        if self.push:
+            self.cache.push_status(stream)
+        else:
+            torch.cuda.synchronize()
 
     def evict(self, n: int, lists: bool = True):
         """Collective: evict the n globally lowest-keyed items (entries in entry mode; every
@@ -181,9 +213,9 @@ class ShardedCache:
         if not lists:
             return res   # this rank's (evicted count, dirty count)
         ev, dirty = res
-        evs = self.comm.all_gather_object(ev.tolist())
+        evs = self.comm.all_gather_object(self.cache.last_evicted_keys().tolist())
         dts = self.comm.all_gather_object(dirty.tolist())
-        return _merge_evicted(evs), np.array(sorted(x for d in dts for x in d), dtype=np.uint64)
+        return _merge_evicted(evs, self.cache), np.array(sorted(x for d in dts for x in d), dtype=np.uint64)
 
 
 class VirtualShards:
@@ -246,7 +278,8 @@ class VirtualShards:
                 for c in self.caches:
                     c.push_evict_pick(p)
             res = [c.push_evict_apply(n) for c in self.caches]
-            return (_merge_evicted([r[0].tolist() for r in res]),
+            keys = [c.last_evicted_keys().tolist() for c in self.caches]
+            return (_merge_evicted(keys, self.caches[0]),
                     np.array(sorted(x for r in res for x in r[1].tolist()), dtype=np.uint64))
         sts = [torch.tensor([0, 0, n], dtype=torch.int64, device="cuda") for _ in self.caches]
         hists = [torch.zeros(256, dtype=torch.int32, device="cuda") for _ in self.caches]
@@ -258,7 +291,8 @@ class VirtualShards:
                 h.copy_(tot)
                 c.evict_pick(h, st, p)
         res = [c.evict_apply(st, n) for c, st in zip(self.caches, sts)]
-        return (_merge_evicted([r[0].tolist() for r in res]),
+        keys = [c.last_evicted_keys().tolist() for c in self.caches]
+        return (_merge_evicted(keys, self.caches[0]),
                 np.array(sorted(x for r in res for x in r[1].tolist()), dtype=np.uint64))
 
     def meta(self, id_: int):
@@ -277,11 +311,11 @@ class VirtualShards:
         return {k: sum(s[k] for s in ss) if k not in ("next_id",) else ss[0][k] for k in ss[0]}
 
 
-def _merge_evicted(lists):
-    """Per-rank eviction lists are each in key order; the global order is by key too, but the
-    key (f*K) is not recoverable from (id << 3 | j): the caller gets the union sorted by
-    (id, j) when more than one rank evicted."""
-    allv = [x for l in lists for x in l]
-    if sum(1 for l in lists if l) <= 1:
-        return np.array(allv, dtype=np.uint64)
-    return np.array(sorted(allv), dtype=np.uint64)
+def _merge_evicted(key_lists, cache):
+    """The global eviction order (the API's: ascending unit key, R11 / R24) from the ranks'
+    full 64-bit keys (cache_last_evicted_keys; keys are unique across ranks), mapped to what
+    cache_evict reports: id << 3 | j per item, or the entry id in entry mode."""
+    keys = np.sort(np.array([x for l in key_lists for x in l], dtype=np.uint64))
+    entry = getattr(cache, "granularity", B.EVICT_ITEM) == B.EVICT_ENTRY
+    mask = np.uint64(0xFFFFFFFF) if entry else np.uint64((1 << 35) - 1)
+    return keys & mask

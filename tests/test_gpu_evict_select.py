@@ -1,0 +1,119 @@
+"""The fused eviction (evict.cu: one cooperative launch selects the exact n smallest unit keys
+and applies them, readings R11-R13, R24) against the oracle, on every path the
+selection can take: compaction after the first linear level (the common case), late or no
+compaction (forced through the candidate-buffer cap), selection finished at level 0, n = 1,
+n = every live unit, heavy-hitter counters whose keys spread over many log bins; plus the
+sorts the eviction lists go through (one-CTA bitonic, LSD over a narrow key range)."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from tests.parity import check_batch, gpu_to_numpy
+
+pytestmark = pytest.mark.gpu
+L = 64
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 1000, 4097, 16384])
+def test_small_sort(n):
+    from paper_2312_04429_b200 import binding as B
+    rng = np.random.default_rng(n)
+    k = rng.integers(0, 2**63, n, dtype=np.int64).view(np.uint64) * np.uint64(2)
+    k[: n // 3] = k[0]   # duplicates
+    t = torch.from_numpy(k.view(np.int64).copy()).cuda()
+    B.debug_sort_u64_ex(t, small=True)
+    assert np.array_equal(t.cpu().numpy().view(np.uint64), np.sort(k))
+
+
+@pytest.mark.parametrize("n", [2, 20_000, 300_001])
+@pytest.mark.parametrize("bits", [1, 9, 23, 40])
+def test_range_sort(n, bits):
+    from paper_2312_04429_b200 import binding as B
+    rng = np.random.default_rng(bits)
+    base = np.uint64(123456789) << np.uint64(20)
+    k = base + (rng.integers(0, 2**bits, n, dtype=np.int64).astype(np.uint64))
+    t = torch.from_numpy(k.view(np.int64).copy()).cuda()
+    B.debug_sort_u64_ex(t, bits=bits, base=int(base))
+    assert np.array_equal(t.cpu().numpy().view(np.uint64), np.sort(k))
+
+
+def _pair(oracle_mod, n, policy, gran, seed, nq_batches=3, zipf_hot=False):
+    from paper_2312_04429_b200 import binding as B
+    emb, cl = synth.entries(n, seed=seed)
+    pres = synth.present_masks(n, seed=seed, hole_frac=0.2)
+    lat = synth.latents_np(np.arange(n), 5, L, seed=seed)
+    g = B.NirvanaCache(entry_capacity=n + 64, latent_capacity=5 * n + 64, dim=768, latent_bytes=L,
+                       evict_granularity=gran)
+    g.set_evict_policy(policy)
+    o = oracle_mod.OracleCache(dim=768, entry_capacity=n + 64, latent_capacity=5 * n + 64, latent_bytes=L)
+    g.insert(torch.from_numpy(emb).cuda(), torch.from_numpy(lat).cuda(), present=pres)
+    o.insert(emb, latents=lat, present=pres)
+    for r in range(nq_batches):
+        if zipf_hot:   # the same few prompts again and again: counters / clocks far apart
+            q = np.repeat(emb[(np.arange(64) * 7) % n], 4, axis=0)
+        else:
+            q, _, _ = synth.queries(emb, cl, 256, seed=seed * 100 + r)
+        _query_both(g, o, q)
+    return B, g, o
+
+
+def _query_both(g, o, q):
+    """One batch on both sides; the harness makes the oracle adopt the GPU's accepted
+    (entry, K) on near-ties so the counters / clocks stay equal."""
+    out = gpu_to_numpy(g.query(torch.from_numpy(np.ascontiguousarray(q, dtype=np.float32)).cuda(), topk=1))
+    check_batch(out, o, q, 1, expected_latent=None)
+
+
+def _evict_both(B, g, o, n, policy, gran):
+    if gran:
+        ev, dirty = g.evict(n)
+        rc, oev = o.evict_entries(n, policy=policy)
+        assert rc == 0
+        assert np.array_equal(ev, oev)
+        assert np.array_equal(np.sort(dirty), np.sort(oev))
+    else:
+        ev, dirty = g.evict(n)
+        rc, oev, od = o.evict(n, policy=policy)
+        assert rc == 0
+        assert np.array_equal(ev, oev)
+        assert np.array_equal(dirty, od)
+    return B.debug_evict_stats(g)
+
+
+@pytest.mark.parametrize("gran", [0, 1])
+@pytest.mark.parametrize("policy", [0, 1, 2, 3])
+@pytest.mark.parametrize("cap", [-1, 0, 1, 37, 5000])
+def test_fused_evict_paths(oracle_mod, policy, gran, cap):
+    """Rounds of query / evict with the candidate buffer capped: cap 0 never compacts (the
+    level sweeps and the apply run over the slot columns), small caps compact late."""
+    B, g, o = _pair(oracle_mod, 1500, policy, gran, seed=70 + policy, zipf_hot=(policy in (0, 2)))
+    B.debug_set_evict_cand_cap(g, cap)
+    rng = np.random.default_rng(policy * 10 + gran)
+    for rnd in range(4):
+        units = g.evict_units
+        n = int(rng.integers(1, max(2, units // 3)))
+        st = _evict_both(B, g, o, n, policy, gran)
+        if cap == 0:
+            assert st["compact_level"] == 0
+        _query_both(g, o, np.asarray(synth.entries(32, seed=500 + rnd)[0]))
+
+
+@pytest.mark.parametrize("gran", [0, 1])
+def test_fused_evict_extremes(oracle_mod, gran):
+    """n = 1, then nearly everything, then every remaining unit."""
+    B, g, o = _pair(oracle_mod, 800, 0, gran, seed=91, zipf_hot=True)
+    _evict_both(B, g, o, 1, 0, gran)
+    _evict_both(B, g, o, g.evict_units - 3, 0, gran)
+    _evict_both(B, g, o, g.evict_units, 0, gran)
+    assert g.evict_units == 0
+    assert g.stats()["live_entries"] == 0
+
+
+def test_fused_evict_hot_counters_spread(oracle_mod):
+    """LCBFU with heavy hitters: the keys of accessed items spread over many log bins, and the
+    cut falls among them when almost everything goes."""
+    B, g, o = _pair(oracle_mod, 2000, 0, 0, seed=93, nq_batches=6, zipf_hot=True)
+    units = g.evict_units
+    st = _evict_both(B, g, o, units - 40, 0, 0)
+    assert st["levels"] >= 1

@@ -51,12 +51,12 @@ def test_virtual_shards_equal_single_cache(mods, oracle_mod, world, topk):
         check_batch(s, o, q, topk, expected_latent=lambda e, k: lat[e, synth.K_VALUES.index(k)])
     for e in range(0, n, 7):
         assert np.array_equal(single.meta(e)[0], vs.meta(e)[0]) and single.meta(e)[1] == vs.meta(e)[1]
-    # distributed eviction == single-cache eviction == oracle (as sets; keys are unique)
+    # distributed eviction == single-cache eviction == oracle, in eviction order (keys are unique)
     for nev in (333, 1200):
         e1, d1 = single.evict(nev)
         e2, d2 = vs.evict(nev)
         rc, e3, d3 = o.evict(nev)
-        assert np.array_equal(np.sort(e1), e2) and np.array_equal(np.sort(e3), e2)
+        assert np.array_equal(e1, e2) and np.array_equal(e3, e2)   # same order (the API contract)
         assert np.array_equal(d1, d2) and np.array_equal(d3, d2)
     q, _, _ = synth.queries(emb, cl, b, seed=300)
     qt = torch.from_numpy(q).cuda()

@@ -14,6 +14,7 @@ class OracleAdapter:
     def __init__(self, oracle_mod, dim, entries, items, policy=0):
         self.o = oracle_mod.OracleCache(dim=dim, entry_capacity=entries, latent_capacity=items)
         self.cap_e, self.cap_i, self.policy = entries, items, policy
+        self.capacity_entries, self.capacity_items = entries, items
 
     def lookup(self, q):
         r = self.o.query(q, topk=1, want_latents=False, apply_counters=True)
