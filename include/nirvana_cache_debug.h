@@ -27,8 +27,9 @@ int64_t cache_debug_slot_of(cache_t *c, uint64_t id);
  * place (LSD radix, 8 x 8-bit stable passes).  Synchronises `stream`. */
 cache_status cache_debug_sort_u64(uint64_t *keys, int64_t n, void *stream);
 /* The same with the options the eviction uses: keys in [base, base + 2^bits) sorted by
- * ceil(bits/8) LSD passes over key - base, or (small != 0, n <= 16384) the one-CTA bitonic
- * sort in shared memory.  Synchronises `stream`. */
+ * ceil(bits/8) LSD passes over key - base (small = 0: 3 launches per pass; small = 2: the
+ * one-launch cooperative version), or (small = 1, n <= 16384) the one-CTA bitonic sort in
+ * shared memory.  Synchronises `stream`. */
 cache_status cache_debug_sort_u64_ex(uint64_t *keys, int64_t n, int32_t bits, uint64_t base, int32_t small,
                                      void *stream);
 /* Statistics of the last cache_evict (fused select + apply): out4 = {levels, full sweeps of
@@ -37,6 +38,9 @@ cache_status cache_debug_evict_stats(cache_t *c, int64_t *out4);
 /* Cap the fused eviction's candidate buffer (cap < 0: automatic), so the tests can force the
  * paths that compact late or never. */
 cache_status cache_debug_set_evict_cand_cap(cache_t *c, int64_t cap);
+/* Set the LCBFU access count f of item (id, K_j) (host-synchronous): the tests reach counts no
+ * query stream could (the key saturation of reading R11). */
+cache_status cache_debug_set_count(cache_t *c, uint64_t id, int32_t j, uint32_t f);
 
 #ifdef __cplusplus
 }

@@ -52,6 +52,7 @@ def lib():
         L.oracle_insert.argtypes = [P, I64, P, I32, P, P, P, P]
         L.oracle_query.argtypes = [P, I64, P, I32, I32, P, P, P, P, P, P, P, I32]
         L.oracle_record_access.argtypes = [P, I64, P, P]
+        L.oracle_set_count.argtypes = [P, U64, ctypes.c_int32, U64]
         L.oracle_score_id.argtypes = [P, P, I32, U64]
         L.oracle_score_id.restype = D
         L.oracle_evict.argtypes = [P, I64, P, P, P]
@@ -166,6 +167,10 @@ class OracleCache:
         ids = np.empty(max(n, 1), dtype=np.uint64)
         rc = lib().oracle_evict_entries(self._h, n, policy, _p(ids))
         return rc, ids[:n].copy()
+
+    def set_count(self, id_, j, f):
+        """Test hook: access count f of item (id, K_j)."""
+        return lib().oracle_set_count(self._h, int(id_), int(j), int(f))
 
     def tick(self):
         lib().oracle_tick(self._h)

@@ -460,6 +460,16 @@ int oracle_record_access(oracle_cache *c, int64_t n, const uint64_t *ids, const 
     return ORC_OK;
 }
 
+/* Test hook: set the access count f of item (id, K_j) (e.g. past the GPU key's saturation
+ * point, reading R11, which no test could reach through queries). */
+int oracle_set_count(oracle_cache *c, uint64_t id, int32_t j, uint64_t f)
+{
+    oentry *e = find_id(c, id);
+    if (!e || j < 0 || j >= c->num_k || !e->present[j]) return ORC_E_INVALID_ARG;
+    e->f[j] = f;
+    return ORC_OK;
+}
+
 /* Advance the LRU clock by one batch without accesses (a query batch with no hits). */
 void oracle_tick(oracle_cache *c) { c->clock++; }
 

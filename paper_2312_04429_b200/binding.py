@@ -83,7 +83,8 @@ EXPORTS = ("cache_default_config", "cache_create", "cache_destroy", "cache_inser
            "cache_set_evict_granularity", "cache_live_entries", "cache_push_reserve", "cache_push_queries",
            "cache_push_scan", "cache_push_merge", "cache_push_evict_hist", "cache_push_evict_pick",
            "cache_push_evict_apply", "cache_profile_thresholds", "cache_set_thresholds", "cache_query_peek",
-           "cache_push_status", "cache_set_peer_timeout", "cache_last_evicted_keys")
+           "cache_push_status", "cache_set_peer_timeout", "cache_last_evicted_keys",
+           "cache_evict_view")
 
 
 def load_library(path: str = LIB_PATH):
@@ -100,6 +101,8 @@ def load_library(path: str = LIB_PATH):
     L.cache_query_batch_host.argtypes = [P, I64, P, I32, I32, P, P, P, P, P, P]
     L.cache_query_peek.argtypes = [P, I64, P, I32, I32, P, P, P, P, P]
     L.cache_query_peek.restype = ctypes.c_int
+    L.cache_evict_view.argtypes = [P, I64, P, P, P, P]
+    L.cache_evict_view.restype = ctypes.c_int
     L.cache_last_evicted_keys.argtypes = [P, P, I64, P]
     L.cache_last_evicted_keys.restype = ctypes.c_int
     L.cache_push_status.argtypes = [P, P]
@@ -306,12 +309,30 @@ class NirvanaCache:
         _check(rc)
         return out
 
-    def evict(self, n: int, stream=None):
-        ev = np.empty(max(n, 1), dtype=np.uint64)
-        dirty = np.empty(max(n, 1), dtype=np.uint64)
+    def evict(self, n: int, stream=None, out=None, view: bool = False):
+        """Returns (evicted, dirty ids).  out: optional (evicted, dirty) uint64 arrays of capacity
+        >= n, reused across calls.  view=True: read-only numpy views of the library's pinned lists
+        (cache_evict_view; no copy), valid until this cache's next eviction."""
+        if view:
+            pe, pd = ctypes.c_void_p(), ctypes.c_void_p()
+            nd = ctypes.c_int64()
+            _check(_lib.cache_evict_view(self._h, n, ctypes.byref(pe), ctypes.byref(pd), ctypes.byref(nd),
+                                         _stream(stream)))
+            def arr(p, k):
+                if k == 0 or not p.value:
+                    return np.zeros(0, np.uint64)
+                a = np.ctypeslib.as_array(ctypes.cast(p, ctypes.POINTER(ctypes.c_uint64)), shape=(k,))
+                a.flags.writeable = False
+                return a
+            return arr(pe, n), arr(pd, nd.value)
+        if out is not None and len(out[0]) >= max(n, 1) and len(out[1]) >= max(n, 1):
+            ev, dirty = out
+        else:
+            ev = np.empty(max(n, 1), dtype=np.uint64)
+            dirty = np.empty(max(n, 1), dtype=np.uint64)
         nd = np.zeros(1, dtype=np.int64)
         _check(_lib.cache_evict(self._h, n, _ptr(ev), _ptr(dirty), _ptr(nd), _stream(stream)))
-        return ev[:n].copy(), dirty[: int(nd[0])].copy()
+        return ev[:n], dirty[: int(nd[0])]   # views (no copy of the lists)
 
     def meta(self, id_: int):
         f = np.empty(self.num_k, dtype=np.uint64)
@@ -553,8 +574,9 @@ _lib.cache_debug_set_evict_cand_cap.argtypes = [ctypes.c_void_p, ctypes.c_int64]
 _lib.cache_debug_set_evict_cand_cap.restype = ctypes.c_int
 
 
-def debug_sort_u64_ex(keys: torch.Tensor, bits: int = 64, base: int = 0, small: bool = False, stream=None):
-    """The eviction sorts with their options: keys in [base, base + 2^bits), or the one-CTA sort."""
+def debug_sort_u64_ex(keys: torch.Tensor, bits: int = 64, base: int = 0, small=False, stream=None):
+    """The eviction sorts with their options: keys in [base, base + 2^bits); small = 1 / True:
+    the one-CTA sort, 2: the cooperative one-launch LSD sort."""
     _check(_lib.cache_debug_sort_u64_ex(_ptr(keys), keys.numel(), bits, base, int(small), _stream(stream)))
     return keys
 
@@ -568,3 +590,11 @@ def debug_evict_stats(cache: NirvanaCache) -> dict:
 
 def debug_set_evict_cand_cap(cache: NirvanaCache, cap: int):
     _check(_lib.cache_debug_set_evict_cand_cap(cache._h, int(cap)))
+
+
+_lib.cache_debug_set_count.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int32, ctypes.c_uint32]
+_lib.cache_debug_set_count.restype = ctypes.c_int
+
+
+def debug_set_count(cache: NirvanaCache, id_: int, j: int, f: int):
+    _check(_lib.cache_debug_set_count(cache._h, int(id_), int(j), int(f)))

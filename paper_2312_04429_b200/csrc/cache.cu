@@ -60,6 +60,7 @@ constexpr int64_t kHostSplitMin = 2048;
 // whose gather is large relative to the scan (bigger latents, smaller caches).
 constexpr int kDevSplitMax = 8;
 constexpr int kDevSplitAuto = 1;
+constexpr int64_t kEvBitsWords = 1 << 18;   // 1 MB: evicted keys spanning < 2^23 values are sorted in-kernel
 constexpr int64_t kDevSplitMin = 2048;
 
 cache_status fail(cache_status st, const std::string& msg) {
@@ -220,10 +221,14 @@ struct cache_t {
     DevBuf<unsigned long long> edirty, edid;   // dirty entries: slots, ids (each sorted on the GPU)
     DevBuf<unsigned long long> ckey;     // fused eviction (evict.cu): candidate keys / slots
     DevBuf<uint32_t> cslot;
-    DevBuf<uint8_t> selws;               // per-level histograms + SelOut
+    DevBuf<uint8_t> selws;               // per-level histograms + SelOut + compaction totals
+    DevBuf<uint32_t> ebits;              // dirty-slot / dirty-id / freed-pool-slot / evicted-key bitmaps
+    DevBuf<unsigned long long> eout;     // kernel-sorted evicted keys: full | masked
     int64_t last_sel[4] = {0, 0, 0, 0};  // levels, full sweeps, compaction level, candidates
     int64_t cand_cap_override = -1;      // test hook (cache_debug_set_evict_cand_cap); -1 = auto
-    int64_t last_ev_n = 0;               // unit keys of the last eviction (in hev_sorted), in order
+    int64_t last_ev_n = 0;               // unit keys of the last eviction (sorted, in ekey), in order
+    int64_t last_nd = 0;
+    unsigned long long* ev_full = nullptr;   // device: the sorted full keys of the last eviction
     // match predictor (NEXT-3)
     DevBuf<float> pw, prho, pgpart;
     DevBuf<uint32_t> pkeys;
@@ -304,7 +309,12 @@ static cudaError_t reserve_evict(cache_t* c, int64_t items, int64_t entries) {
     const int64_t ccap = std::max<int64_t>(65536, c->cap * c->num_k / 16);
     if ((e = c->ckey.ensure_grow(ccap)) != cudaSuccess) return e;
     if ((e = c->cslot.ensure_grow(ccap)) != cudaSuccess) return e;
-    if ((e = c->selws.ensure((size_t)kSelMaxLevels * kSelBins * 4 + sizeof(SelOut))) != cudaSuccess) return e;
+    if ((e = c->selws.ensure((size_t)kSelMaxLevels * kSelBins * 4 + sizeof(SelOut) + 4 * 4096 * 4)) != cudaSuccess)
+        return e;
+    if ((e = c->ebits.ensure_grow(2 * (c->cap_pad / 32) + (c->alias ? 0 : (c->lcap + 31) / 32) + kEvBitsWords + 1024)) !=
+        cudaSuccess)
+        return e;
+    if ((e = c->eout.ensure_grow(2 * items)) != cudaSuccess) return e;
     return c->hev_did.ensure(entries * 8);
 }
 
@@ -430,7 +440,7 @@ cache_status cache_destroy(cache_t* c) {
     c->hev_sorted.release(); c->hev_pool.release(); c->hev_ds.release();
     c->hev_did.release();
     c->epool.release(); c->edirty.release(); c->edid.release();
-    c->ckey.release(); c->cslot.release(); c->selws.release();
+    c->ckey.release(); c->cslot.release(); c->selws.release(); c->ebits.release(); c->eout.release();
     c->abortw.release();
     if (c->errw_h) cudaFreeHost(c->errw_h);
     delete c;
@@ -1041,7 +1051,10 @@ cache_status cache_attach_peers(cache_t* c, int32_t world, const cache_peer_desc
 cache_status cache_last_evicted_keys(cache_t* c, uint64_t* out, int64_t cap, int64_t* out_n) {
     if (!c || cap < 0 || (cap > 0 && !out)) return fail(CACHE_E_INVALID_ARG, "cache_last_evicted_keys: bad argument");
     const int64_t n = std::min<int64_t>(cap, c->last_ev_n);
-    if (n > 0) std::memcpy(out, c->hev_sorted.p, (size_t)n * 8);
+    if (n > 0) {   // the sorted full keys stay on the device until the next eviction
+        DeviceGuard g(c->device);
+        CK(cudaMemcpy(out, c->ev_full ? c->ev_full : c->ekey.p, (size_t)n * 8, cudaMemcpyDeviceToHost));
+    }
     if (out_n) *out_n = c->last_ev_n;
     return CACHE_OK;
 }
@@ -1368,15 +1381,31 @@ static void merge_free(std::vector<int64_t>& fl, const unsigned long long* asc, 
 // a single launch, longer ones by LSD radix over only the bits their range spans (evicted keys:
 // [kbase, kbase + 2^kbits)) -- copied to pinned host memory, and the host's entry mirror and
 // free lists are updated.  n / nd / nfreed: evicted units, dirty entries, freed pool slots.
+// NIRVANA_EVICT_TRACE=1: one line per cache_evict on stderr with the host-side phase times
+static bool evict_trace() {
+    static const bool on = std::getenv("NIRVANA_EVICT_TRACE") != nullptr;
+    return on;
+}
+static double now_us() {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// want_ev / want_did: produce the evicted list / the dirty-id list in the library's pinned
+// staging (hev_sorted: the reported values id << 3 | j or entry ids, masked on the GPU;
+// hev_did); out_evicted / out_dirty_ids (may be null) receive a copy of them.  The full 64-bit
+// keys stay on the device (c->ekey) for cache_last_evicted_keys.
+// ev_ready: the kernel already emitted the evicted list sorted -- full keys in ev_full, the
+// reported values in ev_ready (device) -- so no sort and no mask launch.
 static cache_status evict_finish(cache_t* c, int64_t n, int64_t nd, int64_t nfreed, unsigned long long kbase, int kbits,
-                                 uint64_t* out_evicted, uint64_t* out_dirty_ids, int64_t* out_n_dirty,
-                                 cudaStream_t s) {
+                                 bool want_ev, bool want_did, uint64_t* out_evicted, uint64_t* out_dirty_ids,
+                                 int64_t* out_n_dirty, cudaStream_t s, double* tr = nullptr, bool presorted = false,
+                                 const unsigned long long* ev_ready = nullptr, unsigned long long* ev_full = nullptr) {
     const bool entry_mode = c->km.gran == CACHE_EVICT_ENTRY;
     const bool pool_freed = !c->alias && nfreed > 0;
     CK(c->hev_pool.ensure((pool_freed ? nfreed : 0) * 8));
     CK(c->hev_ds.ensure(nd * 8));
-    if (out_dirty_ids) CK(c->hev_did.ensure(nd * 8));
-    if (out_evicted) CK(c->hev_sorted.ensure(n * 8));
+    if (want_did) CK(c->hev_did.ensure(nd * 8));
+    if (want_ev) CK(c->hev_sorted.ensure(n * 8));
     struct Job {
         unsigned long long* keys;
         int64_t n;
@@ -1387,52 +1416,68 @@ static cache_status evict_finish(cache_t* c, int64_t n, int64_t nd, int64_t nfre
     };
     Job jobs[4];
     int nj = 0;
+    // presorted (fused path): the pool / dirty lists come out of the kernel's ordered bitmap
+    // compaction already ascending; only the evicted keys need a sort
     if (pool_freed) jobs[nj++] = Job{c->epool.p, nfreed, std::max(1, bitlen((unsigned long long)std::max<int64_t>(1, c->lcap) - 1)), 0ull, c->hev_pool.p, nullptr};
     if (nd) {
         jobs[nj++] = Job{c->edirty.p, nd, std::max(1, bitlen((unsigned long long)std::max<int64_t>(1, c->hwm) - 1)), 0ull, c->hev_ds.p, nullptr};
-        if (out_dirty_ids)
+        if (want_did)
             jobs[nj++] = Job{c->edid.p, nd, std::max(1, bitlen(c->next_id ? c->next_id - 1 : 0)), 0ull, c->hev_did.p, nullptr};
     }
-    if (out_evicted && n) jobs[nj++] = Job{c->ekey.p, n, std::max(1, kbits), kbase, c->hev_sorted.p, nullptr};
+    if (want_ev && n && !ev_ready) jobs[nj++] = Job{c->ekey.p, n, std::max(1, kbits), kbase, c->hev_sorted.p, nullptr};
     SortSegs small{};
+    SortJobs big{};
+    int64_t big_n = 0;
     for (int i = 0; i < nj; ++i) {
         Job& jb = jobs[i];
+        jb.res = jb.keys;   // every sort lands in the list's own buffer
+        if (jb.n <= 1 || (presorted && jb.keys != c->ekey.p)) continue;
         if (jb.n <= kSmallSort) {
             small.s[small.k++] = SortSeg{jb.keys, jb.n};
-            jb.res = jb.keys;
         } else {
-            jb.res = launch_sort_u64(jb.keys, c->ekey2.p, jb.n, c->escr.p, s, jb.bits, jb.base);
-            c->launches += sort_launches(jb.n, jb.bits);
-            if (jb.res == c->ekey2.p) {   // tmp is shared by the lists: land this one in its own buffer
-                CK(cudaMemcpyAsync(jb.keys, jb.res, jb.n * 8, cudaMemcpyDeviceToDevice, s));
-                jb.res = jb.keys;
-            }
+            big.j[big.k++] = SortJob{jb.keys, c->ekey2.p, jb.n, (std::min(64, std::max(1, jb.bits)) + 7) / 8, jb.base};
+            big_n = std::max(big_n, jb.n);
         }
+    }
+    if (big.k) {
+        CK(c->ekey2.ensure_grow(big_n));
+        for (int i = 0; i < big.k; ++i) big.j[i].tmp = c->ekey2.p;
+        CK(c->escr.ensure_grow(sort_coop_scratch_words(big_n)));
+        CK(launch_sort_coop(big, c->escr.p, s));
+        c->launches++;
     }
     if (small.k) {
         launch_sort_small(small, s);
         c->launches++;
     }
+    c->ev_full = ev_ready ? ev_full : c->ekey.p;
+    if (want_ev && n && ev_ready) {
+        CK(cudaMemcpyAsync(c->hev_sorted.p, ev_ready, n * 8, cudaMemcpyDeviceToHost, s));
+    } else if (want_ev && n) {   // the reported values, masked on the GPU: item key -> id << 3 | j, entry key -> id
+        CK(c->ekey2.ensure_grow(n));
+        launch_mask_u64(c->ekey.p, c->ekey2.p, n, entry_mode ? 0xFFFFFFFFull : ((1ull << 35) - 1), s);
+        c->launches++;
+        jobs[nj - 1].res = c->ekey2.p;
+    }
     CK(cudaGetLastError());
     for (int i = 0; i < nj; ++i) CK(cudaMemcpyAsync(jobs[i].host, jobs[i].res, jobs[i].n * 8, cudaMemcpyDeviceToHost, s));
     c->live_items -= nfreed;
+    if (tr) tr[0] = now_us();
     CK(cudaStreamSynchronize(s));   // sorted lists landed
+    if (tr) tr[1] = now_us();
     const unsigned long long* ds = static_cast<const unsigned long long*>(c->hev_ds.p);
     if (pool_freed) merge_free(c->free_l, static_cast<const unsigned long long*>(c->hev_pool.p), nfreed, c->free_tmp);
     for (int64_t i = 0; i < nd; ++i) c->h_live[(int64_t)ds[i]] = 0;
     c->live_entries -= nd;
     merge_free(c->free_e, ds, nd, c->free_tmp);
-    if (out_dirty_ids) std::memcpy(out_dirty_ids, c->hev_did.p, nd * 8);
+    if (out_dirty_ids && nd) std::memcpy(out_dirty_ids, c->hev_did.p, nd * 8);
     if (out_n_dirty) *out_n_dirty = nd;
+    c->last_nd = want_did ? nd : 0;
     // shrink the scan high-water mark past trailing empty slots
     while (c->hwm > 0 && c->h_live[c->hwm - 1] == 0) c->hwm--;
-    c->last_ev_n = out_evicted ? n : 0;
-    if (out_evicted && n) {
-        const unsigned long long* sorted = static_cast<const unsigned long long*>(c->hev_sorted.p);
-        // item key = score << 35 | id << 3 | j -> (id << 3 | j); entry key = score << 32 | id -> id
-        const unsigned long long m = entry_mode ? 0xFFFFFFFFull : ((1ull << 35) - 1);
-        for (int64_t i = 0; i < n; ++i) out_evicted[i] = sorted[i] & m;
-    }
+    c->last_ev_n = want_ev ? n : 0;
+    if (out_evicted && n) std::memcpy(out_evicted, c->hev_sorted.p, n * 8);
+    if (tr) tr[2] = now_us();
     return CACHE_OK;
 }
 
@@ -1450,8 +1495,30 @@ static cudaError_t evict_lists(cache_t* c, int64_t bound, int64_t dbound, int64_
 // cache_evict: the fused select + apply of evict.cu (one cooperative launch), then
 // evict_finish.  The protocol's building blocks (cache_evict_hist / _pick / _apply) remain for
 // the distributed eviction, whose histograms are summed over ranks between passes.
+static cache_status evict_impl(cache_t* c, int64_t n, bool want_ev, bool want_did, uint64_t* out_evicted,
+                               uint64_t* out_dirty_ids, int64_t* out_n_dirty, void* stream);
+
 cache_status cache_evict(cache_t* c, int64_t n, uint64_t* out_evicted, uint64_t* out_dirty_ids,
                          int64_t* out_n_dirty, void* stream) {
+    return evict_impl(c, n, out_evicted != nullptr, out_dirty_ids != nullptr, out_evicted, out_dirty_ids, out_n_dirty,
+                      stream);
+}
+
+cache_status cache_evict_view(cache_t* c, int64_t n, const uint64_t** out_evicted, const uint64_t** out_dirty_ids,
+                              int64_t* out_n_dirty, void* stream) {
+    if (!c || !out_evicted || !out_dirty_ids || !out_n_dirty)
+        return fail(CACHE_E_INVALID_ARG, "cache_evict_view: null argument");
+    *out_evicted = *out_dirty_ids = nullptr;
+    *out_n_dirty = 0;
+    cache_status r = evict_impl(c, n, true, true, nullptr, nullptr, out_n_dirty, stream);
+    if (r != CACHE_OK) return r;
+    *out_evicted = static_cast<const uint64_t*>(c->hev_sorted.p);
+    *out_dirty_ids = static_cast<const uint64_t*>(c->hev_did.p);
+    return CACHE_OK;
+}
+
+static cache_status evict_impl(cache_t* c, int64_t n, bool want_ev, bool want_did, uint64_t* out_evicted,
+                               uint64_t* out_dirty_ids, int64_t* out_n_dirty, void* stream) {
     if (!c) return fail(CACHE_E_INVALID_ARG, "cache_evict: null cache");
     if (n < 0) return fail(CACHE_E_INVALID_ARG, "cache_evict: n < 0");
     const bool entry_mode = c->km.gran == CACHE_EVICT_ENTRY;
@@ -1470,9 +1537,18 @@ cache_status cache_evict(cache_t* c, int64_t n, uint64_t* out_evicted, uint64_t*
     CK(c->ckey.ensure_grow(ccap));
     CK(c->cslot.ensure_grow(ccap));
     const size_t ws = (size_t)kSelMaxLevels * kSelBins * 4 + sizeof(SelOut);
-    CK(c->selws.ensure(ws));
+    CK(c->selws.ensure(ws + 4 * 4096 * 4));
     CK(cudaMemsetAsync(c->selws.p, 0, ws, s));
     SelOut* so = reinterpret_cast<SelOut*>(c->selws.p + (size_t)kSelMaxLevels * kSelBins * 4);
+    // bitmaps of the ordered outputs: dirty slots (< hwm), dirty ids / world (< next_id), freed
+    // pool slots (< latent capacity; not tracked under aliasing)
+    const int64_t w_slot = (c->hwm + 31) / 32;
+    const int64_t w_id = ((int64_t)(c->next_id / (uint64_t)c->world) + 1 + 31) / 32;
+    const int64_t w_pool = c->alias ? 0 : (c->lcap + 31) / 32;
+    const int64_t w_ev = want_ev ? kEvBitsWords : 0;   // evicted keys spanning < 2^23 values: bitmap-sorted
+    CK(c->ebits.ensure_grow(w_slot + w_id + w_pool + w_ev));
+    CK(cudaMemsetAsync(c->ebits.p, 0, (size_t)(w_slot + w_id + w_pool + w_ev) * 4, s));
+    CK(c->eout.ensure_grow(2 * std::max<int64_t>(n, 1)));
     SelArgs a{};
     a.present = c->present;
     a.fcnt = c->fcnt;
@@ -1492,14 +1568,37 @@ cache_status cache_evict(cache_t* c, int64_t n, uint64_t* out_evicted, uint64_t*
     a.dirty_slot = c->edirty.p;
     a.dirty_id = c->edid.p;
     a.ev_cap = (unsigned long long)n;
-    a.pool_cap = (unsigned long long)pbound;
-    a.dirty_cap = (unsigned long long)dbound;
+    a.dslot_bits = c->ebits.p;
+    a.did_bits = c->ebits.p + w_slot;
+    a.pool_bits = w_pool ? c->ebits.p + w_slot + w_id : nullptr;
+    a.dslot_words = w_slot;
+    a.did_words = w_id;
+    a.pool_words = w_pool;
+    a.world = c->world;
+    a.rank = c->rank;
+    a.part = reinterpret_cast<uint32_t*>(c->selws.p + ws);
+    a.ev_bits = w_ev ? c->ebits.p + w_slot + w_id + w_pool : nullptr;
+    a.ev_bits_words = w_ev;
+    a.ev_sorted = c->eout.p;
+    a.ev_masked = c->eout.p + std::max<int64_t>(n, 1);
+    a.ev_mask = entry_mode ? 0xFFFFFFFFull : ((1ull << 35) - 1);
     a.out = so;
+    const bool trace = evict_trace();
+    double t0 = trace ? now_us() : 0.0, t1 = 0.0, t2 = 0.0, tf[3] = {0, 0, 0};
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    if (trace) {
+        cudaEventCreate(&ev0);
+        cudaEventCreate(&ev1);
+        cudaEventRecord(ev0, s);
+    }
     CK(launch_evict_select(a, c->km, s));
     c->launches++;
+    if (trace) cudaEventRecord(ev1, s);
     SelOut h{};
     CK(cudaMemcpyAsync(&h, so, sizeof(h), cudaMemcpyDeviceToHost, s));
+    if (trace) t1 = now_us();
     CK(cudaStreamSynchronize(s));
+    if (trace) t2 = now_us();
     c->last_sel[0] = h.levels;
     c->last_sel[1] = h.full_sweeps;
     c->last_sel[2] = h.compact_level;
@@ -1509,7 +1608,24 @@ cache_status cache_evict(cache_t* c, int64_t n, uint64_t* out_evicted, uint64_t*
     if (h.err || got != n || nd > dbound || nfreed > pbound)
         return fail(CACHE_E_STATE, "cache_evict: selection count mismatch (internal error); handle state undefined");
     const unsigned long long kmin = ~h.kmin_inv;
-    return evict_finish(c, n, nd, nfreed, kmin, bitlen(h.T - kmin), out_evicted, out_dirty_ids, out_n_dirty, s);
+    cache_status r = evict_finish(c, n, nd, nfreed, kmin, bitlen(h.T - kmin), want_ev || out_evicted,
+                                  want_did || out_dirty_ids, out_evicted, out_dirty_ids, out_n_dirty, s,
+                                  trace ? tf : nullptr, /*presorted=*/true, h.ev_sorted ? a.ev_masked : nullptr,
+                                  h.ev_sorted ? a.ev_sorted : nullptr);
+    if (trace) {
+        float kms = 0.f;
+        cudaEventElapsedTime(&kms, ev0, ev1);
+        cudaEventDestroy(ev0);
+        cudaEventDestroy(ev1);
+        std::fprintf(stderr,
+                     "{\"evict_trace\": {\"n\": %lld, \"slots\": %lld, \"select_kernel_us\": %.1f, \"launch_us\": %.1f, "
+                     "\"select_wait_us\": %.1f, \"sort_enqueue_us\": %.1f, \"sort_wait_us\": %.1f, \"host_us\": %.1f, "
+                     "\"total_us\": %.1f, \"levels\": %u, \"full_sweeps\": %u, \"compact_level\": %u, "
+                     "\"candidates\": %llu, \"key_bits\": %d, \"dirty\": %lld}}\n",
+                     (long long)n, (long long)c->hwm, kms * 1e3, t1 - t0, t2 - t1, tf[0] - t2, tf[1] - tf[0], tf[2] - tf[1],
+                     tf[2] - t0, h.levels, h.full_sweeps, h.compact_level, h.cnt[3], bitlen(h.T - kmin), (long long)nd);
+    }
+    return r;
 }
 
 cache_status cache_evict_apply(cache_t* c, const cache_evict_state* st, int64_t cap, uint64_t* out_evicted,
@@ -1544,7 +1660,8 @@ cache_status cache_evict_apply(cache_t* c, const cache_evict_state* st, int64_t 
         return fail(CACHE_E_STATE, "cache_evict_apply: more evictions than the output capacity (n differs "
                                    "between the selection and the apply?); handle state undefined");
     // evicted keys are <= the selected key (st->prefix)
-    return evict_finish(c, n, nd, nfreed, 0ull, bitlen(hst.prefix), out_evicted, out_dirty_ids, out_n_dirty, s);
+    return evict_finish(c, n, nd, nfreed, 0ull, bitlen(hst.prefix), out_evicted != nullptr, out_dirty_ids != nullptr,
+                        out_evicted, out_dirty_ids, out_n_dirty, s);
 }
 
 // Entry slot of id, or -1 (a scan of the host mirrors: only the inspection calls need it).
@@ -1679,12 +1796,12 @@ extern "C" cache_status cache_debug_sort_u64(uint64_t* keys, int64_t n, void* st
 
 extern "C" cache_status cache_debug_sort_u64_ex(uint64_t* keys, int64_t n, int32_t bits, uint64_t base, int32_t small,
                                                 void* stream) {
-    if (n < 0 || (n > 0 && !keys) || bits < 1 || bits > 64 || (small && n > kSmallSort))
+    if (n < 0 || (n > 0 && !keys) || bits < 1 || bits > 64 || (small == 1 && n > kSmallSort))
         return fail(CACHE_E_INVALID_ARG, "cache_debug_sort_u64_ex: bad argument");
     if (n <= 1) return CACHE_OK;
     cudaStream_t s = (cudaStream_t)stream;
     auto* k = reinterpret_cast<unsigned long long*>(keys);
-    if (small) {
+    if (small == 1) {
         SortSegs sg{};
         sg.s[0] = SortSeg{k, n};
         sg.k = 1;
@@ -1696,6 +1813,18 @@ extern "C" cache_status cache_debug_sort_u64_ex(uint64_t* keys, int64_t n, int32
     DevBuf<unsigned long long> tmp;
     DevBuf<uint32_t> scr;
     CK(tmp.ensure(n));
+    if (small == 2) {   // the eviction's cooperative one-launch sort
+        CK(scr.ensure(sort_coop_scratch_words(n)));
+        SortJobs jb{};
+        jb.j[0] = SortJob{k, tmp.p, n, (bits + 7) / 8, (unsigned long long)base};
+        jb.k = 1;
+        cudaError_t e = launch_sort_coop(jb, scr.p, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        tmp.release();
+        scr.release();
+        CK(e);
+        return CACHE_OK;
+    }
     CK(scr.ensure(sort_scratch_words(n)));
     unsigned long long* r = launch_sort_u64(k, tmp.p, n, scr.p, s, bits, base);
     if (r != k) cudaMemcpyAsync(k, r, n * 8, cudaMemcpyDeviceToDevice, s);
@@ -1710,6 +1839,15 @@ extern "C" cache_status cache_debug_sort_u64_ex(uint64_t* keys, int64_t n, int32
 extern "C" cache_status cache_debug_evict_stats(cache_t* c, int64_t* out4) {
     if (!c || !out4) return fail(CACHE_E_INVALID_ARG, "cache_debug_evict_stats: bad argument");
     for (int i = 0; i < 4; ++i) out4[i] = c->last_sel[i];
+    return CACHE_OK;
+}
+
+extern "C" cache_status cache_debug_set_count(cache_t* c, uint64_t id, int32_t j, uint32_t f) {
+    if (!c || j < 0 || j >= c->num_k) return fail(CACHE_E_INVALID_ARG, "cache_debug_set_count: bad argument");
+    const int64_t e = find_slot(c, id);
+    if (e < 0) return fail(CACHE_E_INVALID_ARG, "cache_debug_set_count: id not live");
+    DeviceGuard g(c->device);
+    CK(cudaMemcpy(c->fcnt + e * c->num_k + j, &f, 4, cudaMemcpyHostToDevice));
     return CACHE_OK;
 }
 

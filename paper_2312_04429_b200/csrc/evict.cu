@@ -100,7 +100,33 @@ struct SelLevel {
     unsigned long long lo, T;
     int w, shift;          // range [lo, lo + 2^w); digit = (key - lo) >> shift
     bool compact;
+    unsigned long long kb, ev_lim;   // evicted-key bitmap over [kb, kb + ev_lim) (ev_lim 0: off)
 };
+
+// Evicted keys are also marked, as they are evicted, in a bitmap over [min key, min key +
+// 32 x words): when none falls beyond it the kernel emits the list sorted by an ordered
+// compaction (keys are unique).  One atomic per (lane, word) run.
+struct BitRun {
+    long long w = -1;
+    uint32_t m = 0u;
+    __device__ __forceinline__ void add(const SelArgs& a, const SelLevel& L, unsigned long long key) {
+        if (!L.ev_lim) return;
+        const unsigned long long d = key - L.kb;
+        if (d >= L.ev_lim) { atomicExch(&a.out->ev_over, 1u); return; }   // overflow: sort on the host side
+        const long long ww = (long long)(d >> 5);
+        if (ww != w) { flush(a); w = ww; }
+        m |= 1u << (d & 31);
+    }
+    __device__ __forceinline__ void flush(const SelArgs& a) {
+        if (m) atomicOr(a.ev_bits + w, m);
+        m = 0u;
+    }
+};
+__device__ __forceinline__ void ev_mark(const SelArgs& a, const SelLevel& L, unsigned long long key) {
+    BitRun r;
+    r.add(a, L, key);
+    r.flush(a);
+}
 
 template <int POLICY, int GRAN>
 __device__ __forceinline__ void sel_unit_common(const SelArgs& a, int mode, const SelLevel& L,
@@ -124,37 +150,61 @@ __device__ __forceinline__ void sel_unit_common(const SelArgs& a, int mode, cons
     }
 }
 
-// One warp-aligned group of 32 entry slots (lane = one slot), every mode of a full sweep.
+// Policy score of an item from its preloaded column value (fcnt for LCBFU / LFU, lastacc for
+// LRU, nothing for FIFO) -- the same scores as evict.cuh's item_score / entry_key.
+template <int POLICY>
+__device__ __forceinline__ unsigned long long score_v(uint32_t col, int kvj) {
+    if constexpr (POLICY == CACHE_POLICY_LRU || POLICY == CACHE_POLICY_LFU) return col;
+    else if constexpr (POLICY == CACHE_POLICY_FIFO) return 0ull;
+    else return (unsigned long long)col * (unsigned long long)(unsigned)kvj;
+}
+
+// Dirty entries and freed pool slots are marked in bitmaps (compacted in index order at the
+// end of the kernel: the host's free lists and the API's ascending dirty-id list need sorted
+// lists, and an ordered compaction of a bitmap is far cheaper than sorting them).
+__device__ __forceinline__ void mark_dirty(const SelArgs& a, int64_t e, uint32_t id) {
+    atomicOr(a.dslot_bits + (e >> 5), 1u << (e & 31));
+    const uint32_t x = id / (uint32_t)a.world;   // ids of this rank: id % world == rank
+    atomicOr(a.did_bits + (x >> 5), 1u << (x & 31));
+}
+__device__ __forceinline__ void mark_pool(const SelArgs& a, int32_t slot) {
+    if (a.pool_bits && slot >= 0) atomicOr(a.pool_bits + (slot >> 5), 1u << (slot & 31));
+}
+
+// One entry slot (lane-parallel, warp-uniform control flow), every mode of a full sweep, from
+// the slot's preloaded presence mask, id and policy column (col[j] for j < nk).
 template <int POLICY, int GRAN>
-__device__ __forceinline__ void sel_sweep_slot(const SelArgs& a, const KMap& km, const int (&kv)[CACHE_MAX_K],
-                                               int mode, const SelLevel& L, int64_t e, bool valid, unsigned* sh,
-                                               DigitRun& run, unsigned long long& kmin, int lane) {
-    const int nk = km.num_k;
-    const uint32_t m = valid ? a.present[e] : 0u;
-    const uint32_t id = m ? a.ids[e] : 0u;
+__device__ __forceinline__ void sel_slot(const SelArgs& a, int nk, const int (&kv)[CACHE_MAX_K], int mode,
+                                         const SelLevel& L, int64_t e, uint32_t m, uint32_t id,
+                                         const uint32_t (&col)[CACHE_MAX_K], unsigned* sh, DigitRun& run,
+                                         unsigned long long& kmin, int lane) {
     if constexpr (GRAN == CACHE_EVICT_ENTRY) {
-        const unsigned long long key = m ? entry_key<POLICY>(a.fcnt, a.lastacc, e, m, id, nk, kv) : 0ull;
+        unsigned long long sc = 0ull;
+#pragma unroll
+        for (int j = 0; j < CACHE_MAX_K; ++j) {
+            if (j >= nk || !((m >> j) & 1u)) continue;
+            const unsigned long long v = score_v<POLICY>(col[j], kv[j]);
+            if constexpr (POLICY == CACHE_POLICY_LRU) sc = v > sc ? v : sc;
+            else sc += v;
+        }
+        if (sc > 0xFFFFFFFFull) sc = 0xFFFFFFFFull;
+        const unsigned long long key = m ? ((sc << 32) | (unsigned long long)id) : 0ull;
         bool ev;
         sel_unit_common<POLICY, GRAN>(a, mode, L, key, m != 0u, (uint32_t)e, sh, run, kmin, lane, ev);
         if (mode == kSweepL0) return;
         const unsigned long long at = warp_claim(&a.out->cnt[0], ev, lane);
-#pragma unroll
-        for (int j = 0; j < CACHE_MAX_K; ++j) {
-            if (j >= nk) break;   // warp-uniform
-            const bool freed = ev && ((m >> j) & 1u);
-            const unsigned long long pat = warp_claim(&a.out->cnt[2], freed, lane);
-            if (freed && pat < a.pool_cap) a.ev_pool[pat] = (unsigned long long)(uint32_t)a.lslot[e * nk + j];
-        }
         (void)warp_claim(&a.out->cnt[1], ev, lane);   // dirty count = evicted count in entry mode
         if (ev) {
-            for (int j = 0; j < nk; ++j) a.fcnt[e * nk + j] = 0u;
+            atomicAdd(&a.out->cnt[2], (unsigned long long)__popc(m));   // stored states freed
+            for (int j = 0; j < nk; ++j) {
+                if ((m >> j) & 1u) mark_pool(a, a.lslot[e * nk + j]);
+                a.fcnt[e * nk + j] = 0u;
+            }
             a.present[e] = 0u;
             a.inv_e[e] = __int_as_float(0x7FC00000);
-            if (at < a.ev_cap && at < a.dirty_cap) {
-                a.ev_key[at] = key;
-                a.dirty_slot[at] = (unsigned long long)e;
-                a.dirty_id[at] = id;
-            }
+            mark_dirty(a, e, id);
+            if (at < a.ev_cap) a.ev_key[at] = key;
+            ev_mark(a, L, key);
         }
     } else {
         uint32_t keep = m;
@@ -162,18 +212,16 @@ __device__ __forceinline__ void sel_sweep_slot(const SelArgs& a, const KMap& km,
         for (int j = 0; j < CACHE_MAX_K; ++j) {
             if (j >= nk) break;   // warp-uniform
             const bool has = (m >> j) & 1u;
-            const unsigned long long key =
-                has ? item_key(item_score<POLICY>(a.fcnt, a.lastacc, e * nk + j, kv[j]), id, j) : 0ull;
+            const unsigned long long key = has ? item_key(score_v<POLICY>(col[j], kv[j]), id, j) : 0ull;
             bool ev;
             sel_unit_common<POLICY, GRAN>(a, mode, L, key, has, (uint32_t)e, sh, run, kmin, lane, ev);
             if (mode == kSweepL0) continue;
             const unsigned long long at = warp_claim(&a.out->cnt[0], ev, lane);
             if (ev) {
                 keep &= ~(1u << j);
-                if (at < a.ev_cap) {
-                    a.ev_key[at] = key;
-                    a.ev_pool[at] = (unsigned long long)(uint32_t)a.lslot[e * nk + j];
-                }
+                if (at < a.ev_cap) a.ev_key[at] = key;
+                ev_mark(a, L, key);
+                mark_pool(a, a.lslot[e * nk + j]);
                 a.fcnt[e * nk + j] = 0u;
             }
         }
@@ -181,14 +229,201 @@ __device__ __forceinline__ void sel_sweep_slot(const SelArgs& a, const KMap& km,
         const bool dirty = m && keep == 0u;
         if (keep != m) {
             a.present[e] = keep;
-            if (dirty) a.inv_e[e] = __int_as_float(0x7FC00000);
+            if (dirty) {
+                a.inv_e[e] = __int_as_float(0x7FC00000);
+                mark_dirty(a, e, id);
+            }
         }
-        const unsigned long long at = warp_claim(&a.out->cnt[1], dirty, lane);
-        if (dirty && at < a.dirty_cap) {
-            a.dirty_slot[at] = (unsigned long long)e;
-            a.dirty_id[at] = id;
+        (void)warp_claim(&a.out->cnt[1], dirty, lane);
+    }
+}
+
+// ---- item mode, |K| = 5, 4 slots per lane (the common case, C2-C5) ----
+// Per slot, if every stored item has the same policy score (LCBFU: all f = 0, the never-
+// accessed bulk; LRU / LFU: equal columns; FIFO: always) its keys are S<<35 | id<<3 | j, a run
+// of <= 5 consecutive values: one bin / range test for the whole slot instead of 5 key builds.
+// The output claims are aggregated per lane (20-bit masks) and per warp (one scan, one atomic
+// per list and warp iteration) instead of a warp ballot + atomic per item.
+__device__ __forceinline__ unsigned long long warp_excl_scan_u64(unsigned long long x, int lane,
+                                                                 unsigned long long* total) {
+    unsigned long long v = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xFFFFFFFFu, v, o);
+        if (lane >= o) v += y;
+    }
+    *total = __shfl_sync(0xFFFFFFFFu, v, 31);
+    return v - x;
+}
+// one atomic per warp: this lane's first output index of `cnt` items
+__device__ __forceinline__ unsigned long long warp_reserve(unsigned long long* counter, uint32_t cnt, int lane) {
+    unsigned long long tot = 0;
+    const unsigned long long ex = warp_excl_scan_u64(cnt, lane, &tot);
+    unsigned long long base = 0;
+    if (lane == 0 && tot) base = atomicAdd(counter, tot);
+    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+    return base + ex;
+}
+
+template <int POLICY>
+__device__ __forceinline__ uint32_t sat_score(uint32_t col, int kvj, uint32_t limj) {
+    if constexpr (POLICY == CACHE_POLICY_LCBFU) return col > limj ? 0x1FFFFFFFu : col * (uint32_t)kvj;
+    else if constexpr (POLICY == CACHE_POLICY_FIFO) return 0u;
+    else return col > 0x1FFFFFFFu ? 0x1FFFFFFFu : col;
+}
+__device__ __forceinline__ unsigned long long mk_key(uint32_t sc, uint32_t id, int j) {
+    return ((unsigned long long)sc << 35) | ((unsigned long long)id << 3) | (unsigned long long)j;
+}
+
+template <int POLICY>
+__device__ __forceinline__ void sweep_items_v4(const SelArgs& a, const int (&kv)[CACHE_MAX_K],
+                                               const uint32_t (&lim)[CACHE_MAX_K], int mode, const SelLevel& L,
+                                               int64_t e4, const uint32_t (&pm)[4], const uint32_t (&pid)[4],
+                                               const uint32_t (&c)[20], unsigned* sh, DigitRun& run,
+                                               unsigned long long& kmin, int lane) {
+    uint32_t evm = 0u, inm = 0u;   // bit 5q + j: item j of slot q is evicted / in the range
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint32_t m = pm[q] & 31u, id = pid[q];
+        if (!m) continue;
+        bool uni;
+        uint32_t S = 0u;
+        if constexpr (POLICY == CACHE_POLICY_FIFO) uni = true;
+        else if constexpr (POLICY == CACHE_POLICY_LCBFU)
+            uni = (c[5 * q] | c[5 * q + 1] | c[5 * q + 2] | c[5 * q + 3] | c[5 * q + 4]) == 0u;
+        else {
+            uni = c[5 * q] == c[5 * q + 1] && c[5 * q] == c[5 * q + 2] && c[5 * q] == c[5 * q + 3] &&
+                  c[5 * q] == c[5 * q + 4];
+            S = sat_score<POLICY>(c[5 * q], 0, 0u);
+        }
+        const unsigned long long k0 = mk_key(S, id, __ffs(m) - 1), k1 = mk_key(S, id, 31 - __clz(m));
+        bool done = false;
+        if (uni) {
+            if (mode == kSweepL0) {
+                const uint32_t b = sel_bin0(k0);
+                if (b == sel_bin0(k1)) {
+                    run.add_n(sh, b, (unsigned)__popc(m));
+                    kmin = k0 < kmin ? k0 : kmin;
+                    done = true;
+                }
+            } else if (mode == kSweepFinal) {
+                if (k1 <= L.T) { evm |= m << (5 * q); done = true; }
+                else if (k0 > L.T) done = true;
+            } else {
+                if (k1 < L.lo) { evm |= m << (5 * q); done = true; }
+                else if (k0 >= L.lo && ((k0 - L.lo) >> L.w) != 0ull) done = true;   // above the range
+                else if (k0 >= L.lo && ((k1 - L.lo) >> L.w) == 0ull &&
+                         ((k0 - L.lo) >> L.shift) == ((k1 - L.lo) >> L.shift)) {
+                    inm |= m << (5 * q);
+                    const uint32_t d = (uint32_t)((k0 - L.lo) >> L.shift);
+                    run.add_n(sh, d, (unsigned)__popc(m));
+                    done = true;
+                }
+            }
+        }
+        if (!done) {
+#pragma unroll
+            for (int j = 0; j < 5; ++j) {
+                if (!((m >> j) & 1u)) continue;
+                const unsigned long long key = mk_key(sat_score<POLICY>(c[5 * q + j], kv[j], lim[j]), id, j);
+                if (mode == kSweepL0) {
+                    run.add(sh, sel_bin0(key));
+                    kmin = key < kmin ? key : kmin;
+                } else if (mode == kSweepFinal) {
+                    if (key <= L.T) evm |= 1u << (5 * q + j);
+                } else if (key < L.lo) {
+                    evm |= 1u << (5 * q + j);
+                } else if (((key - L.lo) >> L.w) == 0ull) {
+                    inm |= 1u << (5 * q + j);
+                    run.add(sh, (uint32_t)((key - L.lo) >> L.shift));
+                }
+            }
         }
     }
+    if (mode == kSweepL0) return;
+    // outputs: evicted keys (one warp reservation), candidates, presence / counters / dirty
+    unsigned long long pos = warp_reserve(&a.out->cnt[0], (uint32_t)__popc(evm), lane);
+    unsigned long long cpos = 0;
+    if (mode == kSweepLevel && L.compact) cpos = warp_reserve(&a.out->cnt[3], (uint32_t)__popc(inm), lane);
+    uint32_t ndirty = 0;
+    BitRun evr;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint32_t m = pm[q] & 31u, id = pid[q];
+        const uint32_t evq = (evm >> (5 * q)) & 31u, inq = (inm >> (5 * q)) & 31u;
+        if (!(evq | (L.compact ? inq : 0u))) continue;
+        const int64_t e = e4 + q;
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+            if (!(((evq | inq) >> j) & 1u)) continue;
+            const unsigned long long key = mk_key(sat_score<POLICY>(c[5 * q + j], kv[j], lim[j]), id, j);
+            if ((evq >> j) & 1u) {
+                if (pos < a.ev_cap) a.ev_key[pos] = key;
+                ++pos;
+                evr.add(a, L, key);
+                mark_pool(a, a.lslot[e * 5 + j]);
+                a.fcnt[e * 5 + j] = 0u;
+            } else if (mode == kSweepLevel && L.compact) {
+                if (cpos < a.cand_cap) { a.cand_key[cpos] = key; a.cand_slot[cpos] = (uint32_t)e; }
+                ++cpos;
+            }
+        }
+        if (evq) {
+            const uint32_t keep = m & ~evq;
+            a.present[e] = keep | (pm[q] & ~31u);
+            if (!keep) {
+                a.inv_e[e] = __int_as_float(0x7FC00000);
+                mark_dirty(a, e, id);
+                ++ndirty;
+            }
+        }
+    }
+    evr.flush(a);
+    unsigned long long dt = 0;
+    (void)warp_excl_scan_u64(ndirty, lane, &dt);
+    if (lane == 0 && dt) atomicAdd(&a.out->cnt[1], dt);
+}
+
+// ---- TMA bulk staging of the slot columns (the |K| = 5 full sweeps): one thread streams
+// 2,048-slot tiles (present 8 KB, ids 8 KB, policy column 40 KB) into a 3-stage shared-memory
+// ring with cp.async.bulk; the 16 warps read their 4 slots per lane from shared memory.  The
+// bytes in flight no longer depend on registers: the register-fed version (7 x 16-B loads per
+// lane, 2 CTAs / SM) reached 2.98 TB/s = 0.45 of the copy peak, latency-bound (ncu). ----
+#ifndef NV_SEL_STAGED
+#define NV_SEL_STAGED 0   // 1: the TMA-staged sweep (measured slower, kept for the record)
+#endif
+constexpr bool kSelStaged = NV_SEL_STAGED != 0;
+constexpr int kTile = 2048, kStages = 3;
+constexpr int kStageBytes = kTile * 4 * 7;   // present + ids + 5 columns
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+    }
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+
+template <int POLICY>
+__device__ __forceinline__ const uint32_t* policy_col(const SelArgs& a) {
+    if constexpr (POLICY == CACHE_POLICY_LRU) return a.lastacc;
+    else return a.fcnt;
 }
 
 // Candidate i (key, slot): histogram (level) or apply (final, key <= T).
@@ -205,59 +440,139 @@ __device__ __forceinline__ void sel_cand(const SelArgs& a, const KMap& km, int m
     const bool ev = valid && key <= L.T;
     const unsigned long long at = warp_claim(&a.out->cnt[0], ev, lane);
     if constexpr (GRAN == CACHE_EVICT_ENTRY) {
-        const uint32_t m = ev ? a.present[e] : 0u;
-#pragma unroll
-        for (int j = 0; j < CACHE_MAX_K; ++j) {
-            if (j >= nk) break;
-            const bool freed = ev && ((m >> j) & 1u);
-            const unsigned long long pat = warp_claim(&a.out->cnt[2], freed, lane);
-            if (freed && pat < a.pool_cap) a.ev_pool[pat] = (unsigned long long)(uint32_t)a.lslot[e * nk + j];
-        }
         (void)warp_claim(&a.out->cnt[1], ev, lane);
         if (ev) {
-            for (int j = 0; j < nk; ++j) a.fcnt[e * nk + j] = 0u;
+            const uint32_t m = a.present[e];
+            atomicAdd(&a.out->cnt[2], (unsigned long long)__popc(m));
+            for (int j = 0; j < nk; ++j) {
+                if ((m >> j) & 1u) mark_pool(a, a.lslot[e * nk + j]);
+                a.fcnt[e * nk + j] = 0u;
+            }
             a.present[e] = 0u;
             a.inv_e[e] = __int_as_float(0x7FC00000);
-            if (at < a.ev_cap && at < a.dirty_cap) {
-                a.ev_key[at] = key;
-                a.dirty_slot[at] = (unsigned long long)e;
-                a.dirty_id[at] = key & 0xFFFFFFFFull;
-            }
+            mark_dirty(a, e, (uint32_t)(key & 0xFFFFFFFFull));
+            if (at < a.ev_cap) a.ev_key[at] = key;
+            ev_mark(a, L, key);
         }
     } else {
         bool dirty = false;
         if (ev) {
             const int j = (int)(key & 7ull);
             const uint32_t bit = 1u << j;
-            if (at < a.ev_cap) {
-                a.ev_key[at] = key;
-                a.ev_pool[at] = (unsigned long long)(uint32_t)a.lslot[e * nk + j];
-            }
+            if (at < a.ev_cap) a.ev_key[at] = key;
+            ev_mark(a, L, key);
+            mark_pool(a, a.lslot[e * nk + j]);
             a.fcnt[e * nk + j] = 0u;
             const uint32_t old = atomicAnd(a.present + e, ~bit);   // the entry's last bit -> dirty
             dirty = (old & ~bit) == 0u;
-            if (dirty) a.inv_e[e] = __int_as_float(0x7FC00000);
+            if (dirty) {
+                a.inv_e[e] = __int_as_float(0x7FC00000);
+                mark_dirty(a, e, (uint32_t)((key >> 3) & 0xFFFFFFFFull));
+            }
         }
-        const unsigned long long dat = warp_claim(&a.out->cnt[1], dirty, lane);
-        if (dirty && dat < a.dirty_cap) {
-            a.dirty_slot[dat] = (unsigned long long)e;
-            a.dirty_id[dat] = (key >> 3) & 0xFFFFFFFFull;
+        (void)warp_claim(&a.out->cnt[1], dirty, lane);
+    }
+}
+
+// Ordered compaction of the bitmaps into ascending lists (dirty slots, dirty ids, freed pool
+// slots): per CTA a contiguous word range, per thread a contiguous sub-range; CTA totals are
+// exchanged through global memory across one grid barrier.
+struct BitJob {
+    const uint32_t* bits;
+    int64_t words;
+    unsigned long long* out;
+    unsigned long long mul, add;   // value of bit i = i * mul + add
+    unsigned long long* out2;      // optional second list: value & mask2
+    unsigned long long mask2;
+};
+
+__device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t x, uint32_t* total) {
+    __shared__ uint32_t s_ws[kSelThreads / 32];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    uint32_t v = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, v, o);
+        if (lane >= o) v += y;
+    }
+    if (lane == 31) s_ws[w] = v;
+    __syncthreads();
+    uint32_t off = 0, tot = 0;
+    for (int i = 0; i < kSelThreads / 32; ++i) {
+        off += i < w ? s_ws[i] : 0u;
+        tot += s_ws[i];
+    }
+    __syncthreads();
+    *total = tot;
+    return off + v - x;
+}
+
+template <int NJ>
+__device__ void compact_bitmaps(const BitJob (&jobs)[NJ], uint32_t* part, cg::grid_group& grid) {
+    uint32_t cnt[NJ];
+    int64_t w0[NJ], w1[NJ];
+#pragma unroll
+    for (int q = 0; q < NJ; ++q) {
+        const int64_t wb = (jobs[q].words + gridDim.x - 1) / gridDim.x;
+        const int64_t r0 = (int64_t)blockIdx.x * wb, r1 = min(jobs[q].words, r0 + wb);
+        const int64_t tw = (wb + kSelThreads - 1) / kSelThreads;
+        w0[q] = min(r1, r0 + (int64_t)threadIdx.x * tw);
+        w1[q] = min(r1, w0[q] + tw);
+        uint32_t c = 0;
+        if (jobs[q].bits)
+            for (int64_t w = w0[q]; w < w1[q]; ++w) c += __popc(__ldcg(jobs[q].bits + w));
+        cnt[q] = c;
+        uint32_t tot = 0;
+        (void)block_excl_scan_u32(c, &tot);
+        if (threadIdx.x == 0) part[q * gridDim.x + blockIdx.x] = tot;
+    }
+    grid.sync();
+#pragma unroll
+    for (int q = 0; q < NJ; ++q) {
+        if (!jobs[q].bits) continue;   // grid-uniform
+        uint32_t lower = 0;
+        for (int b = threadIdx.x; b < (int)blockIdx.x; b += kSelThreads) lower += __ldcg(part + q * gridDim.x + b);
+        uint32_t lower_tot = 0;
+        (void)block_excl_scan_u32(lower, &lower_tot);
+        uint32_t tot = 0;
+        unsigned long long pos = lower_tot + block_excl_scan_u32(cnt[q], &tot);
+        for (int64_t w = w0[q]; w < w1[q]; ++w) {
+            uint32_t m = __ldcg(jobs[q].bits + w);
+            while (m) {
+                const int bit = __ffs(m) - 1;
+                m &= m - 1u;
+                const unsigned long long v = (unsigned long long)(w * 32 + bit) * jobs[q].mul + jobs[q].add;
+                if (jobs[q].out2) jobs[q].out2[pos] = v & jobs[q].mask2;
+                jobs[q].out[pos++] = v;
+            }
         }
     }
 }
 
-template <int POLICY, int GRAN>
-__global__ void __launch_bounds__(kSelThreads) k_evict_select(SelArgs a, KMap km) {
+// NK5: |K| = 5 (the paper's): every lane loads 4 consecutive slots with 16-byte loads (presence,
+// ids, 5 x the policy column = 20 u32) -- 7 independent loads in flight per thread instead of a
+// dependent present -> id -> counter chain per slot (ncu: the first version moved 704 MB in
+// 789 us, 0.9 TB/s, stalled on those chains and on the grid barrier behind them).
+template <int POLICY, int GRAN, bool NK5>
+__global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : 2) k_evict_select(SelArgs a, KMap km) {
     __shared__ unsigned sh[kSelBins];
+    __shared__ __align__(8) unsigned long long s_bar[2 * kStages];   // full[s], empty[s]
+    extern __shared__ __align__(128) unsigned char s_stage[];        // NK5: kStages x kStageBytes
     cg::grid_group grid = cg::this_grid();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int kv[CACHE_MAX_K];
 #pragma unroll
     for (int j = 0; j < CACHE_MAX_K; ++j) kv[j] = km.kv[j];
-    // this CTA's contiguous slice of the slots (warp-aligned)
-    const int64_t per = (((a.n_slots + gridDim.x - 1) / gridDim.x) + 31) & ~(int64_t)31;
-    const int64_t s0 = (int64_t)blockIdx.x * per, s1 = min(a.n_slots, s0 + per);
-
+    // the sweeps interleave 128-slot groups (one warp iteration of the vector path) over all
+    // warps of the grid: the evictions concentrate in the oldest slots, and contiguous
+    // per-CTA slices left a few CTAs with all the output claims behind a grid barrier (ncu:
+    // 41% of the warps' time in stall_barrier).  The arrays are padded to 256 slots and slots
+    // >= hwm are never live.
+    const int64_t n_pad = (a.n_slots + 127) & ~(int64_t)127;
+    const int nk = NK5 ? 5 : km.num_k;
+    uint32_t lim[CACHE_MAX_K];   // LCBFU saturation: f > lim[j] <=> f * K_j > 2^29 - 1 (R11)
+#pragma unroll
+    for (int j = 0; j < CACHE_MAX_K; ++j) lim[j] = kv[j] > 0 ? 0x1FFFFFFFu / (uint32_t)kv[j] : 0xFFFFFFFFu;
     auto clear_sh = [&]() {
         for (int i = threadIdx.x; i < kSelBins; i += kSelThreads) sh[i] = 0u;
         __syncthreads();
@@ -267,11 +582,124 @@ __global__ void __launch_bounds__(kSelThreads) k_evict_select(SelArgs a, KMap km
         for (int i = threadIdx.x; i < kSelBins; i += kSelThreads)
             if (sh[i]) atomicAdd(gh + i, sh[i]);
     };
+    if constexpr (NK5 && kSelStaged) {
+        if (threadIdx.x == 0) {
+            for (int st = 0; st < kStages; ++st) {
+                bar_init(su32(&s_bar[st]), 1);                         // full: the producer's expect_tx
+                bar_init(su32(&s_bar[kStages + st]), kSelThreads / 32); // empty: one arrive per warp
+            }
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+    }
+    uint32_t uses = 0;   // tiles this CTA has staged so far (all sweeps): stage = u % kStages
     auto full_sweep = [&](int mode, const SelLevel& L, unsigned long long& kmin) {
         DigitRun run;
-        for (int64_t e0 = s0 + warp * 32; e0 < s1; e0 += kSelThreads) {
-            const int64_t e = e0 + lane;
-            sel_sweep_slot<POLICY, GRAN>(a, km, kv, mode, L, e, e < s1, sh, run, kmin, lane);
+        const uint32_t* colp = policy_col<POLICY>(a);
+        if constexpr (NK5 && kSelStaged) {
+            const int64_t ntiles = (n_pad + kTile - 1) / kTile;
+            const int64_t mine = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+            // tile k of this CTA = global tile blockIdx.x + k * gridDim.x (interleaved)
+            auto issue = [&](int64_t k) {
+                const uint32_t u = uses + (uint32_t)k, st = u % kStages;
+                if (u >= (uint32_t)kStages) bar_wait(su32(&s_bar[kStages + st]), ((u / kStages) - 1) & 1);
+                const int64_t t0 = (blockIdx.x + k * gridDim.x) * (int64_t)kTile;
+                const uint32_t cnt = (uint32_t)min((int64_t)kTile, n_pad - t0);   // a multiple of 128
+                const uint32_t full = su32(&s_bar[st]);
+                unsigned char* base = s_stage + (size_t)st * kStageBytes;
+                const uint32_t colb = POLICY != CACHE_POLICY_FIFO ? cnt * 20u : 0u;
+                bar_expect_tx(full, cnt * 8u + colb);
+                bulk_g2s(su32(base), a.present + t0, cnt * 4u, full);
+                bulk_g2s(su32(base + kTile * 4), a.ids + t0, cnt * 4u, full);
+                if (colb) bulk_g2s(su32(base + kTile * 8), colp + t0 * 5, colb, full);
+            };
+            if (threadIdx.x == 0) {
+                asm volatile("fence.proxy.async.global;" ::: "memory");   // earlier sweeps' stores -> TMA reads
+                for (int64_t k = 0; k < (mine < kStages ? mine : (int64_t)kStages); ++k) issue(k);
+            }
+            for (int64_t k = 0; k < mine; ++k) {
+                const uint32_t u = uses + (uint32_t)k, st = u % kStages;
+                bar_wait(su32(&s_bar[st]), (u / kStages) & 1);
+                const int64_t t0 = (blockIdx.x + k * gridDim.x) * (int64_t)kTile;
+                const int64_t e4 = t0 + 4 * threadIdx.x;   // 4 slots of this lane
+                const bool in = e4 < n_pad;
+                const unsigned char* base = s_stage + (size_t)st * kStageBytes;
+                const uint4 P = in ? reinterpret_cast<const uint4*>(base)[threadIdx.x] : make_uint4(0, 0, 0, 0);
+                const uint4 I = reinterpret_cast<const uint4*>(base + kTile * 4)[threadIdx.x];
+                uint32_t c[20];
+                if constexpr (POLICY != CACHE_POLICY_FIFO) {
+                    const uint4* cp = reinterpret_cast<const uint4*>(base + kTile * 8) + 5 * threadIdx.x;
+#pragma unroll
+                    for (int v = 0; v < 5; ++v) {
+                        const uint4 w = cp[v];
+                        c[4 * v] = w.x; c[4 * v + 1] = w.y; c[4 * v + 2] = w.z; c[4 * v + 3] = w.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int v = 0; v < 20; ++v) c[v] = 0u;
+                }
+                __syncwarp();
+                if (lane == 0) bar_arrive(su32(&s_bar[kStages + st]));   // this warp is done with the stage
+                if (threadIdx.x == 0 && k + kStages < mine) issue(k + kStages);
+                const uint32_t pm[4] = {P.x, P.y, P.z, P.w}, pid[4] = {I.x, I.y, I.z, I.w};
+                if constexpr (GRAN == CACHE_EVICT_ITEM) {
+                    sweep_items_v4<POLICY>(a, kv, lim, mode, L, e4, pm, pid, c, sh, run, kmin, lane);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        uint32_t col[CACHE_MAX_K];
+#pragma unroll
+                        for (int j = 0; j < CACHE_MAX_K; ++j) col[j] = j < 5 ? c[5 * q + j] : 0u;
+                        sel_slot<POLICY, GRAN>(a, 5, kv, mode, L, e4 + q, pm[q], pid[q], col, sh, run, kmin, lane);
+                    }
+                }
+            }
+            uses += (uint32_t)mine;
+        } else if constexpr (NK5) {
+            // register-fed: 7 independent 16-B loads per lane (present, ids, 5 x the column of
+            // 4 consecutive slots); 128-slot groups interleaved over all warps of the grid
+            for (int64_t g0 = ((int64_t)blockIdx.x * (kSelThreads / 32) + warp) * 128; g0 < n_pad;
+                 g0 += (int64_t)gridDim.x * 4 * kSelThreads) {
+                const int64_t e4 = g0 + 4 * lane;
+                const uint4 P = __ldcg(reinterpret_cast<const uint4*>(a.present + e4));
+                const uint4 I = __ldcg(reinterpret_cast<const uint4*>(a.ids + e4));
+                uint32_t c[20];
+                if constexpr (POLICY != CACHE_POLICY_FIFO) {
+                    const uint4* cp = reinterpret_cast<const uint4*>(colp + e4 * 5);
+#pragma unroll
+                    for (int v = 0; v < 5; ++v) {
+                        const uint4 w = __ldcg(cp + v);
+                        c[4 * v] = w.x; c[4 * v + 1] = w.y; c[4 * v + 2] = w.z; c[4 * v + 3] = w.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int v = 0; v < 20; ++v) c[v] = 0u;
+                }
+                const uint32_t pm[4] = {P.x, P.y, P.z, P.w}, pid[4] = {I.x, I.y, I.z, I.w};
+                if constexpr (GRAN == CACHE_EVICT_ITEM) {
+                    sweep_items_v4<POLICY>(a, kv, lim, mode, L, e4, pm, pid, c, sh, run, kmin, lane);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        uint32_t col[CACHE_MAX_K];
+#pragma unroll
+                        for (int j = 0; j < CACHE_MAX_K; ++j) col[j] = j < 5 ? c[5 * q + j] : 0u;
+                        sel_slot<POLICY, GRAN>(a, 5, kv, mode, L, e4 + q, pm[q], pid[q], col, sh, run, kmin, lane);
+                    }
+                }
+            }
+        } else {
+            for (int64_t e0 = ((int64_t)blockIdx.x * (kSelThreads / 32) + warp) * 32; e0 < n_pad;
+                 e0 += (int64_t)gridDim.x * kSelThreads) {
+                const int64_t e = e0 + lane;
+                const uint32_t m = a.present[e];   // e < n_pad <= the padded capacity
+                const uint32_t id = a.ids[e];
+                uint32_t col[CACHE_MAX_K];
+#pragma unroll
+                for (int j = 0; j < CACHE_MAX_K; ++j)
+                    col[j] = (POLICY != CACHE_POLICY_FIFO && j < nk) ? colp[e * nk + j] : 0u;
+                sel_slot<POLICY, GRAN>(a, nk, kv, mode, L, e, m, id, col, sh, run, kmin, lane);
+            }
         }
         run.flush(sh);
     };
@@ -287,7 +715,7 @@ __global__ void __launch_bounds__(kSelThreads) k_evict_select(SelArgs a, KMap km
     };
 
     // ---- level 0: log-bin histogram + min key ----
-    SelLevel L{0ull, 0ull, 64, 0, false};
+    SelLevel L{0ull, 0ull, 64, 0, false, 0ull, 0ull};
     clear_sh();
     unsigned long long kmin = ~0ull;
     full_sweep(kSweepL0, L, kmin);
@@ -302,6 +730,8 @@ __global__ void __launch_bounds__(kSelThreads) k_evict_select(SelArgs a, KMap km
         if (lane == 0 && inv) atomicMax(&a.out->kmin_inv, inv);
     }
     grid.sync();
+    L.kb = ~__ldcg(&a.out->kmin_inv);
+    L.ev_lim = a.ev_bits ? (unsigned long long)a.ev_bits_words * 32ull : 0ull;
     PickRes p = sel_pick(a.hist, a.n);
     bool fail = p.bin >= (uint32_t)kSelBins;
     unsigned long long rem = a.n - p.before;
@@ -347,23 +777,46 @@ __global__ void __launch_bounds__(kSelThreads) k_evict_select(SelArgs a, KMap km
             ++full;
         }
     }
+    grid.sync();   // every apply is done: the bitmaps and the evicted-key list are complete
+    bool ev_sorted = false;
+    if (!fail) {
+        // evicted keys (unique): marked in the bitmap over [kb, kb + ev_lim) as they went; sorted
+        // by the compaction below unless one fell beyond it (then the host side sorts the list)
+        const unsigned long long kb = L.kb;
+        ev_sorted = L.ev_lim && L.T >= kb && __ldcg(&a.out->ev_over) == 0u;
+        const BitJob jobs[4] = {
+            BitJob{a.dslot_bits, a.dslot_words, a.dirty_slot, 1ull, 0ull, nullptr, 0ull},
+            BitJob{a.did_bits, a.did_words, a.dirty_id, (unsigned long long)a.world, (unsigned long long)a.rank,
+                   nullptr, 0ull},
+            BitJob{a.pool_bits, a.pool_words, a.ev_pool, 1ull, 0ull, nullptr, 0ull},
+            // every evicted key lies in [kb, kb + ev_lim) (no overflow); T itself may lie beyond
+            BitJob{ev_sorted ? a.ev_bits : nullptr,
+                   ev_sorted ? (int64_t)min((L.T - kb) / 32 + 1, (unsigned long long)a.ev_bits_words) : 0,
+                   a.ev_sorted, 1ull, kb, a.ev_masked, a.ev_mask}};
+        compact_bitmaps<4>(jobs, a.part, grid);
+    }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         a.out->T = L.T;
         a.out->levels = (uint32_t)level;
         a.out->full_sweeps = (uint32_t)full;
         a.out->compact_level = (uint32_t)compact_level;
         a.out->err = fail ? 1u : 0u;
+        a.out->ev_sorted = ev_sorted ? 1u : 0u;
     }
 }
 
-template <int POLICY, int GRAN>
+template <int POLICY, int GRAN, bool NK5>
 static cudaError_t launch_select_t(const SelArgs& a, const KMap& km, cudaStream_t s) {
     static int wave = [] {
         int bps = 0, dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_evict_select<POLICY, GRAN>, kSelThreads, 0) !=
-                cudaSuccess || bps < 1)
+        if (NK5 && kSelStaged)
+            cudaFuncSetAttribute(k_evict_select<POLICY, GRAN, NK5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kStages * kStageBytes);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_evict_select<POLICY, GRAN, NK5>, kSelThreads,
+                                                          (NK5 && kSelStaged) ? kStages * kStageBytes : 0) != cudaSuccess ||
+            bps < 1)
             bps = 1;
         return bps * sms;
     }();
@@ -371,12 +824,13 @@ static cudaError_t launch_select_t(const SelArgs& a, const KMap& km, cudaStream_
     SelArgs aa = a;
     KMap kk = km;
     void* args[] = {&aa, &kk};
-    return cudaLaunchCooperativeKernel((const void*)k_evict_select<POLICY, GRAN>, grid, kSelThreads, args, 0, s);
+    return cudaLaunchCooperativeKernel((const void*)k_evict_select<POLICY, GRAN, NK5>, grid, kSelThreads, args,
+                                       (NK5 && kSelStaged) ? (size_t)kStages * kStageBytes : 0, s);
 }
 
 cudaError_t launch_evict_select(const SelArgs& a, const KMap& km, cudaStream_t s) {
     cudaError_t r = cudaSuccess;
-#define NV_SEL(P, G) r = launch_select_t<P, G>(a, km, s)
+#define NV_SEL(P, G) r = km.num_k == 5 ? launch_select_t<P, G, true>(a, km, s) : launch_select_t<P, G, false>(a, km, s)
     NV_EVICT_DISPATCH(NV_SEL);
 #undef NV_SEL
     return r;

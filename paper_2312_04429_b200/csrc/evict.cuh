@@ -52,6 +52,12 @@ struct DigitRun {
         cur = d;
         cnt = 1;
     }
+    __device__ __forceinline__ void add_n(unsigned* sh, unsigned d, unsigned n) {
+        if (d == cur) { cnt += n; return; }
+        if (cnt) atomicAdd(&sh[cur], cnt);
+        cur = d;
+        cnt = n;
+    }
     __device__ __forceinline__ void flush(unsigned* sh) {
         if (cnt) atomicAdd(&sh[cur], cnt);
     }

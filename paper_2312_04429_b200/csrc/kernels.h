@@ -85,6 +85,8 @@ int64_t sort_scratch_words(int64_t n);
 unsigned long long* launch_sort_u64(unsigned long long* keys, unsigned long long* tmp, int64_t n, uint32_t* scratch,
                                     cudaStream_t s, int bits = 64, unsigned long long base = 0ull);
 int sort_launches(int64_t n, int bits);
+void launch_mask_u64(const unsigned long long* in, unsigned long long* out, int64_t n, unsigned long long mask,
+                     cudaStream_t s);
 // Up to 4 lists of <= kSmallSort keys, each sorted in place by one CTA (one launch).
 constexpr int kSmallSort = 16384;
 struct SortSeg {
@@ -96,6 +98,21 @@ struct SortSegs {
     int k;
 };
 void launch_sort_small(const SortSegs& segs, cudaStream_t s);
+// Up to 4 long lists sorted in ONE cooperative launch (sequentially, grid barriers between the
+// LSD steps); each list's result lands in its keys buffer (tmp may be shared by the lists).
+struct SortJob {
+    unsigned long long* keys;
+    unsigned long long* tmp;
+    int64_t n;
+    int passes;                  // ceil(bits / 8)
+    unsigned long long base;     // keys in [base, base + 2^(8 passes))
+};
+struct SortJobs {
+    SortJob j[4];
+    int k;
+};
+int64_t sort_coop_scratch_words(int64_t max_n);
+cudaError_t launch_sort_coop(const SortJobs& jobs, uint32_t* scratch, cudaStream_t s);
 
 // Fused single-cache eviction (evict.cu): the exact n smallest unit keys selected and applied
 // in ONE cooperative launch (see evict.cu for the algorithm).  `out` is zeroed by the caller.
@@ -104,6 +121,7 @@ struct SelOut {
     unsigned long long kmin_inv;  // ~(smallest live key)
     unsigned long long T;         // threshold: every unit with key <= T was evicted
     uint32_t levels, full_sweeps, compact_level, err;
+    uint32_t ev_sorted, ev_over;  // evicted keys emitted sorted (bitmap path) / one fell beyond the bitmap
 };
 constexpr int kSelBins = 4096, kSelMaxLevels = 8;
 struct SelArgs {
@@ -120,10 +138,23 @@ struct SelArgs {
     uint32_t* cand_slot;
     unsigned long long cand_cap;
     unsigned long long* ev_key;        // evicted unit keys (unsorted), capacity ev_cap
-    unsigned long long* ev_pool;       // freed pool slots, capacity pool_cap
-    unsigned long long* dirty_slot;    // dirty entries, capacity dirty_cap
+    unsigned long long* ev_pool;       // freed pool slots, ascending (from pool_bits)
+    unsigned long long* dirty_slot;    // dirty entries: slots ascending, ids ascending
     unsigned long long* dirty_id;
-    unsigned long long ev_cap, pool_cap, dirty_cap;
+    unsigned long long ev_cap;
+    uint32_t* dslot_bits;              // zeroed bitmaps: dirty slots, dirty ids / world, freed
+    uint32_t* did_bits;                //   pool slots (null: pool slots not tracked, aliasing)
+    uint32_t* pool_bits;
+    int64_t dslot_words, did_words, pool_words;
+    int world, rank;                   // ids of this cache: id % world == rank
+    uint32_t* part;                    // [4][grid] CTA totals of the compaction
+    // evicted keys are unique: when they span < 32 * ev_bits_words values above the min key,
+    // they are sorted by an ordered bitmap compaction in the kernel (no sort launches)
+    uint32_t* ev_bits;                 // zeroed, ev_bits_words words (null: never)
+    int64_t ev_bits_words;
+    unsigned long long* ev_sorted;     // full keys, ascending
+    unsigned long long* ev_masked;     // the reported values (key & ev_mask), ascending
+    unsigned long long ev_mask;
     SelOut* out;
 };
 cudaError_t launch_evict_select(const SelArgs& a, const KMap& km, cudaStream_t s);

@@ -40,7 +40,7 @@ def main():
         k = max(1, units // 100)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        ev, dirty = g.evict(k)
+        ev, dirty = g.evict(k, view=True)   # the lists in the library's pinned staging, no copy
         t = time.perf_counter() - t0
         # re-insert as many fresh prompts as entries were removed (the C5 round's second half)
         nn = len(dirty)

@@ -26,15 +26,16 @@ def test_small_sort(n):
     assert np.array_equal(t.cpu().numpy().view(np.uint64), np.sort(k))
 
 
+@pytest.mark.parametrize("coop", [0, 2])
 @pytest.mark.parametrize("n", [2, 20_000, 300_001])
 @pytest.mark.parametrize("bits", [1, 9, 23, 40])
-def test_range_sort(n, bits):
+def test_range_sort(n, bits, coop):
     from paper_2312_04429_b200 import binding as B
     rng = np.random.default_rng(bits)
     base = np.uint64(123456789) << np.uint64(20)
     k = base + (rng.integers(0, 2**bits, n, dtype=np.int64).astype(np.uint64))
     t = torch.from_numpy(k.view(np.int64).copy()).cuda()
-    B.debug_sort_u64_ex(t, bits=bits, base=int(base))
+    B.debug_sort_u64_ex(t, bits=bits, base=int(base), small=coop)
     assert np.array_equal(t.cpu().numpy().view(np.uint64), np.sort(k))
 
 
@@ -117,3 +118,52 @@ def test_fused_evict_hot_counters_spread(oracle_mod):
     units = g.evict_units
     st = _evict_both(B, g, o, units - 40, 0, 0)
     assert st["levels"] >= 1
+
+
+def test_key_saturation_reading_r11(oracle_mod):
+    """R11: the GPU item key saturates the LCBFU score f*K at 2^29 - 1.  (1) A cut below the
+    saturated items gives exactly the oracle's eviction; (2) a cut AMONG them orders the
+    saturated items by (id, K) on the GPU and by their exact f*K in the oracle -- the documented
+    deviation, which needs > 5.4e8 / K accesses of one item to arise."""
+    B, g, o = _pair(oracle_mod, 200, 0, 0, seed=95, nq_batches=0)
+    picks = []
+    for id_ in range(5, 200):
+        _, mask = g.meta(id_)
+        j = 4 if (mask >> 4) & 1 else (0 if mask & 1 else None)
+        if j is not None:
+            picks.append((id_, j))
+        if len(picks) == 3:
+            break
+    kvals = (5, 10, 15, 20, 25)
+    # exact f*K all > 2^29 - 1, DEcreasing with the id: the two orders then disagree
+    fs = [-(-t // kvals[j]) for t, (_, j) in zip((4_000_000_000, 3_000_000_000, 2_000_000_000), picks)]
+    for (i, j), f in zip(picks, fs):
+        B.debug_set_count(g, i, j, f)
+        assert o.set_count(i, j, f) == 0
+    _evict_both(B, g, o, g.evict_units - 3, 0, 0)          # (1) identical
+    exact = sorted(picks, key=lambda p: (fs[picks.index(p)] * kvals[p[1]], p[0], p[1]))
+    ev, _ = g.evict(1)
+    rc, oev, _ = o.evict(1)
+    assert rc == 0
+    assert int(ev[0]) == (min(picks)[0] << 3 | min(picks)[1])           # GPU: (id, j) among the saturated
+    assert int(oev[0]) == (exact[0][0] << 3 | exact[0][1])               # oracle: exact f*K
+    assert int(ev[0]) != int(oev[0])
+
+
+@pytest.mark.parametrize("gran", [0, 1])
+def test_evict_view_and_keys(oracle_mod, gran):
+    """cache_evict_view hands out the same lists as cache_evict (in the library's pinned
+    staging, no copy); cache_last_evicted_keys returns the full keys of that eviction, whose
+    masked values are the list, ascending."""
+    B, g, o = _pair(oracle_mod, 1200, 0, gran, seed=97, zipf_hot=True)
+    ev, dirty = g.evict(g.evict_units // 5, view=True)
+    if gran:
+        rc, oev = o.evict_entries(len(ev))
+        assert np.array_equal(ev, oev) and np.array_equal(dirty, np.sort(oev))
+    else:
+        rc, oev, od = o.evict(len(ev))
+        assert np.array_equal(ev, oev) and np.array_equal(dirty, od)
+    keys = g.last_evicted_keys()
+    mask = np.uint64(0xFFFFFFFF) if gran else np.uint64((1 << 35) - 1)
+    assert len(keys) == len(ev) and np.all(np.diff(keys.astype(np.float64)) >= 0)
+    assert np.array_equal(keys & mask, ev)
