@@ -252,6 +252,22 @@ cache_status cache_query_batch_host(cache_t *c, int64_t b, const void *queries, 
                                     int32_t *out_k, void *latent_out, int32_t *row_status,
                                     void *stream);
 
+/* Pipelined host calls (two slots): cache_query_submit enqueues one batch -- the upload of
+ * `queries` (HOST memory, pinned for overlap; must stay valid until the slot completes) on the
+ * library's copy stream, the lookup of cache_query_batch on `stream` once it has landed, the
+ * download of the results into pinned staging -- and returns at once; cache_query_complete
+ * waits for that slot and copies ids / scores / K / status to the caller's host arrays.  While
+ * slot i's lookup runs, slot i^1's upload proceeds, so a loop
+ *     submit(0, q0); submit(1, q1); complete(0); submit(0, q2); complete(1); ...
+ * overlaps each batch's host-to-device copy with the previous batch's scan (the synchronous
+ * cache_query_batch_host cannot).  latent_out: DEVICE pointer (the denoiser's input buffer for
+ * this batch) or NULL.  One LRU clock tick per submitted batch; batches run in submit order.
+ * CACHE_E_STATE: submit on a pending slot / complete on an idle one. */
+cache_status cache_query_submit(cache_t *c, int32_t slot, int64_t b, const void *queries, int32_t q_dtype,
+                                int32_t topk, void *latent_out, void *stream);
+cache_status cache_query_complete(cache_t *c, int32_t slot, uint64_t *out_ids, float *out_scores,
+                                  int32_t *out_k, int32_t *row_status);
+
 /* LCBFU eviction: remove the n stored items with the smallest LCBFU score
  * f_i x K_i, ties by (entry id, K) ascending (R11); then every entry left with no
  * stored K is dirty and is removed from the index in the same call (R13).

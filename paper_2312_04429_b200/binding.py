@@ -84,7 +84,7 @@ EXPORTS = ("cache_default_config", "cache_create", "cache_destroy", "cache_inser
            "cache_push_scan", "cache_push_merge", "cache_push_evict_hist", "cache_push_evict_pick",
            "cache_push_evict_apply", "cache_profile_thresholds", "cache_set_thresholds", "cache_query_peek",
            "cache_push_status", "cache_set_peer_timeout", "cache_last_evicted_keys",
-           "cache_evict_view")
+           "cache_evict_view", "cache_query_submit", "cache_query_complete")
 
 
 def load_library(path: str = LIB_PATH):
@@ -101,6 +101,10 @@ def load_library(path: str = LIB_PATH):
     L.cache_query_batch_host.argtypes = [P, I64, P, I32, I32, P, P, P, P, P, P]
     L.cache_query_peek.argtypes = [P, I64, P, I32, I32, P, P, P, P, P]
     L.cache_query_peek.restype = ctypes.c_int
+    L.cache_query_submit.argtypes = [P, I32, I64, P, I32, I32, P, P]
+    L.cache_query_submit.restype = ctypes.c_int
+    L.cache_query_complete.argtypes = [P, I32, P, P, P, P]
+    L.cache_query_complete.restype = ctypes.c_int
     L.cache_evict_view.argtypes = [P, I64, P, P, P, P]
     L.cache_evict_view.restype = ctypes.c_int
     L.cache_last_evicted_keys.argtypes = [P, P, I64, P]
@@ -285,6 +289,20 @@ class NirvanaCache:
         assert q.is_cuda and q.is_contiguous() and q.dim() == 2 and q.shape[1] == self.dim
         out = self.alloc_outputs(q.shape[0], topk, latents)
         return self.query_into(q, out, topk, stream)
+
+    def submit(self, slot: int, q_host: torch.Tensor, topk: int = 1, latent_out: torch.Tensor | None = None,
+               stream=None):
+        """Pipelined lookup (cache_query_submit): q_host = pinned CPU tensor, kept alive by the
+        caller until complete(slot); latent_out = device buffer or None."""
+        dt = DTYPE_BF16 if q_host.dtype == torch.bfloat16 else DTYPE_F32
+        _check(_lib.cache_query_submit(self._h, slot, q_host.shape[0], _ptr(q_host), dt, topk, _ptr(latent_out),
+                                       _stream(stream)))
+
+    def complete(self, slot: int, out: dict):
+        """Wait for slot; out: host tensors ids [b][topk] int64, scores f32, k i32, status i32."""
+        _check(_lib.cache_query_complete(self._h, slot, _ptr(out["ids"]), _ptr(out["scores"]), _ptr(out["k"]),
+                                         _ptr(out.get("status"))))
+        return out
 
     def peek(self, q: torch.Tensor, topk: int = 1, stream=None):
         """Read-only lookup (cache_query_peek): ids / scores / K as query() would report them,

@@ -179,6 +179,17 @@ struct cache_t {
     DevBuf<InsertPlan> iplan;
     DevBuf<CopyPlan> cplan;
     DevBuf<uint8_t> hq_in, hq_lat, hq_out;
+    // pipelined host calls (cache_query_submit / _complete): per slot an input and an output
+    // buffer on the device, pinned output staging, and the events of its last use
+    struct AsyncSlot {
+        DevBuf<uint8_t> in, out;
+        void* h_out = nullptr;
+        size_t h_out_n = 0;
+        cudaEvent_t copied = nullptr, consumed = nullptr, done = nullptr;
+        int64_t b = 0;
+        int32_t topk = 0;
+        bool pending = false;
+    } aslot[2];
     // pinned host staging of an eviction's lists (keys, sorted keys, pool slots, entry slots,
     // dirty slots): reused across calls, so no pageable copies or fresh-page faults
     struct PinnedBuf {
@@ -422,6 +433,13 @@ cache_status cache_destroy(cache_t* c) {
     cudaDeviceSynchronize();
     for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
     if (c->h_out) cudaFreeHost(c->h_out);
+    for (auto& a : c->aslot) {
+        a.in.release();
+        a.out.release();
+        if (a.h_out) cudaFreeHost(a.h_out);
+        for (cudaEvent_t e : {a.copied, a.consumed, a.done})
+            if (e) cudaEventDestroy(e);
+    }
     for (cudaEvent_t e : c->hev)
         if (e) cudaEventDestroy(e);
     if (c->hcopy) cudaStreamDestroy(c->hcopy);
@@ -1247,6 +1265,73 @@ cache_status cache_push_merge(cache_t* c, int64_t nb, int32_t topk, uint64_t* ou
     c->queries += nb;
     c->push_phase = 3;
     CK(cudaGetLastError());
+    return CACHE_OK;
+}
+
+// ---- pipelined host calls: batch i+1's upload (copy stream) overlaps batch i's lookup ----
+cache_status cache_query_submit(cache_t* c, int32_t slot, int64_t b, const void* queries, int32_t q_dtype,
+                                int32_t topk, void* latent_out, void* stream) {
+    if (!c) return fail(CACHE_E_INVALID_ARG, "cache_query_submit: null cache");
+    if (slot < 0 || slot > 1 || b <= 0 || b > 0x7FFFFFFF || topk < 1 || topk > c->cfg.max_topk || !queries ||
+        (q_dtype != CACHE_DTYPE_F32 && q_dtype != CACHE_DTYPE_BF16))
+        return fail(CACHE_E_INVALID_ARG, "cache_query_submit: bad slot / b / topk / dtype / queries");
+    if (latent_out && !c->pool) return fail(CACHE_E_INVALID_ARG, "cache_query_submit: no latent pool");
+    cache_t::AsyncSlot& a = c->aslot[slot];
+    if (a.pending) return fail(CACHE_E_STATE, "cache_query_submit: slot still pending (call cache_query_complete)");
+    DeviceGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!c->hcopy) CK(cudaStreamCreateWithFlags(&c->hcopy, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&a.copied, &a.consumed, &a.done})
+        if (!*e) CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    const size_t qbytes = (size_t)b * c->dim * (q_dtype == CACHE_DTYPE_BF16 ? 2 : 4);
+    const size_t o_sc = (size_t)b * topk * 8, o_k = o_sc + (size_t)b * topk * 4, o_st = o_k + (size_t)b * 4;
+    const size_t obytes = o_st + (size_t)b * 4;
+    if (a.in.n < qbytes) {   // growing the input buffer frees it: its last reader must be done
+        CK(cudaEventSynchronize(a.consumed));
+        CK(a.in.ensure(qbytes));
+    }
+    CK(a.out.ensure(obytes));
+    if (a.h_out_n < obytes) {
+        if (a.h_out) cudaFreeHost(a.h_out);
+        a.h_out = nullptr;
+        a.h_out_n = 0;
+        CK(cudaHostAlloc(&a.h_out, obytes, cudaHostAllocDefault));
+        a.h_out_n = obytes;
+    }
+    // upload on the copy stream once the slot's previous lookup has read its input
+    CK(cudaStreamWaitEvent(c->hcopy, a.consumed, 0));
+    CK(cudaMemcpyAsync(a.in.p, queries, qbytes, cudaMemcpyHostToDevice, c->hcopy));
+    CK(cudaEventRecord(a.copied, c->hcopy));
+    CK(cudaStreamWaitEvent(s, a.copied, 0));
+    uint8_t* ob = a.out.p;
+    cache_status r = query_core(c, b, a.in.p, q_dtype, topk, (uint64_t*)ob, (float*)(ob + o_sc), (int32_t*)(ob + o_k),
+                                latent_out, nullptr, (int32_t*)(ob + o_st), s);
+    if (r != CACHE_OK) return r;
+    CK(cudaEventRecord(a.consumed, s));
+    CK(cudaMemcpyAsync(a.h_out, ob, obytes, cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(a.done, s));
+    a.b = b;
+    a.topk = topk;
+    a.pending = true;
+    return CACHE_OK;
+}
+
+cache_status cache_query_complete(cache_t* c, int32_t slot, uint64_t* out_ids, float* out_scores, int32_t* out_k,
+                                  int32_t* row_status) {
+    if (!c || slot < 0 || slot > 1 || !out_ids || !out_scores || !out_k)
+        return fail(CACHE_E_INVALID_ARG, "cache_query_complete: bad argument");
+    cache_t::AsyncSlot& a = c->aslot[slot];
+    if (!a.pending) return fail(CACHE_E_STATE, "cache_query_complete: nothing submitted on this slot");
+    DeviceGuard g(c->device);
+    CK(cudaEventSynchronize(a.done));
+    a.pending = false;
+    const int64_t b = a.b, topk = a.topk;
+    const size_t o_sc = (size_t)b * topk * 8, o_k = o_sc + (size_t)b * topk * 4, o_st = o_k + (size_t)b * 4;
+    const uint8_t* hb = static_cast<const uint8_t*>(a.h_out);
+    std::memcpy(out_ids, hb, (size_t)b * topk * 8);
+    std::memcpy(out_scores, hb + o_sc, (size_t)b * topk * 4);
+    std::memcpy(out_k, hb + o_k, (size_t)b * 4);
+    if (row_status) std::memcpy(row_status, hb + o_st, (size_t)b * 4);
     return CACHE_OK;
 }
 

@@ -658,8 +658,8 @@ __global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : 2) k_ev
         } else if constexpr (NK5) {
             // register-fed: 7 independent 16-B loads per lane (present, ids, 5 x the column of
             // 4 consecutive slots); 128-slot groups interleaved over all warps of the grid
-            for (int64_t g0 = ((int64_t)blockIdx.x * (kSelThreads / 32) + warp) * 128; g0 < n_pad;
-                 g0 += (int64_t)gridDim.x * 4 * kSelThreads) {
+            const int64_t gstride = (int64_t)gridDim.x * 4 * kSelThreads;
+            for (int64_t g0 = ((int64_t)blockIdx.x * (kSelThreads / 32) + warp) * 128; g0 < n_pad; g0 += gstride) {
                 const int64_t e4 = g0 + 4 * lane;
                 const uint4 P = __ldcg(reinterpret_cast<const uint4*>(a.present + e4));
                 const uint4 I = __ldcg(reinterpret_cast<const uint4*>(a.ids + e4));

@@ -70,3 +70,40 @@ def test_host_call_split_upload_equals_device(oracle_mod, b):
     assert rc == 0 and np.array_equal(ev, oev) and np.array_equal(dirty, od)
     evd, _ = gd.evict(900)
     assert np.array_equal(ev, evd)
+
+
+def test_pipelined_submit_complete_matches_device_call(oracle_mod):
+    """cache_query_submit / _complete (two slots, uploads on the copy stream): every batch's
+    ids / scores / K / status and gathered states equal the device call's for the same cache
+    state; one LRU clock tick per batch (the oracle ticks once per batch too)."""
+    import torch
+    from paper_2312_04429_b200 import binding as B
+    n, b, L = 3000, 700, 256
+    emb, cl = synth.entries(n, seed=81)
+    lat = synth.latents_np(np.arange(n), 5, L, seed=81)
+    caches = []
+    for _ in range(2):
+        g = B.NirvanaCache(entry_capacity=n, dim=768, latent_bytes=L)
+        g.set_evict_policy(1)
+        g.insert(torch.from_numpy(emb).cuda(), torch.from_numpy(lat).cuda())
+        caches.append(g)
+    pipe, ref = caches
+    qs = [synth.queries(emb, cl, b, seed=90 + i)[0] for i in range(5)]
+    qh = [torch.from_numpy(q).pin_memory() for q in qs]
+    lats = [torch.empty((b, L), dtype=torch.uint8, device="cuda") for _ in range(2)]
+    outs = [dict(ids=torch.empty((b, 1), dtype=torch.int64), scores=torch.empty((b, 1), dtype=torch.float32),
+                 k=torch.empty(b, dtype=torch.int32), status=torch.empty(b, dtype=torch.int32)) for _ in range(2)]
+    pipe.submit(0, qh[0], 1, lats[0])
+    for i in range(5):
+        if i + 1 < 5:
+            pipe.submit((i + 1) % 2, qh[i + 1], 1, lats[(i + 1) % 2])
+        o = pipe.complete(i % 2, outs[i % 2])
+        r = ref.query(torch.from_numpy(qs[i]).cuda(), topk=1)
+        assert np.array_equal(o["ids"].numpy(), r["ids"].cpu().numpy())
+        assert np.array_equal(o["k"].numpy(), r["k"].cpu().numpy())
+        assert np.array_equal(o["scores"].numpy().view(np.uint32), r["scores"].cpu().numpy().view(np.uint32))
+        hit = r["k"].cpu().numpy() > 0
+        assert np.array_equal(lats[i % 2].cpu().numpy()[hit], r["latents"].cpu().numpy()[hit])
+    with pytest.raises(B.CacheError):
+        pipe.complete(0, outs[0])            # nothing pending
+    assert np.array_equal(pipe.evict(2000)[0], ref.evict(2000)[0])   # same LRU clocks
