@@ -19,6 +19,7 @@
 // so the CTAs running at the same time share the same entry tiles (L2 reuse).  Each unit
 // ends with one partial top-k record list per query -> ws[chunk][query][KMAX]; k_finalize
 // merges the n_chunks lists under the same total order (R3).
+#include <cstdlib>
 #include <cuda.h>
 
 #include "kernels.h"
@@ -920,6 +921,10 @@ TcPlan tc_plan(int64_t b, int64_t n_slots, int sm_count, bool pair) {
             best = mk;
             p.chunk_tiles = nc;
         }
+    }
+    if (const char* ev = std::getenv("NIRVANA_TC_CHUNK")) {   // experiments: fixed entry tiles per unit
+        const int nc = std::atoi(ev);
+        if (nc >= 1) p.chunk_tiles = std::min(nc, p.n_tiles);
     }
     p.n_chunks = (p.n_tiles + p.chunk_tiles - 1) / p.chunk_tiles;
     p.grid = (int)std::min<int64_t>(sm_count, (int64_t)p.n_chunks * p.m_tiles);

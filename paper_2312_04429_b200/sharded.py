@@ -200,6 +200,9 @@ class ShardedCache:
                                                      device="cuda")).item()
         if n > live:
             raise B.CacheError(B.E_EVICT_RANGE, "sharded evict: n exceeds live items / entries")
+        if self.comm.world == 1:   # one shard: no exchange, the fused single-launch eviction
+            ev, dirty = self.cache.evict(n, view=True)
+            return (len(ev), len(dirty)) if not lists else (ev.copy(), dirty.copy())
         if self.push:   # histograms reduced over peer memory by the kernels themselves
             for p in range(8):
                 self.cache.push_evict_hist(n, p)

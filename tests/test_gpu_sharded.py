@@ -63,3 +63,38 @@ def test_virtual_shards_equal_single_cache(mods, oracle_mod, world, topk):
     a = gpu_to_numpy(single.query(qt, topk=topk))
     s = gpu_to_numpy(vs.query(qt, topk=topk))
     assert np.array_equal(a["ids"], s["ids"]) and np.array_equal(a["k"], s["k"])
+
+
+def test_sharded_world1_evict_is_the_fused_eviction(oracle_mod):
+    """A one-rank ShardedCache (bench C5 at N = 1) evicts through the fused single-launch path:
+    the same lists as one cache and the oracle."""
+    import socket
+    import torch.distributed as dist
+    from paper_2312_04429_b200 import binding as B, sharded as S
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("gloo", rank=0, world_size=1, init_method=f"tcp://127.0.0.1:{port}")
+    try:
+        n = 900
+        emb, cl = synth.entries(n, seed=23)
+        sc = S.ShardedCache(S.TorchComm(device="cpu"), entry_capacity=n, dim=768, latent_bytes=0,
+                            push_max_nb=64, push_max_topk=1)
+        single = B.NirvanaCache(entry_capacity=n, dim=768, latent_bytes=0)
+        o = oracle_mod.OracleCache(dim=768, entry_capacity=n, latent_capacity=5 * n)
+        for c in (sc, single):
+            c.insert(torch.from_numpy(emb).cuda())
+        o.insert(emb)
+        q, _, _ = synth.queries(emb, cl, 64, seed=24)
+        out = sc.alloc_outputs(64, 1, False)
+        sc.query_into(torch.from_numpy(q).cuda(), out)
+        single.query(torch.from_numpy(q).cuda(), latents=False)
+        check_batch(gpu_to_numpy(out), o, q, 1)
+        e1, d1 = sc.evict(700)
+        e2, d2 = single.evict(700)
+        rc, e3, d3 = o.evict(700)
+        assert np.array_equal(e1, e2) and np.array_equal(e1, e3) and np.array_equal(d1, d2) and np.array_equal(d1, d3)
+        assert sc.evict(10, lists=False) == (10, len(single.evict(10)[1]))
+    finally:
+        dist.destroy_process_group()
