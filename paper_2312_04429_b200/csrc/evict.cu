@@ -33,7 +33,13 @@ namespace nv {
 
 namespace cg = cooperative_groups;
 
-constexpr int kSelThreads = 512;
+#ifndef NV_SEL_CPASYNC
+#define NV_SEL_CPASYNC 0   // 1: |K| = 5 sweeps fed by per-lane cp.async rings (measured slower, kept for the record)
+#endif
+constexpr bool kSelCpAsync = NV_SEL_CPASYNC != 0;
+constexpr int kSelThreads = kSelCpAsync ? 256 : 512;
+constexpr int kCpStages = 3;                           // groups per lane: 2 loading + 1 being processed
+constexpr int kCpRingBytes = kCpStages * kSelThreads * 112;
 
 __device__ __forceinline__ uint32_t sel_bin0(unsigned long long key) {
     if (key < 64ull) return (uint32_t)key;
@@ -58,12 +64,15 @@ struct PickRes {
 __device__ PickRes sel_pick(const uint32_t* h, unsigned long long target) {
     __shared__ unsigned long long s_w[kSelThreads / 32];
     __shared__ PickRes s_res;
-    constexpr int PER = kSelBins / kSelThreads;   // 8 bins per thread
+    constexpr int PER = kSelBins / kSelThreads;   // 8 or 16 bins per thread
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     uint32_t v[PER];
     const uint4* h4 = reinterpret_cast<const uint4*>(h + t * PER);
-    const uint4 a = __ldcg(h4), b = __ldcg(h4 + 1);
-    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+#pragma unroll
+    for (int q = 0; q < PER / 4; ++q) {
+        const uint4 x4 = __ldcg(h4 + q);
+        v[4 * q] = x4.x; v[4 * q + 1] = x4.y; v[4 * q + 2] = x4.z; v[4 * q + 3] = x4.w;
+    }
     unsigned long long s = 0;
 #pragma unroll
     for (int i = 0; i < PER; ++i) s += v[i];
@@ -554,10 +563,11 @@ __device__ void compact_bitmaps(const BitJob (&jobs)[NJ], uint32_t* part, cg::gr
 // dependent present -> id -> counter chain per slot (ncu: the first version moved 704 MB in
 // 789 us, 0.9 TB/s, stalled on those chains and on the grid barrier behind them).
 template <int POLICY, int GRAN, bool NK5>
-__global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : 2) k_evict_select(SelArgs a, KMap km) {
+__global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : (kSelCpAsync ? 3 : 2))
+    k_evict_select(SelArgs a, KMap km) {
     __shared__ unsigned sh[kSelBins];
     __shared__ __align__(8) unsigned long long s_bar[2 * kStages];   // full[s], empty[s]
-    extern __shared__ __align__(128) unsigned char s_stage[];        // NK5: kStages x kStageBytes
+    extern __shared__ __align__(128) unsigned char s_stage[];        // NK5: TMA stages / cp.async ring
     cg::grid_group grid = cg::this_grid();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int kv[CACHE_MAX_K];
@@ -655,6 +665,65 @@ __global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : 2) k_ev
                 }
             }
             uses += (uint32_t)mine;
+        } else if constexpr (NK5 && kSelCpAsync) {
+            // per-lane cp.async ring: each lane copies its own 112 B per group (present, ids and
+            // the 5-word column of 4 consecutive slots) straight into shared memory, two groups
+            // ahead of the one it processes -- loads in flight without holding registers
+            // (the register-fed loop keeps one group in flight per lane, 0.44 of the copy peak)
+            const int64_t gstride = (int64_t)gridDim.x * 4 * kSelThreads;
+            const int64_t gfirst = ((int64_t)blockIdx.x * (kSelThreads / 32) + warp) * 128;
+            uint4* ring = reinterpret_cast<uint4*>(s_stage);
+            auto slot_of = [&](int st) { return ring + ((size_t)st * kSelThreads + threadIdx.x) * 7; };
+            auto issue = [&](int64_t g0, int st) {
+                if (g0 < n_pad) {
+                    const int64_t e4 = g0 + 4 * lane;
+                    const uint32_t d = su32(slot_of(st));
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(a.present + e4) : "memory");
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16), "l"(a.ids + e4) : "memory");
+                    if constexpr (POLICY != CACHE_POLICY_FIFO) {
+#pragma unroll
+                        for (int v = 0; v < 5; ++v)
+                            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 32 + 16 * v),
+                                         "l"(colp + e4 * 5 + 4 * v) : "memory");
+                    }
+                }
+                asm volatile("cp.async.commit_group;" ::: "memory");   // (possibly empty) one group per iteration
+            };
+            issue(gfirst, 0);
+            issue(gfirst + gstride, 1);
+            int st = 0;
+            for (int64_t g0 = gfirst; g0 < n_pad; g0 += gstride) {
+                issue(g0 + 2 * gstride, (st + 2) % kCpStages);
+                asm volatile("cp.async.wait_group 2;" ::: "memory");   // this iteration's group landed
+                const uint4* sl = slot_of(st);
+                const uint4 P = sl[0], I = sl[1];
+                uint32_t c[20];
+                if constexpr (POLICY != CACHE_POLICY_FIFO) {
+#pragma unroll
+                    for (int v = 0; v < 5; ++v) {
+                        const uint4 w = sl[2 + v];
+                        c[4 * v] = w.x; c[4 * v + 1] = w.y; c[4 * v + 2] = w.z; c[4 * v + 3] = w.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int v = 0; v < 20; ++v) c[v] = 0u;
+                }
+                st = (st + 1) % kCpStages;
+                const int64_t e4 = g0 + 4 * lane;
+                const uint32_t pm[4] = {P.x, P.y, P.z, P.w}, pid[4] = {I.x, I.y, I.z, I.w};
+                if constexpr (GRAN == CACHE_EVICT_ITEM) {
+                    sweep_items_v4<POLICY>(a, kv, lim, mode, L, e4, pm, pid, c, sh, run, kmin, lane);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        uint32_t col[CACHE_MAX_K];
+#pragma unroll
+                        for (int j = 0; j < CACHE_MAX_K; ++j) col[j] = j < 5 ? c[5 * q + j] : 0u;
+                        sel_slot<POLICY, GRAN>(a, 5, kv, mode, L, e4 + q, pm[q], pid[q], col, sh, run, kmin, lane);
+                    }
+                }
+            }
+            asm volatile("cp.async.wait_group 0;" ::: "memory");   // drain the empty tail groups
         } else if constexpr (NK5) {
             // register-fed: 7 independent 16-B loads per lane (present, ids, 5 x the column of
             // 4 consecutive slots); 128-slot groups interleaved over all warps of the grid
@@ -811,11 +880,13 @@ static cudaError_t launch_select_t(const SelArgs& a, const KMap& km, cudaStream_
         int bps = 0, dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (NK5 && kSelStaged)
+        if (NK5 && (kSelStaged || kSelCpAsync))
             cudaFuncSetAttribute(k_evict_select<POLICY, GRAN, NK5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kStages * kStageBytes);
+                                 kSelStaged ? kStages * kStageBytes : kCpRingBytes);
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_evict_select<POLICY, GRAN, NK5>, kSelThreads,
-                                                          (NK5 && kSelStaged) ? kStages * kStageBytes : 0) != cudaSuccess ||
+                                                          NK5 ? (kSelStaged ? kStages * kStageBytes
+                                                                            : (kSelCpAsync ? kCpRingBytes : 0))
+                                                              : 0) != cudaSuccess ||
             bps < 1)
             bps = 1;
         return bps * sms;
@@ -824,8 +895,9 @@ static cudaError_t launch_select_t(const SelArgs& a, const KMap& km, cudaStream_
     SelArgs aa = a;
     KMap kk = km;
     void* args[] = {&aa, &kk};
-    return cudaLaunchCooperativeKernel((const void*)k_evict_select<POLICY, GRAN, NK5>, grid, kSelThreads, args,
-                                       (NK5 && kSelStaged) ? (size_t)kStages * kStageBytes : 0, s);
+    const size_t dyn = NK5 ? (kSelStaged ? (size_t)kStages * kStageBytes : (kSelCpAsync ? (size_t)kCpRingBytes : 0))
+                           : 0;
+    return cudaLaunchCooperativeKernel((const void*)k_evict_select<POLICY, GRAN, NK5>, grid, kSelThreads, args, dyn, s);
 }
 
 cudaError_t launch_evict_select(const SelArgs& a, const KMap& km, cudaStream_t s) {
