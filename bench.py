@@ -479,10 +479,11 @@ def run_sharded(args, cfg):
                 evict_items=m_items[1:], evict_ms=m_ev[1:], dirty_removed=m_dirty[1:], insert_entries=m_dirty[1:],
                 insert_ms=m_ins[1:], round_ms=[lk + a + c for a, c in zip(m_ev[1:], m_ins[1:])],
                 lookups_per_s_incl_maintenance=b * args.steps / ((tot + sum(m_ev[1:]) + sum(m_ins[1:])) / 1e3),
-                note="per timed round, after the lookup: LCBFU eviction of 1% of the live items (8 radix-select "
-                     "passes, histograms summed over peer memory, apply + dirty-entry removal; host wall clock "
-                     "max over ranks) and the insertion of as many fresh prompts as it removed (normalise + "
-                     "slot allocation + metadata; aliased latent pool); value counts the lookups only")
+                note="per timed round, after the lookup: LCBFU eviction of 1% of the live items (N = 1: the "
+                     "fused single-launch eviction; N > 1: 8 radix-select passes with the histograms summed "
+                     "over peer memory, then apply + dirty-entry removal; host wall clock, max over ranks) and "
+                     "the insertion of as many fresh prompts as it removed (normalise + slot allocation + "
+                     "metadata; aliased latent pool); value counts the lookups only")
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
 

@@ -327,6 +327,12 @@ class NirvanaCache:
         _check(rc)
         return out
 
+    def evict_count(self, n: int, stream=None):
+        """Evict without producing the lists (cache_evict with NULL outputs): (evicted, dirty)."""
+        nd = np.zeros(1, dtype=np.int64)
+        _check(_lib.cache_evict(self._h, n, None, None, _ptr(nd), _stream(stream)))
+        return n, int(nd[0])
+
     def evict(self, n: int, stream=None, out=None, view: bool = False):
         """Returns (evicted, dirty ids).  out: optional (evicted, dirty) uint64 arrays of capacity
         >= n, reused across calls.  view=True: read-only numpy views of the library's pinned lists

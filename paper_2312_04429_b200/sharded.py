@@ -201,8 +201,10 @@ class ShardedCache:
         if n > live:
             raise B.CacheError(B.E_EVICT_RANGE, "sharded evict: n exceeds live items / entries")
         if self.comm.world == 1:   # one shard: no exchange, the fused single-launch eviction
+            if not lists:
+                return self.cache.evict_count(n)
             ev, dirty = self.cache.evict(n, view=True)
-            return (len(ev), len(dirty)) if not lists else (ev.copy(), dirty.copy())
+            return ev.copy(), dirty.copy()
         if self.push:   # histograms reduced over peer memory by the kernels themselves
             for p in range(8):
                 self.cache.push_evict_hist(n, p)
