@@ -376,6 +376,32 @@ cache_status cache_push_merge(cache_t *c, int64_t nb, int32_t topk, uint64_t *ou
                               int32_t *out_k, void *latent_out, void **out_latent_ptr, int32_t *row_status,
                               void *stream);
 
+/* Distributed FUSED eviction (round 2; replaces the 8-pass radix protocol above for sharded
+ * caches): cache_evict's single-launch algorithm cut at its histogram exchanges -- level 0 a
+ * sweep of this shard into 4,096 log bins, levels >= 1 a sweep that applies the units certain
+ * to go and compacts the chosen range's candidates (later levels sweep only those), every
+ * level's histogram summed over ranks before every rank takes the same pick; then the final
+ * apply and the ordered lists.  Typically 2 sweeps of the slot columns instead of 9.
+ * Collective, every rank with the same n (the GLOBAL number of units to evict):
+ *   cache_evict_sel_begin(c, n)
+ *   for level = 0, 1, ...:
+ *     cache_evict_sel_level(c, level, hist)     hist: device u32[4096], this rank's histogram
+ *     (sum hist over the ranks, e.g. an NCCL all-reduce)
+ *     cache_evict_sel_pick(c, level, hist_sum, &done)   host-synchronous; stop when done != 0
+ *   cache_evict_sel_apply(c, cap, ...)          outputs as cache_evict_apply (this rank's share)
+ * or, with the push arenas (cache_push_reserve), the exchange over peer memory instead:
+ *   cache_push_evict_sel_level(c, level); cache_push_evict_sel_pick(c, level, &done)
+ * (virtual ranks in one process: level on every rank, then pick on every rank).  Every rank
+ * runs the same number of levels (the picks agree).  Errors: CACHE_E_STATE out of order. */
+cache_status cache_evict_sel_begin(cache_t *c, int64_t n, void *stream);
+cache_status cache_evict_sel_level(cache_t *c, int32_t level, uint32_t *hist, void *stream);
+cache_status cache_evict_sel_pick(cache_t *c, int32_t level, const uint32_t *hist_sum, int32_t *out_done,
+                                  void *stream);
+cache_status cache_evict_sel_apply(cache_t *c, int64_t cap, uint64_t *out_evicted, int64_t *out_n,
+                                   uint64_t *out_dirty_ids, int64_t *out_n_dirty, void *stream);
+cache_status cache_push_evict_sel_level(cache_t *c, int32_t level, void *stream);
+cache_status cache_push_evict_sel_pick(cache_t *c, int32_t level, int32_t *out_done, void *stream);
+
 /* Fused distributed eviction (the radix-select histograms of cache_evict_hist / _pick without
  * a collective): pass p's histogram kernel adds its counts straight into EVERY rank's arena
  * accumulator (P2P atomics over NVLink) and publishes a per-pass epoch flag; the pick waits

@@ -84,7 +84,9 @@ EXPORTS = ("cache_default_config", "cache_create", "cache_destroy", "cache_inser
            "cache_push_scan", "cache_push_merge", "cache_push_evict_hist", "cache_push_evict_pick",
            "cache_push_evict_apply", "cache_profile_thresholds", "cache_set_thresholds", "cache_query_peek",
            "cache_push_status", "cache_set_peer_timeout", "cache_last_evicted_keys",
-           "cache_evict_view", "cache_query_submit", "cache_query_complete")
+           "cache_evict_view", "cache_query_submit", "cache_query_complete", "cache_evict_sel_begin",
+           "cache_evict_sel_level", "cache_evict_sel_pick", "cache_evict_sel_apply", "cache_push_evict_sel_level",
+           "cache_push_evict_sel_pick")
 
 
 def load_library(path: str = LIB_PATH):
@@ -101,6 +103,15 @@ def load_library(path: str = LIB_PATH):
     L.cache_query_batch_host.argtypes = [P, I64, P, I32, I32, P, P, P, P, P, P]
     L.cache_query_peek.argtypes = [P, I64, P, I32, I32, P, P, P, P, P]
     L.cache_query_peek.restype = ctypes.c_int
+    L.cache_evict_sel_begin.argtypes = [P, I64, P]
+    L.cache_evict_sel_level.argtypes = [P, I32, P, P]
+    L.cache_evict_sel_pick.argtypes = [P, I32, P, P, P]
+    L.cache_evict_sel_apply.argtypes = [P, I64, P, P, P, P, P]
+    L.cache_push_evict_sel_level.argtypes = [P, I32, P]
+    L.cache_push_evict_sel_pick.argtypes = [P, I32, P, P]
+    for fn in ("cache_evict_sel_begin", "cache_evict_sel_level", "cache_evict_sel_pick", "cache_evict_sel_apply",
+               "cache_push_evict_sel_level", "cache_push_evict_sel_pick"):
+        getattr(L, fn).restype = ctypes.c_int
     L.cache_query_submit.argtypes = [P, I32, I64, P, I32, I32, P, P]
     L.cache_query_submit.restype = ctypes.c_int
     L.cache_query_complete.argtypes = [P, I32, P, P, P, P]
@@ -452,6 +463,38 @@ class NirvanaCache:
         out = np.empty(max(int(n[0]), 1), dtype=np.uint64)
         _check(_lib.cache_last_evicted_keys(self._h, _ptr(out), int(n[0]), _ptr(n)))
         return out[: int(n[0])]
+
+    # ---- distributed fused eviction (cache_evict_sel_*) ----
+    def evict_sel_begin(self, n: int, stream=None):
+        _check(_lib.cache_evict_sel_begin(self._h, n, _stream(stream)))
+
+    def evict_sel_level(self, level: int, hist: torch.Tensor, stream=None):
+        """This rank's 4,096-bin histogram of the level into hist (cuda int32[4096])."""
+        _check(_lib.cache_evict_sel_level(self._h, level, _ptr(hist), _stream(stream)))
+
+    def evict_sel_pick(self, level: int, hist_sum: torch.Tensor, stream=None) -> bool:
+        done = np.zeros(1, dtype=np.int32)
+        _check(_lib.cache_evict_sel_pick(self._h, level, _ptr(hist_sum), _ptr(done), _stream(stream)))
+        return bool(done[0])
+
+    def evict_sel_apply(self, cap: int, stream=None, lists: bool = True):
+        """This rank's share: (evicted, dirty) lists, or (n evicted, n dirty) with lists=False."""
+        ev = np.empty(max(cap, 1), dtype=np.uint64) if lists else None
+        dirty = np.empty(max(cap, 1), dtype=np.uint64) if lists else None
+        n = np.zeros(1, dtype=np.int64)
+        nd = np.zeros(1, dtype=np.int64)
+        _check(_lib.cache_evict_sel_apply(self._h, cap, _ptr(ev), _ptr(n), _ptr(dirty), _ptr(nd), _stream(stream)))
+        if not lists:
+            return int(n[0]), int(nd[0])
+        return ev[: int(n[0])], dirty[: int(nd[0])]
+
+    def push_evict_sel_level(self, level: int, stream=None):
+        _check(_lib.cache_push_evict_sel_level(self._h, level, _stream(stream)))
+
+    def push_evict_sel_pick(self, level: int, stream=None) -> bool:
+        done = np.zeros(1, dtype=np.int32)
+        _check(_lib.cache_push_evict_sel_pick(self._h, level, _ptr(done), _stream(stream)))
+        return bool(done[0])
 
     def push_status(self, stream=None):
         """Synchronise the stream; CacheError(E_NCCL) if a peer wait of this handle timed out."""

@@ -27,7 +27,7 @@ thread_local std::string g_err = "no error";
 // offsets from the descriptor): flags | CTA counters | inv-norms | statuses | record inbox |
 // bf16 query rows (rows padded to a multiple of 128 for the scan's TMA boxes).
 struct ArenaLayout {
-    size_t qflag, rflag, done, eflag, invq, qstat, inbox, qg, ehist, total;
+    size_t qflag, rflag, done, eflag, invq, qstat, inbox, qg, ehist, esel, total;
     int64_t rows;   // padded global rows
 };
 ArenaLayout arena_layout(int world, int64_t max_nb, int topk, int dim) {
@@ -44,6 +44,7 @@ ArenaLayout arena_layout(int world, int64_t max_nb, int topk, int dim) {
     L.inbox = off; off = al(off + (size_t)world * max_nb * topk * sizeof(cache_shard_rec));
     L.qg = off;    off = al(off + (size_t)L.rows * dim * 2);
     L.ehist = off; off = al(off + 8 * 256 * 4);   // global eviction histogram per radix pass
+    L.esel = off;  off = al(off + (size_t)kSelMaxLevels * kSelBins * 4);   // fused eviction: per level
     L.total = off;
     return L;
 }
@@ -237,6 +238,12 @@ struct cache_t {
     DevBuf<unsigned long long> eout;     // kernel-sorted evicted keys: full | masked
     int64_t last_sel[4] = {0, 0, 0, 0};  // levels, full sweeps, compaction level, candidates
     int64_t cand_cap_override = -1;      // test hook (cache_debug_set_evict_cand_cap); -1 = auto
+    // distributed fused eviction (cache_evict_sel_*): the kernel arguments across the phases
+    SelArgs dsel{};
+    int dsel_level = -1;                 // next level expected (-1: none begun)
+    bool dsel_push = false;
+    DevBuf<SelState> dstate;
+    DevBuf<uint32_t> dlhist;             // this rank's local level histograms [levels][4096]
     int64_t last_ev_n = 0;               // unit keys of the last eviction (sorted, in ekey), in order
     int64_t last_nd = 0;
     unsigned long long* ev_full = nullptr;   // device: the sorted full keys of the last eviction
@@ -459,6 +466,7 @@ cache_status cache_destroy(cache_t* c) {
     c->hev_did.release();
     c->epool.release(); c->edirty.release(); c->edid.release();
     c->ckey.release(); c->cslot.release(); c->selws.release(); c->ebits.release(); c->eout.release();
+    c->dstate.release(); c->dlhist.release();
     c->abortw.release();
     if (c->errw_h) cudaFreeHost(c->errw_h);
     delete c;
@@ -1602,18 +1610,13 @@ cache_status cache_evict_view(cache_t* c, int64_t n, const uint64_t** out_evicte
     return CACHE_OK;
 }
 
-static cache_status evict_impl(cache_t* c, int64_t n, bool want_ev, bool want_did, uint64_t* out_evicted,
-                               uint64_t* out_dirty_ids, int64_t* out_n_dirty, void* stream) {
-    if (!c) return fail(CACHE_E_INVALID_ARG, "cache_evict: null cache");
-    if (n < 0) return fail(CACHE_E_INVALID_ARG, "cache_evict: n < 0");
+// Workspaces, zeroed scratch and kernel arguments of one fused eviction.  n_sel: the number of
+// units the selection evicts (globally, for a distributed eviction); n_loc: a bound on this
+// cache's share (its list capacities).
+static cache_status evict_setup(cache_t* c, int64_t n_sel, int64_t n_loc, bool want_ev, SelArgs& a, cudaStream_t s) {
     const bool entry_mode = c->km.gran == CACHE_EVICT_ENTRY;
-    if (entry_mode ? n > c->live_entries : n > c->live_items)
-        return fail(CACHE_E_EVICT_RANGE, "cache_evict: n exceeds live items (entries in entry mode)");
-    if (out_n_dirty) *out_n_dirty = 0;
-    if (n == 0) return CACHE_OK;
-    DeviceGuard g(c->device);
-    cudaStream_t s = (cudaStream_t)stream;
-    // exactly n units go; dirty entries: n in entry mode, <= min(n, live entries) in item mode
+    const int64_t n = std::max<int64_t>(1, n_loc);
+    // dirty entries: n in entry mode, <= min(n, live entries) in item mode
     const int64_t dbound = std::max<int64_t>(1, std::min<int64_t>(n, c->live_entries));
     const int64_t pbound = entry_mode ? n * c->num_k : n;
     CK(evict_lists(c, n, dbound, pbound));
@@ -1633,8 +1636,8 @@ static cache_status evict_impl(cache_t* c, int64_t n, bool want_ev, bool want_di
     const int64_t w_ev = want_ev ? kEvBitsWords : 0;   // evicted keys spanning < 2^23 values: bitmap-sorted
     CK(c->ebits.ensure_grow(w_slot + w_id + w_pool + w_ev));
     CK(cudaMemsetAsync(c->ebits.p, 0, (size_t)(w_slot + w_id + w_pool + w_ev) * 4, s));
-    CK(c->eout.ensure_grow(2 * std::max<int64_t>(n, 1)));
-    SelArgs a{};
+    CK(c->eout.ensure_grow(2 * n));
+    a = SelArgs{};
     a.present = c->present;
     a.fcnt = c->fcnt;
     a.lastacc = c->lastacc;
@@ -1642,7 +1645,7 @@ static cache_status evict_impl(cache_t* c, int64_t n, bool want_ev, bool want_di
     a.lslot = c->lslot;
     a.inv_e = c->inv_e;
     a.n_slots = c->hwm;
-    a.n = (unsigned long long)n;
+    a.n = (unsigned long long)n_sel;
     a.hist = reinterpret_cast<uint32_t*>(c->selws.p);
     a.cand_key = c->ckey.p;
     a.cand_slot = c->cslot.p;
@@ -1665,9 +1668,30 @@ static cache_status evict_impl(cache_t* c, int64_t n, bool want_ev, bool want_di
     a.ev_bits = w_ev ? c->ebits.p + w_slot + w_id + w_pool : nullptr;
     a.ev_bits_words = w_ev;
     a.ev_sorted = c->eout.p;
-    a.ev_masked = c->eout.p + std::max<int64_t>(n, 1);
+    a.ev_masked = c->eout.p + n;
     a.ev_mask = entry_mode ? 0xFFFFFFFFull : ((1ull << 35) - 1);
     a.out = so;
+    a.phase = kPhaseAll;
+    return CACHE_OK;
+}
+
+static cache_status evict_impl(cache_t* c, int64_t n, bool want_ev, bool want_did, uint64_t* out_evicted,
+                               uint64_t* out_dirty_ids, int64_t* out_n_dirty, void* stream) {
+    if (!c) return fail(CACHE_E_INVALID_ARG, "cache_evict: null cache");
+    if (n < 0) return fail(CACHE_E_INVALID_ARG, "cache_evict: n < 0");
+    const bool entry_mode = c->km.gran == CACHE_EVICT_ENTRY;
+    if (entry_mode ? n > c->live_entries : n > c->live_items)
+        return fail(CACHE_E_EVICT_RANGE, "cache_evict: n exceeds live items (entries in entry mode)");
+    if (out_n_dirty) *out_n_dirty = 0;
+    if (n == 0) return CACHE_OK;
+    DeviceGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    SelArgs a;
+    cache_status rs = evict_setup(c, n, n, want_ev, a, s);
+    if (rs != CACHE_OK) return rs;
+    SelOut* so = a.out;
+    const int64_t dbound = std::max<int64_t>(1, std::min<int64_t>(n, c->live_entries));
+    const int64_t pbound = entry_mode ? n * c->num_k : n;
     const bool trace = evict_trace();
     double t0 = trace ? now_us() : 0.0, t1 = 0.0, t2 = 0.0, tf[3] = {0, 0, 0};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -1711,6 +1735,142 @@ static cache_status evict_impl(cache_t* c, int64_t n, bool want_ev, bool want_di
                      tf[2] - t0, h.levels, h.full_sweeps, h.compact_level, h.cnt[3], bitlen(h.T - kmin), (long long)nd);
     }
     return r;
+}
+
+// ---- distributed fused eviction (SURVEY 8(e) a9 across shards): the single-cache kernel's
+// levels, one launch each, with the 4,096-bin histograms summed over ranks between them ----
+static cache_status sel_launch(cache_t* c, int phase, uint32_t* level_hist, cudaStream_t s) {
+    SelArgs a = c->dsel;
+    a.phase = phase;
+    a.level_hist = level_hist;
+    CK(launch_evict_select(a, c->km, s));
+    c->launches++;
+    return CACHE_OK;
+}
+
+cache_status cache_evict_sel_begin(cache_t* c, int64_t n, void* stream) {
+    if (!c || n < 1) return fail(CACHE_E_INVALID_ARG, "cache_evict_sel_begin: bad argument");
+    if (peer_failed(c)) return peer_fail("cache_evict_sel_begin");
+    DeviceGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool entry_mode = c->km.gran == CACHE_EVICT_ENTRY;
+    const int64_t units = entry_mode ? c->live_entries : c->live_items;
+    cache_status r = evict_setup(c, n, std::min<int64_t>(n, units), /*want_ev=*/true, c->dsel, s);
+    if (r != CACHE_OK) return r;
+    CK(c->dstate.ensure(1));
+    CK(cudaMemsetAsync(c->dstate.p, 0, sizeof(SelState), s));
+    CK(c->dlhist.ensure((size_t)kSelMaxLevels * kSelBins));
+    CK(cudaMemsetAsync(c->dlhist.p, 0, (size_t)kSelMaxLevels * kSelBins * 4, s));
+    c->dsel.state = c->dstate.p;
+    c->dsel_level = 0;
+    c->dsel_push = false;
+    return CACHE_OK;
+}
+
+cache_status cache_evict_sel_level(cache_t* c, int32_t level, uint32_t* hist, void* stream) {
+    if (!c || !hist) return fail(CACHE_E_INVALID_ARG, "cache_evict_sel_level: bad argument");
+    if (level != c->dsel_level || level >= kSelMaxLevels)
+        return fail(CACHE_E_STATE, "cache_evict_sel_level: levels out of order (begin, then level / pick 0, 1, ...)");
+    DeviceGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    CK(cudaMemsetAsync(hist, 0, (size_t)kSelBins * 4, s));
+    return sel_launch(c, level == 0 ? kPhaseL0 : kPhaseLevel, hist, s);
+}
+
+static cache_status sel_pick_done(cache_t* c, int32_t level, const uint32_t* ghist, int32_t* out_done, cudaStream_t s) {
+    CK(launch_evict_dpick(c->dsel, ghist, level, s));
+    c->launches++;
+    SelState h{};
+    CK(cudaMemcpyAsync(&h, c->dstate.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (out_done) *out_done = (int32_t)(h.done | h.fail);
+    c->dsel_level = level + 1;
+    return CACHE_OK;
+}
+
+cache_status cache_evict_sel_pick(cache_t* c, int32_t level, const uint32_t* ghist, int32_t* out_done, void* stream) {
+    if (!c || !ghist) return fail(CACHE_E_INVALID_ARG, "cache_evict_sel_pick: bad argument");
+    if (level + 1 != c->dsel_level + 1 || level != c->dsel_level)
+        return fail(CACHE_E_STATE, "cache_evict_sel_pick: call after cache_evict_sel_level of the same level");
+    DeviceGuard g(c->device);
+    return sel_pick_done(c, level, ghist, out_done, (cudaStream_t)stream);
+}
+
+cache_status cache_evict_sel_apply(cache_t* c, int64_t cap, uint64_t* out_evicted, int64_t* out_n,
+                                   uint64_t* out_dirty_ids, int64_t* out_n_dirty, void* stream) {
+    if (!c || cap < 0) return fail(CACHE_E_INVALID_ARG, "cache_evict_sel_apply: bad argument");
+    if (c->dsel_level < 1) return fail(CACHE_E_STATE, "cache_evict_sel_apply: no selection (begin, level/pick 0..)");
+    if (peer_failed(c)) return peer_fail("cache_evict_sel_apply");
+    DeviceGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool entry_mode = c->km.gran == CACHE_EVICT_ENTRY;
+    c->dsel_level = -1;
+    cache_status r = sel_launch(c, kPhaseFinal, nullptr, s);
+    if (r != CACHE_OK) return r;
+    SelOut h{};
+    CK(cudaMemcpyAsync(&h, c->dsel.out, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const int64_t n = (int64_t)h.cnt[0], nd = (int64_t)h.cnt[1];
+    const int64_t nfreed = entry_mode ? (int64_t)h.cnt[2] : n;
+    if (out_n) *out_n = n;
+    c->last_sel[0] = h.levels;
+    c->last_sel[1] = h.full_sweeps;
+    c->last_sel[2] = h.compact_level;
+    c->last_sel[3] = (int64_t)h.cnt[3];
+    if (h.err || n > cap || nd > cap || (unsigned long long)n > c->dsel.ev_cap)
+        return fail(CACHE_E_STATE, "cache_evict_sel_apply: selection failed or more evictions than the output "
+                                   "capacity (ranks passed different n?); handle state undefined");
+    const unsigned long long kmin = ~h.kmin_inv;
+    return evict_finish(c, n, nd, nfreed, kmin, bitlen(h.T - kmin), true, true, out_evicted, out_dirty_ids, out_n_dirty,
+                        s, nullptr, /*presorted=*/true, h.ev_sorted ? c->dsel.ev_masked : nullptr,
+                        h.ev_sorted ? c->dsel.ev_sorted : nullptr);
+}
+
+// push variants: the level histogram goes into every rank's arena over NVLink (P2P atomics) and
+// the pick waits for every rank's level flag, then reads the summed histogram from its own arena
+cache_status cache_push_evict_sel_level(cache_t* c, int32_t level, void* stream) {
+    if (!c) return fail(CACHE_E_INVALID_ARG, "cache_push_evict_sel_level: null cache");
+    if (peer_failed(c)) return peer_fail("cache_push_evict_sel_level");
+    if (!c->push_ok) return fail(CACHE_E_STATE, "cache_push_evict_sel_level: no push arenas");
+    if (level != c->dsel_level || level >= kSelMaxLevels)
+        return fail(CACHE_E_STATE, "cache_push_evict_sel_level: levels out of order");
+    DeviceGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (level == 0) c->evict_epoch++;
+    c->dsel_push = true;
+    uint32_t* local = c->dlhist.p + (size_t)level * kSelBins;
+    cache_status r = sel_launch(c, level == 0 ? kPhaseL0 : kPhaseLevel, local, s);
+    if (r != CACHE_OK) return r;
+    const ArenaLayout L = arena_layout(c->world, c->arena_nb, c->arena_topk, c->dim);
+    PushHist ph{};
+    for (int q = 0; q < c->world; ++q) ph.dst[q] = (unsigned int*)(c->peer_arena[q] + L.esel) + (size_t)level * kSelBins;
+    ph.world = c->world;
+    PushSignal sig = push_signal_of(c, L.eflag + (size_t)level * kMaxWorld * 4, 2);
+    sig.epoch = c->evict_epoch;
+    launch_push_hist_bins(local, kSelBins, ph, sig, s);
+    c->launches++;
+    CK(cudaGetLastError());
+    return CACHE_OK;
+}
+
+cache_status cache_push_evict_sel_pick(cache_t* c, int32_t level, int32_t* out_done, void* stream) {
+    if (!c) return fail(CACHE_E_INVALID_ARG, "cache_push_evict_sel_pick: null cache");
+    if (peer_failed(c)) return peer_fail("cache_push_evict_sel_pick");
+    if (!c->push_ok || level != c->dsel_level || !c->dsel_push)
+        return fail(CACHE_E_STATE, "cache_push_evict_sel_pick: call after cache_push_evict_sel_level of the same level");
+    DeviceGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const ArenaLayout L = arena_layout(c->world, c->arena_nb, c->arena_topk, c->dim);
+    wait_flags(c, (const uint32_t*)(c->arena + L.eflag + (size_t)level * kMaxWorld * 4), c->evict_epoch, s);
+    c->launches++;
+    uint32_t* acc = (uint32_t*)(c->arena + L.esel) + (size_t)level * kSelBins;
+    cache_status r = sel_pick_done(c, level, acc, out_done, s);
+    if (r != CACHE_OK) return r;
+    // the summed histogram is consumed: clear it for this level of the next eviction (a peer adds
+    // into it again only after this rank has published that eviction's earlier levels)
+    CK(cudaMemsetAsync(acc, 0, (size_t)kSelBins * 4, s));
+    if (peer_failed(c)) return peer_fail("cache_push_evict_sel_pick");
+    return CACHE_OK;
 }
 
 cache_status cache_evict_apply(cache_t* c, const cache_evict_state* st, int64_t cap, uint64_t* out_evicted,

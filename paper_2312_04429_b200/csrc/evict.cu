@@ -783,13 +783,47 @@ __global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : (kSelCp
         run.flush(sh);
     };
 
-    // ---- level 0: log-bin histogram + min key ----
-    SelLevel L{0ull, 0ull, 64, 0, false, 0ull, 0ull};
-    clear_sh();
-    unsigned long long kmin = ~0ull;
-    full_sweep(kSweepL0, L, kmin);
-    flush_sh(a.hist);
-    {
+    // final apply (the candidates <= T, or one more full sweep), then the ordered lists
+    auto finish = [&](SelLevel L, bool compacted, int64_t ncand, bool fail, int level, int full,
+                      int compact_level) {
+        unsigned long long kmin_unused = ~0ull;
+        L.T = L.lo + ((1ull << L.w) - 1ull);
+        if (!fail) {
+            if (compacted) {
+                cand_sweep(kSweepFinal, L, ncand);
+            } else {
+                full_sweep(kSweepFinal, L, kmin_unused);
+                ++full;
+            }
+        }
+        grid.sync();   // every apply is done: the bitmaps and the evicted-key list are complete
+        bool ev_sorted = false;
+        if (!fail) {
+            // evicted keys (unique): marked in the bitmap over [kb, kb + ev_lim) as they went;
+            // sorted by the compaction below unless one fell beyond it (then the host side sorts)
+            const unsigned long long kb = L.kb;
+            ev_sorted = L.ev_lim && L.T >= kb && __ldcg(&a.out->ev_over) == 0u;
+            const BitJob jobs[4] = {
+                BitJob{a.dslot_bits, a.dslot_words, a.dirty_slot, 1ull, 0ull, nullptr, 0ull},
+                BitJob{a.did_bits, a.did_words, a.dirty_id, (unsigned long long)a.world, (unsigned long long)a.rank,
+                       nullptr, 0ull},
+                BitJob{a.pool_bits, a.pool_words, a.ev_pool, 1ull, 0ull, nullptr, 0ull},
+                // every evicted key lies in [kb, kb + ev_lim) (no overflow); T itself may lie beyond
+                BitJob{ev_sorted ? a.ev_bits : nullptr,
+                       ev_sorted ? (int64_t)min((L.T - kb) / 32 + 1, (unsigned long long)a.ev_bits_words) : 0,
+                       a.ev_sorted, 1ull, kb, a.ev_masked, a.ev_mask}};
+            compact_bitmaps<4>(jobs, a.part, grid);
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            a.out->T = L.T;
+            a.out->levels = (uint32_t)level;
+            a.out->full_sweeps = (uint32_t)full;
+            a.out->compact_level = (uint32_t)compact_level;
+            a.out->err = fail ? 1u : 0u;
+            a.out->ev_sorted = ev_sorted ? 1u : 0u;
+        }
+    };
+    auto kmin_to_global = [&](unsigned long long kmin) {
         unsigned long long inv = ~kmin;
 #pragma unroll
         for (int o = 16; o >= 1; o >>= 1) {
@@ -797,7 +831,43 @@ __global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : (kSelCp
             inv = y > inv ? y : inv;
         }
         if (lane == 0 && inv) atomicMax(&a.out->kmin_inv, inv);
+    };
+
+    // ---- distributed phases: one level per launch, the state in a.state ----
+    if (a.phase == kPhaseL0) {
+        SelLevel L{0ull, 0ull, 64, 0, false, 0ull, 0ull};
+        clear_sh();
+        unsigned long long kmin = ~0ull;
+        full_sweep(kSweepL0, L, kmin);
+        flush_sh(a.level_hist);
+        kmin_to_global(kmin);
+        return;
     }
+    if (a.phase == kPhaseLevel || a.phase == kPhaseFinal) {
+        const SelState S = *a.state;
+        SelLevel L{S.lo, 0ull, S.w, S.shift, false, S.kb, S.ev_lim};
+        if (a.phase == kPhaseFinal) {
+            finish(L, S.compacted != 0u, S.ncand, S.fail != 0u, (int)S.level, (int)S.full, (int)S.compact_level);
+            return;
+        }
+        if (S.done) return;
+        L.compact = !S.compacted && S.pcnt <= a.cand_cap;
+        clear_sh();
+        unsigned long long kmin = ~0ull;
+        if (!S.compacted) full_sweep(kSweepLevel, L, kmin);
+        else cand_sweep(kSweepLevel, L, S.ncand);
+        flush_sh(a.level_hist);
+        return;
+    }
+
+    // ---- single cache: the whole selection in this launch ----
+    // level 0: log-bin histogram + min key
+    SelLevel L{0ull, 0ull, 64, 0, false, 0ull, 0ull};
+    clear_sh();
+    unsigned long long kmin = ~0ull;
+    full_sweep(kSweepL0, L, kmin);
+    flush_sh(a.hist);
+    kmin_to_global(kmin);
     grid.sync();
     L.kb = ~__ldcg(&a.out->kmin_inv);
     L.ev_lim = a.ev_bits ? (unsigned long long)a.ev_bits_words * 32ull : 0ull;
@@ -837,40 +907,60 @@ __global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : (kSelCp
         done = p.cnt == rem || L.w == 0;
         ++level;
     }
-    L.T = L.lo + ((1ull << L.w) - 1ull);
-    if (!fail) {
-        if (compacted) {
-            cand_sweep(kSweepFinal, L, ncand);
-        } else {
-            full_sweep(kSweepFinal, L, kmin);
-            ++full;
+    finish(L, compacted, ncand, fail, level, full, compact_level);
+}
+
+// Pick of one distributed level (one CTA): the single-cache kernel's pick arithmetic on the
+// rank-summed histogram, applied to the state in device memory (every rank reaches the same
+// state from the same histogram).
+__global__ void __launch_bounds__(kSelThreads) k_evict_dpick(SelArgs a, const uint32_t* ghist, int level) {
+    __shared__ SelState S;
+    if (threadIdx.x == 0) S = *a.state;
+    __syncthreads();
+    if (level > 0 && (S.done || S.fail)) return;   // block-uniform
+    if (level == 0) {
+        const PickRes p = sel_pick(ghist, a.n);
+        if (threadIdx.x == 0) {
+            S.kb = ~__ldcg(&a.out->kmin_inv);   // this rank's own min key: the base of its lists
+            S.ev_lim = a.ev_bits ? (unsigned long long)a.ev_bits_words * 32ull : 0ull;
+            S.fail = p.bin >= (uint32_t)kSelBins;
+            S.rem = a.n - p.before;
+            S.pcnt = p.cnt;
+            sel_bin0_range(p.bin, S.lo, S.w);
+            S.done = S.fail || p.cnt == S.rem || S.w == 0;
+            S.compacted = 0u;
+            S.ncand = 0;
+            S.level = 1u;
+            S.full = 1u;
+            S.compact_level = 0u;
+        }
+    } else {
+        // this level's sweep compacted iff the state allowed it before the sweep (same rule)
+        const bool compacted_now = !S.compacted && S.pcnt <= a.cand_cap;
+        const PickRes p = sel_pick(ghist, S.rem);
+        if (threadIdx.x == 0) {
+            if (!S.compacted) S.full++;
+            if (compacted_now) {
+                S.compacted = 1u;
+                S.ncand = (long long)__ldcg(&a.out->cnt[3]);
+                S.compact_level = (uint32_t)level;
+            }
+            if (p.bin >= (uint32_t)kSelBins || S.level + 1 >= (uint32_t)kSelMaxLevels) {
+                S.fail = 1u;
+                S.done = 1u;
+            } else {
+                S.lo += (unsigned long long)p.bin << S.shift;
+                S.w = S.shift;
+                S.rem -= p.before;
+                S.pcnt = p.cnt;
+                S.done = p.cnt == S.rem || S.w == 0;
+                S.level++;
+            }
         }
     }
-    grid.sync();   // every apply is done: the bitmaps and the evicted-key list are complete
-    bool ev_sorted = false;
-    if (!fail) {
-        // evicted keys (unique): marked in the bitmap over [kb, kb + ev_lim) as they went; sorted
-        // by the compaction below unless one fell beyond it (then the host side sorts the list)
-        const unsigned long long kb = L.kb;
-        ev_sorted = L.ev_lim && L.T >= kb && __ldcg(&a.out->ev_over) == 0u;
-        const BitJob jobs[4] = {
-            BitJob{a.dslot_bits, a.dslot_words, a.dirty_slot, 1ull, 0ull, nullptr, 0ull},
-            BitJob{a.did_bits, a.did_words, a.dirty_id, (unsigned long long)a.world, (unsigned long long)a.rank,
-                   nullptr, 0ull},
-            BitJob{a.pool_bits, a.pool_words, a.ev_pool, 1ull, 0ull, nullptr, 0ull},
-            // every evicted key lies in [kb, kb + ev_lim) (no overflow); T itself may lie beyond
-            BitJob{ev_sorted ? a.ev_bits : nullptr,
-                   ev_sorted ? (int64_t)min((L.T - kb) / 32 + 1, (unsigned long long)a.ev_bits_words) : 0,
-                   a.ev_sorted, 1ull, kb, a.ev_masked, a.ev_mask}};
-        compact_bitmaps<4>(jobs, a.part, grid);
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        a.out->T = L.T;
-        a.out->levels = (uint32_t)level;
-        a.out->full_sweeps = (uint32_t)full;
-        a.out->compact_level = (uint32_t)compact_level;
-        a.out->err = fail ? 1u : 0u;
-        a.out->ev_sorted = ev_sorted ? 1u : 0u;
+    if (threadIdx.x == 0) {
+        if (!S.done) S.shift = S.w - (S.w < 12 ? S.w : 12);   // the next level's digit
+        *a.state = S;
     }
 }
 
@@ -898,6 +988,11 @@ static cudaError_t launch_select_t(const SelArgs& a, const KMap& km, cudaStream_
     const size_t dyn = NK5 ? (kSelStaged ? (size_t)kStages * kStageBytes : (kSelCpAsync ? (size_t)kCpRingBytes : 0))
                            : 0;
     return cudaLaunchCooperativeKernel((const void*)k_evict_select<POLICY, GRAN, NK5>, grid, kSelThreads, args, dyn, s);
+}
+
+cudaError_t launch_evict_dpick(const SelArgs& a, const uint32_t* ghist, int level, cudaStream_t s) {
+    k_evict_dpick<<<1, kSelThreads, 0, s>>>(a, ghist, level);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_evict_select(const SelArgs& a, const KMap& km, cudaStream_t s) {

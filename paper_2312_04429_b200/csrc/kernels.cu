@@ -868,6 +868,23 @@ void launch_evict_hist_push(const uint32_t* present, const uint32_t* fcnt, const
 #undef NV_HISTP
 }
 
+// Distributed fused eviction: this rank's 4,096-bin level histogram added into every rank's
+// arena accumulator (P2P atomics over NVLink), then the grid publishes the level's epoch flag.
+__global__ void __launch_bounds__(256) k_push_hist_bins(const uint32_t* __restrict__ local, int nbins, PushHist ph,
+                                                        PushSignal sig) {
+    if (push_aborted(sig)) return;
+    for (int i = blockIdx.x * 256 + threadIdx.x; i < nbins; i += gridDim.x * 256) {
+        const uint32_t v = local[i];
+        if (v)
+            for (int r = 0; r < ph.world; ++r) atomicAdd(ph.dst[r] + i, v);
+    }
+    push_signal(sig);
+}
+
+void launch_push_hist_bins(const uint32_t* local, int nbins, const PushHist& ph, const PushSignal& sig, cudaStream_t s) {
+    k_push_hist_bins<<<(nbins + 255) / 256, 256, 0, s>>>(local, nbins, ph, sig);
+}
+
 void launch_evict_pick(unsigned int* hist, EvictState* st, int pass, cudaStream_t s) {
     k_evict_pick<<<1, 256, 0, s>>>(hist, st, 56 - 8 * pass);
 }

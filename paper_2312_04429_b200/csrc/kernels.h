@@ -124,6 +124,17 @@ struct SelOut {
     uint32_t ev_sorted, ev_over;  // evicted keys emitted sorted (bitmap path) / one fell beyond the bitmap
 };
 constexpr int kSelBins = 4096, kSelMaxLevels = 8;
+// Selection state between the host-driven phases of the DISTRIBUTED fused eviction (each rank
+// sweeps its shard, the 4,096-bin histograms are summed over ranks between phases, every rank
+// picks identically).  Device memory, one per cache.
+struct SelState {
+    unsigned long long lo, T, kb, ev_lim;   // the SelLevel of the current level
+    int w, shift, compact, pad0;
+    unsigned long long rem, pcnt;           // rank wanted inside [lo, lo + 2^w), keys in it (global)
+    long long ncand;                        // this rank's compacted candidates
+    uint32_t done, fail, compacted, level, full, compact_level, pad1, pad2;
+};
+enum { kPhaseAll = 0, kPhaseL0 = 1, kPhaseLevel = 2, kPhaseFinal = 3 };
 struct SelArgs {
     uint32_t* present;
     uint32_t* fcnt;
@@ -156,8 +167,16 @@ struct SelArgs {
     unsigned long long* ev_masked;     // the reported values (key & ev_mask), ascending
     unsigned long long ev_mask;
     SelOut* out;
+    // distributed phases (phase != kPhaseAll): the state, and this phase's LOCAL histogram
+    // (zeroed by the caller; summed over ranks before the pick)
+    int phase;
+    SelState* state;
+    uint32_t* level_hist;
 };
 cudaError_t launch_evict_select(const SelArgs& a, const KMap& km, cudaStream_t s);
+// The pick of one distributed level from the rank-summed histogram ghist (every rank runs it
+// with the same ghist, so every rank reaches the same state).
+cudaError_t launch_evict_dpick(const SelArgs& a, const uint32_t* ghist, int level, cudaStream_t s);
 
 // Cache-selector profiling (Alg. 2): per profiling query i with a live nearest entry
 // (rec[i].key != 0), s_i = clamp(t_i * inv_q[i]); for every K_j with quality[j*b + i] <= alpha,
@@ -235,6 +254,7 @@ struct PushHist {
     unsigned int* dst[kMaxWorld];
     int world;
 };
+void launch_push_hist_bins(const uint32_t* local, int nbins, const PushHist& ph, const PushSignal& sig, cudaStream_t s);
 void launch_evict_hist_push(const uint32_t* present, const uint32_t* fcnt, const uint32_t* lastacc,
                             const uint32_t* ids, int64_t n_slots, const KMap& km, const EvictState* st, int pass,
                             const PushHist& ph, const PushSignal& sig, cudaStream_t s);

@@ -11,9 +11,12 @@ collectives (torch.distributed / NCCL over NVLink, or in-process copies for virt
           -> cache_query_merge for the rank's own rows: merge under (score desc, id asc),
              Fig. 11 + holes, and the winning state copied straight out of the OWNER's latent
              pool over NVLink (peer pointers from CUDA IPC), access counted on the owner's f
-  evict   8 radix passes: per-rank key histograms (cache_evict_hist) summed with an
-          all-reduce, digit picked identically everywhere (cache_evict_pick), then each rank
-          applies the global threshold to its own items (cache_evict_apply)
+  evict   the fused eviction's levels (cache_evict_sel_*): per rank a sweep of its shard into a
+          4,096-bin histogram (level 0: log bins; later levels: 12-bit digits, applying the units
+          certain to go and compacting the candidates), the histograms summed over ranks (an
+          all-reduce, or P2P atomics into every rank's arena), the same pick on every rank; then
+          each rank applies the global threshold to its own units.  Round 1's 8-pass radix
+          protocol (cache_evict_hist / _pick / _apply) stays selectable (evict_protocol).
 
 Because a query's answer is a max over shards under a total order and ids are global, the
 results are identical to one unsharded cache (tested with virtual ranks on one GPU).
@@ -114,6 +117,8 @@ def _desc_from_bytes(b: bytes) -> B.PeerDesc:
 class ShardedCache:
     """One rank's handle of an entry-sharded cache (one process per GPU)."""
 
+    evict_protocol = "levels"   # or "radix8": round 1's 8-pass radix-select protocol
+
     def __init__(self, comm: TorchComm, entry_capacity: int, latent_capacity: int | None = None,
                  push_max_nb: int = 0, push_max_topk: int = 1, **kw):
         """push_max_nb > 0: reserve the exchange arena for the fused push path (query_into
@@ -205,7 +210,22 @@ class ShardedCache:
                 return self.cache.evict_count(n)
             ev, dirty = self.cache.evict(n, view=True)
             return ev.copy(), dirty.copy()
-        if self.push:   # histograms reduced over peer memory by the kernels themselves
+        if self.evict_protocol == "levels":   # the fused levels, histograms summed between them
+            cap = max(1, min(n, self.cache.evict_units))
+            self.cache.evict_sel_begin(n)
+            for level in range(8):
+                if self.push:   # summed over peer memory by the kernels themselves
+                    self.cache.push_evict_sel_level(level)
+                    done = self.cache.push_evict_sel_pick(level)
+                else:
+                    hist = torch.empty(4096, dtype=torch.int32, device="cuda")
+                    self.cache.evict_sel_level(level, hist)
+                    self.comm.all_reduce_sum(hist)
+                    done = self.cache.evict_sel_pick(level, hist)
+                if done:
+                    break
+            res = self.cache.evict_sel_apply(cap, lists=lists)
+        elif self.push:   # round 1's 8-pass radix protocol, histograms over peer memory
             for p in range(8):
                 self.cache.push_evict_hist(n, p)
                 self.cache.push_evict_pick(p)
@@ -227,6 +247,8 @@ class VirtualShards:
     """P shards of one cache held by ONE process on one GPU (virtual ranks): the same kernels
     and the same merge/P2P code path as ShardedCache, with collectives replaced by copies.
     Used to test sharding invariance on a single B200."""
+
+    evict_protocol = "levels"   # or "radix8"
 
     def __init__(self, world: int, entry_capacity: int, latent_capacity: int | None = None,
                  push_max_nb: int = 0, push_max_topk: int = 1, **kw):
@@ -276,6 +298,28 @@ class VirtualShards:
         live = sum(c.evict_units for c in self.caches)
         if n > live:
             raise B.CacheError(B.E_EVICT_RANGE, "sharded evict: n exceeds live items / entries")
+        if self.evict_protocol == "levels":   # the fused levels (one stream: level on every rank, then picks)
+            caps = [max(1, min(n, c.evict_units)) for c in self.caches]
+            for c in self.caches:
+                c.evict_sel_begin(n)
+            for level in range(8):
+                if self.push:
+                    for c in self.caches:
+                        c.push_evict_sel_level(level)
+                    dones = [c.push_evict_sel_pick(level) for c in self.caches]
+                else:
+                    hists = [torch.empty(4096, dtype=torch.int32, device="cuda") for _ in self.caches]
+                    for c, h in zip(self.caches, hists):
+                        c.evict_sel_level(level, h)
+                    tot = torch.stack(hists).sum(0).to(torch.int32)
+                    dones = [c.evict_sel_pick(level, tot) for c in self.caches]
+                assert len(set(dones)) == 1, "ranks disagree on the selection (internal error)"
+                if dones[0]:
+                    break
+            res = [c.evict_sel_apply(cap) for c, cap in zip(self.caches, caps)]
+            keys = [c.last_evicted_keys().tolist() for c in self.caches]
+            return (_merge_evicted(keys, self.caches[0]),
+                    np.array(sorted(x for r in res for x in r[1].tolist()), dtype=np.uint64))
         if self.push:   # one stream: pass p's histogram on every rank, then every rank's pick
             for p in range(8):
                 for c in self.caches:

@@ -167,3 +167,59 @@ def test_evict_view_and_keys(oracle_mod, gran):
     mask = np.uint64(0xFFFFFFFF) if gran else np.uint64((1 << 35) - 1)
     assert len(keys) == len(ev) and np.all(np.diff(keys.astype(np.float64)) >= 0)
     assert np.array_equal(keys & mask, ev)
+
+
+@pytest.mark.parametrize("world,push", [(2, True), (3, False), (4, True)])
+@pytest.mark.parametrize("policy,gran", [(0, 0), (1, 0), (2, 1), (3, 0)])
+@pytest.mark.parametrize("cap", [-1, 0, 13])
+def test_distributed_levels_equal_single_cache(world, push, policy, gran, cap):
+    """The distributed fused eviction (cache_evict_sel_*: the levels with the histograms summed
+    over ranks, by peer memory or by the caller) evicts exactly what one cache evicts, in the
+    same order, under every policy / granularity and with the candidate buffer capped (0: the
+    levels sweep the shards in full)."""
+    from paper_2312_04429_b200 import binding as B, sharded as S
+    n = 1500
+    emb, cl = synth.entries(n, seed=31 + world)
+    pres = synth.present_masks(n, seed=31, hole_frac=0.2)
+    kw = dict(dim=768, latent_bytes=0, evict_granularity=gran)
+    single = B.NirvanaCache(entry_capacity=n + 64, **kw)
+    vs = S.VirtualShards(world, entry_capacity=n + 64, push_max_nb=(256 if push else 0), push_max_topk=1, **kw)
+    for c in (single, vs):
+        c.set_evict_policy(policy)
+        c.insert(torch.from_numpy(emb).cuda(), None, present=pres)
+    for c in vs.caches:
+        B.debug_set_evict_cand_cap(c, cap)
+    rng = np.random.default_rng(world * 7 + policy)
+    for r in range(3):
+        q = torch.from_numpy(synth.queries(emb, cl, 128 * world, seed=400 + r)[0]).cuda()
+        a = single.query(q, latents=False)
+        b = vs.query(q, latents=False)
+        assert torch.equal(a["ids"], b["ids"]) and torch.equal(a["k"], b["k"])
+        units = single.evict_units
+        nev = int(rng.integers(1, max(2, units // 3)))
+        e1, d1 = single.evict(nev)
+        e2, d2 = vs.evict(nev)
+        assert np.array_equal(e1, e2) and np.array_equal(d1, d2), (r, nev)
+        ne, _ = synth.entries(40, seed=700 + r)
+        single.insert(torch.from_numpy(ne).cuda())
+        vs.insert(torch.from_numpy(ne).cuda())
+
+
+def test_radix8_protocol_still_equal(oracle_mod):
+    """Round 1's 8-pass radix protocol (kept selectable) against one cache."""
+    from paper_2312_04429_b200 import binding as B, sharded as S
+    n = 900
+    emb, cl = synth.entries(n, seed=47)
+    single = B.NirvanaCache(entry_capacity=n, dim=768, latent_bytes=0)
+    for push in (True, False):
+        vs = S.VirtualShards(3, entry_capacity=n, dim=768, latent_bytes=0, push_max_nb=(128 if push else 0))
+        vs.evict_protocol = "radix8"
+        s1 = B.NirvanaCache(entry_capacity=n, dim=768, latent_bytes=0)
+        for c in (s1, vs):
+            c.insert(torch.from_numpy(emb).cuda())
+        q = torch.from_numpy(synth.queries(emb, cl, 384, seed=48)[0]).cuda()
+        s1.query(q, latents=False)
+        vs.query(q, latents=False)
+        e1, d1 = s1.evict(777)
+        e2, d2 = vs.evict(777)
+        assert np.array_equal(e1, e2) and np.array_equal(d1, d2)
