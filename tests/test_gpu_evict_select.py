@@ -223,3 +223,30 @@ def test_radix8_protocol_still_equal(oracle_mod):
         e1, d1 = s1.evict(777)
         e2, d2 = vs.evict(777)
         assert np.array_equal(e1, e2) and np.array_equal(d1, d2)
+
+
+@pytest.mark.parametrize("policy", [0, 1])
+def test_fused_evict_parity_1m_entries(oracle_mod, policy):
+    """At scale: 1M entries (4.75M items; dim 64 so the fp64 oracle holds the cache), Zipf query
+    batches (every row checked against the oracle, accesses adopted), then 1% and 5% evictions:
+    the fused eviction's lists equal the oracle's exactly (ids, order, dirty entries)."""
+    from paper_2312_04429_b200 import binding as B
+    n, dim = 1_000_000, 64
+    emb, cl = synth.entries(n, seed=303, dim=dim)
+    pres = synth.present_masks(n, seed=303)
+    g = B.NirvanaCache(entry_capacity=n, latent_capacity=5 * n, dim=dim, latent_bytes=0)
+    g.set_evict_policy(policy)
+    o = oracle_mod.OracleCache(dim=dim, entry_capacity=n, latent_capacity=5 * n)
+    for s0 in range(0, n, 200_000):
+        g.insert(torch.from_numpy(emb[s0:s0 + 200_000]).cuda(), None, present=pres[s0:s0 + 200_000])
+        o.insert(emb[s0:s0 + 200_000], present=pres[s0:s0 + 200_000])
+    for r in range(3):
+        q, _, _ = synth.queries(emb, cl, 256, seed=310 + r)
+        _query_both(g, o, q)
+    for frac in (0.01, 0.05):
+        nev = int(g.live_items * frac)
+        ev, dirty = g.evict(nev)
+        rc, oev, od = o.evict(nev, policy=policy)
+        assert rc == 0 and np.array_equal(ev, oev) and np.array_equal(dirty, od), frac
+        st = B.debug_evict_stats(g)
+        assert st["full_sweeps"] <= 3
