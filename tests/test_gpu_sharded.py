@@ -98,3 +98,58 @@ def test_sharded_world1_evict_is_the_fused_eviction(oracle_mod):
         assert sc.evict(10, lists=False) == (10, len(single.evict(10)[1]))
     finally:
         dist.destroy_process_group()
+
+
+def _proc_nccl_path(rank, port, ret):
+    """One rank of the all-gather (non-push) path: queries and records all-gathered by the
+    process group, the fused eviction's level histograms all-reduced by it."""
+    import os
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        torch.cuda.set_device(0)
+        from paper_2312_04429_b200 import binding as B, sharded as S
+        n, bl = 800, 32
+        emb, cl = synth.entries(n, seed=57)
+        sc = S.ShardedCache(S.TorchComm(device="cpu"), entry_capacity=n, dim=768, latent_bytes=0)
+        sc.insert(torch.from_numpy(emb).cuda())
+        single = B.NirvanaCache(entry_capacity=n, dim=768, latent_bytes=0)
+        single.insert(torch.from_numpy(emb).cuda())
+        ok = True
+        for rnd in range(2):
+            q, _, _ = synth.queries(emb, cl, 2 * bl, seed=58 + rnd)
+            out = sc.alloc_outputs(bl, 1, False)
+            sc.query_into(torch.from_numpy(q[rank * bl:(rank + 1) * bl]).cuda(), out)
+            full = single.query(torch.from_numpy(q).cuda(), latents=False)
+            ok &= bool(torch.equal(out["ids"], full["ids"][rank * bl:(rank + 1) * bl]))
+            e1, d1 = sc.evict(150)
+            e2, d2 = single.evict(150)
+            ok &= bool(np.array_equal(e1, e2) and np.array_equal(d1, d2))
+        ret[rank] = ok
+    except Exception as e:   # noqa: BLE001
+        ret[rank] = repr(e)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_processes_allgather_path_levels_eviction():
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    mgr = ctx.Manager()
+    ret = mgr.dict()
+    procs = [ctx.Process(target=_proc_nccl_path, args=(r, port, ret)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+    for p in procs:
+        if p.is_alive():
+            p.kill()
+    assert dict(ret) == {0: True, 1: True}, dict(ret)
