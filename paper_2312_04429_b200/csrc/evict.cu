@@ -37,7 +37,11 @@ namespace cg = cooperative_groups;
 #define NV_SEL_CPASYNC 0   // 1: |K| = 5 sweeps fed by per-lane cp.async rings (measured slower, kept for the record)
 #endif
 constexpr bool kSelCpAsync = NV_SEL_CPASYNC != 0;
-constexpr int kSelThreads = kSelCpAsync ? 256 : 512;
+#ifndef NV_SEL_PREFETCH
+#define NV_SEL_PREFETCH 0   // 1: next group's loads issued before this group's work (measured: no gain)
+#endif
+constexpr bool kSelPrefetch = NV_SEL_PREFETCH != 0 && !kSelCpAsync;
+constexpr int kSelThreads = (kSelCpAsync || kSelPrefetch) ? 256 : 512;
 constexpr int kCpStages = 3;                           // groups per lane: 2 loading + 1 being processed
 constexpr int kCpRingBytes = kCpStages * kSelThreads * 112;
 
@@ -563,7 +567,7 @@ __device__ void compact_bitmaps(const BitJob (&jobs)[NJ], uint32_t* part, cg::gr
 // dependent present -> id -> counter chain per slot (ncu: the first version moved 704 MB in
 // 789 us, 0.9 TB/s, stalled on those chains and on the grid barrier behind them).
 template <int POLICY, int GRAN, bool NK5>
-__global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : (kSelCpAsync ? 3 : 2))
+__global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : ((kSelCpAsync || kSelPrefetch) ? 3 : 2))
     k_evict_select(SelArgs a, KMap km) {
     __shared__ unsigned sh[kSelBins];
     __shared__ __align__(8) unsigned long long s_bar[2 * kStages];   // full[s], empty[s]
@@ -728,21 +732,40 @@ __global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : (kSelCp
             // register-fed: 7 independent 16-B loads per lane (present, ids, 5 x the column of
             // 4 consecutive slots); 128-slot groups interleaved over all warps of the grid
             const int64_t gstride = (int64_t)gridDim.x * 4 * kSelThreads;
-            for (int64_t g0 = ((int64_t)blockIdx.x * (kSelThreads / 32) + warp) * 128; g0 < n_pad; g0 += gstride) {
-                const int64_t e4 = g0 + 4 * lane;
-                const uint4 P = __ldcg(reinterpret_cast<const uint4*>(a.present + e4));
-                const uint4 I = __ldcg(reinterpret_cast<const uint4*>(a.ids + e4));
-                uint32_t c[20];
+            const int64_t gfirst = ((int64_t)blockIdx.x * (kSelThreads / 32) + warp) * 128;
+            // kSelPrefetch: the next group's seven loads are issued before this group is
+            // processed (3 CTAs of 256 threads per SM at <= 85 registers), so a lane keeps one
+            // group in flight while it works instead of alternating load and work
+            uint4 nP = make_uint4(0, 0, 0, 0), nI = nP, nC[5] = {nP, nP, nP, nP, nP};
+            auto load = [&](int64_t g, uint4& P_, uint4& I_, uint4 (&C_)[5]) {
+                const int64_t e = g + 4 * lane;
+                P_ = __ldcg(reinterpret_cast<const uint4*>(a.present + e));
+                I_ = __ldcg(reinterpret_cast<const uint4*>(a.ids + e));
                 if constexpr (POLICY != CACHE_POLICY_FIFO) {
-                    const uint4* cp = reinterpret_cast<const uint4*>(colp + e4 * 5);
+                    const uint4* cp = reinterpret_cast<const uint4*>(colp + e * 5);
 #pragma unroll
-                    for (int v = 0; v < 5; ++v) {
-                        const uint4 w = __ldcg(cp + v);
-                        c[4 * v] = w.x; c[4 * v + 1] = w.y; c[4 * v + 2] = w.z; c[4 * v + 3] = w.w;
-                    }
+                    for (int v = 0; v < 5; ++v) C_[v] = __ldcg(cp + v);
+                }
+            };
+            if (kSelPrefetch && gfirst < n_pad) load(gfirst, nP, nI, nC);
+            for (int64_t g0 = gfirst; g0 < n_pad; g0 += gstride) {
+                const int64_t e4 = g0 + 4 * lane;
+                uint4 P, I, C[5] = {nP, nP, nP, nP, nP};
+                if constexpr (kSelPrefetch) {
+                    P = nP;
+                    I = nI;
+#pragma unroll
+                    for (int v = 0; v < 5; ++v) C[v] = nC[v];
+                    if (g0 + gstride < n_pad) load(g0 + gstride, nP, nI, nC);
                 } else {
+                    load(g0, P, I, C);
+                }
+                uint32_t c[20];
 #pragma unroll
-                    for (int v = 0; v < 20; ++v) c[v] = 0u;
+                for (int v = 0; v < 5; ++v) {
+                    const bool z = POLICY == CACHE_POLICY_FIFO;
+                    c[4 * v] = z ? 0u : C[v].x; c[4 * v + 1] = z ? 0u : C[v].y;
+                    c[4 * v + 2] = z ? 0u : C[v].z; c[4 * v + 3] = z ? 0u : C[v].w;
                 }
                 const uint32_t pm[4] = {P.x, P.y, P.z, P.w}, pid[4] = {I.x, I.y, I.z, I.w};
                 if constexpr (GRAN == CACHE_EVICT_ITEM) {

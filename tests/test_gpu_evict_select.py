@@ -250,3 +250,38 @@ def test_fused_evict_parity_1m_entries(oracle_mod, policy):
         assert rc == 0 and np.array_equal(ev, oev) and np.array_equal(dirty, od), frac
         st = B.debug_evict_stats(g)
         assert st["full_sweeps"] <= 3
+
+
+def test_distributed_calls_out_of_order_fail_cleanly():
+    """cache_evict_sel_*: levels out of order, a pick without its level, an apply without a
+    selection -> CACHE_E_STATE, and the cache keeps working afterwards."""
+    from paper_2312_04429_b200 import binding as B
+    n = 600
+    emb, _ = synth.entries(n, seed=61)
+    g = B.NirvanaCache(entry_capacity=n, dim=768, latent_bytes=0)
+    g.insert(torch.from_numpy(emb).cuda())
+    h = torch.zeros(4096, dtype=torch.int32, device="cuda")
+    with pytest.raises(B.CacheError) as ei:
+        g.evict_sel_apply(10)                       # nothing begun
+    assert ei.value.code == B.E_STATE
+    g.evict_sel_begin(100)
+    with pytest.raises(B.CacheError) as ei:
+        g.evict_sel_level(1, h)                     # level 0 first
+    assert ei.value.code == B.E_STATE
+    with pytest.raises(B.CacheError) as ei:
+        g.push_evict_sel_level(0)                   # no push arenas
+    assert ei.value.code == B.E_STATE
+    g.evict_sel_level(0, h)
+    assert int(h.sum()) == g.live_items            # level 0 counts every live unit
+    done = g.evict_sel_pick(0, h)
+    lvl = 1
+    while not done:
+        g.evict_sel_level(lvl, h)
+        done = g.evict_sel_pick(lvl, h)
+        lvl += 1
+    ev, dirty = g.evict_sel_apply(100)
+    ref = B.NirvanaCache(entry_capacity=n, dim=768, latent_bytes=0)
+    ref.insert(torch.from_numpy(emb).cuda())
+    e2, d2 = ref.evict(100)
+    assert np.array_equal(ev, e2) and np.array_equal(dirty, d2)
+    assert len(g.evict(50)[0]) == 50                # the single-cache path still works
