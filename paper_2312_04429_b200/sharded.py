@@ -104,6 +104,12 @@ def evict_protocol(comm, n: int, state, hist, hist_fn, pick_fn):
     return state
 
 
+def _dev() -> str:
+    """Device of the small protocol tensors: the GPU's (the kernels write them); CPU only for the
+    gloo protocol tests, whose ranks are played by numpy stand-ins."""
+    return "cuda" if torch.cuda.is_available() else "cpu"
+
+
 def _desc_bytes(d: B.PeerDesc) -> bytes:
     return ctypes.string_at(ctypes.addressof(d), ctypes.sizeof(d))
 
@@ -202,7 +208,7 @@ class ShardedCache:
         rank passes the same n).  lists=False skips gathering the evicted / dirty id lists to
         every rank and returns this rank's (evicted count, dirty count) instead."""
         live = self.comm.all_reduce_sum(torch.tensor([self.cache.evict_units], dtype=torch.int64,
-                                                     device="cuda")).item()
+                                                     device=_dev())).item()
         if n > live:
             raise B.CacheError(B.E_EVICT_RANGE, "sharded evict: n exceeds live items / entries")
         if self.comm.world == 1:   # one shard: no exchange, the fused single-launch eviction
@@ -218,7 +224,7 @@ class ShardedCache:
                     self.cache.push_evict_sel_level(level)
                     done = self.cache.push_evict_sel_pick(level)
                 else:
-                    hist = torch.empty(4096, dtype=torch.int32, device="cuda")
+                    hist = torch.empty(4096, dtype=torch.int32, device=_dev())
                     self.cache.evict_sel_level(level, hist)
                     self.comm.all_reduce_sum(hist)
                     done = self.cache.evict_sel_pick(level, hist)

@@ -109,3 +109,107 @@ def test_sharded_protocol_gloo_world2():
     ret = mp.Manager().dict()
     mp.spawn(_worker, args=(port, ret), nprocs=WORLD, join=True)
     assert ret[0] == (True, True) and ret[1] == (True, True), dict(ret)
+
+
+# ---- the levels protocol of ShardedCache.evict (the distributed fused eviction) ----
+def _bin0(k):
+    k = np.asarray(k, dtype=np.uint64)
+    out = np.empty(len(k), dtype=np.int64)
+    small = k < 64
+    out[small] = k[small].astype(np.int64)
+    kb = k[~small]
+    e = np.floor(np.log2(kb.astype(np.float64))).astype(np.int64)
+    e = np.where((np.uint64(1) << e.astype(np.uint64)) > kb, e - 1, e)            # exact floor(log2)
+    e = np.where((np.uint64(2) << e.astype(np.uint64)) <= kb, e + 1, e)
+    m = ((kb >> (e - 6).astype(np.uint64)) & np.uint64(63)).astype(np.int64)
+    out[~small] = 64 + (e - 6) * 64 + m
+    return out
+
+
+class _FakeLevelsCache:
+    """Numpy stand-in of one rank's k_evict_select phases (level 0: 4,096 log bins; later
+    levels: 12-bit digits of key - lo; the same pick on every rank); what is under test is
+    ShardedCache.evict's orchestration: levels until done, histograms all-reduced by the
+    process group, the ranks' lists merged into the global eviction order."""
+    granularity = 0
+
+    def __init__(self, keys):
+        self.keys = np.sort(np.asarray(keys, dtype=np.uint64))
+
+    @property
+    def evict_units(self):
+        return len(self.keys)
+
+    def evict_sel_begin(self, n):
+        self.n = n
+
+    def evict_sel_level(self, level, hist):
+        k = self.keys
+        if level == 0:
+            h = np.bincount(_bin0(k), minlength=4096)
+        else:
+            inr = k[(k >= np.uint64(self.lo)) & ((k - np.uint64(self.lo)) >> np.uint64(self.w) == 0)]
+            h = np.bincount(((inr - np.uint64(self.lo)) >> np.uint64(self.shift)).astype(np.int64), minlength=4096)
+        hist.copy_(torch.from_numpy(h.astype(np.int32)))
+
+    def evict_sel_pick(self, level, hist):
+        h = hist.numpy().astype(np.int64)
+        target = self.n if level == 0 else self.rem
+        cum = np.cumsum(h)
+        b = int(np.searchsorted(cum, target))
+        before = int(cum[b] - h[b])
+        if level == 0:
+            if b < 64:
+                self.lo, self.w = b, 0
+            else:
+                e, m = (b - 64) // 64 + 6, (b - 64) % 64
+                self.w, self.lo = e - 6, (64 + m) << (e - 6)
+            self.rem = self.n - before
+        else:
+            self.lo += b << self.shift
+            self.w = self.shift
+            self.rem -= before
+        done = int(h[b]) == self.rem or self.w == 0
+        self.shift = self.w - min(12, self.w)
+        return done
+
+    def evict_sel_apply(self, cap, lists=True):
+        T = self.lo + (1 << self.w) - 1
+        self.last = self.keys[self.keys <= np.uint64(T)]
+        self.keys = self.keys[self.keys > np.uint64(T)]
+        return self.last & np.uint64((1 << 35) - 1), np.zeros(0, np.uint64)
+
+    def last_evicted_keys(self):
+        return self.last
+
+
+def _levels_worker(rank, port, ret):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    try:
+        from paper_2312_04429_b200.sharded import ShardedCache, TorchComm
+        rng = np.random.default_rng(11)
+        # item keys score << 35 | id << 3 | j: a never-accessed bulk plus hot items
+        ids = rng.permutation(50_000)[:20_000].astype(np.uint64)
+        score = np.where(rng.random(20_000) < 0.8, 0, rng.integers(1, 3000, 20_000)).astype(np.uint64)
+        keys_all = np.unique((score << np.uint64(35)) | (ids << np.uint64(3)) | rng.integers(0, 5, 20_000).astype(np.uint64))
+        sc = object.__new__(ShardedCache)
+        sc.comm, sc.push, sc.cache = TorchComm(device="cpu"), False, _FakeLevelsCache(keys_all[rank::WORLD])
+        ok = True
+        taken = 0
+        for nsel in (1, 777, 5000, 9000):
+            ev, _ = sc.evict(nsel)
+            want = np.sort(keys_all)[taken:taken + nsel] & np.uint64((1 << 35) - 1)
+            ok &= bool(np.array_equal(ev, want))
+            taken += nsel
+        ret[rank] = ok
+    finally:
+        dist.destroy_process_group()
+
+
+def test_levels_protocol_gloo_world2():
+    port = _free_port()
+    ret = mp.Manager().dict()
+    mp.spawn(_levels_worker, args=(port, ret), nprocs=WORLD, join=True)
+    assert ret[0] is True and ret[1] is True, dict(ret)
