@@ -242,6 +242,7 @@ struct cache_t {
     SelArgs dsel{};
     int dsel_level = -1;                 // next level expected (-1: none begun)
     bool dsel_push = false;
+    bool dsel_done = false;              // the last pick finished the selection
     DevBuf<SelState> dstate;
     DevBuf<uint32_t> dlhist;             // this rank's local level histograms [levels][4096]
     int64_t last_ev_n = 0;               // unit keys of the last eviction (sorted, in ekey), in order
@@ -1805,6 +1806,7 @@ cache_status cache_evict_sel_begin(cache_t* c, int64_t n, void* stream) {
     c->dsel.state = c->dstate.p;
     c->dsel_level = 0;
     c->dsel_push = false;
+    c->dsel_done = false;
     return CACHE_OK;
 }
 
@@ -1825,6 +1827,7 @@ static cache_status sel_pick_done(cache_t* c, int32_t level, const uint32_t* ghi
     CK(cudaMemcpyAsync(&h, c->dstate.p, sizeof(h), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (out_done) *out_done = (int32_t)(h.done | h.fail);
+    c->dsel_done = (h.done | h.fail) != 0u;
     c->dsel_level = level + 1;
     return CACHE_OK;
 }
@@ -1840,7 +1843,9 @@ cache_status cache_evict_sel_pick(cache_t* c, int32_t level, const uint32_t* ghi
 cache_status cache_evict_sel_apply(cache_t* c, int64_t cap, uint64_t* out_evicted, int64_t* out_n,
                                    uint64_t* out_dirty_ids, int64_t* out_n_dirty, void* stream) {
     if (!c || cap < 0) return fail(CACHE_E_INVALID_ARG, "cache_evict_sel_apply: bad argument");
-    if (c->dsel_level < 1) return fail(CACHE_E_STATE, "cache_evict_sel_apply: no selection (begin, level/pick 0..)");
+    if (c->dsel_level < 1 || !c->dsel_done)
+        return fail(CACHE_E_STATE, "cache_evict_sel_apply: the selection is not finished (begin, then level / pick "
+                                   "0, 1, ... until a pick reports done)");
     if (peer_failed(c)) return peer_fail("cache_evict_sel_apply");
     DeviceGuard g(c->device);
     cudaStream_t s = (cudaStream_t)stream;

@@ -273,6 +273,9 @@ def test_distributed_calls_out_of_order_fail_cleanly():
     assert ei.value.code == B.E_STATE
     g.evict_sel_level(0, h)
     assert int(h.sum()) == g.live_items            # level 0 counts every live unit
+    with pytest.raises(B.CacheError) as ei:
+        g.evict_sel_apply(100)                      # picks not finished: nothing applied
+    assert ei.value.code == B.E_STATE
     done = g.evict_sel_pick(0, h)
     lvl = 1
     while not done:
@@ -285,3 +288,53 @@ def test_distributed_calls_out_of_order_fail_cleanly():
     e2, d2 = ref.evict(100)
     assert np.array_equal(ev, e2) and np.array_equal(dirty, d2)
     assert len(g.evict(50)[0]) == 50                # the single-cache path still works
+
+
+@pytest.mark.parametrize("dist", ["plateau", "geometric", "huge", "mixed"])
+@pytest.mark.parametrize("gran", [0, 1])
+def test_fused_evict_adversarial_counters(oracle_mod, dist, gran):
+    """Counters set directly (both sides) to distributions the query streams never produce: one
+    big plateau of equal scores (the level-0 log bin holds almost everything), geometric spreads,
+    scores near the key's saturation, and a mix -- then evictions of random sizes under LCBFU and
+    LFU: the selection must still be exact (order and dirty lists)."""
+    from paper_2312_04429_b200 import binding as B
+    n = 2500
+    emb, _ = synth.entries(n, seed=500 + gran)
+    pres = synth.present_masks(n, seed=500, hole_frac=0.3)
+    rng = np.random.default_rng({"plateau": 1, "geometric": 2, "huge": 3, "mixed": 4}[dist] * 10 + gran)
+    for policy in (0, 2):
+        g = B.NirvanaCache(entry_capacity=n, latent_capacity=5 * n, dim=768, latent_bytes=0, evict_granularity=gran)
+        g.set_evict_policy(policy)
+        o = oracle_mod.OracleCache(dim=768, entry_capacity=n, latent_capacity=5 * n)
+        g.insert(torch.from_numpy(emb).cuda(), None, present=pres)
+        o.insert(emb, present=pres)
+        for id_ in range(n):
+            for j in range(5):
+                if not (int(pres[id_]) >> j) & 1:
+                    continue
+                if dist == "plateau":
+                    f = 3 if rng.random() < 0.9 else int(rng.integers(0, 6))
+                elif dist == "geometric":
+                    f = int(rng.geometric(0.05)) - 1
+                elif dist == "huge":
+                    f = int(rng.integers(0, 40_000_000))   # f * K up to 1e9: beyond the 2^29 - 1 key cap
+                else:
+                    f = int(rng.choice([0, 1, 7, 1000, 123456]))
+                if dist == "huge" and policy == 0:
+                    f = min(f, (2 ** 29 - 1) // (5 * (j + 1)))   # keep LCBFU below the cap (R11 is tested apart)
+                if f:
+                    B.debug_set_count(g, id_, j, f)
+                    assert o.set_count(id_, j, f) == 0
+        for _ in range(3):
+            units = g.evict_units
+            if units < 2:
+                break
+            nev = int(rng.integers(1, units))
+            if gran:
+                ev, dirty = g.evict(nev)
+                rc, oev = o.evict_entries(nev, policy=policy)
+                assert rc == 0 and np.array_equal(ev, oev), (dist, policy)
+            else:
+                ev, dirty = g.evict(nev)
+                rc, oev, od = o.evict(nev, policy=policy)
+                assert rc == 0 and np.array_equal(ev, oev) and np.array_equal(dirty, od), (dist, policy)
