@@ -41,6 +41,11 @@ constexpr bool kSelCpAsync = NV_SEL_CPASYNC != 0;
 #define NV_SEL_PREFETCH 0   // 1: next group's loads issued before this group's work (measured: no gain)
 #endif
 constexpr bool kSelPrefetch = NV_SEL_PREFETCH != 0 && !kSelCpAsync;
+#ifndef NV_SEL_COLT
+#define NV_SEL_COLT 0   // 1: coalesced column loads + shared-memory redistribution (measured: no gain)
+#endif
+constexpr bool kSelColT = NV_SEL_COLT != 0;
+constexpr int kColTBytes = (kSelCpAsync ? 256 : 512) / 32 * 160 * 16;   // per-warp 2,560-B transposes
 constexpr int kSelThreads = (kSelCpAsync || kSelPrefetch) ? 256 : 512;
 constexpr int kCpStages = 3;                           // groups per lane: 2 loading + 1 being processed
 constexpr int kCpRingBytes = kCpStages * kSelThreads * 112;
@@ -742,9 +747,25 @@ __global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : ((kSelC
                 P_ = __ldcg(reinterpret_cast<const uint4*>(a.present + e));
                 I_ = __ldcg(reinterpret_cast<const uint4*>(a.ids + e));
                 if constexpr (POLICY != CACHE_POLICY_FIFO) {
-                    const uint4* cp = reinterpret_cast<const uint4*>(colp + e * 5);
+                    if constexpr (kSelColT) {
+                        // the warp's 2,560-B column block in five fully coalesced 512-B loads,
+                        // redistributed through shared memory to the lanes' own 4 slots (the
+                        // per-lane 80-B reads touched 20 lines per load instruction)
+                        const uint4* cp = reinterpret_cast<const uint4*>(colp + g * 5);
+                        uint4* tr = reinterpret_cast<uint4*>(s_stage) + warp * 160;   // dynamic smem
 #pragma unroll
-                    for (int v = 0; v < 5; ++v) C_[v] = __ldcg(cp + v);
+                        for (int v = 0; v < 5; ++v) C_[v] = __ldcg(cp + lane + 32 * v);
+#pragma unroll
+                        for (int v = 0; v < 5; ++v) tr[lane + 32 * v] = C_[v];
+                        __syncwarp();
+#pragma unroll
+                        for (int v = 0; v < 5; ++v) C_[v] = tr[5 * lane + v];
+                        __syncwarp();
+                    } else {
+                        const uint4* cp = reinterpret_cast<const uint4*>(colp + e * 5);
+#pragma unroll
+                        for (int v = 0; v < 5; ++v) C_[v] = __ldcg(cp + v);
+                    }
                 }
             };
             if (kSelPrefetch && gfirst < n_pad) load(gfirst, nP, nI, nC);
@@ -993,13 +1014,12 @@ static cudaError_t launch_select_t(const SelArgs& a, const KMap& km, cudaStream_
         int bps = 0, dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (NK5 && (kSelStaged || kSelCpAsync))
-            cudaFuncSetAttribute(k_evict_select<POLICY, GRAN, NK5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kSelStaged ? kStages * kStageBytes : kCpRingBytes);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_evict_select<POLICY, GRAN, NK5>, kSelThreads,
-                                                          NK5 ? (kSelStaged ? kStages * kStageBytes
-                                                                            : (kSelCpAsync ? kCpRingBytes : 0))
-                                                              : 0) != cudaSuccess ||
+        const int dyn0 = NK5 ? (kSelStaged ? kStages * kStageBytes : (kSelCpAsync ? kCpRingBytes : (kSelColT ? kColTBytes : 0)))
+                             : 0;
+        if (dyn0 > 0)
+            cudaFuncSetAttribute(k_evict_select<POLICY, GRAN, NK5>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn0);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_evict_select<POLICY, GRAN, NK5>, kSelThreads, dyn0) !=
+                cudaSuccess ||
             bps < 1)
             bps = 1;
         return bps * sms;
@@ -1008,7 +1028,8 @@ static cudaError_t launch_select_t(const SelArgs& a, const KMap& km, cudaStream_
     SelArgs aa = a;
     KMap kk = km;
     void* args[] = {&aa, &kk};
-    const size_t dyn = NK5 ? (kSelStaged ? (size_t)kStages * kStageBytes : (kSelCpAsync ? (size_t)kCpRingBytes : 0))
+    const size_t dyn = NK5 ? (kSelStaged ? (size_t)kStages * kStageBytes
+                                         : (kSelCpAsync ? (size_t)kCpRingBytes : (kSelColT ? (size_t)kColTBytes : 0)))
                            : 0;
     return cudaLaunchCooperativeKernel((const void*)k_evict_select<POLICY, GRAN, NK5>, grid, kSelThreads, args, dyn, s);
 }
