@@ -1740,6 +1740,7 @@ static cache_status evict_impl(cache_t* c, int64_t n, bool want_ev, bool want_di
     if (trace) {
         cudaEventCreate(&ev0);
         cudaEventCreate(&ev1);
+        sel_trace_reset(s);
         cudaEventRecord(ev0, s);
     }
     CK(launch_evict_select(a, c->km, s));
@@ -1775,6 +1776,18 @@ static cache_status evict_impl(cache_t* c, int64_t n, bool want_ev, bool want_di
                      "\"candidates\": %llu, \"key_bits\": %d, \"dirty\": %lld}}\n",
                      (long long)n, (long long)c->hwm, kms * 1e3, t1 - t0, t2 - t1, tf[0] - t2, tf[1] - tf[0], tf[2] - tf[1],
                      tf[2] - t0, h.levels, h.full_sweeps, h.compact_level, h.cnt[3], bitlen(h.T - kmin), (long long)nd);
+        // NV_SEL_TRACE builds: phase stamps relative to the earliest CTA start (us), first / last CTA
+        unsigned long long lo[kSelTraceN], hi[kSelTraceN];
+        const int ns = sel_trace_read(lo, hi);
+        if (ns) {
+            std::fprintf(stderr, "{\"sel_phases_us\": [");
+            bool first = true;
+            for (int i = 0; i < ns && hi[i]; ++i) {
+                std::fprintf(stderr, "%s[%.2f, %.2f]", first ? "" : ", ", (lo[i] - lo[0]) * 1e-3, (hi[i] - lo[0]) * 1e-3);
+                first = false;
+            }
+            std::fprintf(stderr, "]}\n");
+        }
     }
     return r;
 }

@@ -50,6 +50,25 @@ constexpr int kSelThreads = (kSelCpAsync || kSelPrefetch) ? 256 : 512;
 constexpr int kCpStages = 3;                           // groups per lane: 2 loading + 1 being processed
 constexpr int kCpRingBytes = kCpStages * kSelThreads * 112;
 
+// NV_SEL_TRACE=1 (experiments only): every CTA's thread 0 stamps %globaltimer at each phase
+// boundary of the fused kernel; per stamp index the earliest and latest CTA are kept
+// (cache_debug_sel_trace), so a phase's cost and its slowest-CTA tail can be read apart.
+#ifndef NV_SEL_TRACE
+#define NV_SEL_TRACE 0
+#endif
+__device__ unsigned long long g_sel_tmin[kSelTraceN], g_sel_tmax[kSelTraceN];
+__device__ __forceinline__ void sel_stamp(int& i) {
+    if constexpr (NV_SEL_TRACE != 0) {
+        if (threadIdx.x == 0 && i < kSelTraceN) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            atomicMin(&g_sel_tmin[i], t);
+            atomicMax(&g_sel_tmax[i], t);
+        }
+        ++i;
+    }
+}
+
 __device__ __forceinline__ uint32_t sel_bin0(unsigned long long key) {
     if (key < 64ull) return (uint32_t)key;
     const int e = 63 - __clzll((long long)key);   // 6..63
@@ -188,6 +207,37 @@ __device__ __forceinline__ void mark_dirty(const SelArgs& a, int64_t e, uint32_t
 __device__ __forceinline__ void mark_pool(const SelArgs& a, int32_t slot) {
     if (a.pool_bits && slot >= 0) atomicOr(a.pool_bits + (slot >> 5), 1u << (slot & 31));
 }
+
+// Per-lane run of bits in one bitmap word (one atomic per word change); the final flush is
+// warp-collective and ORs the words of neighbouring lanes first (a segmented reduction over
+// contiguous lanes with the same word), so the common case -- consecutive slots, ids and pool
+// slots across the warp -- costs one atomic per word instead of up to 32 same-address atomics.
+struct WordRun {
+    uint32_t w = 0xFFFFFFFFu, m = 0u;   // word index < 2^27 (32-bit ids / slots)
+    __device__ __forceinline__ void add(uint32_t* bits, uint32_t i) {
+        const uint32_t ww = i >> 5;
+        if (ww != w) {
+            if (m) atomicOr(bits + w, m);
+            w = ww;
+            m = 0u;
+        }
+        m |= 1u << (i & 31);
+    }
+    __device__ __forceinline__ void warp_flush(uint32_t* bits, int lane) {   // all 32 lanes, converged
+        const uint32_t mw = m ? w : 0xFFFFFFFFu;
+        uint32_t acc = m;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t ow = __shfl_down_sync(0xFFFFFFFFu, mw, o);
+            const uint32_t om = __shfl_down_sync(0xFFFFFFFFu, acc, o);
+            if (lane + o < 32 && ow == mw) acc |= om;
+        }
+        const uint32_t pw = __shfl_up_sync(0xFFFFFFFFu, mw, 1);
+        if (m && (lane == 0 || pw != mw)) atomicOr(bits + w, acc);
+        m = 0u;
+        w = 0xFFFFFFFFu;
+    }
+};
 
 // One entry slot (lane-parallel, warp-uniform control flow), every mode of a full sweep, from
 // the slot's preloaded presence mask, id and policy column (col[j] for j < nk).
@@ -365,6 +415,29 @@ __device__ __forceinline__ void sweep_items_v4(const SelArgs& a, const int (&kv)
     if (mode == kSweepLevel && L.compact) cpos = warp_reserve(&a.out->cnt[3], (uint32_t)__popc(inm), lane);
     uint32_t ndirty = 0;
     BitRun evr;
+    // dirty slots: the lane's 4 slots lie in one bitmap word, shared by lanes 8k .. 8k+7 (one
+    // atomic per word after a 3-step OR); dirty ids / world: a word run per lane, then OR'ed
+    // across neighbouring lanes (consecutive ids)
+    uint32_t dsm = 0u;
+    WordRun dir;
+    // LCBFU / LFU: the lane's 20 counters are in c[] -- written back with 5 vector stores, the
+    // evicted ones zeroed (no query runs during an eviction)
+    constexpr bool kVecF = POLICY == CACHE_POLICY_LCBFU || POLICY == CACHE_POLICY_LFU;
+    if constexpr (kVecF) {
+        if (evm) {
+            uint4* fp = reinterpret_cast<uint4*>(a.fcnt + e4 * 5);
+#pragma unroll
+            for (int v = 0; v < 5; ++v) {
+                if (!((evm >> (4 * v)) & 15u)) continue;
+                uint4 o;
+                o.x = (evm >> (4 * v)) & 1u ? 0u : c[4 * v];
+                o.y = (evm >> (4 * v + 1)) & 1u ? 0u : c[4 * v + 1];
+                o.z = (evm >> (4 * v + 2)) & 1u ? 0u : c[4 * v + 2];
+                o.w = (evm >> (4 * v + 3)) & 1u ? 0u : c[4 * v + 3];
+                fp[v] = o;
+            }
+        }
+    }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const uint32_t m = pm[q] & 31u, id = pid[q];
@@ -379,8 +452,7 @@ __device__ __forceinline__ void sweep_items_v4(const SelArgs& a, const int (&kv)
                 if (pos < a.ev_cap) a.ev_key[pos] = key;
                 ++pos;
                 evr.add(a, L, key);
-                mark_pool(a, a.lslot[e * 5 + j]);
-                a.fcnt[e * 5 + j] = 0u;
+                if constexpr (!kVecF) a.fcnt[e * 5 + j] = 0u;
             } else if (mode == kSweepLevel && L.compact) {
                 if (cpos < a.cand_cap) { a.cand_key[cpos] = key; a.cand_slot[cpos] = (uint32_t)e; }
                 ++cpos;
@@ -391,11 +463,38 @@ __device__ __forceinline__ void sweep_items_v4(const SelArgs& a, const int (&kv)
             a.present[e] = keep | (pm[q] & ~31u);
             if (!keep) {
                 a.inv_e[e] = __int_as_float(0x7FC00000);
-                mark_dirty(a, e, id);
+                dsm |= 1u << (e & 31);
+                dir.add(a.did_bits, id / (uint32_t)a.world);   // ids of this rank: id % world == rank
                 ++ndirty;
             }
         }
     }
+    // freed pool slots: the lane's 20 latent-slot entries by 5 independent vector loads (a
+    // scalar load per evicted item behind the previous item's atomic was a chain of up to 20
+    // round trips: the C2 eviction's slowest warps, NV_SEL_TRACE)
+    if (a.pool_bits && evm) {
+        int4 lv[5];
+        const int4* lp = reinterpret_cast<const int4*>(a.lslot + e4 * 5);
+#pragma unroll
+        for (int v = 0; v < 5; ++v) lv[v] = __ldg(lp + v);
+        WordRun plr;
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+            const int32_t x[4] = {lv[v].x, lv[v].y, lv[v].z, lv[v].w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (((evm >> (4 * v + k)) & 1u) && x[k] >= 0) plr.add(a.pool_bits, (uint32_t)x[k]);
+        }
+        if (plr.m) atomicOr(a.pool_bits + plr.w, plr.m);
+    }
+    {
+        uint32_t x = dsm;
+        x |= __shfl_xor_sync(0xFFFFFFFFu, x, 1);
+        x |= __shfl_xor_sync(0xFFFFFFFFu, x, 2);
+        x |= __shfl_xor_sync(0xFFFFFFFFu, x, 4);
+        if ((lane & 7) == 0 && x) atomicOr(a.dslot_bits + (e4 >> 5), x);
+    }
+    dir.warp_flush(a.did_bits, lane);
     evr.flush(a);
     unsigned long long dt = 0;
     (void)warp_excl_scan_u64(ndirty, lane, &dt);
@@ -493,8 +592,13 @@ __device__ __forceinline__ void sel_cand(const SelArgs& a, const KMap& km, int m
 }
 
 // Ordered compaction of the bitmaps into ascending lists (dirty slots, dirty ids, freed pool
-// slots): per CTA a contiguous word range, per thread a contiguous sub-range; CTA totals are
-// exchanged through global memory across one grid barrier.
+// slots, evicted keys): per CTA a contiguous word range; CTA totals are exchanged through global
+// memory across one grid barrier.  Inside a CTA the range goes in rounds of kSelThreads words
+// (one per thread, a block scan of their popcounts), and each warp emits its words' bits one
+// word at a time with lane = bit, so every output store is coalesced.  (The first version gave
+// each thread a contiguous sub-range and wrote its bits one by one: the dirty bitmaps are dense
+// in the oldest slots, so the first CTAs issued ~200 scattered 8-B stores per thread -- a 60-us
+// tail at 12.5M entries, NV_SEL_TRACE.)
 struct BitJob {
     const uint32_t* bits;
     int64_t words;
@@ -526,44 +630,54 @@ __device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t x, uint32_t* to
 }
 
 template <int NJ>
-__device__ void compact_bitmaps(const BitJob (&jobs)[NJ], uint32_t* part, cg::grid_group& grid) {
-    uint32_t cnt[NJ];
-    int64_t w0[NJ], w1[NJ];
+__device__ void compact_bitmaps(const BitJob (&jobs)[NJ], uint32_t* part, cg::grid_group& grid, int& ts) {
+    int64_t r0[NJ], r1[NJ];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
     for (int q = 0; q < NJ; ++q) {
         const int64_t wb = (jobs[q].words + gridDim.x - 1) / gridDim.x;
-        const int64_t r0 = (int64_t)blockIdx.x * wb, r1 = min(jobs[q].words, r0 + wb);
-        const int64_t tw = (wb + kSelThreads - 1) / kSelThreads;
-        w0[q] = min(r1, r0 + (int64_t)threadIdx.x * tw);
-        w1[q] = min(r1, w0[q] + tw);
+        r0[q] = min(jobs[q].words, (int64_t)blockIdx.x * wb);
+        r1[q] = min(jobs[q].words, r0[q] + wb);
         uint32_t c = 0;
         if (jobs[q].bits)
-            for (int64_t w = w0[q]; w < w1[q]; ++w) c += __popc(__ldcg(jobs[q].bits + w));
-        cnt[q] = c;
+            for (int64_t w = r0[q] + threadIdx.x; w < r1[q]; w += kSelThreads) c += __popc(__ldcg(jobs[q].bits + w));
         uint32_t tot = 0;
         (void)block_excl_scan_u32(c, &tot);
         if (threadIdx.x == 0) part[q * gridDim.x + blockIdx.x] = tot;
     }
+    sel_stamp(ts);
     grid.sync();
+    sel_stamp(ts);
 #pragma unroll
     for (int q = 0; q < NJ; ++q) {
         if (!jobs[q].bits) continue;   // grid-uniform
         uint32_t lower = 0;
         for (int b = threadIdx.x; b < (int)blockIdx.x; b += kSelThreads) lower += __ldcg(part + q * gridDim.x + b);
-        uint32_t lower_tot = 0;
-        (void)block_excl_scan_u32(lower, &lower_tot);
-        uint32_t tot = 0;
-        unsigned long long pos = lower_tot + block_excl_scan_u32(cnt[q], &tot);
-        for (int64_t w = w0[q]; w < w1[q]; ++w) {
-            uint32_t m = __ldcg(jobs[q].bits + w);
-            while (m) {
-                const int bit = __ffs(m) - 1;
-                m &= m - 1u;
-                const unsigned long long v = (unsigned long long)(w * 32 + bit) * jobs[q].mul + jobs[q].add;
-                if (jobs[q].out2) jobs[q].out2[pos] = v & jobs[q].mask2;
-                jobs[q].out[pos++] = v;
+        uint32_t base = 0;
+        (void)block_excl_scan_u32(lower, &base);   // the CTAs before this one
+        const BitJob J = jobs[q];
+        for (int64_t rb = r0[q]; rb < r1[q]; rb += kSelThreads) {   // CTA-uniform
+            const int64_t w = rb + threadIdx.x;
+            const uint32_t m = w < r1[q] ? __ldcg(J.bits + w) : 0u;
+            uint32_t tot = 0;
+            const uint32_t off = block_excl_scan_u32((uint32_t)__popc(m), &tot);
+            unsigned nz = __ballot_sync(0xFFFFFFFFu, m != 0u);
+            while (nz) {   // warp-uniform
+                const int j = __ffs(nz) - 1;
+                nz &= nz - 1u;
+                const uint32_t mj = __shfl_sync(0xFFFFFFFFu, m, j);
+                const uint32_t oj = __shfl_sync(0xFFFFFFFFu, off, j);
+                if ((mj >> lane) & 1u) {
+                    const unsigned long long pos = (unsigned long long)base + oj + __popc(mj & ((1u << lane) - 1u));
+                    const int64_t bit = (rb + warp * 32 + j) * 32 + lane;
+                    const unsigned long long v = (unsigned long long)bit * J.mul + J.add;
+                    if (J.out2) J.out2[pos] = v & J.mask2;
+                    J.out[pos] = v;
+                }
             }
+            base += tot;
         }
+        sel_stamp(ts);
     }
 }
 
@@ -829,7 +943,9 @@ __global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : ((kSelC
 
     // final apply (the candidates <= T, or one more full sweep), then the ordered lists
     auto finish = [&](SelLevel L, bool compacted, int64_t ncand, bool fail, int level, int full,
-                      int compact_level) {
+                      int compact_level, int* tsp = nullptr) {
+        int ts_dummy = 0;
+        int& ts = tsp ? *tsp : ts_dummy;
         unsigned long long kmin_unused = ~0ull;
         L.T = L.lo + ((1ull << L.w) - 1ull);
         if (!fail) {
@@ -840,7 +956,9 @@ __global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : ((kSelC
                 ++full;
             }
         }
+        sel_stamp(ts);
         grid.sync();   // every apply is done: the bitmaps and the evicted-key list are complete
+        sel_stamp(ts);
         bool ev_sorted = false;
         if (!fail) {
             // evicted keys (unique): marked in the bitmap over [kb, kb + ev_lim) as they went;
@@ -856,7 +974,7 @@ __global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : ((kSelC
                 BitJob{ev_sorted ? a.ev_bits : nullptr,
                        ev_sorted ? (int64_t)min((L.T - kb) / 32 + 1, (unsigned long long)a.ev_bits_words) : 0,
                        a.ev_sorted, 1ull, kb, a.ev_masked, a.ev_mask}};
-            compact_bitmaps<4>(jobs, a.part, grid);
+            compact_bitmaps<4>(jobs, a.part, grid, ts);
         }
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             a.out->T = L.T;
@@ -906,13 +1024,17 @@ __global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : ((kSelC
 
     // ---- single cache: the whole selection in this launch ----
     // level 0: log-bin histogram + min key
+    int ts = 0;
+    sel_stamp(ts);
     SelLevel L{0ull, 0ull, 64, 0, false, 0ull, 0ull};
     clear_sh();
     unsigned long long kmin = ~0ull;
     full_sweep(kSweepL0, L, kmin);
+    sel_stamp(ts);
     flush_sh(a.hist);
     kmin_to_global(kmin);
     grid.sync();
+    sel_stamp(ts);
     L.kb = ~__ldcg(&a.out->kmin_inv);
     L.ev_lim = a.ev_bits ? (unsigned long long)a.ev_bits_words * 32ull : 0ull;
     PickRes p = sel_pick(a.hist, a.n);
@@ -935,9 +1057,11 @@ __global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : ((kSelC
             L.compact = false;
             cand_sweep(kSweepLevel, L, ncand);
         }
+        sel_stamp(ts);
         uint32_t* gh = a.hist + (size_t)(level < kSelMaxLevels ? level : kSelMaxLevels - 1) * kSelBins;
         flush_sh(gh);
         grid.sync();
+        sel_stamp(ts);
         if (L.compact) {
             compacted = true;
             ncand = (int64_t)__ldcg(&a.out->cnt[3]);
@@ -951,7 +1075,9 @@ __global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : ((kSelC
         done = p.cnt == rem || L.w == 0;
         ++level;
     }
-    finish(L, compacted, ncand, fail, level, full, compact_level);
+    sel_stamp(ts);
+    finish(L, compacted, ncand, fail, level, full, compact_level, &ts);
+    sel_stamp(ts);
 }
 
 // Pick of one distributed level (one CTA): the single-cache kernel's pick arithmetic on the
@@ -1024,7 +1150,11 @@ static cudaError_t launch_select_t(const SelArgs& a, const KMap& km, cudaStream_
             bps = 1;
         return bps * sms;
     }();
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(wave, (a.n_slots + kSelThreads - 1) / kSelThreads));
+    // |K| = 5: a lane takes 4 slots per group, so a CTA covers 4 x kSelThreads slots per pass --
+    // small caches get no idle CTAs (each grid barrier costs more with more CTAs: C2's 100K
+    // slots ran 196 CTAs, of which 3/4 had no slot)
+    const int64_t per_cta = NK5 ? 4 * kSelThreads : kSelThreads;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(wave, (a.n_slots + per_cta - 1) / per_cta));
     SelArgs aa = a;
     KMap kk = km;
     void* args[] = {&aa, &kk};
@@ -1032,6 +1162,18 @@ static cudaError_t launch_select_t(const SelArgs& a, const KMap& km, cudaStream_
                                          : (kSelCpAsync ? (size_t)kCpRingBytes : (kSelColT ? (size_t)kColTBytes : 0)))
                            : 0;
     return cudaLaunchCooperativeKernel((const void*)k_evict_select<POLICY, GRAN, NK5>, grid, kSelThreads, args, dyn, s);
+}
+
+void sel_trace_reset(cudaStream_t s) {
+    static unsigned long long lo[kSelTraceN], hi[kSelTraceN];
+    for (int i = 0; i < kSelTraceN; ++i) { lo[i] = ~0ull; hi[i] = 0ull; }
+    cudaMemcpyToSymbolAsync(g_sel_tmin, lo, sizeof(lo), 0, cudaMemcpyHostToDevice, s);
+    cudaMemcpyToSymbolAsync(g_sel_tmax, hi, sizeof(hi), 0, cudaMemcpyHostToDevice, s);
+}
+int sel_trace_read(unsigned long long* tmin, unsigned long long* tmax) {
+    cudaMemcpyFromSymbol(tmin, g_sel_tmin, sizeof(unsigned long long) * kSelTraceN);
+    cudaMemcpyFromSymbol(tmax, g_sel_tmax, sizeof(unsigned long long) * kSelTraceN);
+    return NV_SEL_TRACE != 0 ? kSelTraceN : 0;
 }
 
 cudaError_t launch_evict_dpick(const SelArgs& a, const uint32_t* ghist, int level, cudaStream_t s) {

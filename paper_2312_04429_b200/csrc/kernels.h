@@ -174,6 +174,10 @@ struct SelArgs {
     uint32_t* level_hist;
 };
 cudaError_t launch_evict_select(const SelArgs& a, const KMap& km, cudaStream_t s);
+// experiments (NV_SEL_TRACE=1 builds): per phase-stamp index, the earliest / latest CTA time
+constexpr int kSelTraceN = 32;
+void sel_trace_reset(cudaStream_t s);
+int sel_trace_read(unsigned long long* tmin, unsigned long long* tmax);   // -> stamps compiled in (0: none)
 // The pick of one distributed level from the rank-summed histogram ghist (every rank runs it
 // with the same ghist, so every rank reaches the same state).
 cudaError_t launch_evict_dpick(const SelArgs& a, const uint32_t* ghist, int level, cudaStream_t s);

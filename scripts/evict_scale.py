@@ -2,7 +2,9 @@
 LCBFU cache_evict of 1% of the live items after a few query batches, timed end to end (the
 call is host-synchronous), then the re-insertion of as many fresh prompts as entries were
 removed; EVICT_REPS rounds (default 3).
-usage: [EVICT_REPS=n] python scripts/evict_scale.py [n_entries] [policy] [granularity]"""
+usage: [EVICT_REPS=n] python scripts/evict_scale.py [n_entries] [policy] [granularity] [alias]
+(alias 0: a latent pool of 5 slots per entry, 256 B each, whose freed slots the eviction lists
+-- as in the C2 bench cache; default 1: the aliased pool of C4/C5)"""
 import json
 import sys
 import time
@@ -18,9 +20,10 @@ def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 12_500_000
     policy = int(sys.argv[2]) if len(sys.argv) > 2 else 0
     gran = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+    alias = int(sys.argv[4]) if len(sys.argv) > 4 else 1
     D = 768
-    g = B.NirvanaCache(entry_capacity=n + 1024, latent_capacity=1 << 16, dim=D, latent_bytes=256, latent_alias=True,
-                       evict_granularity=gran)
+    g = B.NirvanaCache(entry_capacity=n + 1024, latent_capacity=(1 << 16) if alias else 5 * (n + 1024), dim=D,
+                       latent_bytes=256, latent_alias=bool(alias), evict_granularity=gran)
     g.set_evict_policy(policy)
     E = synth.TorchEntries(n, seed=5, device="cuda")
     pres = synth.present_masks(n, seed=5)
@@ -34,7 +37,7 @@ def main():
         q, _, _ = E.queries(16384, qseed=11 + r)
         g.query(q, topk=1, latents=False)
     torch.cuda.synchronize()
-    res = dict(entries=n, policy=policy, granularity=gran, insert_s=t_ins, live_items=g.live_items)
+    res = dict(entries=n, policy=policy, granularity=gran, alias=alias, insert_s=t_ins, live_items=g.live_items)
     units = g.live_entries if gran else g.live_items
     for rep in range(int(__import__("os").environ.get("EVICT_REPS", "3"))):
         k = max(1, units // 100)
