@@ -38,6 +38,12 @@ cache_status cache_debug_evict_stats(cache_t *c, int64_t *out4);
 /* Cap the fused eviction's candidate buffer (cap < 0: automatic), so the tests can force the
  * paths that compact late or never. */
 cache_status cache_debug_set_evict_cand_cap(cache_t *c, int64_t cap);
+/* The single-sweep window of cache_evict (a systematic 1/S sample estimates the n-th key, the
+ * level-0 sweep compacts every key below the estimate, the selection finishes on them): with
+ * set != 0, stride -1 = automatic, 0 = off (the two-sweep path), S = a fixed 1/S sample (S = 1:
+ * the whole cache, an exact estimate; a huge S: a biased estimate, so the tests reach the
+ * fall-back).  *last (may be null) = the last eviction's window: 0 off, 1 used, 2 missed. */
+cache_status cache_debug_evict_window(cache_t *c, int32_t stride, int32_t set, int32_t *last);
 /* Set the LCBFU access count f of item (id, K_j) (host-synchronous): the tests reach counts no
  * query stream could (the key saturation of reading R11). */
 cache_status cache_debug_set_count(cache_t *c, uint64_t id, int32_t j, uint32_t f);

@@ -659,6 +659,19 @@ def debug_set_evict_cand_cap(cache: NirvanaCache, cap: int):
     _check(_lib.cache_debug_set_evict_cand_cap(cache._h, int(cap)))
 
 
+_lib.cache_debug_evict_window.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p]
+_lib.cache_debug_evict_window.restype = ctypes.c_int
+
+
+def debug_evict_window(cache: NirvanaCache, stride=None) -> int:
+    """Set the single-sweep window's sample stride (-1 auto, 0 off, S fixed; None: leave it) and
+    return the last eviction's window outcome (0 off, 1 used, 2 estimate missed)."""
+    last = ctypes.c_int32(0)
+    _check(_lib.cache_debug_evict_window(cache._h, -1 if stride is None else int(stride), int(stride is not None),
+                                         ctypes.byref(last)))
+    return last.value
+
+
 _lib.cache_debug_set_count.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int32, ctypes.c_uint32]
 _lib.cache_debug_set_count.restype = ctypes.c_int
 

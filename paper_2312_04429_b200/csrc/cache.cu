@@ -237,6 +237,8 @@ struct cache_t {
     DevBuf<uint32_t> ebits;              // dirty-slot / dirty-id / freed-pool-slot / evicted-key bitmaps
     DevBuf<unsigned long long> eout;     // kernel-sorted evicted keys: full | masked
     int64_t last_sel[4] = {0, 0, 0, 0};  // levels, full sweeps, compaction level, candidates
+    uint32_t last_window = 0;            // single-sweep window: 0 off, 1 used, 2 estimate missed
+    int evict_sample = -1;               // window sample stride: -1 auto, 0 off, S fixed (debug)
     int64_t cand_cap_override = -1;      // test hook (cache_debug_set_evict_cand_cap); -1 = auto
     // distributed fused eviction (cache_evict_sel_*): the kernel arguments across the phases
     SelArgs dsel{};
@@ -330,7 +332,7 @@ static cudaError_t reserve_evict(cache_t* c, int64_t items, int64_t entries) {
     const int64_t ccap = std::max<int64_t>(65536, c->cap * c->num_k / 16);
     if ((e = c->ckey.ensure_grow(ccap)) != cudaSuccess) return e;
     if ((e = c->cslot.ensure_grow(ccap)) != cudaSuccess) return e;
-    if ((e = c->selws.ensure((size_t)kSelMaxLevels * kSelBins * 4 + sizeof(SelOut) + 4 * 4096 * 4)) != cudaSuccess)
+    if ((e = c->selws.ensure((size_t)(kSelMaxLevels + 1) * kSelBins * 4 + sizeof(SelOut) + 4 * 4096 * 4)) != cudaSuccess)
         return e;
     if ((e = c->ebits.ensure_grow(2 * (c->cap_pad / 32) + (c->alias ? 0 : (c->lcap + 31) / 32) + kEvBitsWords + 1024)) !=
         cudaSuccess)
@@ -1501,6 +1503,11 @@ static int bitlen(unsigned long long v) { return v ? 64 - __builtin_clzll(v) : 0
 // free slot, so allocation stays lowest-first and deterministic): one linear merge.
 static void merge_free(std::vector<int64_t>& fl, const unsigned long long* asc, int64_t k, std::vector<int64_t>& tmp) {
     if (k <= 0) return;
+    if (fl.empty() || (int64_t)asc[k - 1] < fl.back()) {   // all below the lowest free slot (the
+        fl.reserve(fl.size() + (size_t)k);                  // usual case: evictions free the oldest
+        for (int64_t j = k - 1; j >= 0; --j) fl.push_back((int64_t)asc[j]);   // slots): append
+        return;
+    }
     tmp.resize(fl.size() + (size_t)k);
     size_t i = 0, o = 0;
     int64_t j = k - 1;   // asc read backwards = descending
@@ -1666,10 +1673,14 @@ static cache_status evict_setup(cache_t* c, int64_t n_sel, int64_t n_loc, bool w
     const int64_t ccap = std::max<int64_t>(65536, units / 16);
     CK(c->ckey.ensure_grow(ccap));
     CK(c->cslot.ensure_grow(ccap));
-    const size_t ws = (size_t)kSelMaxLevels * kSelBins * 4 + sizeof(SelOut);
-    CK(c->selws.ensure(ws + 4 * 4096 * 4));
+    // [level histograms][the window estimate's sample histogram][SelOut] (zeroed), compaction totals
+    const size_t ws = (size_t)(kSelMaxLevels + 1) * kSelBins * 4 + sizeof(SelOut);
+    // compaction totals: one per 512-word chunk of each ordered-output bitmap (evict.cu)
+    const int64_t nchunks = (c->hwm + 31) / 32 / 512 + ((int64_t)(c->next_id / (uint64_t)c->world) + 32) / 32 / 512 +
+                            (c->alias ? 0 : (c->lcap + 31) / 32 / 512) + kEvBitsWords / 512 + 8;
+    CK(c->selws.ensure(ws + 4 * (size_t)std::max<int64_t>(4 * 4096, nchunks)));
     CK(cudaMemsetAsync(c->selws.p, 0, ws, s));
-    SelOut* so = reinterpret_cast<SelOut*>(c->selws.p + (size_t)kSelMaxLevels * kSelBins * 4);
+    SelOut* so = reinterpret_cast<SelOut*>(c->selws.p + (size_t)(kSelMaxLevels + 1) * kSelBins * 4);
     // bitmaps of the ordered outputs: dirty slots (< hwm), dirty ids / world (< next_id), freed
     // pool slots (< latent capacity; not tracked under aliasing)
     const int64_t w_slot = (c->hwm + 31) / 32;
@@ -1689,6 +1700,9 @@ static cache_status evict_setup(cache_t* c, int64_t n_sel, int64_t n_loc, bool w
     a.n_slots = c->hwm;
     a.n = (unsigned long long)n_sel;
     a.hist = reinterpret_cast<uint32_t*>(c->selws.p);
+    a.hist_s = a.hist + (size_t)kSelMaxLevels * kSelBins;
+    a.units = (unsigned long long)units;
+    a.sample = 0;   // the single-cache call turns the window on (evict_impl)
     a.cand_key = c->ckey.p;
     a.cand_slot = c->cslot.p;
     a.cand_cap = (unsigned long long)(c->cand_cap_override >= 0 ? std::min<int64_t>(c->cand_cap_override, c->ckey.n)
@@ -1731,6 +1745,15 @@ static cache_status evict_impl(cache_t* c, int64_t n, bool want_ev, bool want_di
     SelArgs a;
     cache_status rs = evict_setup(c, n, n, want_ev, a, s);
     if (rs != CACHE_OK) return rs;
+    // Single-sweep window (evict.cu): estimate the n-th key from every S-th slot (S <= 64, >= ~16K
+    // sampled slots), then one full sweep histograms every key
+    // AND compacts every key below the estimate's upper bin edge; when the n-th key's bin lies
+    // below it (else the two-sweep path runs), the selection and the apply run on the candidates.
+    if (c->evict_sample != 0 && 2 * (unsigned long long)n <= a.cand_cap)
+        // odd strides: a power-of-two stride kept hitting the same HBM channels (the 1/64 sample of
+        // 12.5M slots took 15 us, NV_SEL_TRACE)
+        a.sample = c->evict_sample > 0 ? c->evict_sample
+                                       : (int)(std::max<int64_t>(1, std::min<int64_t>(63, c->hwm / 16384)) | 1);
     SelOut* so = a.out;
     const int64_t dbound = std::max<int64_t>(1, std::min<int64_t>(n, c->live_entries));
     const int64_t pbound = entry_mode ? n * c->num_k : n;
@@ -1754,7 +1777,8 @@ static cache_status evict_impl(cache_t* c, int64_t n, bool want_ev, bool want_di
     c->last_sel[0] = h.levels;
     c->last_sel[1] = h.full_sweeps;
     c->last_sel[2] = h.compact_level;
-    c->last_sel[3] = (int64_t)h.cnt[3];
+    c->last_sel[3] = (int64_t)(h.window == 1 ? h.cnt_w : h.cnt[3]);
+    c->last_window = h.window;
     const int64_t got = (int64_t)h.cnt[0], nd = (int64_t)h.cnt[1];
     const int64_t nfreed = entry_mode ? (int64_t)h.cnt[2] : got;
     if (h.err || got != n || nd > dbound || nfreed > pbound)
@@ -1778,8 +1802,24 @@ static cache_status evict_impl(cache_t* c, int64_t n, bool want_ev, bool want_di
                      tf[2] - t0, h.levels, h.full_sweeps, h.compact_level, h.cnt[3], bitlen(h.T - kmin), (long long)nd);
         // NV_SEL_TRACE builds: phase stamps relative to the earliest CTA start (us), first / last CTA
         unsigned long long lo[kSelTraceN], hi[kSelTraceN];
-        const int ns = sel_trace_read(lo, hi);
+        static unsigned long long cta[kSelTraceCta][1024];
+        const int ns = sel_trace_read(lo, hi, &cta[0][0]);
         if (ns) {
+            // per-CTA: the time between consecutive early stamps, the 6 slowest CTAs of each
+            int grid = 0;
+            while (grid < 1024 && cta[0][grid] >= lo[0] && cta[0][grid] - lo[0] < 100000000ull) ++grid;
+            std::fprintf(stderr, "{\"sel_cta_grid\": %d, \"slowest\": [", grid);
+            for (int st = 1; st < kSelTraceCta && hi[st]; ++st) {
+                std::vector<std::pair<double, int>> d;
+                for (int b = 0; b < grid; ++b) d.push_back({(cta[st][b] - cta[st - 1][b]) * 1e-3, b});
+                std::sort(d.begin(), d.end());
+                std::fprintf(stderr, "%s{\"stamp\": %d, \"median_us\": %.2f, \"top\": [", st > 1 ? ", " : "", st,
+                             d.empty() ? 0.0 : d[d.size() / 2].first);
+                for (int k = 0; k < 6 && k < (int)d.size(); ++k)
+                    std::fprintf(stderr, "%s[%d, %.2f]", k ? ", " : "", d[d.size() - 1 - k].second, d[d.size() - 1 - k].first);
+                std::fprintf(stderr, "]}");
+            }
+            std::fprintf(stderr, "]}\n");
             std::fprintf(stderr, "{\"sel_phases_us\": [");
             bool first = true;
             for (int i = 0; i < ns && hi[i]; ++i) {
@@ -2152,6 +2192,15 @@ extern "C" cache_status cache_debug_set_count(cache_t* c, uint64_t id, int32_t j
     if (e < 0) return fail(CACHE_E_INVALID_ARG, "cache_debug_set_count: id not live");
     DeviceGuard g(c->device);
     CK(cudaMemcpy(c->fcnt + e * c->num_k + j, &f, 4, cudaMemcpyHostToDevice));
+    return CACHE_OK;
+}
+
+// Single-sweep window of the fused eviction: stride -1 = auto, 0 = off, S = a fixed 1/S sample.
+// Returns the last eviction's window outcome in *last (0 off, 1 used, 2 estimate missed).
+extern "C" cache_status cache_debug_evict_window(cache_t* c, int32_t stride, int32_t set, int32_t* last) {
+    if (!c) return fail(CACHE_E_INVALID_ARG, "cache_debug_evict_window: null cache");
+    if (set) c->evict_sample = stride < 0 ? -1 : stride;
+    if (last) *last = (int32_t)c->last_window;
     return CACHE_OK;
 }
 

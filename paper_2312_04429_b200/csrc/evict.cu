@@ -57,6 +57,7 @@ constexpr int kCpRingBytes = kCpStages * kSelThreads * 112;
 #define NV_SEL_TRACE 0
 #endif
 __device__ unsigned long long g_sel_tmin[kSelTraceN], g_sel_tmax[kSelTraceN];
+__device__ unsigned long long g_sel_cta[kSelTraceCta][1024];   // the first stamps, per CTA
 __device__ __forceinline__ void sel_stamp(int& i) {
     if constexpr (NV_SEL_TRACE != 0) {
         if (threadIdx.x == 0 && i < kSelTraceN) {
@@ -64,6 +65,7 @@ __device__ __forceinline__ void sel_stamp(int& i) {
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
             atomicMin(&g_sel_tmin[i], t);
             atomicMax(&g_sel_tmax[i], t);
+            if (i < kSelTraceCta && blockIdx.x < 1024) g_sel_cta[i][blockIdx.x] = t;
         }
         ++i;
     }
@@ -130,6 +132,21 @@ __device__ PickRes sel_pick(const uint32_t* h, unsigned long long target) {
     return r;
 }
 
+// Every CTA: the number of keys in histogram h.
+__device__ unsigned long long sel_total(const uint32_t* h) {
+    __shared__ unsigned long long s_t[kSelThreads / 32];
+    unsigned long long x = 0;
+    for (int i = threadIdx.x; i < kSelBins; i += kSelThreads) x += __ldcg(h + i);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
+    if ((threadIdx.x & 31) == 0) s_t[threadIdx.x >> 5] = x;
+    __syncthreads();
+    unsigned long long t = 0;
+    for (int i = 0; i < kSelThreads / 32; ++i) t += s_t[i];
+    __syncthreads();
+    return t;
+}
+
 // Sweep modes (uniform over the grid within a phase)
 enum { kSweepL0 = 0, kSweepLevel = 1, kSweepFinal = 2 };
 
@@ -175,6 +192,11 @@ __device__ __forceinline__ void sel_unit_common(const SelArgs& a, int mode, cons
         if (live) {
             run.add(sh, sel_bin0(key));
             kmin = key < kmin ? key : kmin;
+        }
+        if (L.compact) {   // warp-uniform: the single-sweep window, every key < L.T
+            const bool inw = live && key < L.T;
+            const unsigned long long at = warp_claim(&a.out->cnt_w, inw, lane);
+            if (inw && at < a.cand_cap) { a.cand_key[at] = key; a.cand_slot[at] = slot; }
         }
         return;
     }
@@ -366,6 +388,7 @@ __device__ __forceinline__ void sweep_items_v4(const SelArgs& a, const int (&kv)
         }
         const unsigned long long k0 = mk_key(S, id, __ffs(m) - 1), k1 = mk_key(S, id, 31 - __clz(m));
         bool done = false;
+        bool wdone = !(mode == kSweepL0 && L.compact);   // single-sweep window bits (keys < L.T)
         if (uni) {
             if (mode == kSweepL0) {
                 const uint32_t b = sel_bin0(k0);
@@ -373,6 +396,10 @@ __device__ __forceinline__ void sweep_items_v4(const SelArgs& a, const int (&kv)
                     run.add_n(sh, b, (unsigned)__popc(m));
                     kmin = k0 < kmin ? k0 : kmin;
                     done = true;
+                }
+                if (!wdone) {
+                    if (k1 < L.T) { inm |= m << (5 * q); wdone = true; }
+                    else if (k0 >= L.T) wdone = true;
                 }
             } else if (mode == kSweepFinal) {
                 if (k1 <= L.T) { evm |= m << (5 * q); done = true; }
@@ -389,14 +416,17 @@ __device__ __forceinline__ void sweep_items_v4(const SelArgs& a, const int (&kv)
                 }
             }
         }
-        if (!done) {
+        if (!done || !wdone) {
 #pragma unroll
             for (int j = 0; j < 5; ++j) {
                 if (!((m >> j) & 1u)) continue;
                 const unsigned long long key = mk_key(sat_score<POLICY>(c[5 * q + j], kv[j], lim[j]), id, j);
                 if (mode == kSweepL0) {
-                    run.add(sh, sel_bin0(key));
-                    kmin = key < kmin ? key : kmin;
+                    if (!done) {
+                        run.add(sh, sel_bin0(key));
+                        kmin = key < kmin ? key : kmin;
+                    }
+                    if (!wdone && key < L.T) inm |= 1u << (5 * q + j);
                 } else if (mode == kSweepFinal) {
                     if (key <= L.T) evm |= 1u << (5 * q + j);
                 } else if (key < L.lo) {
@@ -408,7 +438,26 @@ __device__ __forceinline__ void sweep_items_v4(const SelArgs& a, const int (&kv)
             }
         }
     }
-    if (mode == kSweepL0) return;
+    if (mode == kSweepL0) {
+        if (L.compact && __any_sync(0xFFFFFFFFu, inm != 0u)) {   // warp-uniform: the window's (key, slot) pairs
+            unsigned long long wpos = warp_reserve(&a.out->cnt_w, (uint32_t)__popc(inm), lane);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t inq = (inm >> (5 * q)) & 31u;
+                if (!inq) continue;
+#pragma unroll
+                for (int j = 0; j < 5; ++j) {
+                    if (!((inq >> j) & 1u)) continue;
+                    if (wpos < a.cand_cap) {
+                        a.cand_key[wpos] = mk_key(sat_score<POLICY>(c[5 * q + j], kv[j], lim[j]), pid[q], j);
+                        a.cand_slot[wpos] = (uint32_t)(e4 + q);
+                    }
+                    ++wpos;
+                }
+            }
+        }
+        return;
+    }
     // outputs: evicted keys (one warp reservation), candidates, presence / counters / dirty
     unsigned long long pos = warp_reserve(&a.out->cnt[0], (uint32_t)__popc(evm), lane);
     unsigned long long cpos = 0;
@@ -591,6 +640,75 @@ __device__ __forceinline__ void sel_cand(const SelArgs& a, const KMap& km, int m
     }
 }
 
+// The final apply over the candidates, item mode (the single-sweep window's whole apply: ~n
+// candidates), warp-aggregated: the candidates of one slot sit in consecutive buffer positions
+// (a lane compacts a slot's items together), so each run of lanes with the same slot clears its
+// presence bits with ONE atomicAnd (the run that clears the slot's last bit makes it dirty), and
+// the evicted-key, pool-slot, dirty-slot and dirty-id bitmaps take one atomic per word.  (Per
+// candidate, the atomics on shared words serialised: 41 us for 619K candidates, NV_SEL_TRACE.)
+// ev_list: also write the unsorted evicted-key list (only when the key bitmap may not cover every
+// evicted key: one counter claim per warp and iteration -- one address, so ~20K serialised
+// atomics over a 619K-item apply); the counts go to *nev / *ndirty (per lane, summed by the caller).
+__device__ __forceinline__ void cand_apply_item(const SelArgs& a, int nk, const SelLevel& L, int64_t i, bool valid,
+                                                int lane, bool ev_list, uint32_t& nev, uint32_t& ndirty) {
+    const unsigned long long key = valid ? __ldcg(a.cand_key + i) : ~0ull;
+    const uint32_t e = valid ? __ldcg(a.cand_slot + i) : 0xFFFFFFFFu;
+    const bool ev = valid && key <= L.T;
+    const int j = (int)(key & 7ull);
+    if (ev_list) {   // grid-uniform
+        const unsigned long long at = warp_claim(&a.out->cnt[0], ev, lane);
+        if (ev && at < a.ev_cap) a.ev_key[at] = key;
+    } else {
+        nev += ev ? 1u : 0u;
+    }
+    if (L.ev_lim) {   // grid-uniform
+        WordRun r;
+        if (ev) {
+            const unsigned long long d = key - L.kb;
+            if (d >= L.ev_lim) atomicExch(&a.out->ev_over, 1u);   // overflow: sort on the host side
+            else r.add(a.ev_bits, (uint32_t)d);
+        }
+        r.warp_flush(a.ev_bits, lane);
+    }
+    if (a.pool_bits) {   // grid-uniform
+        WordRun r;
+        if (ev) {
+            const int32_t ps = __ldg(a.lslot + (int64_t)e * nk + j);
+            if (ps >= 0) r.add(a.pool_bits, (uint32_t)ps);
+        }
+        r.warp_flush(a.pool_bits, lane);
+    }
+    if (ev) a.fcnt[(int64_t)e * nk + j] = 0u;
+    // presence: a segmented OR over runs of lanes with the same slot (strictly contiguous runs:
+    // a slot repeated further on forms its own run with disjoint bits)
+    const uint32_t me = ev ? e : 0xFFFFFFFFu;
+    const uint32_t prev = __shfl_up_sync(0xFFFFFFFFu, me, 1);
+    const bool start = lane == 0 || prev != me;
+    const unsigned starts = __ballot_sync(0xFFFFFFFFu, start);
+    const unsigned after = starts & ~((2u << lane) - 1u);   // (2u << 31) == 0: no later run
+    const int nh = after ? __ffs(after) - 1 : 32;           // first lane of the next run
+    uint32_t acc = ev ? (1u << j) : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t ob = __shfl_down_sync(0xFFFFFFFFu, acc, o);
+        if (lane + o < nh) acc |= ob;
+    }
+    bool dirty = false;
+    if (ev && start) {
+        const uint32_t old = atomicAnd(a.present + e, ~acc);
+        dirty = (old & ~acc) == 0u;
+        if (dirty) a.inv_e[e] = __int_as_float(0x7FC00000);
+    }
+    WordRun ds, di;
+    if (dirty) {
+        ds.add(a.dslot_bits, e);
+        di.add(a.did_bits, (uint32_t)((key >> 3) & 0xFFFFFFFFull) / (uint32_t)a.world);
+    }
+    ds.warp_flush(a.dslot_bits, lane);
+    di.warp_flush(a.did_bits, lane);
+    ndirty += dirty ? 1u : 0u;
+}
+
 // Ordered compaction of the bitmaps into ascending lists (dirty slots, dirty ids, freed pool
 // slots, evicted keys): per CTA a contiguous word range; CTA totals are exchanged through global
 // memory across one grid barrier.  Inside a CTA the range goes in rounds of kSelThreads words
@@ -631,54 +749,130 @@ __device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t x, uint32_t* to
 
 template <int NJ>
 __device__ void compact_bitmaps(const BitJob (&jobs)[NJ], uint32_t* part, cg::grid_group& grid, int& ts) {
-    int64_t r0[NJ], r1[NJ];
+    // Chunks of kSelThreads words (one per thread) of the jobs' bitmaps, concatenated and dealt
+    // round-robin to the CTAs (flat chunk f -> CTA f % grid): the dense runs of the dirty bitmaps
+    // (the oldest slots) land on many CTAs (contiguous per-CTA ranges left 3 CTAs emitting 125K
+    // values each: a 25-us tail per list, NV_SEL_TRACE).  part[f] = chunk totals; after the grid
+    // barrier every CTA scans ALL the totals (a few per thread) for the bases of its own chunks,
+    // so no chunk waits on another; loads are batched kCB chunks at a time.
+    constexpr int kCB = 8, kOwnMax = 256;
+    __shared__ uint32_t s_red[kCB][kSelThreads / 32];
+    __shared__ uint32_t s_base[kOwnMax];    // global prefix of own chunk k (all jobs)
+    __shared__ uint32_t s_jpre[NJ];         // global prefix at each job's first chunk
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t G = gridDim.x;
+    int64_t nch[NJ], off[NJ];
+    int64_t total = 0;
 #pragma unroll
     for (int q = 0; q < NJ; ++q) {
-        const int64_t wb = (jobs[q].words + gridDim.x - 1) / gridDim.x;
-        r0[q] = min(jobs[q].words, (int64_t)blockIdx.x * wb);
-        r1[q] = min(jobs[q].words, r0[q] + wb);
-        uint32_t c = 0;
-        if (jobs[q].bits)
-            for (int64_t w = r0[q] + threadIdx.x; w < r1[q]; w += kSelThreads) c += __popc(__ldcg(jobs[q].bits + w));
-        uint32_t tot = 0;
-        (void)block_excl_scan_u32(c, &tot);
-        if (threadIdx.x == 0) part[q * gridDim.x + blockIdx.x] = tot;
+        nch[q] = jobs[q].bits ? (jobs[q].words + kSelThreads - 1) / kSelThreads : 0;
+        off[q] = total;
+        total += nch[q];
+    }
+    auto job_of = [&](int64_t f) {
+        int q = 0;
+#pragma unroll
+        for (int k = 1; k < NJ; ++k)
+            if (f >= off[k] && nch[k]) q = k;
+        return q;
+    };
+    auto word_of = [&](int64_t f) -> uint32_t {   // this thread's word of flat chunk f
+        if (f >= total) return 0u;
+        const int q = job_of(f);
+        const int64_t w = (f - off[q]) * kSelThreads + threadIdx.x;
+        uint32_t m = 0u;
+#pragma unroll
+        for (int k = 0; k < NJ; ++k)
+            if (k == q && w < jobs[k].words) m = __ldcg(jobs[k].bits + w);
+        return m;
+    };
+    // part 1: the totals of this CTA's chunks
+    for (int64_t f0 = blockIdx.x; f0 < total; f0 += kCB * G) {   // CTA-uniform
+        uint32_t cnt[kCB];
+#pragma unroll
+        for (int k = 0; k < kCB; ++k) cnt[k] = word_of(f0 + k * G);
+#pragma unroll
+        for (int k = 0; k < kCB; ++k) {
+            uint32_t v = __popc(cnt[k]);
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+            if (lane == 0) s_red[k][warp] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x < kCB && f0 + threadIdx.x * G < total) {
+            uint32_t t = 0;
+#pragma unroll
+            for (int i = 0; i < kSelThreads / 32; ++i) t += s_red[threadIdx.x][i];
+            part[f0 + threadIdx.x * G] = t;
+        }
+        __syncthreads();
     }
     sel_stamp(ts);
     grid.sync();
     sel_stamp(ts);
+    // every CTA: exclusive scan of all totals (thread t: a contiguous run of them)
+    {
+        const int64_t per = (total + kSelThreads - 1) / kSelThreads;
+        const int64_t i0 = min(total, (int64_t)threadIdx.x * per), i1 = min(total, i0 + per);
+        uint32_t sum = 0;
+        for (int64_t i = i0; i < i1; ++i) sum += __ldcg(part + i);
+        uint32_t tot = 0;
+        uint32_t run = block_excl_scan_u32(sum, &tot);
+        for (int64_t i = i0; i < i1; ++i) {
 #pragma unroll
-    for (int q = 0; q < NJ; ++q) {
-        if (!jobs[q].bits) continue;   // grid-uniform
-        uint32_t lower = 0;
-        for (int b = threadIdx.x; b < (int)blockIdx.x; b += kSelThreads) lower += __ldcg(part + q * gridDim.x + b);
-        uint32_t base = 0;
-        (void)block_excl_scan_u32(lower, &base);   // the CTAs before this one
-        const BitJob J = jobs[q];
-        for (int64_t rb = r0[q]; rb < r1[q]; rb += kSelThreads) {   // CTA-uniform
-            const int64_t w = rb + threadIdx.x;
-            const uint32_t m = w < r1[q] ? __ldcg(J.bits + w) : 0u;
+            for (int q = 0; q < NJ; ++q)
+                if (nch[q] && i == off[q]) s_jpre[q] = run;
+            if (i >= blockIdx.x && (i - blockIdx.x) % G == 0 && (i - blockIdx.x) / G < kOwnMax)
+                s_base[(i - blockIdx.x) / G] = run;
+            run += __ldcg(part + i);
+        }
+        __syncthreads();
+    }
+    // part 2: emission, kCB own chunks per batch (their words loaded together)
+    for (int64_t f0 = blockIdx.x, k0 = 0; f0 < total; f0 += kCB * G, k0 += kCB) {   // CTA-uniform
+        uint32_t mw[kCB];
+#pragma unroll
+        for (int k = 0; k < kCB; ++k) mw[k] = word_of(f0 + k * G);
+#pragma unroll
+        for (int k = 0; k < kCB; ++k) {
+            const int64_t f = f0 + k * G;
+            if (f >= total) break;   // CTA-uniform
+            const int q = job_of(f);
+            const int64_t c = f - off[q];
+            uint32_t base;
+            if (k0 + k < kOwnMax) {
+                base = s_base[k0 + k] - s_jpre[q];
+            } else {   // more own chunks than the table holds: sum the job's earlier totals
+                uint32_t v = 0;
+                for (int64_t i = off[q] + threadIdx.x; i < f; i += kSelThreads) v += __ldcg(part + i);
+                (void)block_excl_scan_u32(v, &base);
+            }
+            const uint32_t m = mw[k];
             uint32_t tot = 0;
-            const uint32_t off = block_excl_scan_u32((uint32_t)__popc(m), &tot);
+            const uint32_t offw = block_excl_scan_u32((uint32_t)__popc(m), &tot);
+            unsigned long long* out = nullptr;
+            unsigned long long* out2 = nullptr;
+            unsigned long long mul = 0, add = 0, mask2 = 0;
+#pragma unroll
+            for (int kk = 0; kk < NJ; ++kk)
+                if (kk == q) { out = jobs[kk].out; out2 = jobs[kk].out2; mul = jobs[kk].mul; add = jobs[kk].add; mask2 = jobs[kk].mask2; }
             unsigned nz = __ballot_sync(0xFFFFFFFFu, m != 0u);
-            while (nz) {   // warp-uniform
+            while (nz) {   // warp-uniform: one word at a time, lane = bit (coalesced stores)
                 const int j = __ffs(nz) - 1;
                 nz &= nz - 1u;
                 const uint32_t mj = __shfl_sync(0xFFFFFFFFu, m, j);
-                const uint32_t oj = __shfl_sync(0xFFFFFFFFu, off, j);
+                const uint32_t oj = __shfl_sync(0xFFFFFFFFu, offw, j);
                 if ((mj >> lane) & 1u) {
                     const unsigned long long pos = (unsigned long long)base + oj + __popc(mj & ((1u << lane) - 1u));
-                    const int64_t bit = (rb + warp * 32 + j) * 32 + lane;
-                    const unsigned long long v = (unsigned long long)bit * J.mul + J.add;
-                    if (J.out2) J.out2[pos] = v & J.mask2;
-                    J.out[pos] = v;
+                    const int64_t bit = (c * kSelThreads + warp * 32 + j) * 32 + lane;
+                    const unsigned long long v = (unsigned long long)bit * mul + add;
+                    if (out2) out2[pos] = v & mask2;
+                    out[pos] = v;
                 }
             }
-            base += tot;
         }
-        sel_stamp(ts);
     }
+    sel_stamp(ts);
 }
 
 // NK5: |K| = 5 (the paper's): every lane loads 4 consecutive slots with 16-byte loads (presence,
@@ -934,16 +1128,42 @@ __global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : ((kSelC
         const int64_t cper = (((nc + gridDim.x - 1) / gridDim.x) + 31) & ~(int64_t)31;
         const int64_t c0 = (int64_t)blockIdx.x * cper, c1 = min(nc, c0 + cper);
         DigitRun run;
+        // item-mode apply: the evicted-key list only if the bitmap can miss a key (the host side
+        // then sorts it); counts summed per CTA, one global atomic per CTA
+        const bool ev_list = !(L.ev_lim && L.T >= L.kb && L.T - L.kb < L.ev_lim);
+        uint32_t nev = 0, ndirty = 0;
         for (int64_t i0 = c0 + warp * 32; i0 < c1; i0 += kSelThreads) {
             const int64_t i = i0 + lane;
-            sel_cand<POLICY, GRAN>(a, km, mode, L, i, i < c1, sh, run, lane);
+            if (GRAN == CACHE_EVICT_ITEM && mode == kSweepFinal)
+                cand_apply_item(a, km.num_k, L, i, i < c1, lane, ev_list, nev, ndirty);
+            else
+                sel_cand<POLICY, GRAN>(a, km, mode, L, i, i < c1, sh, run, lane);
         }
         run.flush(sh);
+        if (GRAN == CACHE_EVICT_ITEM && mode == kSweepFinal) {
+            __shared__ unsigned long long s_cnt[2];
+            if (threadIdx.x < 2) s_cnt[threadIdx.x] = 0ull;
+            __syncthreads();
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) {
+                nev += __shfl_xor_sync(0xFFFFFFFFu, nev, o);
+                ndirty += __shfl_xor_sync(0xFFFFFFFFu, ndirty, o);
+            }
+            if (lane == 0) {
+                if (nev) atomicAdd(&s_cnt[0], (unsigned long long)nev);
+                if (ndirty) atomicAdd(&s_cnt[1], (unsigned long long)ndirty);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                if (s_cnt[0]) atomicAdd(&a.out->cnt[0], s_cnt[0]);
+                if (s_cnt[1]) atomicAdd(&a.out->cnt[1], s_cnt[1]);
+            }
+        }
     };
 
     // final apply (the candidates <= T, or one more full sweep), then the ordered lists
     auto finish = [&](SelLevel L, bool compacted, int64_t ncand, bool fail, int level, int full,
-                      int compact_level, int* tsp = nullptr) {
+                      int compact_level, int* tsp = nullptr, uint32_t window = 0u) {
         int ts_dummy = 0;
         int& ts = tsp ? *tsp : ts_dummy;
         unsigned long long kmin_unused = ~0ull;
@@ -977,6 +1197,7 @@ __global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : ((kSelC
             compact_bitmaps<4>(jobs, a.part, grid, ts);
         }
         if (blockIdx.x == 0 && threadIdx.x == 0) {
+            a.out->window = window;
             a.out->T = L.T;
             a.out->levels = (uint32_t)level;
             a.out->full_sweeps = (uint32_t)full;
@@ -1027,6 +1248,56 @@ __global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : ((kSelC
     int ts = 0;
     sel_stamp(ts);
     SelLevel L{0ull, 0ull, 64, 0, false, 0ull, 0ull};
+    // Single-sweep window: a systematic 1/S sample of the slots estimates the n-th key; its
+    // rank r = n * (sampled units / live units) is padded by 4 sqrt(r) + 16, and the upper edge
+    // of the sample bin holding that rank becomes the window hi.  The level-0 sweep then also
+    // compacts every key < hi.  If the n-th key's level-0 bin ends below hi (and nothing
+    // overflowed the buffer), every key the selection can still pick is a candidate: the levels
+    // and the apply run on the candidates and the second full sweep is skipped.  Otherwise the
+    // usual path runs -- the estimate only decides speed, never the result.
+    if (a.sample > 0) {
+        // every S-th block of 32 slots, a warp per block (lane = slot: every load a full line).
+        // Single slots every S slots (random 4-B accesses) ran at a fraction of the HBM rate:
+        // 15 us for the 1/63 sample of 12.5M slots (NV_SEL_TRACE)
+        clear_sh();
+        unsigned long long kdummy = ~0ull;
+        DigitRun run;
+        const uint32_t* colp = policy_col<POLICY>(a);
+        const int64_t S = a.sample, nblk = (a.n_slots + 31) / 32, nw = (int64_t)gridDim.x * (kSelThreads / 32);
+        for (int64_t bi = (int64_t)blockIdx.x * (kSelThreads / 32) + warp; bi * S < nblk; bi += nw) {
+            const int64_t e = bi * S * 32 + lane;   // e < the 256-padded capacity
+            const uint32_t m = e < a.n_slots ? __ldcg(a.present + e) : 0u, id = __ldcg(a.ids + e);
+            uint32_t col[CACHE_MAX_K];
+#pragma unroll
+            for (int j = 0; j < CACHE_MAX_K; ++j)
+                col[j] = (POLICY != CACHE_POLICY_FIFO && j < nk) ? __ldcg(colp + e * nk + j) : 0u;
+            sel_slot<POLICY, GRAN>(a, nk, kv, kSweepL0, L, e, m, id, col, sh, run, kdummy, lane);
+        }
+        run.flush(sh);
+        sel_stamp(ts);
+        flush_sh(a.hist_s);
+        grid.sync();
+        sel_stamp(ts);
+        const unsigned long long ns = sel_total(a.hist_s);
+        if (ns && a.units) {
+            // pad: 4 sigma of the sampling noise + two sample blocks' worth of units (on keys
+            // that grow with the slot, a 32-slot block is the sample's resolution)
+            const double r = ceil((double)a.n * (double)ns / (double)a.units);
+            const unsigned long long rhi =
+                (unsigned long long)(r + 4.0 * sqrt(r) + 64.0 * (GRAN == CACHE_EVICT_ITEM ? nk : 1) + 16.0);
+            if (rhi <= ns) {
+                const PickRes ps = sel_pick(a.hist_s, rhi);
+                unsigned long long lo_s = 0;
+                int w_s = 0;
+                if (ps.bin < (uint32_t)kSelBins) {
+                    sel_bin0_range(ps.bin, lo_s, w_s);
+                    const unsigned long long hi = lo_s + (1ull << w_s);
+                    if (hi > lo_s) { L.T = hi; L.compact = true; }   // not past 2^64
+                }
+            }
+        }
+        sel_stamp(ts);
+    }
     clear_sh();
     unsigned long long kmin = ~0ull;
     full_sweep(kSweepL0, L, kmin);
@@ -1035,6 +1306,10 @@ __global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : ((kSelC
     kmin_to_global(kmin);
     grid.sync();
     sel_stamp(ts);
+    const bool windowed = L.compact;
+    const unsigned long long whi = L.T;
+    L.compact = false;
+    L.T = 0ull;
     L.kb = ~__ldcg(&a.out->kmin_inv);
     L.ev_lim = a.ev_bits ? (unsigned long long)a.ev_bits_words * 32ull : 0ull;
     PickRes p = sel_pick(a.hist, a.n);
@@ -1045,6 +1320,18 @@ __global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : ((kSelC
     bool compacted = false;
     int64_t ncand = 0;
     int level = 1, full = 1, compact_level = 0;
+    uint32_t window = 0;
+    if (windowed) {
+        const unsigned long long nw = __ldcg(&a.out->cnt_w);
+        // T <= lo + 2^w - 1 whatever the levels pick: inside the window iff that is < whi
+        if (!fail && nw <= a.cand_cap && L.lo + ((1ull << L.w) - 1ull) < whi) {
+            compacted = true;
+            ncand = (int64_t)nw;
+            window = 1;
+        } else {
+            window = 2;
+        }
+    }
     while (!done) {
         const int D = L.w < 12 ? L.w : 12;
         L.shift = L.w - D;
@@ -1076,7 +1363,7 @@ __global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : ((kSelC
         ++level;
     }
     sel_stamp(ts);
-    finish(L, compacted, ncand, fail, level, full, compact_level, &ts);
+    finish(L, compacted, ncand, fail, level, full, compact_level, &ts, window);
     sel_stamp(ts);
 }
 
@@ -1170,9 +1457,10 @@ void sel_trace_reset(cudaStream_t s) {
     cudaMemcpyToSymbolAsync(g_sel_tmin, lo, sizeof(lo), 0, cudaMemcpyHostToDevice, s);
     cudaMemcpyToSymbolAsync(g_sel_tmax, hi, sizeof(hi), 0, cudaMemcpyHostToDevice, s);
 }
-int sel_trace_read(unsigned long long* tmin, unsigned long long* tmax) {
+int sel_trace_read(unsigned long long* tmin, unsigned long long* tmax, unsigned long long* cta) {
     cudaMemcpyFromSymbol(tmin, g_sel_tmin, sizeof(unsigned long long) * kSelTraceN);
     cudaMemcpyFromSymbol(tmax, g_sel_tmax, sizeof(unsigned long long) * kSelTraceN);
+    if (cta) cudaMemcpyFromSymbol(cta, g_sel_cta, sizeof(unsigned long long) * kSelTraceCta * 1024);
     return NV_SEL_TRACE != 0 ? kSelTraceN : 0;
 }
 

@@ -122,6 +122,8 @@ struct SelOut {
     unsigned long long T;         // threshold: every unit with key <= T was evicted
     uint32_t levels, full_sweeps, compact_level, err;
     uint32_t ev_sorted, ev_over;  // evicted keys emitted sorted (bitmap path) / one fell beyond the bitmap
+    unsigned long long cnt_w;     // single-sweep window: keys compacted by the level-0 sweep
+    uint32_t window, pad;         // 0 off, 1 the selection ran on the window, 2 the estimate missed
 };
 constexpr int kSelBins = 4096, kSelMaxLevels = 8;
 // Selection state between the host-driven phases of the DISTRIBUTED fused eviction (each rank
@@ -145,6 +147,9 @@ struct SelArgs {
     int64_t n_slots;
     unsigned long long n;              // units to evict (<= live units)
     uint32_t* hist;                    // [kSelMaxLevels][kSelBins], zeroed by the caller
+    uint32_t* hist_s;                  // [kSelBins] zeroed: the window estimate's sample histogram
+    unsigned long long units;          // live units (the sample's rank scale)
+    int sample;                        // single cache: window sample stride S (0: two-sweep path)
     unsigned long long* cand_key;      // candidate compaction buffers
     uint32_t* cand_slot;
     unsigned long long cand_cap;
@@ -175,9 +180,10 @@ struct SelArgs {
 };
 cudaError_t launch_evict_select(const SelArgs& a, const KMap& km, cudaStream_t s);
 // experiments (NV_SEL_TRACE=1 builds): per phase-stamp index, the earliest / latest CTA time
-constexpr int kSelTraceN = 32;
+constexpr int kSelTraceN = 32, kSelTraceCta = 6;
 void sel_trace_reset(cudaStream_t s);
-int sel_trace_read(unsigned long long* tmin, unsigned long long* tmax);   // -> stamps compiled in (0: none)
+// -> stamps compiled in (0: none); cta (may be null): [kSelTraceCta][1024] per-CTA times of the first stamps
+int sel_trace_read(unsigned long long* tmin, unsigned long long* tmax, unsigned long long* cta);
 // The pick of one distributed level from the rank-summed histogram ghist (every rank runs it
 // with the same ghist, so every rank reaches the same state).
 cudaError_t launch_evict_dpick(const SelArgs& a, const uint32_t* ghist, int level, cudaStream_t s);

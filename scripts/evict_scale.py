@@ -25,6 +25,8 @@ def main():
     g = B.NirvanaCache(entry_capacity=n + 1024, latent_capacity=(1 << 16) if alias else 5 * (n + 1024), dim=D,
                        latent_bytes=256, latent_alias=bool(alias), evict_granularity=gran)
     g.set_evict_policy(policy)
+    if "EVICT_WINDOW" in __import__("os").environ:   # the single-sweep window's stride (-1 auto, 0 off)
+        B.debug_evict_window(g, int(__import__("os").environ["EVICT_WINDOW"]))
     E = synth.TorchEntries(n, seed=5, device="cuda")
     pres = synth.present_masks(n, seed=5)
     t0 = time.perf_counter()

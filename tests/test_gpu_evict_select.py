@@ -90,6 +90,7 @@ def test_fused_evict_paths(oracle_mod, policy, gran, cap):
     level sweeps and the apply run over the slot columns), small caps compact late."""
     B, g, o = _pair(oracle_mod, 1500, policy, gran, seed=70 + policy, zipf_hot=(policy in (0, 2)))
     B.debug_set_evict_cand_cap(g, cap)
+    B.debug_evict_window(g, 0)   # the two-sweep path (the window has its own test)
     rng = np.random.default_rng(policy * 10 + gran)
     for rnd in range(4):
         units = g.evict_units
@@ -98,6 +99,64 @@ def test_fused_evict_paths(oracle_mod, policy, gran, cap):
         if cap == 0:
             assert st["compact_level"] == 0
         _query_both(g, o, np.asarray(synth.entries(32, seed=500 + rnd)[0]))
+
+
+@pytest.mark.parametrize("gran", [0, 1])
+@pytest.mark.parametrize("policy", [0, 1, 2, 3])
+@pytest.mark.parametrize("stride", [1, 3, -1])
+def test_single_sweep_window(oracle_mod, policy, gran, stride):
+    """The single-sweep window: stride 1 samples every slot (the estimate is exact, so the
+    selection always finishes on the level-0 candidates), 3 every third slot, -1 the automatic
+    stride.  Every outcome must evict exactly what the oracle evicts."""
+    B, g, o = _pair(oracle_mod, 1500, policy, gran, seed=170 + policy, zipf_hot=(policy in (0, 2)))
+    B.debug_evict_window(g, stride)
+    rng = np.random.default_rng(policy * 10 + gran + stride % 7)
+    for rnd in range(4):
+        units = g.evict_units
+        n = int(rng.integers(1, max(2, units // 3)))
+        _evict_both(B, g, o, n, policy, gran)
+        w = B.debug_evict_window(g)
+        assert w in (0, 1, 2)
+        if stride == 1:
+            assert w == 1, (rnd, n)
+        _query_both(g, o, np.asarray(synth.entries(32, seed=600 + rnd)[0]))
+
+
+@pytest.mark.parametrize("gran", [0, 1])
+def test_single_sweep_window_missed(oracle_mod, gran):
+    """An estimate that must miss: with stride 7 the sample is every 7th block of 32 slots; those
+    blocks hold never-accessed items, every other slot items with f > 0, and a third of the
+    units go -- the sample places the n-th key among the f = 0 keys while it lies far above them.
+    The kernel sees that the n-th key's bin ends beyond the window and takes the two-sweep path;
+    the eviction stays exact."""
+    from paper_2312_04429_b200 import binding as B
+    n = 1400
+    emb, _ = synth.entries(n, seed=177)
+    pres = synth.present_masks(n, seed=177, hole_frac=0.2)
+    g = B.NirvanaCache(entry_capacity=n, latent_capacity=5 * n, dim=768, latent_bytes=0, evict_granularity=gran)
+    o = oracle_mod.OracleCache(dim=768, entry_capacity=n, latent_capacity=5 * n)
+    g.insert(torch.from_numpy(emb).cuda(), None, present=pres)
+    o.insert(emb, present=pres)
+    rng = np.random.default_rng(gran)
+    for id_ in range(n):
+        if (B.debug_slot_of(g, id_) // 32) % 7 == 0:
+            continue
+        for j in range(5):
+            if (int(pres[id_]) >> j) & 1:
+                f = int(rng.integers(1, 50))
+                B.debug_set_count(g, id_, j, f)
+                assert o.set_count(id_, j, f) == 0
+    B.debug_evict_window(g, 7)
+    nev = g.evict_units // 3
+    if gran:
+        ev, _ = g.evict(nev)
+        rc, oev = o.evict_entries(nev)
+        assert rc == 0 and np.array_equal(ev, oev)
+    else:
+        ev, dirty = g.evict(nev)
+        rc, oev, od = o.evict(nev)
+        assert rc == 0 and np.array_equal(ev, oev) and np.array_equal(dirty, od)
+    assert B.debug_evict_window(g) == 2
 
 
 @pytest.mark.parametrize("gran", [0, 1])
@@ -250,6 +309,8 @@ def test_fused_evict_parity_1m_entries(oracle_mod, policy):
         assert rc == 0 and np.array_equal(ev, oev) and np.array_equal(dirty, od), frac
         st = B.debug_evict_stats(g)
         assert st["full_sweeps"] <= 3
+        if frac == 0.01:   # the single-sweep window holds the cut: one full sweep
+            assert B.debug_evict_window(g) == 1 and st["full_sweeps"] == 1, st
 
 
 def test_distributed_calls_out_of_order_fail_cleanly():
