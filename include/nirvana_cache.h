@@ -464,6 +464,26 @@ cache_status cache_get_row(cache_t *c, uint64_t id, uint16_t *out_bf16);
 /* Host-synchronous statistics. */
 cache_status cache_stats(cache_t *c, cache_stats_t *out);
 
+/* The handle's live configuration: cache_create's, with the threshold table, k_bias, policy and
+ * granularity as later calls set them (cache_set_thresholds / _evict_policy / _granularity).
+ * *out is caller-owned. */
+cache_status cache_get_config(cache_t *c, cache_config *out);
+
+/* Checkpoint / resume (the paper's cache persists as EFS files + a Qdrant collection,
+ * P:508-511).  cache_save writes the handle's whole state to the file `path`: the live
+ * configuration, the stored bf16 rows and inverse norms, ids, presence masks, latent-pool slots,
+ * LCBFU counters and LRU clocks of slots [0, high-water mark), the host allocator state (entry /
+ * pool free lists, next id, LRU batch clock, query count), the trained match predictor if any,
+ * and -- with_latents != 0 -- the occupied prefix of the latent pool (aliased pools: all of it).
+ * cache_load creates a handle on `device` holding exactly that state: every later call answers
+ * as the saved handle would have (tested bit for bit).  A shard saves its own state; push
+ * arenas and peer mappings are not saved (re-run cache_push_reserve / cache_attach_peers).
+ * Host-synchronous; the file is this library version's layout (magic + version checked).
+ * Errors: CACHE_E_INVALID_ARG (null, file not writable / readable, foreign or truncated file),
+ * CACHE_E_OOM / CACHE_E_CUDA (device allocation or copies); *out is NULL on failure. */
+cache_status cache_save(cache_t *c, const char *path, int32_t with_latents);
+cache_status cache_load(const char *path, int32_t device, cache_t **out);
+
 /* Select the eviction policy (CACHE_POLICY_*) used by later cache_evict calls. */
 cache_status cache_set_evict_policy(cache_t *c, int32_t policy);
 /* Select the eviction granularity (CACHE_EVICT_ITEM / CACHE_EVICT_ENTRY) of later evictions. */

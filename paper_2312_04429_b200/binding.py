@@ -86,7 +86,7 @@ EXPORTS = ("cache_default_config", "cache_create", "cache_destroy", "cache_inser
            "cache_push_status", "cache_set_peer_timeout", "cache_last_evicted_keys",
            "cache_evict_view", "cache_query_submit", "cache_query_complete", "cache_evict_sel_begin",
            "cache_evict_sel_level", "cache_evict_sel_pick", "cache_evict_sel_apply", "cache_push_evict_sel_level",
-           "cache_push_evict_sel_pick")
+           "cache_push_evict_sel_pick", "cache_get_config", "cache_save", "cache_load")
 
 
 def load_library(path: str = LIB_PATH):
@@ -98,6 +98,12 @@ def load_library(path: str = LIB_PATH):
     L.cache_default_config.argtypes = [ctypes.POINTER(CacheConfig)]
     L.cache_create.argtypes = [ctypes.POINTER(CacheConfig), ctypes.c_int, ctypes.POINTER(P)]
     L.cache_destroy.argtypes = [P]
+    L.cache_get_config.argtypes = [P, ctypes.POINTER(CacheConfig)]
+    L.cache_get_config.restype = ctypes.c_int
+    L.cache_save.argtypes = [P, ctypes.c_char_p, I32]
+    L.cache_save.restype = ctypes.c_int
+    L.cache_load.argtypes = [ctypes.c_char_p, I32, ctypes.POINTER(P)]
+    L.cache_load.restype = ctypes.c_int
     L.cache_insert.argtypes = [P, I64, P, I32, P, P, P, P, P]
     L.cache_query_batch.argtypes = [P, I64, P, I32, I32, P, P, P, P, P, P, P]
     L.cache_query_batch_host.argtypes = [P, I64, P, I32, I32, P, P, P, P, P, P]
@@ -216,6 +222,21 @@ def default_config(**kw) -> CacheConfig:
     return cfg
 
 
+class _ArrIface:
+    """A read-only numpy view of library memory through __array_interface__ (np.ctypeslib's
+    as_array builds a new ctypes array type per length: tens of microseconds per call)."""
+    __slots__ = ("__array_interface__",)
+
+    def __init__(self, addr: int, k: int):
+        self.__array_interface__ = {"data": (addr, True), "shape": (k,), "typestr": "<u8", "version": 3}
+
+
+def _u64_view(addr, k: int) -> np.ndarray:
+    if k == 0 or not addr:
+        return np.zeros(0, np.uint64)
+    return np.asarray(_ArrIface(addr, k))
+
+
 class NirvanaCache:
     """One cache handle on one CUDA device (see include/nirvana_cache.h)."""
 
@@ -242,6 +263,34 @@ class NirvanaCache:
         h = ctypes.c_void_p()
         _check(_lib.cache_create(ctypes.byref(self.cfg), device, ctypes.byref(h)))
         self._h = h
+
+    def _adopt_config(self):
+        """Attributes from the handle's live configuration (cache_get_config)."""
+        c = CacheConfig()
+        _check(_lib.cache_get_config(self._h, ctypes.byref(c)))
+        self.cfg = c
+        self.granularity = c.evict_granularity
+        self.latent_capacity = c.latent_capacity
+        self.shard_rank, self.shard_world = c.shard_rank, c.shard_world
+        self.dim, self.latent_bytes, self.num_k = c.dim, c.latent_bytes, c.num_k
+        self.k_values = tuple(c.k_values[: c.num_k])
+
+    def save(self, path: str, with_latents: bool = True):
+        """cache_save: the whole state to `path` (checkpoint)."""
+        _check(_lib.cache_save(self._h, os.fsencode(path), int(bool(with_latents))))
+
+    @classmethod
+    def load(cls, path: str, device: int | None = None) -> "NirvanaCache":
+        """cache_load: a new handle holding the state saved in `path` (resume)."""
+        if device is None:
+            device = torch.cuda.current_device()
+        self = cls.__new__(cls)
+        self.device = device
+        h = ctypes.c_void_p()
+        _check(_lib.cache_load(os.fsencode(path), device, ctypes.byref(h)))
+        self._h = h
+        self._adopt_config()
+        return self
 
     def close(self):
         if getattr(self, "_h", None):
@@ -353,13 +402,7 @@ class NirvanaCache:
             nd = ctypes.c_int64()
             _check(_lib.cache_evict_view(self._h, n, ctypes.byref(pe), ctypes.byref(pd), ctypes.byref(nd),
                                          _stream(stream)))
-            def arr(p, k):
-                if k == 0 or not p.value:
-                    return np.zeros(0, np.uint64)
-                a = np.ctypeslib.as_array(ctypes.cast(p, ctypes.POINTER(ctypes.c_uint64)), shape=(k,))
-                a.flags.writeable = False
-                return a
-            return arr(pe, n), arr(pd, nd.value)
+            return _u64_view(pe.value, n), _u64_view(pd.value, nd.value)
         if out is not None and len(out[0]) >= max(n, 1) and len(out[1]) >= max(n, 1):
             ev, dirty = out
         else:

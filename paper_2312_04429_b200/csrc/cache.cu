@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <nvtx3/nvToolsExt.h>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -139,6 +140,12 @@ bool encode_rows(CUtensorMap* tm, const void* base, int64_t rows, int dim, int b
     return r == CUDA_SUCCESS;
 }
 }  // namespace
+
+// NVTX range per public call (nsys / ncu --nvtx filter the library's phases; ~ns without a tool)
+struct NvtxScope {
+    explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+    ~NvtxScope() { nvtxRangePop(); }
+};
 
 struct cache_t {
     cache_config cfg;
@@ -484,6 +491,7 @@ cache_status cache_destroy(cache_t* c) {
 
 cache_status cache_insert(cache_t* c, int64_t n, const void* emb, int32_t emb_dtype, const void* latents,
                           const uint8_t* present, uint64_t* out_ids, int32_t* row_status, void* stream) {
+    NvtxScope nvtx_scope_("cache_insert");
     if (!c) return fail(CACHE_E_INVALID_ARG, "cache_insert: null cache");
     if (n < 0 || (n > 0 && !emb) || (emb_dtype != CACHE_DTYPE_F32 && emb_dtype != CACHE_DTYPE_BF16))
         return fail(CACHE_E_INVALID_ARG, "cache_insert: bad n / emb / dtype");
@@ -766,6 +774,7 @@ static cache_status query_core(cache_t* c, int64_t b, const void* queries, int32
 cache_status cache_query_batch(cache_t* c, int64_t b, const void* queries, int32_t q_dtype, int32_t topk,
                                uint64_t* out_ids, float* out_scores, int32_t* out_k, void* latent_out,
                                void** out_latent_ptr, int32_t* row_status, void* stream) {
+    NvtxScope nvtx_scope_("cache_query_batch");
     if (!c) return fail(CACHE_E_INVALID_ARG, "cache_query_batch: null cache");
     if (b < 0 || b > 0x7FFFFFFF || topk < 1 || topk > c->cfg.max_topk ||
         (q_dtype != CACHE_DTYPE_F32 && q_dtype != CACHE_DTYPE_BF16))
@@ -782,6 +791,7 @@ cache_status cache_query_batch(cache_t* c, int64_t b, const void* queries, int32
 cache_status cache_query_peek(cache_t* c, int64_t b, const void* queries, int32_t q_dtype, int32_t topk,
                               uint64_t* out_ids, float* out_scores, int32_t* out_k, int32_t* row_status,
                               void* stream) {
+    NvtxScope nvtx_scope_("cache_query_peek");
     if (!c) return fail(CACHE_E_INVALID_ARG, "cache_query_peek: null cache");
     if (b < 0 || b > 0x7FFFFFFF || topk < 1 || topk > c->cfg.max_topk ||
         (q_dtype != CACHE_DTYPE_F32 && q_dtype != CACHE_DTYPE_BF16))
@@ -795,6 +805,7 @@ cache_status cache_query_peek(cache_t* c, int64_t b, const void* queries, int32_
 
 cache_status cache_query_local(cache_t* c, int64_t b, const void* queries, int32_t q_dtype, int32_t topk,
                                cache_shard_rec* out_recs, void* stream) {
+    NvtxScope nvtx_scope_("cache_query_local");
     if (!c) return fail(CACHE_E_INVALID_ARG, "cache_query_local: null cache");
     if (b < 0 || b > 0x7FFFFFFF || topk < 1 || topk > c->cfg.max_topk ||
         (q_dtype != CACHE_DTYPE_F32 && q_dtype != CACHE_DTYPE_BF16))
@@ -816,6 +827,7 @@ cache_status cache_query_local(cache_t* c, int64_t b, const void* queries, int32
 cache_status cache_query_merge(cache_t* c, int64_t b, int64_t row0, int64_t nb, int32_t topk,
                                const cache_shard_rec* recs, uint64_t* out_ids, float* out_scores, int32_t* out_k,
                                void* latent_out, void** out_latent_ptr, int32_t* row_status, void* stream) {
+    NvtxScope nvtx_scope_("cache_query_merge");
     if (!c) return fail(CACHE_E_INVALID_ARG, "cache_query_merge: null cache");
     if (b < 0 || row0 < 0 || nb < 0 || row0 + nb > b || topk < 1 || topk > c->cfg.max_topk)
         return fail(CACHE_E_INVALID_ARG, "cache_query_merge: bad b / row range / topk");
@@ -838,6 +850,7 @@ cache_status cache_query_merge(cache_t* c, int64_t b, int64_t row0, int64_t nb, 
 // ---- cache-selector profiling (Alg. 2) ----
 cache_status cache_profile_thresholds(cache_t* c, int64_t b, const void* queries, int32_t q_dtype, const float* quality,
                                       double alpha, double* out_thresholds, int64_t* out_failed, void* stream) {
+    NvtxScope nvtx_scope_("cache_profile_thresholds");
     if (!c) return fail(CACHE_E_INVALID_ARG, "cache_profile_thresholds: null cache");
     if (b <= 0 || b > 0x7FFFFFFF || !queries || !quality || !out_thresholds ||
         (q_dtype != CACHE_DTYPE_F32 && q_dtype != CACHE_DTYPE_BF16) || !(alpha == alpha))
@@ -892,6 +905,7 @@ cache_status cache_set_thresholds(cache_t* c, const double* thresholds) {
 }
 
 cache_status cache_predictor_train(cache_t* c, double nu, int32_t epochs, double lr0, void* stream) {
+    NvtxScope nvtx_scope_("cache_predictor_train");
     if (!c || !(nu > 0.0 && nu < 1.0) || epochs < 0 || !(lr0 > 0.0))
         return fail(CACHE_E_INVALID_ARG, "cache_predictor_train: bad nu / epochs / lr0");
     if (c->live_entries <= 0) return fail(CACHE_E_STATE, "cache_predictor_train: empty cache");
@@ -971,6 +985,7 @@ cache_status cache_predictor_train(cache_t* c, double nu, int32_t epochs, double
 
 cache_status cache_predict(cache_t* c, int64_t b, const void* queries, int32_t q_dtype, uint8_t* out_flags,
                            float* out_margin, void* stream) {
+    NvtxScope nvtx_scope_("cache_predict");
     if (!c || b < 0 || (b > 0 && !queries) || (q_dtype != CACHE_DTYPE_F32 && q_dtype != CACHE_DTYPE_BF16))
         return fail(CACHE_E_INVALID_ARG, "cache_predict: bad argument");
     if (!c->pred_ok) return fail(CACHE_E_STATE, "cache_predict: predictor not trained");
@@ -1236,6 +1251,7 @@ cache_status cache_push_evict_apply(cache_t* c, int64_t n, uint64_t* out_evicted
 }
 
 cache_status cache_push_queries(cache_t* c, int64_t nb, const void* queries, int32_t q_dtype, void* stream) {
+    NvtxScope nvtx_scope_("cache_push_queries");
     if (!c) return fail(CACHE_E_INVALID_ARG, "cache_push_queries: null cache");
     if (peer_failed(c)) return peer_fail("cache_push_queries");
     if (!c->push_ok) return fail(CACHE_E_STATE, "cache_push_queries: no push arenas (cache_push_reserve on every rank, then export / attach)");
@@ -1262,6 +1278,7 @@ cache_status cache_push_queries(cache_t* c, int64_t nb, const void* queries, int
 }
 
 cache_status cache_push_scan(cache_t* c, int64_t nb, int32_t topk, void* stream) {
+    NvtxScope nvtx_scope_("cache_push_scan");
     if (!c) return fail(CACHE_E_INVALID_ARG, "cache_push_scan: null cache");
     if (peer_failed(c)) return peer_fail("cache_push_scan");
     if (c->push_phase != 1 || nb != c->push_nb) return fail(CACHE_E_STATE, "cache_push_scan: call after cache_push_queries with the same nb");
@@ -1295,6 +1312,7 @@ cache_status cache_push_scan(cache_t* c, int64_t nb, int32_t topk, void* stream)
 cache_status cache_push_merge(cache_t* c, int64_t nb, int32_t topk, uint64_t* out_ids, float* out_scores,
                               int32_t* out_k, void* latent_out, void** out_latent_ptr, int32_t* row_status,
                               void* stream) {
+    NvtxScope nvtx_scope_("cache_push_merge");
     if (!c) return fail(CACHE_E_INVALID_ARG, "cache_push_merge: null cache");
     if (peer_failed(c)) return peer_fail("cache_push_merge");
     if (c->push_phase != 2 || nb != c->push_nb) return fail(CACHE_E_STATE, "cache_push_merge: call after cache_push_scan with the same nb");
@@ -1323,6 +1341,7 @@ cache_status cache_push_merge(cache_t* c, int64_t nb, int32_t topk, uint64_t* ou
 // ---- pipelined host calls: batch i+1's upload (copy stream) overlaps batch i's lookup ----
 cache_status cache_query_submit(cache_t* c, int32_t slot, int64_t b, const void* queries, int32_t q_dtype,
                                 int32_t topk, void* latent_out, void* stream) {
+    NvtxScope nvtx_scope_("cache_query_submit");
     if (!c) return fail(CACHE_E_INVALID_ARG, "cache_query_submit: null cache");
     if (slot < 0 || slot > 1 || b <= 0 || b > 0x7FFFFFFF || topk < 1 || topk > c->cfg.max_topk || !queries ||
         (q_dtype != CACHE_DTYPE_F32 && q_dtype != CACHE_DTYPE_BF16))
@@ -1370,6 +1389,7 @@ cache_status cache_query_submit(cache_t* c, int32_t slot, int64_t b, const void*
 
 cache_status cache_query_complete(cache_t* c, int32_t slot, uint64_t* out_ids, float* out_scores, int32_t* out_k,
                                   int32_t* row_status) {
+    NvtxScope nvtx_scope_("cache_query_complete");
     if (!c || slot < 0 || slot > 1 || !out_ids || !out_scores || !out_k)
         return fail(CACHE_E_INVALID_ARG, "cache_query_complete: bad argument");
     cache_t::AsyncSlot& a = c->aslot[slot];
@@ -1390,6 +1410,7 @@ cache_status cache_query_complete(cache_t* c, int32_t slot, uint64_t* out_ids, f
 cache_status cache_query_batch_host(cache_t* c, int64_t b, const void* queries, int32_t q_dtype, int32_t topk,
                                     uint64_t* out_ids, float* out_scores, int32_t* out_k, void* latent_out,
                                     int32_t* row_status, void* stream) {
+    NvtxScope nvtx_scope_("cache_query_batch_host");
     if (!c) return fail(CACHE_E_INVALID_ARG, "cache_query_batch_host: null cache");
     if (b < 0 || b > 0x7FFFFFFF || topk < 1 || topk > c->cfg.max_topk ||
         (q_dtype != CACHE_DTYPE_F32 && q_dtype != CACHE_DTYPE_BF16))
@@ -1642,12 +1663,14 @@ static cache_status evict_impl(cache_t* c, int64_t n, bool want_ev, bool want_di
 
 cache_status cache_evict(cache_t* c, int64_t n, uint64_t* out_evicted, uint64_t* out_dirty_ids,
                          int64_t* out_n_dirty, void* stream) {
+    NvtxScope nvtx_scope_("cache_evict");
     return evict_impl(c, n, out_evicted != nullptr, out_dirty_ids != nullptr, out_evicted, out_dirty_ids, out_n_dirty,
                       stream);
 }
 
 cache_status cache_evict_view(cache_t* c, int64_t n, const uint64_t** out_evicted, const uint64_t** out_dirty_ids,
                               int64_t* out_n_dirty, void* stream) {
+    NvtxScope nvtx_scope_("cache_evict_view");
     if (!c || !out_evicted || !out_dirty_ids || !out_n_dirty)
         return fail(CACHE_E_INVALID_ARG, "cache_evict_view: null argument");
     *out_evicted = *out_dirty_ids = nullptr;
@@ -1711,7 +1734,7 @@ static cache_status evict_setup(cache_t* c, int64_t n_sel, int64_t n_loc, bool w
     a.ev_pool = c->epool.p;
     a.dirty_slot = c->edirty.p;
     a.dirty_id = c->edid.p;
-    a.ev_cap = (unsigned long long)n;
+    a.ev_cap = want_ev ? (unsigned long long)n : 0ull;   // 0: no unsorted key list (count-only evictions)
     a.dslot_bits = c->ebits.p;
     a.did_bits = c->ebits.p + w_slot;
     a.pool_bits = w_pool ? c->ebits.p + w_slot + w_id : nullptr;
@@ -1844,6 +1867,7 @@ static cache_status sel_launch(cache_t* c, int phase, uint32_t* level_hist, cuda
 }
 
 cache_status cache_evict_sel_begin(cache_t* c, int64_t n, void* stream) {
+    NvtxScope nvtx_scope_("cache_evict_sel_begin");
     if (!c || n < 1) return fail(CACHE_E_INVALID_ARG, "cache_evict_sel_begin: bad argument");
     if (peer_failed(c)) return peer_fail("cache_evict_sel_begin");
     DeviceGuard g(c->device);
@@ -1864,6 +1888,7 @@ cache_status cache_evict_sel_begin(cache_t* c, int64_t n, void* stream) {
 }
 
 cache_status cache_evict_sel_level(cache_t* c, int32_t level, uint32_t* hist, void* stream) {
+    NvtxScope nvtx_scope_("cache_evict_sel_level");
     if (!c || !hist) return fail(CACHE_E_INVALID_ARG, "cache_evict_sel_level: bad argument");
     if (level != c->dsel_level || level >= kSelMaxLevels)
         return fail(CACHE_E_STATE, "cache_evict_sel_level: levels out of order (begin, then level / pick 0, 1, ...)");
@@ -1886,6 +1911,7 @@ static cache_status sel_pick_done(cache_t* c, int32_t level, const uint32_t* ghi
 }
 
 cache_status cache_evict_sel_pick(cache_t* c, int32_t level, const uint32_t* ghist, int32_t* out_done, void* stream) {
+    NvtxScope nvtx_scope_("cache_evict_sel_pick");
     if (!c || !ghist) return fail(CACHE_E_INVALID_ARG, "cache_evict_sel_pick: bad argument");
     if (level + 1 != c->dsel_level + 1 || level != c->dsel_level)
         return fail(CACHE_E_STATE, "cache_evict_sel_pick: call after cache_evict_sel_level of the same level");
@@ -1895,6 +1921,7 @@ cache_status cache_evict_sel_pick(cache_t* c, int32_t level, const uint32_t* ghi
 
 cache_status cache_evict_sel_apply(cache_t* c, int64_t cap, uint64_t* out_evicted, int64_t* out_n,
                                    uint64_t* out_dirty_ids, int64_t* out_n_dirty, void* stream) {
+    NvtxScope nvtx_scope_("cache_evict_sel_apply");
     if (!c || cap < 0) return fail(CACHE_E_INVALID_ARG, "cache_evict_sel_apply: bad argument");
     if (c->dsel_level < 1 || !c->dsel_done)
         return fail(CACHE_E_STATE, "cache_evict_sel_apply: the selection is not finished (begin, then level / pick "
@@ -1928,6 +1955,7 @@ cache_status cache_evict_sel_apply(cache_t* c, int64_t cap, uint64_t* out_evicte
 // push variants: the level histogram goes into every rank's arena over NVLink (P2P atomics) and
 // the pick waits for every rank's level flag, then reads the summed histogram from its own arena
 cache_status cache_push_evict_sel_level(cache_t* c, int32_t level, void* stream) {
+    NvtxScope nvtx_scope_("cache_push_evict_sel_level");
     if (!c) return fail(CACHE_E_INVALID_ARG, "cache_push_evict_sel_level: null cache");
     if (peer_failed(c)) return peer_fail("cache_push_evict_sel_level");
     if (!c->push_ok) return fail(CACHE_E_STATE, "cache_push_evict_sel_level: no push arenas");
@@ -1953,6 +1981,7 @@ cache_status cache_push_evict_sel_level(cache_t* c, int32_t level, void* stream)
 }
 
 cache_status cache_push_evict_sel_pick(cache_t* c, int32_t level, int32_t* out_done, void* stream) {
+    NvtxScope nvtx_scope_("cache_push_evict_sel_pick");
     if (!c) return fail(CACHE_E_INVALID_ARG, "cache_push_evict_sel_pick: null cache");
     if (peer_failed(c)) return peer_fail("cache_push_evict_sel_pick");
     if (!c->push_ok || level != c->dsel_level || !c->dsel_push)
@@ -2054,6 +2083,179 @@ cache_status cache_stats(cache_t* c, cache_stats_t* out) {
     out->queries = c->queries;
     out->free_entries = (int64_t)c->free_e.size();
     out->free_items = (int64_t)c->free_l.size();
+    return CACHE_OK;
+}
+
+// ---- checkpoint / resume (the paper's cache persists as EFS files + a Qdrant
+// collection) ----
+namespace {
+constexpr char kSnapMagic[8] = {'N', 'V', 'C', 'A', 'C', 'H', 'E', '1'};
+constexpr uint32_t kSnapVersion = 1;
+struct SnapHeader {
+    char magic[8];
+    uint32_t version, cfg_bytes;
+    cache_config cfg;   // the configuration with the live threshold table / policy / granularity
+    int64_t hwm, live_entries, live_items, queries, n_free_e, n_free_l, pool_hi;
+    uint64_t next_id;
+    uint32_t clock;
+    int32_t scorer, pred_ok, pad;
+};
+// device <-> file through a pinned staging buffer, 64 MiB at a time
+struct SnapIO {
+    std::FILE* f = nullptr;
+    void* stage = nullptr;
+    size_t stage_n = 0;
+    bool ok = true;
+    cudaError_t err = cudaSuccess;
+    ~SnapIO() {
+        if (stage) cudaFreeHost(stage);
+        if (f) std::fclose(f);
+    }
+    bool host(void* p, size_t n, bool wr) {
+        if (!ok || !n) return ok;
+        ok = (wr ? std::fwrite(p, 1, n, f) : std::fread(p, 1, n, f)) == n;
+        return ok;
+    }
+    bool dev(void* d, size_t n, bool wr) {
+        if (!ok || !n) return ok;
+        if (!stage) {
+            stage_n = (size_t)64 << 20;
+            if ((err = cudaHostAlloc(&stage, stage_n, cudaHostAllocDefault)) != cudaSuccess) return ok = false;
+        }
+        for (size_t o = 0; o < n && ok; o += stage_n) {
+            const size_t m = std::min(stage_n, n - o);
+            if (wr) {
+                if ((err = cudaMemcpy(stage, (uint8_t*)d + o, m, cudaMemcpyDeviceToHost)) != cudaSuccess) return ok = false;
+                host(stage, m, true);
+            } else {
+                if (!host(stage, m, false)) return false;
+                if ((err = cudaMemcpy((uint8_t*)d + o, stage, m, cudaMemcpyHostToDevice)) != cudaSuccess) return ok = false;
+            }
+        }
+        return ok;
+    }
+};
+// the state arrays, in file order (rows [0, hwm) of every per-slot array)
+struct SnapArr {
+    void* p;
+    size_t n;
+};
+int snap_arrays(cache_t* c, SnapArr* a) {
+    const size_t h = (size_t)c->hwm, nk = (size_t)c->num_k;
+    a[0] = {c->emb, h * c->dim * 2};
+    a[1] = {c->inv_e, h * 4};
+    a[2] = {c->ids, h * 4};
+    a[3] = {c->present, h * 4};
+    a[4] = {c->lslot, h * nk * 4};
+    a[5] = {c->fcnt, h * nk * 4};
+    a[6] = {c->lastacc, h * nk * 4};
+    return 7;
+}
+}  // namespace
+
+cache_status cache_get_config(cache_t* c, cache_config* out) {
+    if (!c || !out) return fail(CACHE_E_INVALID_ARG, "cache_get_config: null argument");
+    *out = c->cfg;
+    for (int j = 0; j < c->num_k; ++j) out->thresholds[j] = c->km.thr[j];
+    out->k_bias = c->km.k_bias;
+    out->evict_policy = c->km.policy;
+    out->evict_granularity = c->km.gran;
+    return CACHE_OK;
+}
+
+cache_status cache_save(cache_t* c, const char* path, int32_t with_latents) {
+    NvtxScope nvtx_scope_("cache_save");
+    if (!c || !path) return fail(CACHE_E_INVALID_ARG, "cache_save: null argument");
+    DeviceGuard g(c->device);
+    CK(cudaDeviceSynchronize());
+    SnapIO io;
+    if (!(io.f = std::fopen(path, "wb"))) return fail(CACHE_E_INVALID_ARG, std::string("cache_save: cannot write ") + path);
+    SnapHeader hd{};
+    std::memcpy(hd.magic, kSnapMagic, 8);
+    hd.version = kSnapVersion;
+    hd.cfg_bytes = (uint32_t)sizeof(cache_config);
+    cache_get_config(c, &hd.cfg);
+    hd.hwm = c->hwm;
+    hd.live_entries = c->live_entries;
+    hd.live_items = c->live_items;
+    hd.queries = c->queries;
+    hd.n_free_e = (int64_t)c->free_e.size();
+    hd.n_free_l = (int64_t)c->free_l.size();
+    // occupied pool prefix: the free list is sorted descending, so its leading run lcap-1,
+    // lcap-2, ... is the never-used top of the pool (aliased pools: every slot may be in use)
+    int64_t top = 0;
+    if (!c->alias)
+        while (top < hd.n_free_l && c->free_l[(size_t)top] == c->lcap - 1 - top) ++top;
+    hd.pool_hi = (with_latents && c->pool) ? c->lcap - top : 0;
+    hd.next_id = c->next_id;
+    hd.clock = c->clock;
+    hd.scorer = c->scorer;
+    hd.pred_ok = c->pred_ok ? 1 : 0;
+    io.host(&hd, sizeof(hd), true);
+    io.host(c->h_live.data(), (size_t)c->hwm, true);
+    io.host(c->h_ids.data(), (size_t)c->hwm * 4, true);
+    io.host(c->free_e.data(), c->free_e.size() * 8, true);
+    io.host(c->free_l.data(), c->free_l.size() * 8, true);
+    SnapArr arr[8];
+    for (int i = 0, na = snap_arrays(c, arr); i < na; ++i) io.dev(arr[i].p, arr[i].n, true);
+    if (hd.pred_ok) {
+        io.dev(c->pw.p, (size_t)c->dim * 4, true);
+        io.dev(c->prho.p, 4, true);
+    }
+    io.dev(c->pool, (size_t)hd.pool_hi * c->L, true);
+    if (io.err != cudaSuccess) return fail(CACHE_E_CUDA, std::string("cache_save: ") + cudaGetErrorString(io.err));
+    if (!io.ok || std::fflush(io.f) != 0) return fail(CACHE_E_INVALID_ARG, std::string("cache_save: write failed: ") + path);
+    return CACHE_OK;
+}
+
+cache_status cache_load(const char* path, int32_t device, cache_t** out) {
+    NvtxScope nvtx_scope_("cache_load");
+    if (!path || !out) return fail(CACHE_E_INVALID_ARG, "cache_load: null argument");
+    *out = nullptr;
+    SnapIO io;
+    if (!(io.f = std::fopen(path, "rb"))) return fail(CACHE_E_INVALID_ARG, std::string("cache_load: cannot read ") + path);
+    SnapHeader hd{};
+    if (!io.host(&hd, sizeof(hd), false) || std::memcmp(hd.magic, kSnapMagic, 8) != 0 || hd.version != kSnapVersion ||
+        hd.cfg_bytes != sizeof(cache_config))
+        return fail(CACHE_E_INVALID_ARG, "cache_load: not a cache snapshot of this library version");
+    cache_t* c = nullptr;
+    cache_status r = cache_create(&hd.cfg, device, &c);
+    if (r != CACHE_OK) return r;
+    auto bad = [&](cache_status st, const std::string& what) {
+        cache_destroy(c);
+        return fail(st, "cache_load: " + what);
+    };
+    if (hd.hwm < 0 || hd.hwm > c->cap || hd.n_free_e < 0 || hd.n_free_e > c->cap || hd.n_free_l < 0 ||
+        hd.n_free_l > std::max<int64_t>(c->lcap, 0) || hd.pool_hi < 0 || hd.pool_hi > std::max<int64_t>(c->lcap, 0))
+        return bad(CACHE_E_INVALID_ARG, "inconsistent snapshot header");
+    DeviceGuard g(c->device);
+    c->hwm = hd.hwm;
+    c->live_entries = hd.live_entries;
+    c->live_items = hd.live_items;
+    c->queries = hd.queries;
+    c->next_id = hd.next_id;
+    c->clock = hd.clock;
+    c->scorer = hd.scorer;
+    c->free_e.resize((size_t)hd.n_free_e);
+    c->free_l.resize((size_t)hd.n_free_l);
+    io.host(c->h_live.data(), (size_t)c->hwm, false);
+    io.host(c->h_ids.data(), (size_t)c->hwm * 4, false);
+    io.host(c->free_e.data(), c->free_e.size() * 8, false);
+    io.host(c->free_l.data(), c->free_l.size() * 8, false);
+    SnapArr arr[8];
+    for (int i = 0, na = snap_arrays(c, arr); i < na; ++i) io.dev(arr[i].p, arr[i].n, false);
+    if (hd.pred_ok) {
+        if (c->pw.ensure(c->dim) != cudaSuccess || c->prho.ensure(1) != cudaSuccess)
+            return bad(CACHE_E_OOM, "predictor");
+        io.dev(c->pw.p, (size_t)c->dim * 4, false);
+        io.dev(c->prho.p, 4, false);
+        c->pred_ok = io.ok;
+    }
+    io.dev(c->pool, (size_t)hd.pool_hi * c->L, false);
+    if (io.err != cudaSuccess) return bad(CACHE_E_CUDA, cudaGetErrorString(io.err));
+    if (!io.ok) return bad(CACHE_E_INVALID_ARG, std::string("truncated snapshot: ") + path);
+    if (cudaDeviceSynchronize() != cudaSuccess) return bad(CACHE_E_CUDA, "restore");
+    *out = c;
     return CACHE_OK;
 }
 

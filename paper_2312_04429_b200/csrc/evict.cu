@@ -1130,7 +1130,7 @@ __global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : ((kSelC
         DigitRun run;
         // item-mode apply: the evicted-key list only if the bitmap can miss a key (the host side
         // then sorts it); counts summed per CTA, one global atomic per CTA
-        const bool ev_list = !(L.ev_lim && L.T >= L.kb && L.T - L.kb < L.ev_lim);
+        const bool ev_list = a.ev_cap && !(L.ev_lim && L.T >= L.kb && L.T - L.kb < L.ev_lim);
         uint32_t nev = 0, ndirty = 0;
         for (int64_t i0 = c0 + warp * 32; i0 < c1; i0 += kSelThreads) {
             const int64_t i = i0 + lane;
