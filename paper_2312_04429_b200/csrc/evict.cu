@@ -45,6 +45,10 @@ constexpr bool kSelPrefetch = NV_SEL_PREFETCH != 0 && !kSelCpAsync;
 #define NV_SEL_COLT 0   // 1: coalesced column loads + shared-memory redistribution (measured: no gain)
 #endif
 constexpr bool kSelColT = NV_SEL_COLT != 0;
+#ifndef NV_SEL_DYN_PCT
+#define NV_SEL_DYN_PCT 25  // the last 25% of each full sweep's groups are claimed dynamically (two-sweep path: 275-311 -> 227-228 us at 12.5M; the window path: no change)
+#endif
+constexpr int kSelDynPct = NV_SEL_DYN_PCT;
 constexpr int kColTBytes = (kSelCpAsync ? 256 : 512) / 32 * 160 * 16;   // per-warp 2,560-B transposes
 constexpr int kSelThreads = (kSelCpAsync || kSelPrefetch) ? 256 : 512;
 constexpr int kCpStages = 3;                           // groups per lane: 2 loading + 1 being processed
@@ -920,6 +924,7 @@ __global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : ((kSelC
         __syncthreads();
     }
     uint32_t uses = 0;   // tiles this CTA has staged so far (all sweeps): stage = u % kStages
+    int sweep_no = 0;    // full sweeps so far (each has its own claim counter)
     auto full_sweep = [&](int mode, const SelLevel& L, unsigned long long& kmin) {
         DigitRun run;
         const uint32_t* colp = policy_col<POLICY>(a);
@@ -1077,7 +1082,32 @@ __global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : ((kSelC
                 }
             };
             if (kSelPrefetch && gfirst < n_pad) load(gfirst, nP, nI, nC);
-            for (int64_t g0 = gfirst; g0 < n_pad; g0 += gstride) {
+            // NV_SEL_DYN_PCT > 0 (single-cache launch): the last DYN_PCT% of the groups are claimed
+            // (2 per atomic) by whichever warps finish their static share first -- the static
+            // interleave keeps the bulk's access pattern, the claimed tail absorbs the CTAs that
+            // run 20-25% slower than the median (NV_SEL_TRACE)
+            const int64_t ngroups = n_pad / 128, twarps = (int64_t)gridDim.x * (kSelThreads / 32);
+            int64_t dyn_from = ngroups;   // groups >= dyn_from are claimed
+            if (kSelDynPct > 0 && a.phase == kPhaseAll && !kSelPrefetch)
+                dyn_from = (ngroups / twarps) * (100 - kSelDynPct) / 100 * twarps;
+            unsigned long long* gctr = &a.out->gnext[(sweep_no++) & 15];
+            bool in_dyn = gfirst >= dyn_from * 128;
+            int dleft = 0;
+            int64_t dnext = 0, g0 = gfirst;
+            for (;;) {
+                if (in_dyn) {   // warp-uniform
+                    if (dyn_from >= ngroups) break;
+                    if (dleft == 0) {
+                        unsigned long long cl = 0;
+                        if (lane == 0) cl = atomicAdd(gctr, 2ull);
+                        dnext = dyn_from + (int64_t)__shfl_sync(0xFFFFFFFFu, cl, 0);
+                        dleft = 2;
+                    }
+                    if (dnext >= ngroups) break;
+                    g0 = dnext * 128;
+                    ++dnext;
+                    --dleft;
+                }
                 const int64_t e4 = g0 + 4 * lane;
                 uint4 P, I, C[5] = {nP, nP, nP, nP, nP};
                 if constexpr (kSelPrefetch) {
@@ -1107,6 +1137,10 @@ __global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : ((kSelC
                         for (int j = 0; j < CACHE_MAX_K; ++j) col[j] = j < 5 ? c[5 * q + j] : 0u;
                         sel_slot<POLICY, GRAN>(a, 5, kv, mode, L, e4 + q, pm[q], pid[q], col, sh, run, kmin, lane);
                     }
+                }
+                if (!in_dyn) {
+                    g0 += gstride;
+                    if (g0 >= dyn_from * 128) in_dyn = true;
                 }
             }
         } else {

@@ -124,6 +124,7 @@ struct SelOut {
     uint32_t ev_sorted, ev_over;  // evicted keys emitted sorted (bitmap path) / one fell beyond the bitmap
     unsigned long long cnt_w;     // single-sweep window: keys compacted by the level-0 sweep
     uint32_t window, pad;         // 0 off, 1 the selection ran on the window, 2 the estimate missed
+    unsigned long long gnext[16]; // full sweeps (<= 9) of the single-cache launch: claimed tail groups
 };
 constexpr int kSelBins = 4096, kSelMaxLevels = 8;
 // Selection state between the host-driven phases of the DISTRIBUTED fused eviction (each rank
