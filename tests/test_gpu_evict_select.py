@@ -284,16 +284,17 @@ def test_radix8_protocol_still_equal(oracle_mod):
         assert np.array_equal(e1, e2) and np.array_equal(d1, d2)
 
 
-@pytest.mark.parametrize("policy", [0, 1])
-def test_fused_evict_parity_1m_entries(oracle_mod, policy):
+@pytest.mark.parametrize("policy,gran", [(0, 0), (1, 0), (0, 1)])
+def test_fused_evict_parity_1m_entries(oracle_mod, policy, gran):
     """At scale: 1M entries (4.75M items; dim 64 so the fp64 oracle holds the cache), Zipf query
-    batches (every row checked against the oracle, accesses adopted), then 1% and 5% evictions:
-    the fused eviction's lists equal the oracle's exactly (ids, order, dirty entries)."""
+    batches (every row checked against the oracle, accesses adopted), then 1% and 5% evictions
+    (items, or entries in entry mode): the fused eviction's lists equal the oracle's exactly
+    (ids, order, dirty entries); the 1% eviction takes the single-sweep window."""
     from paper_2312_04429_b200 import binding as B
     n, dim = 1_000_000, 64
     emb, cl = synth.entries(n, seed=303, dim=dim)
     pres = synth.present_masks(n, seed=303)
-    g = B.NirvanaCache(entry_capacity=n, latent_capacity=5 * n, dim=dim, latent_bytes=0)
+    g = B.NirvanaCache(entry_capacity=n, latent_capacity=5 * n, dim=dim, latent_bytes=0, evict_granularity=gran)
     g.set_evict_policy(policy)
     o = oracle_mod.OracleCache(dim=dim, entry_capacity=n, latent_capacity=5 * n)
     for s0 in range(0, n, 200_000):
@@ -303,10 +304,14 @@ def test_fused_evict_parity_1m_entries(oracle_mod, policy):
         q, _, _ = synth.queries(emb, cl, 256, seed=310 + r)
         _query_both(g, o, q)
     for frac in (0.01, 0.05):
-        nev = int(g.live_items * frac)
+        nev = int(g.evict_units * frac)
         ev, dirty = g.evict(nev)
-        rc, oev, od = o.evict(nev, policy=policy)
-        assert rc == 0 and np.array_equal(ev, oev) and np.array_equal(dirty, od), frac
+        if gran:
+            rc, oev = o.evict_entries(nev, policy=policy)
+            assert rc == 0 and np.array_equal(ev, oev) and np.array_equal(dirty, np.sort(oev)), frac
+        else:
+            rc, oev, od = o.evict(nev, policy=policy)
+            assert rc == 0 and np.array_equal(ev, oev) and np.array_equal(dirty, od), frac
         st = B.debug_evict_stats(g)
         assert st["full_sweeps"] <= 3
         if frac == 0.01:   # the single-sweep window holds the cut: one full sweep
