@@ -1088,7 +1088,7 @@ __global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : ((kSelC
             // run 20-25% slower than the median (NV_SEL_TRACE)
             const int64_t ngroups = n_pad / 128, twarps = (int64_t)gridDim.x * (kSelThreads / 32);
             int64_t dyn_from = ngroups;   // groups >= dyn_from are claimed
-            if (kSelDynPct > 0 && a.phase == kPhaseAll && !kSelPrefetch)
+            if (kSelDynPct > 0 && a.phase == kPhaseAll && !kSelPrefetch && sweep_no < 16)   // a counter per sweep
                 dyn_from = (ngroups / twarps) * (100 - kSelDynPct) / 100 * twarps;
             unsigned long long* gctr = &a.out->gnext[(sweep_no++) & 15];
             bool in_dyn = gfirst >= dyn_from * 128;
