@@ -1884,6 +1884,12 @@ cache_status cache_evict_sel_begin(cache_t* c, int64_t n, void* stream) {
     CK(c->dlhist.ensure((size_t)kSelMaxLevels * kSelBins));
     CK(cudaMemsetAsync(c->dlhist.p, 0, (size_t)kSelMaxLevels * kSelBins * 4, s));
     c->dsel.state = c->dstate.p;
+    // the single-sweep window on this shard (evict.cu, kPhaseL0): on when this rank's share of
+    // n (n / world) fits twice in its candidate buffer; each rank keeps or drops its window alone
+    const int64_t share = (n + c->world - 1) / c->world;
+    if (c->evict_sample != 0 && 2 * (unsigned long long)share <= c->dsel.cand_cap)
+        c->dsel.sample = c->evict_sample > 0 ? c->evict_sample
+                                             : (int)(std::max<int64_t>(1, std::min<int64_t>(63, c->hwm / 16384)) | 1);
     c->dsel_level = 0;
     c->dsel_push = false;
     c->dsel_done = false;
@@ -1945,7 +1951,8 @@ cache_status cache_evict_sel_apply(cache_t* c, int64_t cap, uint64_t* out_evicte
     c->last_sel[0] = h.levels;
     c->last_sel[1] = h.full_sweeps;
     c->last_sel[2] = h.compact_level;
-    c->last_sel[3] = (int64_t)h.cnt[3];
+    c->last_sel[3] = (int64_t)(h.window == 1 ? h.cnt_w : h.cnt[3]);
+    c->last_window = h.window;
     if (h.err || n > cap || nd > cap || (unsigned long long)n > c->dsel.ev_cap)
         return fail(CACHE_E_STATE, "cache_evict_sel_apply: selection failed or more evictions than the output "
                                    "capacity (ranks passed different n?); handle state undefined");

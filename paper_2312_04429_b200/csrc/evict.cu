@@ -1250,46 +1250,10 @@ __global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : ((kSelC
         if (lane == 0 && inv) atomicMax(&a.out->kmin_inv, inv);
     };
 
-    // ---- distributed phases: one level per launch, the state in a.state ----
-    if (a.phase == kPhaseL0) {
-        SelLevel L{0ull, 0ull, 64, 0, false, 0ull, 0ull};
-        clear_sh();
-        unsigned long long kmin = ~0ull;
-        full_sweep(kSweepL0, L, kmin);
-        flush_sh(a.level_hist);
-        kmin_to_global(kmin);
-        return;
-    }
-    if (a.phase == kPhaseLevel || a.phase == kPhaseFinal) {
-        const SelState S = *a.state;
-        SelLevel L{S.lo, 0ull, S.w, S.shift, false, S.kb, S.ev_lim};
-        if (a.phase == kPhaseFinal) {
-            finish(L, S.compacted != 0u, S.ncand, S.fail != 0u, (int)S.level, (int)S.full, (int)S.compact_level);
-            return;
-        }
-        if (S.done) return;
-        L.compact = !S.compacted && S.pcnt <= a.cand_cap;
-        clear_sh();
-        unsigned long long kmin = ~0ull;
-        if (!S.compacted) full_sweep(kSweepLevel, L, kmin);
-        else cand_sweep(kSweepLevel, L, S.ncand);
-        flush_sh(a.level_hist);
-        return;
-    }
-
-    // ---- single cache: the whole selection in this launch ----
-    // level 0: log-bin histogram + min key
-    int ts = 0;
-    sel_stamp(ts);
-    SelLevel L{0ull, 0ull, 64, 0, false, 0ull, 0ull};
-    // Single-sweep window: a systematic 1/S sample of the slots estimates the n-th key; its
-    // rank r = n * (sampled units / live units) is padded by 4 sqrt(r) + 16, and the upper edge
-    // of the sample bin holding that rank becomes the window hi.  The level-0 sweep then also
-    // compacts every key < hi.  If the n-th key's level-0 bin ends below hi (and nothing
-    // overflowed the buffer), every key the selection can still pick is a candidate: the levels
-    // and the apply run on the candidates and the second full sweep is skipped.  Otherwise the
-    // usual path runs -- the estimate only decides speed, never the result.
-    if (a.sample > 0) {
+    // Single-sweep window estimate: a block sample of this shard (every S-th 32-slot block, a
+    // warp per block) -> the upper bin edge of the sample rank of the target-th key, padded;
+    // sets L.T = that edge and L.compact (the level-0 sweep then compacts every key below it).
+    auto window_estimate = [&](SelLevel& L, unsigned long long target, int& ts) {
         // every S-th block of 32 slots, a warp per block (lane = slot: every load a full line).
         // Single slots every S slots (random 4-B accesses) ran at a fraction of the HBM rate:
         // 15 us for the 1/63 sample of 12.5M slots (NV_SEL_TRACE)
@@ -1316,7 +1280,7 @@ __global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : ((kSelC
         if (ns && a.units) {
             // pad: 4 sigma of the sampling noise + two sample blocks' worth of units (on keys
             // that grow with the slot, a 32-slot block is the sample's resolution)
-            const double r = ceil((double)a.n * (double)ns / (double)a.units);
+            const double r = ceil((double)target * (double)ns / (double)a.units);
             const unsigned long long rhi =
                 (unsigned long long)(r + 4.0 * sqrt(r) + 64.0 * (GRAN == CACHE_EVICT_ITEM ? nk : 1) + 16.0);
             if (rhi <= ns) {
@@ -1331,7 +1295,55 @@ __global__ void __launch_bounds__(kSelThreads, (NK5 && kSelStaged) ? 1 : ((kSelC
             }
         }
         sel_stamp(ts);
+    };
+    // ---- distributed phases: one level per launch, the state in a.state ----
+    if (a.phase == kPhaseL0) {
+        SelLevel L{0ull, 0ull, 64, 0, false, 0ull, 0ull};
+        // the window on this shard: its share of the n keys taken as n / world (ids, hence
+        // keys, interleave over the ranks); whether the window holds is decided per rank by
+        // the level-0 pick (k_evict_dpick) -- a rank whose window misses sweeps again
+        int ts_unused = 0;
+        if (a.sample > 0) window_estimate(L, (a.n + (unsigned long long)a.world - 1ull) / (unsigned long long)a.world, ts_unused);
+        if (blockIdx.x == 0 && threadIdx.x == 0) a.out->whi = L.compact ? L.T : 0ull;
+        clear_sh();
+        unsigned long long kmin = ~0ull;
+        full_sweep(kSweepL0, L, kmin);
+        flush_sh(a.level_hist);
+        kmin_to_global(kmin);
+        return;
     }
+    if (a.phase == kPhaseLevel || a.phase == kPhaseFinal) {
+        const SelState S = *a.state;
+        SelLevel L{S.lo, 0ull, S.w, S.shift, false, S.kb, S.ev_lim};
+        if (a.phase == kPhaseFinal) {
+            int ts_unused = 0;
+            finish(L, S.compacted != 0u, S.ncand, S.fail != 0u, (int)S.level, (int)S.full, (int)S.compact_level,
+                   &ts_unused, S.pad1);
+            return;
+        }
+        if (S.done) return;
+        L.compact = !S.compacted && S.pcnt <= a.cand_cap;
+        clear_sh();
+        unsigned long long kmin = ~0ull;
+        if (!S.compacted) full_sweep(kSweepLevel, L, kmin);
+        else cand_sweep(kSweepLevel, L, S.ncand);
+        flush_sh(a.level_hist);
+        return;
+    }
+
+    // ---- single cache: the whole selection in this launch ----
+    // level 0: log-bin histogram + min key
+    int ts = 0;
+    sel_stamp(ts);
+    SelLevel L{0ull, 0ull, 64, 0, false, 0ull, 0ull};
+    // Single-sweep window: a systematic 1/S sample of the slots estimates the n-th key; its
+    // rank r = n * (sampled units / live units) is padded by 4 sqrt(r) + 16, and the upper edge
+    // of the sample bin holding that rank becomes the window hi.  The level-0 sweep then also
+    // compacts every key < hi.  If the n-th key's level-0 bin ends below hi (and nothing
+    // overflowed the buffer), every key the selection can still pick is a candidate: the levels
+    // and the apply run on the candidates and the second full sweep is skipped.  Otherwise the
+    // usual path runs -- the estimate only decides speed, never the result.
+    if (a.sample > 0) window_estimate(L, a.n, ts);
     clear_sh();
     unsigned long long kmin = ~0ull;
     full_sweep(kSweepL0, L, kmin);
@@ -1424,6 +1436,17 @@ __global__ void __launch_bounds__(kSelThreads) k_evict_dpick(SelArgs a, const ui
             S.level = 1u;
             S.full = 1u;
             S.compact_level = 0u;
+            S.pad1 = 0u;   // single-sweep window: 0 off, 1 this rank's candidates hold the cut, 2 missed
+            const unsigned long long whi = __ldcg(&a.out->whi), nw = __ldcg(&a.out->cnt_w);
+            if (whi) {
+                if (!S.fail && S.lo + ((1ull << S.w) - 1ull) < whi && nw <= a.cand_cap) {
+                    S.compacted = 1u;
+                    S.ncand = (long long)nw;
+                    S.pad1 = 1u;
+                } else {
+                    S.pad1 = 2u;
+                }
+            }
         }
     } else {
         // this level's sweep compacted iff the state allowed it before the sweep (same rule)

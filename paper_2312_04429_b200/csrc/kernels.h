@@ -125,6 +125,7 @@ struct SelOut {
     unsigned long long cnt_w;     // single-sweep window: keys compacted by the level-0 sweep
     uint32_t window, pad;         // 0 off, 1 the selection ran on the window, 2 the estimate missed
     unsigned long long gnext[16]; // full sweeps (<= 9) of the single-cache launch: claimed tail groups
+    unsigned long long whi;       // distributed level 0: this rank's window edge (0: none)
 };
 constexpr int kSelBins = 4096, kSelMaxLevels = 8;
 // Selection state between the host-driven phases of the DISTRIBUTED fused eviction (each rank
@@ -135,7 +136,7 @@ struct SelState {
     int w, shift, compact, pad0;
     unsigned long long rem, pcnt;           // rank wanted inside [lo, lo + 2^w), keys in it (global)
     long long ncand;                        // this rank's compacted candidates
-    uint32_t done, fail, compacted, level, full, compact_level, pad1, pad2;
+    uint32_t done, fail, compacted, level, full, compact_level, pad1, pad2;   // pad1: window (0 off, 1 held, 2 missed)
 };
 enum { kPhaseAll = 0, kPhaseL0 = 1, kPhaseLevel = 2, kPhaseFinal = 3 };
 struct SelArgs {

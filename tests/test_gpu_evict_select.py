@@ -259,6 +259,11 @@ def test_distributed_levels_equal_single_cache(world, push, policy, gran, cap):
         e1, d1 = single.evict(nev)
         e2, d2 = vs.evict(nev)
         assert np.array_equal(e1, e2) and np.array_equal(d1, d2), (r, nev)
+        # each rank's single-sweep window (level 0 compacts below its own estimate): held or
+        # missed per rank, never when the candidate buffer is capped below the share
+        wins = [B.debug_evict_window(c) for c in vs.caches]
+        allowed = {-1: (1, 2), 0: (0,)}.get(cap, (0, 1, 2))
+        assert all(w in allowed for w in wins), (wins, cap)
         ne, _ = synth.entries(40, seed=700 + r)
         single.insert(torch.from_numpy(ne).cuda())
         vs.insert(torch.from_numpy(ne).cuda())
