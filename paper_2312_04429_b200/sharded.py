@@ -244,9 +244,11 @@ class ShardedCache:
         if not lists:
             return res   # this rank's (evicted count, dirty count)
         ev, dirty = res
-        evs = self.comm.all_gather_object(self.cache.last_evicted_keys().tolist())
-        dts = self.comm.all_gather_object(dirty.tolist())
-        return _merge_evicted(evs, self.cache), np.array(sorted(x for d in dts for x in d), dtype=np.uint64)
+        # numpy arrays (pickled as one buffer each), merged vectorised: Python lists of the 619K
+        # keys of a 1% eviction at 12.5M entries per rank cost ~45 ms of host time
+        evs = self.comm.all_gather_object(np.ascontiguousarray(self.cache.last_evicted_keys(), dtype=np.uint64))
+        dts = self.comm.all_gather_object(np.ascontiguousarray(dirty, dtype=np.uint64))
+        return _merge_evicted(evs, self.cache), _sorted_u64(dts)
 
 
 class VirtualShards:
@@ -323,9 +325,8 @@ class VirtualShards:
                 if dones[0]:
                     break
             res = [c.evict_sel_apply(cap) for c, cap in zip(self.caches, caps)]
-            keys = [c.last_evicted_keys().tolist() for c in self.caches]
-            return (_merge_evicted(keys, self.caches[0]),
-                    np.array(sorted(x for r in res for x in r[1].tolist()), dtype=np.uint64))
+            keys = [c.last_evicted_keys() for c in self.caches]
+            return _merge_evicted(keys, self.caches[0]), _sorted_u64([r[1] for r in res])
         if self.push:   # one stream: pass p's histogram on every rank, then every rank's pick
             for p in range(8):
                 for c in self.caches:
@@ -333,9 +334,8 @@ class VirtualShards:
                 for c in self.caches:
                     c.push_evict_pick(p)
             res = [c.push_evict_apply(n) for c in self.caches]
-            keys = [c.last_evicted_keys().tolist() for c in self.caches]
-            return (_merge_evicted(keys, self.caches[0]),
-                    np.array(sorted(x for r in res for x in r[1].tolist()), dtype=np.uint64))
+            keys = [c.last_evicted_keys() for c in self.caches]
+            return _merge_evicted(keys, self.caches[0]), _sorted_u64([r[1] for r in res])
         sts = [torch.tensor([0, 0, n], dtype=torch.int64, device="cuda") for _ in self.caches]
         hists = [torch.zeros(256, dtype=torch.int32, device="cuda") for _ in self.caches]
         for p in range(8):
@@ -346,9 +346,8 @@ class VirtualShards:
                 h.copy_(tot)
                 c.evict_pick(h, st, p)
         res = [c.evict_apply(st, n) for c, st in zip(self.caches, sts)]
-        keys = [c.last_evicted_keys().tolist() for c in self.caches]
-        return (_merge_evicted(keys, self.caches[0]),
-                np.array(sorted(x for r in res for x in r[1].tolist()), dtype=np.uint64))
+        keys = [c.last_evicted_keys() for c in self.caches]
+        return _merge_evicted(keys, self.caches[0]), _sorted_u64([r[1] for r in res])
 
     def meta(self, id_: int):
         return self.caches[id_ % self.world].meta(id_)
@@ -366,11 +365,19 @@ class VirtualShards:
         return {k: sum(s[k] for s in ss) if k not in ("next_id",) else ss[0][k] for k in ss[0]}
 
 
+def _sorted_u64(arrays) -> np.ndarray:
+    """The union of the ranks' uint64 arrays (or lists), ascending.  Each rank's list is already
+    ascending: the stable sort (timsort on integers wider than 16 bits) merges the runs in
+    linear time."""
+    parts = [np.asarray(a, dtype=np.uint64).ravel() for a in arrays]
+    return np.sort(np.concatenate(parts), kind="stable") if parts else np.zeros(0, np.uint64)
+
+
 def _merge_evicted(key_lists, cache):
     """The global eviction order (the API's: ascending unit key, R11 / R24) from the ranks'
     full 64-bit keys (cache_last_evicted_keys; keys are unique across ranks), mapped to what
     cache_evict reports: id << 3 | j per item, or the entry id in entry mode."""
-    keys = np.sort(np.array([x for l in key_lists for x in l], dtype=np.uint64))
+    keys = _sorted_u64(key_lists)
     entry = getattr(cache, "granularity", B.EVICT_ITEM) == B.EVICT_ENTRY
     mask = np.uint64(0xFFFFFFFF) if entry else np.uint64((1 << 35) - 1)
     return keys & mask
